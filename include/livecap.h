@@ -1,0 +1,266 @@
+/*
+ * livecap.h -- C-ABI of liblivecap.so, the sm_100a implementation of the
+ * LiveCap pose + non-rigid Gauss-Newton hot path.
+ *
+ * Plain C types only (pointers + sizes).  All host pointers are owned by the
+ * caller for the duration of the call and never retained; device state lives
+ * inside the opaque handles.  Every entry point returns LC_OK or an error
+ * code; lc_last_error() describes the last failure on the calling thread.
+ * Numerical events (damping, PCG breakdown, halvings, rejected steps,
+ * behind-camera points, gimbal, pruned colours, degenerate edges, snap
+ * walked/reached/stuck) are report fields, never errors -- the reference's
+ * convention (reference pkg/src/montrack/solvers.py:48-54,
+ * pose_stage.py:407-426, nonrigid_stage.py:352-369).
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/montrack/).
+ */
+#ifndef LIVECAP_H
+#define LIVECAP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LC_OK      0
+#define LC_EINVAL  1   /* maps to ValueError (reference raises at construction) */
+#define LC_ECUDA   2   /* maps to RuntimeError */
+#define LC_ENOMEM  3   /* maps to MemoryError / RuntimeError */
+#define LC_ECAP    4   /* a capacity-bounded buffer overflowed (RuntimeError) */
+
+#define LC_MAX_JOINTS 32
+#define LC_N_POSE 36
+#define LC_MAX_LOG 64
+
+typedef struct lc_ctx lc_ctx;
+typedef struct lc_actor lc_actor;
+typedef struct lc_tracker lc_tracker;
+typedef struct lc_field lc_field;
+
+typedef struct {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+} lc_camera;   /* camera.py:20-33 */
+
+/* Actor upload: TemplateMesh + derived connectivity, Skeleton, SkinningWeights
+ * (template.py:68-256).  Derived arrays are passed exactly as the reference's
+ * TemplateMesh.__post_init__ computes them (template.py:84-129). */
+typedef struct {
+    int32_t n_vertices, n_triangles, n_edges, n_joints;
+    const double  *rest_vertices;     /* N*3 */
+    const int64_t *triangles;         /* T*3 */
+    const double  *vertex_colors;     /* N*3 */
+    const int64_t *vertex_labels;     /* N, classes 1..7 */
+    const int64_t *edges;             /* E*2, i<j, lexicographic */
+    const int64_t *edge_tris;         /* E*2, -1 for open boundary */
+    const int64_t *degrees;           /* N */
+    const double  *directed_weights;  /* 2E material weights s_ij */
+    /* skeleton */
+    const int64_t *parents;           /* J */
+    const double  *local_offsets;     /* J*3 */
+    const int64_t *dof_joint;         /* 27 */
+    const double  *dof_axes;          /* 27*3 unit */
+    const double  *theta_min;         /* 27 */
+    const double  *theta_max;         /* 27 */
+    const double  *marker_offsets;    /* 4*3 */
+    int32_t head_index;
+    const int32_t *temporal_group;    /* J, index into lc_pose_hyper.group_weights */
+    const int32_t *joint_parts;       /* J, body part ids (nonrigid_stage.py:55-84) */
+    /* skinning */
+    const int64_t *skin_indices;      /* N*4, -1 padding */
+    const double  *skin_weights;      /* N*4 */
+} lc_actor_desc;
+
+typedef struct {   /* pose_stage.py:37-48 */
+    double lambda_2d, lambda_3d, lambda_sil, lambda_temporal, lambda_anatomic, face_weight;
+    double group_weights[8];   /* temporal weight per group id */
+    int32_t gn_iterations, max_halvings;
+} lc_pose_hyper;
+
+typedef struct {   /* nonrigid_stage.py:33-49 */
+    double w_photo, w_sil, w_smooth, w_edge, w_velocity, w_acceleration, tau_color;
+    int32_t gn_iterations, pcg_iterations, max_halvings;
+    int32_t n_levels;
+    int32_t pyramid_kernels[4];
+    /* optional normalized taps per level (gaussian_kernel, imageproc.py:264-273);
+     * all-zero rows are computed by the library */
+    double pyramid_taps[4][32];
+    int32_t part_dilation;
+    double snap_step;
+    int32_t snap_max_steps;
+    double snap_band;
+} lc_nonrigid_hyper;
+
+typedef struct {   /* pipeline.py:48-61 */
+    int32_t mode;              /* 0 full, 1 pose_only, 2 detections_only */
+    int32_t directional, enable_warping, enable_part_mask, enable_snapping;
+    int32_t frame0_rounds, frame0_iteration_scale;
+    lc_pose_hyper pose;
+    lc_nonrigid_hyper nonrigid;
+} lc_config;
+
+typedef struct {   /* FrameDetections, pose_stage.py:51-64 (joints3d raw, not rescaled) */
+    const double  *joints2d;   /* (J+4)*2 */
+    const double  *joints3d;   /* J*3 root-relative */
+    const uint8_t *valid2d;    /* J+4 */
+    const uint8_t *valid3d;    /* J */
+} lc_detections;
+
+typedef struct {   /* solvers.py:97-101 */
+    int32_t iterations, breakdown;
+    double residual_norms[LC_MAX_LOG];
+} lc_pcg_info;
+
+typedef struct {   /* solvers.py:35-38 */
+    int32_t damped;
+    double damping;
+} lc_dense_info;
+
+typedef struct {   /* pose_stage.py:407-426 (one PoseIterationLog per entry) */
+    int32_t n_iterations, behind_camera, gimbal;
+    double energy_before[LC_MAX_LOG], energy_after[LC_MAX_LOG], step_norm[LC_MAX_LOG];
+    double terms[LC_MAX_LOG][5];      /* detection2d, detection3d, silhouette, temporal, anatomic */
+    int32_t halvings[LC_MAX_LOG], rejected[LC_MAX_LOG], damped[LC_MAX_LOG];
+    int32_t n_contour, has_temporal;
+} lc_pose_report;
+
+typedef struct {   /* nonrigid_stage.py:352-369,409-414 */
+    int32_t n_iterations, pruned, degenerate_edges, behind_camera;
+    int32_t level[LC_MAX_LOG];
+    double energy_before[LC_MAX_LOG], energy_after[LC_MAX_LOG];
+    double terms[LC_MAX_LOG][6];      /* photo, silhouette, smooth, edge, velocity, acceleration */
+    int32_t has_temporal;
+    int32_t halvings[LC_MAX_LOG], rejected[LC_MAX_LOG], pcg_breakdown[LC_MAX_LOG];
+    int32_t snapped, snap_walked, snap_reached, snap_stuck, snap_moved;
+    int32_t n_visible, n_boundary, n_enabled;
+} lc_nonrigid_report;
+
+typedef struct {
+    lc_pose_report pose;
+    lc_nonrigid_report nonrigid;
+    int32_t rescale_fallbacks;
+} lc_frame_report;
+
+/* Per-call problem descriptors (the reference's PoseProblem / NonrigidProblem
+ * fields, pose_stage.py:284-297, nonrigid_stage.py:160-176). */
+typedef struct {
+    const uint8_t *mask;              /* H*W observed silhouette (DistanceField.mask) or NULL */
+    const double  *joints2d;          /* (J+4)*2 */
+    const double  *joints3d;          /* J*3, already bone-length rescaled */
+    const uint8_t *valid2d, *valid3d;
+    int32_t n_contour;
+    const int64_t *contour_indices;   /* B */
+    const double  *contour_normals2d; /* B*2 */
+    const double  *contour_rest;      /* B*3 */
+    const uint8_t *contour_enabled;   /* B or NULL */
+    const double  *prev_positions;    /* J*3 or NULL */
+    int32_t directional;
+    lc_pose_hyper hyper;
+} lc_pose_problem;
+
+typedef struct {
+    const uint8_t *mask;              /* H*W or NULL (no silhouette field) */
+    int32_t n_levels;
+    const double  *pyramid;           /* n_levels*H*W*3, coarse first */
+    const double  *skinned;           /* N*3 V^S */
+    int32_t n_visible;
+    const int64_t *visible;           /* P */
+    int32_t n_boundary;
+    const int64_t *boundary;          /* B */
+    const double  *normals2d;         /* B*2 */
+    const uint8_t *enabled;           /* B */
+    const double  *prev, *prev2;      /* N*3 or NULL */
+    int32_t directional, enable_photo, enable_sil;
+    lc_nonrigid_hyper hyper;
+} lc_nonrigid_problem;
+
+/* ---- context / errors ---- */
+const char *lc_last_error(void);
+int lc_version(void);
+int lc_ctx_create(int32_t device, uint64_t cuda_stream, lc_ctx **out);
+int lc_ctx_destroy(lc_ctx *ctx);
+int lc_ctx_synchronize(lc_ctx *ctx);
+int lc_kernel_launches(lc_ctx *ctx, int64_t *count);   /* kernels launched on ctx so far */
+
+/* ---- actor (template.py:68-256; uploaded once, immutable) ---- */
+int lc_actor_upload(lc_ctx *ctx, const lc_actor_desc *desc, lc_actor **out);
+int lc_actor_destroy(lc_actor *actor);
+
+/* ---- kernel-level seams ---- */
+/* solvers.py:104-145 pcg_solve(BlockSparseSystem) -- explicit layout */
+int lc_pcg_solve_bsr(lc_ctx *ctx, int32_t n, int64_t m, const double *diag, const double *off,
+                     const int64_t *rows, const int64_t *cols, const double *rhs,
+                     int32_t iterations, double *x_out, lc_pcg_info *info);
+/* solvers.py:41-56 dense_solve(DenseNormalSystem) */
+int lc_dense_solve(lc_ctx *ctx, int32_t n, const double *a, const double *b, double *x_out,
+                   lc_dense_info *info);
+/* imageproc.py:264-285 gaussian_pyramid; image H*W*C, out n_levels*H*W*C */
+int lc_gaussian_pyramid(lc_ctx *ctx, int32_t h, int32_t w, int32_t c, const double *image,
+                        int32_t n_levels, const int32_t *kernel_sizes, const double *taps /*n_levels*32 or NULL*/,
+                        double *out);
+/* debug: the library's own tap / rim-probe tables (for host-side checks) */
+int lc_debug_tables(int32_t size, double *taps_out, double *probe_out);
+/* rasterizer.py:77-120 render_depth / render_attributes / render_vertex_ids.
+ * mode 0 depth, 1 attributes (n_attr), 2 vertex ids. */
+int lc_render(lc_ctx *ctx, const lc_camera *cam, int32_t n, const double *verts, int32_t t,
+              const int64_t *tris, int32_t mode, const double *attrs, int32_t n_attr,
+              const int64_t *ids, double bg_attr, int64_t bg_id,
+              double *zbuf_out, double *attr_out, int64_t *id_out);
+/* imageproc.py:177-261 DistanceField: exact nearest contour-pixel centre */
+int lc_field_create(lc_ctx *ctx, int32_t h, int32_t w, const uint8_t *mask, lc_field **out);
+int lc_field_destroy(lc_field *f);
+int lc_field_n_contour(lc_field *f, int32_t *k);
+/* kind 0: value(dist, clamped) 1: interface 2: residual(res, grad2) 3: gradient(vec2)
+ * 4: inside.  out layout: n * 4 doubles [a, b, c, flag]. */
+int lc_field_query(lc_field *f, int64_t n, const double *pos, int32_t kind, double *out);
+/* skinning.py:206-246 forward_kinematics */
+int lc_forward_kinematics(lc_ctx *ctx, const lc_actor *actor, const double *x36,
+                          double *rot_out /*J*9*/, double *pos_out /*J*3*/,
+                          double *markers_out /*12*/, double *dqs_out /*J*8*/, int32_t *gimbal);
+/* skinning.py:378-398 skin_points (subset may be NULL) + optional jac (M*3*36) */
+int lc_skin_points(lc_ctx *ctx, const lc_actor *actor, const double *x36, int32_t m,
+                   const double *rest, const int64_t *subset, double *pos_out, double *rot_out,
+                   double *jac_out);
+/* pose_stage.py:151-191 extract_contour_vertices (+ visibility via own raster);
+ * returns indices/normals, n_out = B; capacity = N. */
+int lc_contour_vertices(lc_ctx *ctx, const lc_actor *actor, const lc_camera *cam,
+                        const double *verts, int32_t *n_out, int64_t *idx_out, double *n2d_out);
+
+/* ---- stage solvers ---- */
+/* pose_stage.py:429-459 solve_pose */
+int lc_pose_solve(lc_ctx *ctx, const lc_actor *actor, const lc_camera *cam,
+                  const lc_pose_problem *pb, const double *x0, double *x_out,
+                  lc_pose_report *report);
+/* nonrigid_stage.py:372-403 solve_nonrigid (+ optional snap_vertices :417-500) */
+int lc_nonrigid_solve(lc_ctx *ctx, const lc_actor *actor, const lc_camera *cam,
+                      const lc_nonrigid_problem *pb, const double *v0, int32_t do_solve,
+                      int32_t do_snap, double *v_out, lc_nonrigid_report *report);
+
+/* ---- batched multi-stream tracker (pipeline.py:263-302 solve_frame, per stream) ---- */
+int lc_tracker_create(lc_ctx *ctx, const lc_actor *actor, const lc_camera *cam,
+                      const lc_config *cfg, int32_t n_streams, lc_tracker **out);
+int lc_tracker_destroy(lc_tracker *tr);
+/* stage frame inputs of one stream: image H*W*3 f64, mask H*W u8.
+ * on_device != 0: pointers are device pointers (already resident in HBM). */
+int lc_tracker_set_frame(lc_tracker *tr, int32_t stream, const double *image,
+                         const uint8_t *mask, const lc_detections *det, int32_t on_device);
+/* preprocess + condition + solve_frame for every stream (asynchronous) */
+int lc_tracker_step(lc_tracker *tr);
+int lc_tracker_get_result(lc_tracker *tr, int32_t stream, double *pose_out, double *verts_out,
+                          double *skinned_out, lc_frame_report *report);
+/* TrackState injection / readout (pipeline.py:135-142); NULL pointers = None */
+int lc_tracker_set_state(lc_tracker *tr, int32_t stream, const double *x_prev,
+                         const double *x_prev2, const double *joints_prev,
+                         const double *disp_rest, const double *v_prev, const double *v_prev2);
+int lc_tracker_get_state(lc_tracker *tr, int32_t stream, int32_t *flags, double *x_prev,
+                         double *x_prev2, double *joints_prev, double *disp_rest,
+                         double *v_prev, double *v_prev2);
+/* device pointer of a stream's resident vertices (N*3) for zero-copy readers */
+int lc_tracker_device_vertices(lc_tracker *tr, int32_t stream, uint64_t *dptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

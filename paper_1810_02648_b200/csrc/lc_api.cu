@@ -1,0 +1,1571 @@
+// C-ABI entry points (include/livecap.h) and the host runtime that schedules
+// the kernels: actor upload, per-stream slots, the per-frame stage schedule
+// of solve_frame (reference pipeline.py:156-302) batched over streams, and
+// the single-call seams used by the Python mirror of the reference API.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+#include "lc_runtime.h"
+
+// ---------------------------------------------------------------------------
+// errors
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(expr)                                                                           \
+    do {                                                                                   \
+        cudaError_t e_ = (expr);                                                           \
+        if (e_ != cudaSuccess) return fail(LC_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define API_BEGIN try {
+#define API_END                                                                            \
+    }                                                                                      \
+    catch (const std::bad_alloc &) { return fail(LC_ENOMEM, "device allocation failed"); } \
+    catch (const std::exception &ex) { return fail(LC_EINVAL, ex.what()); }
+
+struct ApiError : std::exception {
+    std::string m;
+    explicit ApiError(std::string s) : m(std::move(s)) {}
+    const char *what() const noexcept override { return m.c_str(); }
+};
+static void require(bool ok, const char *msg) {
+    if (!ok) throw ApiError(msg);
+}
+
+template <typename K, typename... Args>
+static void launch(lc_ctx *c, K kernel, dim3 g, dim3 b, size_t smem, Args... args) {
+    kernel<<<g, b, smem, c->stream>>>(args...);
+    c->launches++;
+}
+
+static int last_launch_status() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(LC_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+    return LC_OK;
+}
+
+extern "C" const char *lc_last_error(void) { return g_err.c_str(); }
+extern "C" int lc_version(void) { return 1; }
+
+// ---------------------------------------------------------------------------
+// job staging: small per-launch descriptor arrays copied H2D in stream order
+
+struct JobRing {
+    char *dev = nullptr;
+    size_t cap = 0, off = 0;
+    void *put(cudaStream_t st, const void *host, size_t bytes) {
+        bytes = (bytes + 255) & ~size_t(255);
+        if (off + bytes > cap) off = 0;
+        void *d = dev + off;
+        cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, st);
+        off += bytes;
+        return d;
+    }
+};
+static JobRing &ring_of(lc_ctx *c) {
+    static thread_local std::vector<std::pair<lc_ctx *, JobRing>> rings;
+    for (auto &r : rings)
+        if (r.first == c) return r.second;
+    JobRing jr;
+    jr.cap = 8 << 20;
+    if (cudaMalloc(&jr.dev, jr.cap) != cudaSuccess) throw std::bad_alloc();
+    rings.push_back({c, jr});
+    return rings.back().second;
+}
+template <typename T>
+static const T *stage(lc_ctx *c, const std::vector<T> &v) {
+    // pad to 256 B so ring slices stay aligned
+    std::vector<char> buf(((v.size() * sizeof(T)) + 255) & ~size_t(255));
+    std::memcpy(buf.data(), v.data(), v.size() * sizeof(T));
+    return static_cast<const T *>(ring_of(c).put(c->stream, buf.data(), buf.size()));
+}
+
+// ---------------------------------------------------------------------------
+// context
+
+extern "C" int lc_ctx_create(int32_t device, uint64_t cuda_stream, lc_ctx **out) {
+    API_BEGIN
+    require(out != nullptr, "out is null");
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    require(device >= 0 && device < n, "device ordinal out of range");
+    CK(cudaSetDevice(device));
+    lc_ctx *c = new lc_ctx();
+    c->device = device;
+    if (cuda_stream) {
+        c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+    } else {
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    cudaFuncSetAttribute(k_pose_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    *out = c;
+    return LC_OK;
+    API_END
+}
+
+extern "C" int lc_ctx_destroy(lc_ctx *c) {
+    if (!c) return LC_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    delete c->call_slot;
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return LC_OK;
+}
+
+extern "C" int lc_ctx_synchronize(lc_ctx *c) {
+    require(c != nullptr, "null ctx");
+    CK(cudaStreamSynchronize(c->stream));
+    return last_launch_status();
+}
+
+extern "C" int lc_kernel_launches(lc_ctx *c, int64_t *count) {
+    if (!c || !count) return fail(LC_EINVAL, "null argument");
+    *count = c->launches;
+    return LC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// actor upload (template.py:68-256 layout -> device tables)
+
+static const double kClassWeight[8] = {0.0, 1.0, 2.0, 2.5, 3.0, 50.0, 100.0, 200.0};
+
+extern "C" int lc_actor_upload(lc_ctx *c, const lc_actor_desc *d, lc_actor **out) {
+    API_BEGIN
+    require(c && d && out, "null argument");
+    const int N = d->n_vertices, T = d->n_triangles, E = d->n_edges, J = d->n_joints;
+    require(N > 0 && T >= 0 && E >= 0, "mesh needs vertices");
+    require(J > 0 && J <= LC_MAXJ, "skeleton must have 1..32 joints");
+    require(d->head_index >= 0 && d->head_index < J, "head index out of range");
+    CK(cudaSetDevice(c->device));
+    lc_actor *a = new lc_actor();
+    a->ctx = c;
+    cudaStream_t st = c->stream;
+
+    // ---- skeleton
+    SkelDev &s = a->skel;
+    std::memset(&s, 0, sizeof(s));
+    s.J = J;
+    s.head = d->head_index;
+    for (int i = 0; i < J; ++i) {
+        s.parents[i] = (int)d->parents[i];
+        require(i == 0 ? s.parents[i] == -1 : (s.parents[i] >= 0 && s.parents[i] < i),
+                "parents must precede children with a single root");
+        for (int k = 0; k < 3; ++k) s.off[i][k] = d->local_offsets[3 * i + k];
+        for (int k = 0; k < 3; ++k)
+            s.rest[i][k] = s.off[i][k] + (i > 0 ? s.rest[s.parents[i]][k] : 0.0);
+        s.group[i] = d->temporal_group ? d->temporal_group[i] : 0;
+        s.joint_part[i] = d->joint_parts ? d->joint_parts[i] : 1;
+    }
+    for (int k = 0; k < LC_NDOF; ++k) {
+        s.dof_joint[k] = (int)d->dof_joint[k];
+        require(s.dof_joint[k] >= 0 && s.dof_joint[k] < J, "dof joint out of range");
+        for (int q = 0; q < 3; ++q) s.dof_axes[k][q] = d->dof_axes[3 * k + q];
+        s.tmin[k] = d->theta_min[k];
+        s.tmax[k] = d->theta_max[k];
+    }
+    for (int m = 0; m < 4; ++m)
+        for (int q = 0; q < 3; ++q) s.marker[m][q] = d->marker_offsets[3 * m + q];
+    // ancestor masks: dof k moves positions strictly below its joint, frames at/below
+    for (int k = 0; k < LC_NDOF; ++k) {
+        unsigned pos = 0, frame = 0;
+        for (int i = 0; i < J; ++i) {
+            int q = i;
+            bool below = false;
+            while (q != -1) {
+                if (q == s.dof_joint[k]) { below = true; break; }
+                q = s.parents[q];
+            }
+            if (below) {
+                frame |= 1u << i;
+                if (i != s.dof_joint[k]) pos |= 1u << i;
+            }
+        }
+        s.moves_pos[k] = pos;
+        s.moves_frame[k] = frame;
+    }
+    int cur = 0;
+    for (int i = 0; i < J; ++i) {
+        s.dof_start[i] = cur;
+        for (int k = 0; k < LC_NDOF; ++k)
+            if (s.dof_joint[k] == i) s.dof_list[cur++] = k;
+    }
+    s.dof_start[J] = cur;
+    std::vector<int> depth(J, 0);
+    int maxd = 0;
+    for (int i = 1; i < J; ++i) {
+        depth[i] = depth[s.parents[i]] + 1;
+        maxd = std::max(maxd, depth[i]);
+    }
+    cur = 0;
+    for (int L = 0; L <= maxd; ++L) {
+        s.level_start[L] = cur;
+        for (int i = 0; i < J; ++i)
+            if (depth[i] == L) s.level_joint[cur++] = i;
+    }
+    s.level_start[maxd + 1] = cur;
+    s.n_tree_levels = maxd + 1;
+    for (int L = 0; L <= maxd; ++L)
+        require(s.level_start[L + 1] - s.level_start[L] <= 32, "too many joints at one depth");
+    a->skel_dev = a->mem.upload(&s, 1, st);
+
+    // ---- mesh tables
+    std::vector<int> tris(3 * (size_t)T), edges(2 * (size_t)E), etris(2 * (size_t)E), deg(N);
+    for (size_t i = 0; i < tris.size(); ++i) {
+        tris[i] = (int)d->triangles[i];
+        require(tris[i] >= 0 && tris[i] < N, "triangle index out of range");
+    }
+    for (size_t i = 0; i < edges.size(); ++i) {
+        edges[i] = (int)d->edges[i];
+        etris[i] = (int)d->edge_tris[i];
+    }
+    for (int i = 0; i < N; ++i) deg[i] = (int)d->degrees[i];
+    std::vector<double> rest_len(E), rest_dir(3 * (size_t)E);
+    for (int e = 0; e < E; ++e) {
+        const double *pa = d->rest_vertices + 3 * (size_t)edges[2 * e];
+        const double *pb = d->rest_vertices + 3 * (size_t)edges[2 * e + 1];
+        const double dx = pa[0] - pb[0], dy = pa[1] - pb[1], dz = pa[2] - pb[2];
+        const double l = std::sqrt(dx * dx + dy * dy + dz * dz);
+        rest_len[e] = l;
+        rest_dir[3 * e] = dx / l;
+        rest_dir[3 * e + 1] = dy / l;
+        rest_dir[3 * e + 2] = dz / l;
+    }
+    // incident edges per vertex in the directed "as source" order of the
+    // reference (forward edges ascending, then reversed edges ascending)
+    std::vector<int> adj_ptr(N + 1, 0), adj_edge(2 * (size_t)E), adj_nbr(2 * (size_t)E);
+    for (int e = 0; e < E; ++e) {
+        adj_ptr[edges[2 * e] + 1]++;
+        adj_ptr[edges[2 * e + 1] + 1]++;
+    }
+    for (int i = 0; i < N; ++i) adj_ptr[i + 1] += adj_ptr[i];
+    {
+        std::vector<int> fill(adj_ptr.begin(), adj_ptr.end() - 1);
+        for (int e = 0; e < E; ++e) {
+            const int i = edges[2 * e];
+            adj_edge[fill[i]] = e;
+            adj_nbr[fill[i]++] = edges[2 * e + 1];
+        }
+        for (int e = 0; e < E; ++e) {
+            const int i = edges[2 * e + 1];
+            adj_edge[fill[i]] = e;
+            adj_nbr[fill[i]++] = edges[2 * e];
+        }
+    }
+    // incident triangles per vertex in np.add.at slot order
+    std::vector<int> vt_ptr(N + 1, 0), vt_tri(3 * (size_t)T);
+    for (int t = 0; t < T; ++t)
+        for (int k = 0; k < 3; ++k) vt_ptr[tris[3 * t + k] + 1]++;
+    for (int i = 0; i < N; ++i) vt_ptr[i + 1] += vt_ptr[i];
+    {
+        std::vector<int> fill(vt_ptr.begin(), vt_ptr.end() - 1);
+        for (int k = 0; k < 3; ++k)
+            for (int t = 0; t < T; ++t) vt_tri[fill[tris[3 * t + k]]++] = t;
+    }
+    std::vector<int> sidx(4 * (size_t)N), dom(N), vpart(N);
+    std::vector<double> rig(N);
+    for (int i = 0; i < N; ++i) {
+        int best = 0;
+        for (int k = 0; k < 4; ++k) {
+            sidx[4 * i + k] = (int)d->skin_indices[4 * i + k];
+            require(sidx[4 * i + k] < J, "skinning references a joint outside the skeleton");
+            if (d->skin_weights[4 * i + k] > d->skin_weights[4 * i + best]) best = k;
+        }
+        dom[i] = sidx[4 * i + best];
+        require(dom[i] >= 0, "dominant skinning slot is padding");
+        vpart[i] = s.joint_part[dom[i]];
+        const int lab = (int)d->vertex_labels[i];
+        require(lab >= 1 && lab <= 7, "invalid material class");
+        rig[i] = kClassWeight[lab];
+    }
+    ActorDev &A = a->dev;
+    A.N = N; A.T = T; A.E = E; A.J = J;
+    A.rest = a->mem.upload(d->rest_vertices, 3 * (size_t)N, st);
+    A.tris = a->mem.upload(tris.data(), tris.size(), st);
+    A.colors = a->mem.upload(d->vertex_colors, 3 * (size_t)N, st);
+    A.edges = a->mem.upload(edges.data(), edges.size(), st);
+    A.edge_tris = a->mem.upload(etris.data(), etris.size(), st);
+    A.rest_len = a->mem.upload(rest_len.data(), rest_len.size(), st);
+    A.rest_dir = a->mem.upload(rest_dir.data(), rest_dir.size(), st);
+    A.adj_ptr = a->mem.upload(adj_ptr.data(), adj_ptr.size(), st);
+    A.adj_edge = a->mem.upload(adj_edge.data(), adj_edge.size(), st);
+    A.adj_nbr = a->mem.upload(adj_nbr.data(), adj_nbr.size(), st);
+    A.degrees = a->mem.upload(deg.data(), deg.size(), st);
+    A.w_dir = a->mem.upload(d->directed_weights, 2 * (size_t)E, st);
+    A.skin_idx = a->mem.upload(sidx.data(), sidx.size(), st);
+    A.skin_w = a->mem.upload(d->skin_weights, 4 * (size_t)N, st);
+    A.dominant = a->mem.upload(dom.data(), dom.size(), st);
+    A.vt_ptr = a->mem.upload(vt_ptr.data(), vt_ptr.size(), st);
+    A.vt_tri = a->mem.upload(vt_tri.data(), vt_tri.size(), st);
+    A.rigidity = a->mem.upload(rig.data(), rig.size(), st);
+    A.vpart = a->mem.upload(vpart.data(), vpart.size(), st);
+    A.skel = a->skel_dev;
+    a->host_edges = edges;
+    a->host_degrees = deg;
+    a->host_wdir.assign(d->directed_weights, d->directed_weights + 2 * (size_t)E);
+    CK(cudaStreamSynchronize(st));
+    *out = a;
+    return LC_OK;
+    API_END
+}
+
+extern "C" int lc_actor_destroy(lc_actor *a) {
+    if (!a) return LC_OK;
+    cudaStreamSynchronize(a->ctx->stream);
+    if (a->ctx->call_actor == a) a->ctx->call_actor = nullptr;
+    delete a;
+    return LC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// slots
+
+static void alloc_grid(DevArena &m, GridBufs &g, int H, int W) {
+    const int ncx = (W + LC_GRID_CELL - 1) / LC_GRID_CELL, ncy = (H + LC_GRID_CELL - 1) / LC_GRID_CELL;
+    g.row_count = m.alloc<int>(H);
+    g.row_start = m.alloc<int>(H + 1);
+    g.cell_count = m.alloc<int>(ncx * ncy);
+    g.cell_start = m.alloc<int>(ncx * ncy + 1);
+    g.cell_fill = m.alloc<int>(ncx * ncy);
+    g.pts = m.alloc<int2>((size_t)H * W);
+    g.cell_pts = m.alloc<int>((size_t)H * W);
+    g.K = m.alloc<int>(1);
+}
+
+void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) {
+    N = N_; T = T_; E = E_; H = H_; W = W_; levels = levels_;
+    const size_t HW = (size_t)H * W;
+    image = mem.alloc<double>(HW * 3);
+    mask = mem.alloc<uint8_t>(HW);
+    image_src = image;
+    mask_src = mask;
+    pyr = mem.alloc<double>(HW * 3 * std::max(levels, 1));
+    blur_tmp = mem.alloc<double>(HW * 3);
+    alloc_grid(mem, obs, H, W);
+    alloc_grid(mem, own, H, W);
+    own_mask = mem.alloc<uint8_t>(HW);
+    j2d = mem.alloc<double>(2 * (LC_MAXJ + 4));
+    j3d_raw = mem.alloc<double>(3 * LC_MAXJ);
+    j3d = mem.alloc<double>(3 * LC_MAXJ);
+    v2d = mem.alloc<uint8_t>(LC_MAXJ + 4);
+    v3d = mem.alloc<uint8_t>(LC_MAXJ);
+    fallbacks = mem.alloc<int>(1);
+    x_prev = mem.alloc<double>(LC_NP);
+    x_prev2 = mem.alloc<double>(LC_NP);
+    joints_prev = mem.alloc<double>(3 * LC_MAXJ);
+    disp = mem.alloc<double>(3 * (size_t)N);
+    v_prev = mem.alloc<double>(3 * (size_t)N);
+    v_prev2 = mem.alloc<double>(3 * (size_t)N);
+    x = mem.alloc<double>(LC_NP);
+    x0 = mem.alloc<double>(LC_NP);
+    drest = mem.alloc<double>(3 * (size_t)N);
+    model = mem.alloc<double>(3 * (size_t)N);
+    vs = mem.alloc<double>(3 * (size_t)N);
+    rot = mem.alloc<double>(4 * (size_t)N);
+    vinit = mem.alloc<double>(3 * (size_t)N);
+    v = mem.alloc<double>(3 * (size_t)N);
+    fk = mem.alloc<FkState>(1);
+    zbuf = mem.alloc<unsigned long long>(HW);
+    tri_id = mem.alloc<int>(HW);
+    tri_front = mem.alloc<uint8_t>(T);
+    vflag = mem.alloc<uint8_t>(N);
+    enabled = mem.alloc<uint8_t>(N);
+    tri_n = mem.alloc<double>(3 * (size_t)T);
+    n2d = mem.alloc<double>(2 * (size_t)N);
+    crest = mem.alloc<double>(3 * (size_t)N);
+    cidx = mem.alloc<int>(N);
+    B = mem.alloc<int>(1);
+    vis = mem.alloc<int>(N);
+    P = mem.alloc<int>(1);
+    diag = mem.alloc<double>(6 * (size_t)N);
+    minv = mem.alloc<double>(6 * (size_t)N);
+    rhs = mem.alloc<double>(3 * (size_t)N);
+    sx = mem.alloc<double>(3 * (size_t)N);
+    sr = mem.alloc<double>(3 * (size_t)N);
+    sz = mem.alloc<double>(3 * (size_t)N);
+    sp = mem.alloc<double>(3 * (size_t)N);
+    sap = mem.alloc<double>(3 * (size_t)N);
+    sbest = mem.alloc<double>(3 * (size_t)N);
+    edir = mem.alloc<double>(3 * (size_t)E);
+    eg = mem.alloc<double>(3 * (size_t)E);
+    off0 = mem.alloc<double>(3 * (size_t)N);
+    off1 = mem.alloc<double>(3 * (size_t)N);
+    hold = mem.alloc<uint8_t>(N);
+    pose_rep = mem.alloc<lc_pose_report>(1);
+    nr_rep = mem.alloc<lc_nonrigid_report>(1);
+}
+
+static CamDev cam_dev(const lc_camera &c) {
+    CamDev d;
+    d.fx = c.fx; d.fy = c.fy; d.cx = c.cx; d.cy = c.cy; d.W = c.width; d.H = c.height;
+    return d;
+}
+
+static NnGridDev grid_dev(const GridBufs &g, const uint8_t *mask, int H, int W) {
+    NnGridDev d;
+    d.K = 0;
+    d.W = W; d.H = H;
+    d.ncx = (W + LC_GRID_CELL - 1) / LC_GRID_CELL;
+    d.ncy = (H + LC_GRID_CELL - 1) / LC_GRID_CELL;
+    d.pts = g.pts;
+    d.cell_start = g.cell_start;
+    d.cell_pts = g.cell_pts;
+    d.mask = mask;
+    return d;
+}
+
+// contour pixels + grid for a batch of masks
+static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *, const uint8_t *>> &gs,
+                        int H, int W) {
+    if (gs.empty()) return;
+    std::vector<GridJob> jobs;
+    for (auto &p : gs) {
+        GridJob j;
+        j.mask = p.second;
+        j.row_count = p.first->row_count; j.row_start = p.first->row_start;
+        j.pts = p.first->pts; j.cell_count = p.first->cell_count; j.cell_start = p.first->cell_start;
+        j.cell_fill = p.first->cell_fill; j.cell_pts = p.first->cell_pts; j.K = p.first->K;
+        jobs.push_back(j);
+    }
+    const GridJob *dj = stage(c, jobs);
+    const int S = (int)jobs.size();
+    const int ncx = (W + LC_GRID_CELL - 1) / LC_GRID_CELL, ncy = (H + LC_GRID_CELL - 1) / LC_GRID_CELL;
+    const int rows_grid = std::min(H, 1024);
+    launch(c, k_contour_rows, dim3(rows_grid, S), dim3(256), 0, dj, H, W);
+    launch(c, k_contour_scan_rows, dim3(S), dim3(1024), 0, dj, H, ncx * ncy);
+    launch(c, k_contour_emit, dim3(rows_grid, S), dim3(256), 0, dj, H, W, ncx);
+    launch(c, k_contour_scan_cells, dim3(S), dim3(1024), 0, dj, ncx * ncy);
+    launch(c, k_contour_fill, dim3(64, S), dim3(256), 0, dj, ncx);
+}
+
+static void raster(lc_ctx *c, const lc_actor *a, const lc_camera &cam, std::vector<RasterJob> jobs,
+                   bool winner, bool mask) {
+    if (jobs.empty()) return;
+    const RasterJob *dj = stage(c, jobs);
+    const int S = (int)jobs.size();
+    const int HW = cam.width * cam.height;
+    const CamDev cd = cam_dev(cam);
+    const int T = a->dev.T;
+    launch(c, k_raster_clear, dim3(592, S), dim3(256), 0, dj, HW);
+    launch(c, k_raster_depth, dim3((T + 127) / 128, S), dim3(128), 0, dj, cd, a->dev.tris, T);
+    if (winner) launch(c, k_raster_winner, dim3((T + 127) / 128, S), dim3(128), 0, dj, cd, a->dev.tris, T);
+    if (mask) launch(c, k_raster_mask, dim3(592, S), dim3(256), 0, dj, HW);
+}
+
+// ---------------------------------------------------------------------------
+// config -> device constants
+
+static void fill_pose_hyper(PoseHyperDev &h, const lc_pose_hyper &p, const SkelDev &s) {
+    h.l2d = p.lambda_2d; h.l3d = p.lambda_3d; h.lsil = p.lambda_sil; h.ltemp = p.lambda_temporal;
+    h.lanat = p.lambda_anatomic; h.face = p.face_weight;
+    for (int i = 0; i < LC_MAXJ; ++i) h.tw[i] = i < s.J ? p.group_weights[s.group[i] & 7] : 0.0;
+    h.gn = p.gn_iterations;
+    h.max_halvings = p.max_halvings;
+}
+
+static void fill_surf_hyper(SurfHyperDev &h, const lc_nonrigid_hyper &p) {
+    h.w_photo = p.w_photo; h.w_sil = p.w_sil; h.w_smooth = p.w_smooth; h.w_edge = p.w_edge;
+    h.w_vel = p.w_velocity; h.w_acc = p.w_acceleration; h.tau = p.tau_color;
+    h.gn = p.gn_iterations; h.pcg = p.pcg_iterations; h.max_halvings = p.max_halvings;
+    h.n_levels = p.n_levels; h.dilation = p.part_dilation;
+    h.snap_step = p.snap_step; h.snap_band = p.snap_band; h.snap_max_steps = p.snap_max_steps;
+}
+
+// numpy-compatible pairwise sum (n <= 128 blocks of 8)
+static double np_sum(const std::vector<double> &a) {
+    const size_t n = a.size();
+    if (n < 8) {
+        double s = 0.0;
+        for (double v : a) s += v;
+        return s;
+    }
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    size_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+        for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) s += a[i];
+    return s;
+}
+
+// gaussian_kernel (imageproc.py:264-273)
+static std::vector<double> gaussian_taps(int size) {
+    if (size == 1) return {1.0};
+    const double sigma = (size - 1) / 6.0;
+    std::vector<double> k(size);
+    for (int i = 0; i < size; ++i) {
+        const double x = (double)i - (size - 1) / 2.0;
+        const double q = x / sigma;
+        k[i] = std::exp(-0.5 * (q * q));
+    }
+    const double s = np_sum(k);
+    for (double &v : k) v = v / s;
+    return k;
+}
+
+// outer_rim_mask probe offsets (pose_stage.py:255-259): 16 directions x radii 1..8
+static std::vector<double> probe_offsets() {
+    std::vector<double> o(128 * 2);
+    const double step = (2.0 * M_PI - 0.0) / 16.0;
+    for (int a = 0; a < 16; ++a) {
+        const double ang = 0.0 + a * step;
+        const double cs = std::cos(ang), sn = std::sin(ang);
+        for (int r = 0; r < 8; ++r) {
+            o[2 * (a * 8 + r)] = cs * (double)(r + 1);
+            o[2 * (a * 8 + r) + 1] = sn * (double)(r + 1);
+        }
+    }
+    return o;
+}
+
+extern "C" int lc_debug_tables(int32_t size, double *taps_out, double *probe_out) {
+    if (taps_out) {
+        auto k = gaussian_taps(size);
+        std::memcpy(taps_out, k.data(), k.size() * sizeof(double));
+    }
+    if (probe_out) {
+        auto p = probe_offsets();
+        std::memcpy(probe_out, p.data(), p.size() * sizeof(double));
+    }
+    return LC_OK;
+}
+
+static void build_config(lc_ctx *c, const lc_actor *a, const lc_nonrigid_hyper *nh,
+                         const lc_pose_hyper *ph, ConfigDev &cf) {
+    cudaStream_t st = c->stream;
+    const int E = a->dev.E;
+    if (nh) {
+        std::vector<double> csf(E), csr(E), cef(E), cer(E), al(E), be(E);
+        const auto &ed = a->host_edges;
+        const auto &dg = a->host_degrees;
+        const auto &w = a->host_wdir;
+        for (int e = 0; e < E; ++e) {
+            const double da = (double)dg[ed[2 * e]], db = (double)dg[ed[2 * e + 1]];
+            csf[e] = std::sqrt(nh->w_smooth * w[e] / da);
+            csr[e] = std::sqrt(nh->w_smooth * w[e + E] / db);
+            cef[e] = std::sqrt(nh->w_edge * w[e] / da);
+            cer[e] = std::sqrt(nh->w_edge * w[e + E] / db);
+            al[e] = csf[e] * csf[e] + csr[e] * csr[e];
+            be[e] = cef[e] * cef[e] + cer[e] * cer[e];
+        }
+        cf.ec.cs_f = cf.mem.upload(csf.data(), E, st);
+        cf.ec.cs_r = cf.mem.upload(csr.data(), E, st);
+        cf.ec.ce_f = cf.mem.upload(cef.data(), E, st);
+        cf.ec.ce_r = cf.mem.upload(cer.data(), E, st);
+        cf.ec.alpha = cf.mem.upload(al.data(), E, st);
+        cf.ec.beta = cf.mem.upload(be.data(), E, st);
+        fill_surf_hyper(cf.shp, *nh);
+        std::vector<double> taps(4 * 32, 0.0);
+        for (int l = 0; l < nh->n_levels && l < 4; ++l) {
+            const int k = nh->pyramid_kernels[l];
+            require(k >= 1 && k % 2 == 1 && k <= 31, "pyramid kernel sizes must be odd and <= 31");
+            bool given = false;
+            for (int q = 0; q < 32; ++q) given = given || nh->pyramid_taps[l][q] != 0.0;
+            if (given) std::copy(nh->pyramid_taps[l], nh->pyramid_taps[l] + 32, taps.begin() + 32 * l);
+            else {
+                auto t = gaussian_taps(k);
+                std::copy(t.begin(), t.end(), taps.begin() + 32 * l);
+            }
+            cf.half[l] = k / 2;
+        }
+        cf.taps = cf.mem.upload(taps.data(), taps.size(), st);
+    }
+    if (ph) fill_pose_hyper(cf.php, *ph, a->skel);
+    auto pr = probe_offsets();
+    cf.probe = cf.mem.upload(pr.data(), pr.size(), st);
+}
+
+static void pyramid(lc_ctx *c, const ConfigDev &cf, const std::vector<Slot *> &slots, int levels) {
+    if (slots.empty()) return;
+    const int H = slots[0]->H, W = slots[0]->W;
+    const long long n = (long long)H * W * 3;
+    const int grid = (int)std::min<long long>((n + 255) / 256, 2368);
+    for (int l = 0; l < levels; ++l) {
+        std::vector<PyrJob> jobs;
+        for (Slot *s : slots) jobs.push_back(PyrJob{s->image_src, s->blur_tmp, s->pyr + (size_t)l * n});
+        const PyrJob *dj = stage(c, jobs);
+        launch(c, k_blur_axis, dim3(grid, (unsigned)slots.size()), dim3(256), 0, dj, H, W, 3,
+               (const double *)(cf.taps + 32 * l), cf.half[l], 0);
+        launch(c, k_blur_axis, dim3(grid, (unsigned)slots.size()), dim3(256), 0, dj, H, W, 3,
+               (const double *)(cf.taps + 32 * l), cf.half[l], 1);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// small per-stream kernels of the frame schedule
+
+struct PrepJob {
+    const double *rest, *disp;   // disp may be null
+    double *drest;
+    // detection conditioning (pose_stage.py:92-116) + extrapolation (:119-127)
+    const double *j3d_raw;
+    double *j3d;
+    const uint8_t *v3d;
+    int *fallbacks;
+    const double *x_prev, *x_prev2;  // null when absent
+    double *x;                       // out: initial pose
+    int N;
+};
+
+__global__ void k_prep(const PrepJob *jobs, const SkelDev *skg) {
+    const PrepJob J = jobs[blockIdx.y];
+    const SkelDev &sk = *skg;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 3 * J.N; i += gridDim.x * blockDim.x)
+        J.drest[i] = J.disp ? J.rest[i] + J.disp[i] : J.rest[i];
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    // rescale_detections: root outward, bone lengths from local offsets
+    int fb = 0;
+    for (int k = 0; k < 3; ++k) J.j3d[k] = J.j3d_raw[k];
+    for (int i = 1; i < sk.J; ++i) {
+        const int p = sk.parents[i];
+        double d[3] = {J.j3d_raw[3 * i] - J.j3d_raw[3 * p], J.j3d_raw[3 * i + 1] - J.j3d_raw[3 * p + 1],
+                       J.j3d_raw[3 * i + 2] - J.j3d_raw[3 * p + 2]};
+        double n = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+        const bool usable = n > 1e-9 && J.v3d[i] && J.v3d[p];
+        if (!usable) {
+            for (int k = 0; k < 3; ++k) d[k] = sk.rest[i][k] - sk.rest[p][k];
+            n = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+            ++fb;
+        }
+        const double bl = sqrt(sk.off[i][0] * sk.off[i][0] + sk.off[i][1] * sk.off[i][1] + sk.off[i][2] * sk.off[i][2]);
+        for (int k = 0; k < 3; ++k) J.j3d[3 * i + k] = J.j3d[3 * p + k] + bl * d[k] / n;
+    }
+    *J.fallbacks = fb;
+    if (J.x) {
+        for (int k = 0; k < LC_NP; ++k) {
+            double v = 0.0;
+            if (J.x_prev) v = J.x_prev2 ? 2.0 * J.x_prev[k] - J.x_prev2[k] : J.x_prev[k];
+            J.x[k] = v;
+        }
+        if (J.x_prev)
+            for (int k = 0; k < LC_NDOF; ++k) J.x[6 + k] = fmin(fmax(J.x[6 + k], sk.tmin[k]), sk.tmax[k]);
+    }
+}
+
+struct FinishJob {
+    const double *x, *v, *vs, *rot;
+    const FkState *fk;
+    double *x_prev, *x_prev2, *joints_prev, *disp, *v_prev, *v_prev2;
+    int shift_x2, shift_v2;   // copy prev -> prev2 first
+    int warp;                 // 1 rotate, 0 plain delta, -1 zero (pose_only)
+    int N, J;
+};
+
+__global__ void k_finish(const FinishJob *jobs) {
+    const FinishJob F = jobs[blockIdx.y];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < F.N; i += gridDim.x * blockDim.x) {
+        const V3 v = ld3(F.v + 3 * (size_t)i);
+        if (F.shift_v2) st3(F.v_prev2 + 3 * (size_t)i, ld3(F.v_prev + 3 * (size_t)i));
+        st3(F.v_prev + 3 * (size_t)i, v);
+        V3 d = v3(0, 0, 0);
+        if (F.warp >= 0) {
+            d = v - ld3(F.vs + 3 * (size_t)i);
+            if (F.warp == 1) {
+                const double *q = F.rot + 4 * (size_t)i;
+                d = qrot(qconj(Q4{q[0], q[1], q[2], q[3]}), d);
+            }
+        }
+        st3(F.disp + 3 * (size_t)i, d);
+    }
+    if (blockIdx.x == 0) {
+        for (int k = threadIdx.x; k < LC_NP; k += blockDim.x) {
+            if (F.shift_x2) F.x_prev2[k] = F.x_prev[k];
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < LC_NP; k += blockDim.x) F.x_prev[k] = F.x[k];
+        for (int k = threadIdx.x; k < 3 * F.J; k += blockDim.x) F.joints_prev[k] = F.fk->pos[k / 3][k % 3];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// frame schedule (solve_frame, pipeline.py:263-302) for a batch of slots
+
+struct FrameBatch {
+    lc_ctx *c;
+    const lc_actor *a;
+    lc_camera cam;
+    const lc_config *cfg;
+    ConfigDev *cf;
+    std::vector<Slot *> slots;
+};
+
+// FK of each slot's pose (optional) then DQ skinning of the actor rest shape
+// (use_drest = false) or the slot's displaced rest shape (use_drest = true)
+static void fk_skin(FrameBatch &fb, const std::vector<Slot *> &ss, bool from_x, bool use_drest,
+                    double *Slot::*out, double *Slot::*rot_out) {
+    lc_ctx *c = fb.c;
+    std::vector<FkJob> fj;
+    std::vector<SkinJob> sj;
+    for (Slot *s : ss) {
+        fj.push_back(FkJob{s->x, s->fk, 1});
+        SkinJob k{};
+        k.fk = s->fk;
+        k.rest = use_drest ? s->drest : fb.a->dev.rest;
+        k.pos = s->*out;
+        k.rot = rot_out ? s->*rot_out : nullptr;
+        k.M = s->N;
+        k.active = 1;
+        sj.push_back(k);
+    }
+    if (from_x) launch(c, k_fk, dim3((unsigned)ss.size()), dim3(32), 0, stage(c, fj), (const SkelDev *)fb.a->skel_dev);
+    launch(c, k_skin, dim3((fb.a->dev.N + 127) / 128, (unsigned)ss.size()), dim3(128), 0, stage(c, sj), fb.a->dev);
+}
+
+static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, double *Slot::*verts,
+                            bool stage1) {
+    lc_ctx *c = fb.c;
+    const lc_actor *a = fb.a;
+    const int H = fb.cam.height, W = fb.cam.width;
+    std::vector<RasterJob> rj;
+    for (Slot *s : ss) rj.push_back(RasterJob{s->*verts, s->zbuf, s->tri_id, s->own_mask});
+    raster(c, a, fb.cam, rj, !stage1 && fb.cfg->enable_part_mask, true);
+    std::vector<std::pair<const GridBufs *, const uint8_t *>> gs;
+    for (Slot *s : ss) gs.push_back({&s->own, s->own_mask});
+    build_grids(c, gs, H, W);
+    std::vector<ContourJob> cj;
+    for (Slot *s : ss) {
+        ContourJob j{};
+        j.verts = s->*verts; j.zbuf = s->zbuf; j.tri_front = s->tri_front; j.tri_n = s->tri_n;
+        j.vflag = s->vflag; j.idx = s->cidx; j.n2d = s->n2d; j.B = s->B;
+        j.vis = stage1 ? nullptr : s->vis;
+        j.P = stage1 ? nullptr : s->P;
+        j.active = 1;
+        cj.push_back(j);
+    }
+    const ContourJob *dcj = stage(c, cj);
+    const unsigned S = (unsigned)ss.size();
+    launch(c, k_tri_front, dim3(64, S), dim3(256), 0, dcj, a->dev);
+    launch(c, k_sil_edges, dim3(64, S), dim3(256), 0, dcj, a->dev);
+    launch(c, k_contour_compact, dim3(S), dim3(1024), 0, dcj, a->dev, cam_dev(fb.cam));
+    std::vector<RimJob> rjs;
+    for (Slot *s : ss) {
+        RimJob r{};
+        r.verts = s->*verts; r.idx = s->cidx; r.B = s->B;
+        r.own = grid_dev(s->own, s->own_mask, H, W);
+        r.ownK = s->own.K;
+        r.keep = s->enabled;
+        r.stage1 = stage1;
+        r.active = 1;
+        r.tri_id = s->tri_id;
+        r.part_gate = !stage1 && fb.cfg->enable_part_mask;
+        r.dilation = fb.cfg->nonrigid.part_dilation;
+        rjs.push_back(r);
+    }
+    launch(c, k_rim, dim3(32, S), dim3(256), 0, stage(c, rjs), a->dev, cam_dev(fb.cam),
+           (const double *)fb.cf->probe);
+}
+
+static void pose_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, const std::vector<PoseJob> &jobs) {
+    const size_t smem = pose_smem_bytes(a->skel.J);
+    launch(c, k_pose_solve, dim3((unsigned)jobs.size()), dim3(pose_block_threads()), smem, stage(c, jobs),
+           (const SkelDev *)a->skel_dev, a->dev, cam_dev(cam));
+}
+
+static void surface_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, const ConfigDev &cf,
+                           const std::vector<SurfJob> &jobs) {
+    launch(c, k_surface_solve, dim3((unsigned)jobs.size()), dim3(surface_block_threads()), 0, stage(c, jobs),
+           a->dev, cam_dev(cam), cf.ec, cf.shp, cam.height, cam.width);
+}
+
+static void run_frame(FrameBatch &fb) {
+    lc_ctx *c = fb.c;
+    const lc_actor *a = fb.a;
+    const lc_config &cfg = *fb.cfg;
+    const int H = fb.cam.height, W = fb.cam.width;
+    auto &ss = fb.slots;
+    const unsigned S = (unsigned)ss.size();
+    // ---- preprocess (pipeline.py:156-162): pyramid + observed contour grid
+    if (cfg.mode == 0) pyramid(c, *fb.cf, ss, cfg.nonrigid.n_levels);
+    {
+        std::vector<std::pair<const GridBufs *, const uint8_t *>> gs;
+        for (Slot *s : ss) gs.push_back({&s->obs, s->mask_src});
+        build_grids(c, gs, H, W);
+    }
+    // ---- condition (pipeline.py:165-170) + displaced rest + initial pose
+    {
+        std::vector<PrepJob> pj;
+        for (Slot *s : ss) {
+            PrepJob p{};
+            p.rest = a->dev.rest; p.disp = s->has_disp ? s->disp : nullptr; p.drest = s->drest;
+            p.j3d_raw = s->j3d_raw; p.j3d = s->j3d; p.v3d = s->v3d; p.fallbacks = s->fallbacks;
+            p.x_prev = s->has_prev ? s->x_prev : nullptr;
+            p.x_prev2 = s->has_prev2 ? s->x_prev2 : nullptr;
+            p.x = s->x;
+            p.N = a->dev.N;
+            pj.push_back(p);
+        }
+        launch(c, k_prep, dim3(16, S), dim3(256), 0, stage(c, pj), (const SkelDev *)a->skel_dev);
+        for (Slot *s : ss) {
+            cudaMemsetAsync(s->pose_rep, 0, sizeof(lc_pose_report), c->stream);
+            cudaMemsetAsync(s->nr_rep, 0, sizeof(lc_nonrigid_report), c->stream);
+        }
+    }
+    // ---- Stage I (pipeline.py:173-224)
+    int max_rounds = 0;
+    std::vector<int> rounds(S);
+    for (unsigned i = 0; i < S; ++i) {
+        // frame 0: [{l2d=0, lsil=0}, {lsil=0}] + [{}] * max(1, rounds - 2)  (pipeline.py:191-193)
+        rounds[i] = ss[i]->has_prev ? 1 : 2 + std::max(1, cfg.frame0_rounds - 2);
+        max_rounds = std::max(max_rounds, rounds[i]);
+    }
+    std::vector<int> log_off(S, 0);
+    for (int r = 0; r < max_rounds; ++r) {
+        std::vector<Slot *> act;
+        for (unsigned i = 0; i < S; ++i)
+            if (r < rounds[i]) act.push_back(ss[i]);
+        fk_skin(fb, act, true, true, &Slot::model, nullptr);
+        contour_and_rim(fb, act, &Slot::model, true);
+        std::vector<PoseJob> pj;
+        int k = 0;
+        for (unsigned i = 0; i < S; ++i) {
+            if (r >= rounds[i]) continue;
+            Slot *s = ss[i];
+            PoseJob p{};
+            p.active = 1;
+            p.x0 = s->x;
+            p.x_out = s->x;
+            p.obs = grid_dev(s->obs, s->mask_src, H, W);
+            p.obs_K = s->obs.K;
+            p.has_field = 1;
+            p.B = s->B; p.cidx = s->cidx; p.n2d = s->n2d; p.crest = nullptr; p.drest = s->drest;
+            p.enabled = s->enabled;
+            p.j2d = s->j2d; p.j3d = s->j3d; p.v2d = s->v2d; p.v3d = s->v3d;
+            p.prev_pos = s->has_prev ? s->joints_prev : nullptr;
+            lc_pose_hyper h = cfg.pose;
+            if (cfg.mode == 2) h.lambda_sil = 0.0;
+            if (!s->has_prev) {
+                h.gn_iterations *= cfg.frame0_iteration_scale;
+                if (r == 0) { h.lambda_2d = 0.0; h.lambda_sil = 0.0; }
+                if (r == 1) h.lambda_sil = 0.0;
+            }
+            fill_pose_hyper(p.hp, h, a->skel);
+            p.directional = cfg.directional;
+            p.report = s->pose_rep;
+            p.log_offset = log_off[i];
+            log_off[i] += h.gn_iterations;
+            pj.push_back(p);
+            ++k;
+        }
+        pose_launch(c, a, fb.cam, pj);
+    }
+    // ---- Stage II (pipeline.py:227-260) or the pose-only surface
+    if (cfg.mode == 0) {
+        fk_skin(fb, ss, true, true, &Slot::vinit, nullptr);
+        fk_skin(fb, ss, false, false, &Slot::vs, &Slot::rot);
+    } else {
+        fk_skin(fb, ss, true, false, &Slot::vs, &Slot::rot);
+    }
+    if (cfg.mode == 0) {
+        contour_and_rim(fb, ss, &Slot::vinit, false);
+        std::vector<SurfJob> sj;
+        for (Slot *s : ss) {
+            SurfJob j{};
+            j.active = 1;
+            j.do_solve = 1;
+            j.do_snap = cfg.enable_snapping;
+            j.v0 = s->vinit; j.v = s->v; j.vs = s->vs; j.pyr = s->pyr;
+            j.obs = grid_dev(s->obs, s->mask_src, H, W);
+            j.obs_K = s->obs.K;
+            j.has_field = 1;
+            j.vis = s->vis; j.P = s->P; j.bidx = s->cidx; j.B = s->B; j.n2d = s->n2d; j.enabled = s->enabled;
+            j.prev = s->has_vprev ? s->v_prev : nullptr;
+            j.prev2 = s->has_vprev2 ? s->v_prev2 : nullptr;
+            j.directional = cfg.directional; j.enable_photo = 1; j.enable_sil = 1;
+            j.diag = s->diag; j.minv = s->minv; j.rhs = s->rhs; j.x = s->sx; j.r = s->sr; j.z = s->sz;
+            j.p = s->sp; j.ap = s->sap; j.best = s->sbest; j.edir = s->edir; j.eg = s->eg;
+            j.off0 = s->off0; j.off1 = s->off1; j.hold = s->hold;
+            j.report = s->nr_rep;
+            sj.push_back(j);
+        }
+        surface_launch(c, a, fb.cam, *fb.cf, sj);
+    }
+    // ---- state update (pipeline.py:281-299)
+    std::vector<FinishJob> fj;
+    for (Slot *s : ss) {
+        FinishJob f{};
+        f.x = s->x; f.v = cfg.mode == 0 ? s->v : s->vs; f.vs = s->vs; f.rot = s->rot; f.fk = s->fk;
+        f.x_prev = s->x_prev; f.x_prev2 = s->x_prev2; f.joints_prev = s->joints_prev; f.disp = s->disp;
+        f.v_prev = s->v_prev; f.v_prev2 = s->v_prev2;
+        f.shift_x2 = s->has_prev; f.shift_v2 = s->has_vprev;
+        f.warp = cfg.mode == 0 ? (cfg.enable_warping ? 1 : 0) : -1;
+        f.N = a->dev.N; f.J = a->skel.J;
+        fj.push_back(f);
+    }
+    launch(c, k_finish, dim3(16, S), dim3(256), 0, stage(c, fj));
+    for (Slot *s : ss) {
+        s->has_prev2 = s->has_prev;
+        s->has_prev = true;
+        s->has_vprev2 = s->has_vprev;
+        s->has_vprev = true;
+        s->has_disp = true;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// tracker
+
+extern "C" int lc_tracker_create(lc_ctx *c, const lc_actor *a, const lc_camera *cam, const lc_config *cfg,
+                                 int32_t S, lc_tracker **out) {
+    API_BEGIN
+    require(c && a && cam && cfg && out, "null argument");
+    require(S >= 1, "n_streams must be >= 1");
+    require(cam->width >= 2 && cam->height >= 2 && cam->fx > 0 && cam->fy > 0, "invalid camera");
+    require(cfg->mode >= 0 && cfg->mode <= 2, "invalid mode");
+    require(cfg->nonrigid.n_levels >= 1 && cfg->nonrigid.n_levels <= 4, "1..4 pyramid levels");
+    CK(cudaSetDevice(c->device));
+    lc_tracker *t = new lc_tracker();
+    t->ctx = c;
+    t->actor = a;
+    t->cam = *cam;
+    t->cfg = *cfg;
+    t->S = S;
+    build_config(c, a, &cfg->nonrigid, &cfg->pose, t->conf);
+    for (int i = 0; i < S; ++i) {
+        Slot *s = new Slot();
+        s->allocate(a->dev.N, a->dev.T, a->dev.E, cam->height, cam->width, cfg->nonrigid.n_levels, a->skel.J);
+        t->slots.push_back(s);
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    *out = t;
+    return LC_OK;
+    API_END
+}
+
+extern "C" int lc_tracker_destroy(lc_tracker *t) {
+    if (!t) return LC_OK;
+    cudaStreamSynchronize(t->ctx->stream);
+    for (Slot *s : t->slots) delete s;
+    delete t;
+    return LC_OK;
+}
+
+static void upload_dets(lc_ctx *c, Slot *s, const lc_detections *d, int J) {
+    cudaMemcpyAsync(s->j2d, d->joints2d, sizeof(double) * 2 * (J + 4), cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(s->j3d_raw, d->joints3d, sizeof(double) * 3 * J, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(s->v2d, d->valid2d, J + 4, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(s->v3d, d->valid3d, J, cudaMemcpyHostToDevice, c->stream);
+}
+
+extern "C" int lc_tracker_set_frame(lc_tracker *t, int32_t stream, const double *image, const uint8_t *mask,
+                                    const lc_detections *det, int32_t on_device) {
+    API_BEGIN
+    require(t && det, "null argument");
+    require(stream >= 0 && stream < t->S, "stream index out of range");
+    Slot *s = t->slots[stream];
+    lc_ctx *c = t->ctx;
+    const size_t HW = (size_t)s->H * s->W;
+    if (on_device) {
+        s->image_src = image;
+        s->mask_src = mask;
+    } else {
+        CK(cudaMemcpyAsync(s->image, image, HW * 3 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(s->mask, mask, HW, cudaMemcpyHostToDevice, c->stream));
+        s->image_src = s->image;
+        s->mask_src = s->mask;
+    }
+    upload_dets(c, s, det, t->actor->skel.J);
+    return LC_OK;
+    API_END
+}
+
+extern "C" int lc_tracker_step(lc_tracker *t) {
+    API_BEGIN
+    require(t != nullptr, "null tracker");
+    CK(cudaSetDevice(t->ctx->device));
+    FrameBatch fb{t->ctx, t->actor, t->cam, &t->cfg, &t->conf, t->slots};
+    run_frame(fb);
+    t->frame_counter++;
+    return last_launch_status();
+    API_END
+}
+
+extern "C" int lc_tracker_get_result(lc_tracker *t, int32_t stream, double *pose_out, double *verts_out,
+                                     double *skinned_out, lc_frame_report *rep) {
+    API_BEGIN
+    require(t != nullptr, "null tracker");
+    require(stream >= 0 && stream < t->S, "stream index out of range");
+    Slot *s = t->slots[stream];
+    lc_ctx *c = t->ctx;
+    const size_t N = s->N;
+    if (pose_out) CK(cudaMemcpyAsync(pose_out, s->x_prev, sizeof(double) * LC_NP, cudaMemcpyDeviceToHost, c->stream));
+    if (verts_out) CK(cudaMemcpyAsync(verts_out, s->v_prev, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost, c->stream));
+    if (skinned_out) CK(cudaMemcpyAsync(skinned_out, s->vs, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost, c->stream));
+    if (rep) {
+        CK(cudaMemcpyAsync(&rep->pose, s->pose_rep, sizeof(lc_pose_report), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(&rep->nonrigid, s->nr_rep, sizeof(lc_nonrigid_report), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(&rep->rescale_fallbacks, s->fallbacks, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return last_launch_status();
+    API_END
+}
+
+extern "C" int lc_tracker_set_state(lc_tracker *t, int32_t stream, const double *x_prev, const double *x_prev2,
+                                    const double *joints_prev, const double *disp_rest, const double *v_prev,
+                                    const double *v_prev2) {
+    API_BEGIN
+    require(t != nullptr, "null tracker");
+    require(stream >= 0 && stream < t->S, "stream index out of range");
+    Slot *s = t->slots[stream];
+    lc_ctx *c = t->ctx;
+    const size_t N = s->N;
+    const int J = t->actor->skel.J;
+    auto put = [&](double *dst, const double *src, size_t n) {
+        if (src) cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, c->stream);
+    };
+    require(!(x_prev && !joints_prev), "joints_prev is required with pose_prev");
+    put(s->x_prev, x_prev, LC_NP);
+    put(s->x_prev2, x_prev2, LC_NP);
+    put(s->joints_prev, joints_prev, 3 * J);
+    put(s->disp, disp_rest, 3 * N);
+    put(s->v_prev, v_prev, 3 * N);
+    put(s->v_prev2, v_prev2, 3 * N);
+    s->has_prev = x_prev != nullptr;
+    s->has_prev2 = x_prev2 != nullptr;
+    s->has_disp = disp_rest != nullptr;
+    s->has_vprev = v_prev != nullptr;
+    s->has_vprev2 = v_prev2 != nullptr;
+    CK(cudaStreamSynchronize(c->stream));
+    return LC_OK;
+    API_END
+}
+
+extern "C" int lc_tracker_get_state(lc_tracker *t, int32_t stream, int32_t *flags, double *x_prev,
+                                    double *x_prev2, double *joints_prev, double *disp_rest, double *v_prev,
+                                    double *v_prev2) {
+    API_BEGIN
+    require(t != nullptr, "null tracker");
+    require(stream >= 0 && stream < t->S, "stream index out of range");
+    Slot *s = t->slots[stream];
+    lc_ctx *c = t->ctx;
+    const size_t N = s->N;
+    const int J = t->actor->skel.J;
+    auto get = [&](double *dst, const double *src, size_t n) {
+        if (dst) cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+    };
+    get(x_prev, s->x_prev, LC_NP);
+    get(x_prev2, s->x_prev2, LC_NP);
+    get(joints_prev, s->joints_prev, 3 * J);
+    get(disp_rest, s->disp, 3 * N);
+    get(v_prev, s->v_prev, 3 * N);
+    get(v_prev2, s->v_prev2, 3 * N);
+    if (flags) {
+        flags[0] = s->has_prev; flags[1] = s->has_prev2; flags[2] = s->has_disp;
+        flags[3] = s->has_vprev; flags[4] = s->has_vprev2;
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return LC_OK;
+    API_END
+}
+
+extern "C" int lc_tracker_device_vertices(lc_tracker *t, int32_t stream, uint64_t *dptr) {
+    if (!t || !dptr || stream < 0 || stream >= t->S) return fail(LC_EINVAL, "bad argument");
+    *dptr = reinterpret_cast<uint64_t>(t->slots[stream]->v_prev);
+    return LC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// single-call seams (a scratch slot per context, sized to actor + camera)
+
+static Slot *call_slot(lc_ctx *c, const lc_actor *a, int H, int W, int levels) {
+    if (!c->call_slot || c->call_actor != a || c->call_w != W || c->call_h != H || c->call_slot->levels < levels) {
+        cudaStreamSynchronize(c->stream);
+        delete c->call_slot;
+        c->call_slot = new Slot();
+        c->call_slot->allocate(a->dev.N, a->dev.T, a->dev.E, H, W, std::max(levels, 3), a->skel.J);
+        c->call_actor = a;
+        c->call_w = W;
+        c->call_h = H;
+    }
+    return c->call_slot;
+}
+
+extern "C" int lc_pose_solve(lc_ctx *c, const lc_actor *a, const lc_camera *cam, const lc_pose_problem *pb,
+                             const double *x0, double *x_out, lc_pose_report *report) {
+    API_BEGIN
+    require(c && a && cam && pb && x0 && x_out, "null argument");
+    require(pb->n_contour >= 0 && pb->n_contour <= a->dev.N, "contour size out of range");
+    CK(cudaSetDevice(c->device));
+    const int H = cam->height, W = cam->width, J = a->skel.J;
+    Slot *s = call_slot(c, a, H, W, 1);
+    cudaStream_t st = c->stream;
+    const bool has_field = pb->mask != nullptr;
+    if (has_field) {
+        CK(cudaMemcpyAsync(s->mask, pb->mask, (size_t)H * W, cudaMemcpyHostToDevice, st));
+        build_grids(c, {{&s->obs, s->mask}}, H, W);
+    }
+    CK(cudaMemcpyAsync(s->j2d, pb->joints2d, sizeof(double) * 2 * (J + 4), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->j3d, pb->joints3d, sizeof(double) * 3 * J, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->v2d, pb->valid2d, J + 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->v3d, pb->valid3d, J, cudaMemcpyHostToDevice, st));
+    const int B = pb->n_contour;
+    std::vector<int> idx(B);
+    for (int i = 0; i < B; ++i) {
+        idx[i] = (int)pb->contour_indices[i];
+        require(idx[i] >= 0 && idx[i] < a->dev.N, "contour index out of range");
+    }
+    if (B) {
+        CK(cudaMemcpyAsync(s->cidx, idx.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(s->n2d, pb->contour_normals2d, sizeof(double) * 2 * B, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(s->crest, pb->contour_rest, sizeof(double) * 3 * B, cudaMemcpyHostToDevice, st));
+        if (pb->contour_enabled)
+            CK(cudaMemcpyAsync(s->enabled, pb->contour_enabled, B, cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaMemcpyAsync(s->B, &B, sizeof(int), cudaMemcpyHostToDevice, st));
+    if (pb->prev_positions)
+        CK(cudaMemcpyAsync(s->joints_prev, pb->prev_positions, sizeof(double) * 3 * J, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->x0, x0, sizeof(double) * LC_NP, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(s->pose_rep, 0, sizeof(lc_pose_report), st));
+    PoseJob p{};
+    p.active = 1;
+    p.x0 = s->x0;
+    p.x_out = s->x;
+    p.obs = grid_dev(s->obs, s->mask, H, W);
+    p.obs_K = s->obs.K;
+    p.has_field = has_field;
+    p.B = s->B; p.cidx = s->cidx; p.n2d = s->n2d; p.crest = s->crest; p.drest = nullptr;
+    p.enabled = pb->contour_enabled ? s->enabled : nullptr;
+    p.j2d = s->j2d; p.j3d = s->j3d; p.v2d = s->v2d; p.v3d = s->v3d;
+    p.prev_pos = pb->prev_positions ? s->joints_prev : nullptr;
+    fill_pose_hyper(p.hp, pb->hyper, a->skel);
+    p.directional = pb->directional;
+    p.report = s->pose_rep;
+    p.log_offset = 0;
+    require(pb->hyper.gn_iterations <= LC_MAX_LOG, "too many GN iterations for the report");
+    pose_launch(c, a, *cam, {p});
+    CK(cudaMemcpyAsync(x_out, s->x, sizeof(double) * LC_NP, cudaMemcpyDeviceToHost, st));
+    if (report) CK(cudaMemcpyAsync(report, s->pose_rep, sizeof(lc_pose_report), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return last_launch_status();
+    API_END
+}
+
+extern "C" int lc_nonrigid_solve(lc_ctx *c, const lc_actor *a, const lc_camera *cam, const lc_nonrigid_problem *pb,
+                                 const double *v0, int32_t do_solve, int32_t do_snap, double *v_out,
+                                 lc_nonrigid_report *report) {
+    API_BEGIN
+    require(c && a && cam && pb && v0 && v_out, "null argument");
+    require(pb->n_levels >= 1 && pb->n_levels <= 4, "1..4 pyramid levels");
+    require(pb->hyper.gn_iterations <= LC_MAX_LOG, "too many GN iterations for the report");
+    CK(cudaSetDevice(c->device));
+    const int H = cam->height, W = cam->width, N = a->dev.N;
+    Slot *s = call_slot(c, a, H, W, pb->n_levels);
+    cudaStream_t st = c->stream;
+    const bool has_field = pb->mask != nullptr;
+    if (has_field) {
+        CK(cudaMemcpyAsync(s->mask, pb->mask, (size_t)H * W, cudaMemcpyHostToDevice, st));
+        build_grids(c, {{&s->obs, s->mask}}, H, W);
+    }
+    const size_t HW3 = (size_t)H * W * 3;
+    if (pb->pyramid)
+        CK(cudaMemcpyAsync(s->pyr, pb->pyramid, sizeof(double) * HW3 * pb->n_levels, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->vs, pb->skinned, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->vinit, v0, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    auto put_idx = [&](int *dst, const int64_t *src, int n) {
+        std::vector<int> t(n);
+        for (int i = 0; i < n; ++i) {
+            t[i] = (int)src[i];
+            require(t[i] >= 0 && t[i] < N, "vertex index out of range");
+        }
+        if (n) cudaMemcpyAsync(dst, t.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st);
+        cudaStreamSynchronize(st);
+    };
+    put_idx(s->vis, pb->visible, pb->n_visible);
+    put_idx(s->cidx, pb->boundary, pb->n_boundary);
+    CK(cudaMemcpyAsync(s->P, &pb->n_visible, sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->B, &pb->n_boundary, sizeof(int), cudaMemcpyHostToDevice, st));
+    if (pb->n_boundary) {
+        CK(cudaMemcpyAsync(s->n2d, pb->normals2d, sizeof(double) * 2 * pb->n_boundary, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(s->enabled, pb->enabled, pb->n_boundary, cudaMemcpyHostToDevice, st));
+    }
+    if (pb->prev) CK(cudaMemcpyAsync(s->v_prev, pb->prev, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    if (pb->prev2) CK(cudaMemcpyAsync(s->v_prev2, pb->prev2, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(s->nr_rep, 0, sizeof(lc_nonrigid_report), st));
+    ConfigDev cf;
+    lc_nonrigid_hyper nh = pb->hyper;
+    nh.n_levels = pb->n_levels;
+    build_config(c, a, &nh, nullptr, cf);
+    SurfJob j{};
+    j.active = 1;
+    j.do_solve = do_solve;
+    j.do_snap = do_snap;
+    j.v0 = s->vinit; j.v = s->v; j.vs = s->vs; j.pyr = s->pyr;
+    j.obs = grid_dev(s->obs, s->mask, H, W);
+    j.obs_K = s->obs.K;
+    j.has_field = has_field;
+    j.vis = s->vis; j.P = s->P; j.bidx = s->cidx; j.B = s->B; j.n2d = s->n2d; j.enabled = s->enabled;
+    j.prev = pb->prev ? s->v_prev : nullptr;
+    j.prev2 = pb->prev2 ? s->v_prev2 : nullptr;
+    j.directional = pb->directional; j.enable_photo = pb->enable_photo; j.enable_sil = pb->enable_sil;
+    j.diag = s->diag; j.minv = s->minv; j.rhs = s->rhs; j.x = s->sx; j.r = s->sr; j.z = s->sz;
+    j.p = s->sp; j.ap = s->sap; j.best = s->sbest; j.edir = s->edir; j.eg = s->eg;
+    j.off0 = s->off0; j.off1 = s->off1; j.hold = s->hold;
+    j.report = s->nr_rep;
+    surface_launch(c, a, *cam, cf, {j});
+    CK(cudaMemcpyAsync(v_out, s->v, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost, st));
+    if (report) CK(cudaMemcpyAsync(report, s->nr_rep, sizeof(lc_nonrigid_report), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return last_launch_status();
+    API_END
+}
+
+extern "C" int lc_forward_kinematics(lc_ctx *c, const lc_actor *a, const double *x36, double *rot_out,
+                                     double *pos_out, double *markers_out, double *dqs_out, int32_t *gimbal) {
+    API_BEGIN
+    require(c && a && x36, "null argument");
+    CK(cudaSetDevice(c->device));
+    DevArena m;
+    double *dx = m.upload(x36, LC_NP, c->stream);
+    FkState *f = m.alloc<FkState>(1);
+    launch(c, k_fk, dim3(1), dim3(32), 0, stage(c, std::vector<FkJob>{FkJob{dx, f, 1}}),
+           (const SkelDev *)a->skel_dev);
+    FkState h;
+    CK(cudaMemcpyAsync(&h, f, sizeof(FkState), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const int J = a->skel.J;
+    for (int j = 0; j < J; ++j) {
+        if (rot_out) std::memcpy(rot_out + 9 * j, h.rot[j], 9 * sizeof(double));
+        if (pos_out) std::memcpy(pos_out + 3 * j, h.pos[j], 3 * sizeof(double));
+        if (dqs_out) std::memcpy(dqs_out + 8 * j, h.dq[j], 8 * sizeof(double));
+    }
+    if (markers_out) std::memcpy(markers_out, h.markers, 12 * sizeof(double));
+    if (gimbal) *gimbal = h.gimbal;
+    return last_launch_status();
+    API_END
+}
+
+__global__ void k_skin_jac(const FkState *fk, const SkelDev *skg, ActorDev A, int M, const double *rest,
+                           const int *subset, double *jac);
+
+extern "C" int lc_skin_points(lc_ctx *c, const lc_actor *a, const double *x36, int32_t M, const double *rest,
+                              const int64_t *subset, double *pos_out, double *rot_out, double *jac_out) {
+    API_BEGIN
+    require(c && a && x36 && rest && pos_out, "null argument");
+    require(M >= 0, "negative point count");
+    if (!subset) require(M == a->dev.N, "without a subset, rest points must cover every vertex");
+    CK(cudaSetDevice(c->device));
+    if (M == 0) return LC_OK;
+    DevArena m;
+    cudaStream_t st = c->stream;
+    double *dx = m.upload(x36, LC_NP, st);
+    FkState *f = m.alloc<FkState>(1);
+    double *dr = m.upload(rest, 3 * (size_t)M, st);
+    int *ds = nullptr;
+    if (subset) {
+        std::vector<int> t(M);
+        for (int i = 0; i < M; ++i) {
+            t[i] = (int)subset[i];
+            require(t[i] >= 0 && t[i] < a->dev.N, "subset index out of range");
+        }
+        ds = m.upload(t.data(), M, st);
+        CK(cudaStreamSynchronize(st));
+    }
+    double *dp = m.alloc<double>(3 * (size_t)M);
+    double *dq = rot_out ? m.alloc<double>(4 * (size_t)M) : nullptr;
+    launch(c, k_fk, dim3(1), dim3(32), 0, stage(c, std::vector<FkJob>{FkJob{dx, f, 1}}),
+           (const SkelDev *)a->skel_dev);
+    SkinJob j{};
+    j.fk = f; j.rest = dr; j.subset = ds; j.pos = dp; j.rot = dq; j.M = M; j.active = 1;
+    launch(c, k_skin, dim3((M + 127) / 128), dim3(128), 0, stage(c, std::vector<SkinJob>{j}), a->dev);
+    double *dj = nullptr;
+    if (jac_out) {
+        dj = m.alloc<double>((size_t)M * 3 * LC_NP);
+        launch(c, k_skin_jac, dim3((M + 127) / 128), dim3(128), 0, (const FkState *)f,
+               (const SkelDev *)a->skel_dev, a->dev, M, (const double *)dr, (const int *)ds, dj);
+    }
+    CK(cudaMemcpyAsync(pos_out, dp, sizeof(double) * 3 * M, cudaMemcpyDeviceToHost, st));
+    if (rot_out) CK(cudaMemcpyAsync(rot_out, dq, sizeof(double) * 4 * M, cudaMemcpyDeviceToHost, st));
+    if (jac_out) CK(cudaMemcpyAsync(jac_out, dj, sizeof(double) * 3 * LC_NP * M, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return last_launch_status();
+    API_END
+}
+
+extern "C" int lc_contour_vertices(lc_ctx *c, const lc_actor *a, const lc_camera *cam, const double *verts,
+                                   int32_t *n_out, int64_t *idx_out, double *n2d_out) {
+    API_BEGIN
+    require(c && a && cam && verts && n_out, "null argument");
+    CK(cudaSetDevice(c->device));
+    const int H = cam->height, W = cam->width, N = a->dev.N;
+    Slot *s = call_slot(c, a, H, W, 1);
+    cudaStream_t st = c->stream;
+    CK(cudaMemcpyAsync(s->model, verts, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    raster(c, a, *cam, {RasterJob{s->model, s->zbuf, s->tri_id, nullptr}}, false, false);
+    ContourJob j{};
+    j.verts = s->model; j.zbuf = s->zbuf; j.tri_front = s->tri_front; j.tri_n = s->tri_n; j.vflag = s->vflag;
+    j.idx = s->cidx; j.n2d = s->n2d; j.B = s->B; j.vis = nullptr; j.P = nullptr; j.active = 1;
+    const ContourJob *dj = stage(c, std::vector<ContourJob>{j});
+    launch(c, k_tri_front, dim3(64), dim3(256), 0, dj, a->dev);
+    launch(c, k_sil_edges, dim3(64), dim3(256), 0, dj, a->dev);
+    launch(c, k_contour_compact, dim3(1), dim3(1024), 0, dj, a->dev, cam_dev(*cam));
+    int B = 0;
+    CK(cudaMemcpyAsync(&B, s->B, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int> idx(B);
+    if (B) {
+        CK(cudaMemcpyAsync(idx.data(), s->cidx, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+        if (n2d_out) CK(cudaMemcpyAsync(n2d_out, s->n2d, sizeof(double) * 2 * B, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    *n_out = B;
+    if (idx_out)
+        for (int i = 0; i < B; ++i) idx_out[i] = idx[i];
+    return last_launch_status();
+    API_END
+}
+
+// ---------------------------------------------------------------------------
+// stateless seams: render, pyramid, distance field, PCG, dense solve
+
+extern "C" int lc_render(lc_ctx *c, const lc_camera *cam, int32_t n, const double *verts, int32_t t,
+                         const int64_t *tris, int32_t mode, const double *attrs, int32_t n_attr,
+                         const int64_t *ids, double bg_attr, int64_t bg_id, double *zbuf_out,
+                         double *attr_out, int64_t *id_out) {
+    API_BEGIN
+    require(c && cam && verts && tris && zbuf_out, "null argument");
+    require(mode >= 0 && mode <= 2, "mode must be 0, 1 or 2");
+    require(mode != 1 || (attrs && attr_out && n_attr > 0), "attribute mode needs attrs");
+    require(mode != 2 || (ids && id_out), "id mode needs ids");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DevArena m;
+    const size_t HW = (size_t)cam->width * cam->height;
+    std::vector<int> tt(3 * (size_t)t), ii;
+    for (size_t k = 0; k < tt.size(); ++k) {
+        tt[k] = (int)tris[k];
+        require(tt[k] >= 0 && tt[k] < n, "triangle index out of range");
+    }
+    double *dv = m.upload(verts, 3 * (size_t)n, st);
+    int *dt = m.upload(tt.data(), tt.size(), st);
+    unsigned long long *zb = m.alloc<unsigned long long>(HW);
+    int *tid = m.alloc<int>(HW);
+    double *za = m.alloc<double>(HW);
+    double *da = nullptr, *ao = nullptr;
+    int *di = nullptr;
+    long long *io = nullptr;
+    if (mode == 1) {
+        da = m.upload(attrs, (size_t)n * n_attr, st);
+        ao = m.alloc<double>(HW * n_attr);
+    }
+    if (mode == 2) {
+        ii.resize(n);
+        for (int k = 0; k < n; ++k) ii[k] = (int)ids[k];
+        di = m.upload(ii.data(), ii.size(), st);
+        io = m.alloc<long long>(HW);
+    }
+    const RasterJob *dj = stage(c, std::vector<RasterJob>{RasterJob{dv, zb, tid, nullptr}});
+    const CamDev cd = cam_dev(*cam);
+    launch(c, k_raster_clear, dim3(592), dim3(256), 0, dj, (int)HW);
+    launch(c, k_raster_depth, dim3((t + 127) / 128), dim3(128), 0, dj, cd, (const int *)dt, t);
+    if (mode) launch(c, k_raster_winner, dim3((t + 127) / 128), dim3(128), 0, dj, cd, (const int *)dt, t);
+    launch(c, k_raster_resolve, dim3(592), dim3(256), 0, dj, cd, (const int *)dt, mode, (const double *)da,
+           n_attr, (const int *)di, bg_attr, (long long)bg_id, za, ao, io);
+    CK(cudaMemcpyAsync(zbuf_out, za, HW * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (mode == 1) CK(cudaMemcpyAsync(attr_out, ao, HW * n_attr * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (mode == 2) CK(cudaMemcpyAsync(id_out, io, HW * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return last_launch_status();
+    API_END
+}
+
+extern "C" int lc_gaussian_pyramid(lc_ctx *c, int32_t h, int32_t w, int32_t ch, const double *image,
+                                   int32_t n_levels, const int32_t *kernel_sizes, const double *given_taps,
+                                   double *out) {
+    API_BEGIN
+    require(c && image && kernel_sizes && out, "null argument");
+    require(h >= 1 && w >= 1 && ch >= 1, "bad image shape");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DevArena m;
+    const size_t n = (size_t)h * w * ch;
+    double *src = m.upload(image, n, st);
+    double *tmp = m.alloc<double>(n);
+    double *dst = m.alloc<double>(n * n_levels);
+    const int grid = (int)std::min<size_t>((n + 255) / 256, 2368);
+    for (int l = 0; l < n_levels; ++l) {
+        const int k = kernel_sizes[l];
+        require(k >= 1 && k % 2 == 1, "kernel size must be odd and positive");
+        require(k <= 31 || !given_taps, "kernel sizes above 31 need library taps");
+        auto taps = given_taps ? std::vector<double>(given_taps + 32 * l, given_taps + 32 * l + k) : gaussian_taps(k);
+        double *dt = m.upload(taps.data(), taps.size(), st);
+        const PyrJob *dj = stage(c, std::vector<PyrJob>{PyrJob{src, tmp, dst + n * l}});
+        launch(c, k_blur_axis, dim3(grid), dim3(256), 0, dj, h, w, ch, (const double *)dt, k / 2, 0);
+        launch(c, k_blur_axis, dim3(grid), dim3(256), 0, dj, h, w, ch, (const double *)dt, k / 2, 1);
+    }
+    CK(cudaMemcpyAsync(out, dst, n * n_levels * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return last_launch_status();
+    API_END
+}
+
+extern "C" int lc_field_create(lc_ctx *c, int32_t h, int32_t w, const uint8_t *mask, lc_field **out) {
+    API_BEGIN
+    require(c && mask && out, "null argument");
+    require(h >= 1 && w >= 1, "bad mask shape");
+    CK(cudaSetDevice(c->device));
+    lc_field *f = new lc_field();
+    f->ctx = c;
+    f->H = h;
+    f->W = w;
+    f->mask = f->mem.upload(mask, (size_t)h * w, c->stream);
+    alloc_grid(f->mem, f->g, h, w);
+    build_grids(c, {{&f->g, f->mask}}, h, w);
+    CK(cudaMemcpyAsync(&f->K, f->g.K, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (f->K == 0) {
+        delete f;
+        return fail(LC_EINVAL, "mask has no foreground, distance transform undefined");
+    }
+    *out = f;
+    return last_launch_status();
+    API_END
+}
+
+extern "C" int lc_field_destroy(lc_field *f) {
+    delete f;
+    return LC_OK;
+}
+
+extern "C" int lc_field_n_contour(lc_field *f, int32_t *k) {
+    if (!f || !k) return fail(LC_EINVAL, "null argument");
+    *k = f->K;
+    return LC_OK;
+}
+
+__global__ void k_field_query(NnGridDev g, long long n, const double *pos, int kind, double *out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double x = pos[2 * i], y = pos[2 * i + 1];
+        double *o = out + 4 * i;
+        if (kind == 4) {
+            o[0] = field_inside(g, x, y) ? 1.0 : 0.0;
+            o[1] = o[2] = o[3] = 0.0;
+            continue;
+        }
+        const NnResult r = field_nearest(g, x, y);
+        if (kind == 0) { o[0] = r.dist; o[1] = 0.0; o[2] = 0.0; }
+        else if (kind == 1) { o[0] = field_interface(r); o[1] = 0.0; o[2] = 0.0; }
+        else if (kind == 2) { double v, gx, gy; field_residual(r, v, gx, gy); o[0] = v; o[1] = gx; o[2] = gy; }
+        else { o[0] = r.dist; o[1] = r.vx; o[2] = r.vy; }
+        o[3] = r.clamped ? 1.0 : 0.0;
+    }
+}
+
+extern "C" int lc_field_query(lc_field *f, int64_t n, const double *pos, int32_t kind, double *out) {
+    API_BEGIN
+    require(f && pos && out, "null argument");
+    require(kind >= 0 && kind <= 4, "kind must be 0..4");
+    lc_ctx *c = f->ctx;
+    CK(cudaSetDevice(c->device));
+    if (n == 0) return LC_OK;
+    DevArena m;
+    double *dp = m.upload(pos, 2 * (size_t)n, c->stream);
+    double *dout = m.alloc<double>(4 * (size_t)n);
+    NnGridDev g = grid_dev(f->g, f->mask, f->H, f->W);
+    g.K = f->K;
+    launch(c, k_field_query, dim3((unsigned)std::min<long long>((n + 255) / 256, 4096)), dim3(256), 0, g,
+           (long long)n, (const double *)dp, kind, dout);
+    CK(cudaMemcpyAsync(out, dout, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return last_launch_status();
+    API_END
+}
+
+extern "C" int lc_pcg_solve_bsr(lc_ctx *c, int32_t n, int64_t m_, const double *diag, const double *off,
+                                const int64_t *rows, const int64_t *cols, const double *rhs, int32_t iterations,
+                                double *x_out, lc_pcg_info *info) {
+    API_BEGIN
+    require(c && diag && rhs && x_out, "null argument");
+    require(n >= 1, "empty system");
+    require(m_ >= 0 && m_ < INT_MAX, "too many off-diagonal blocks");
+    require(iterations >= 0 && iterations < LC_MAX_LOG, "iterations out of range");
+    const int m = (int)m_;
+    for (int i = 0; i < m; ++i)
+        require(rows[i] >= 0 && rows[i] < n && cols[i] >= 0 && cols[i] < n, "block index out of range");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DevArena mem;
+    BsrJob J{};
+    J.n = n; J.m = m; J.iters = iterations;
+    J.diag = mem.upload(diag, 9 * (size_t)n, st);
+    J.off = mem.upload(off, 9 * (size_t)std::max(m, 1), st);
+    std::vector<int> cc(std::max(m, 1));
+    for (int i = 0; i < m; ++i) cc[i] = (int)cols[i];
+    J.cols = mem.upload(cc.data(), cc.size(), st);
+    long long *drows = mem.upload(reinterpret_cast<const long long *>(rows), std::max(m, 1), st);
+    int *keys = mem.alloc<int>(std::max(m, 1)), *vals = mem.alloc<int>(std::max(m, 1));
+    int *skeys = mem.alloc<int>(std::max(m, 1)), *order = mem.alloc<int>(std::max(m, 1));
+    int *count = mem.alloc<int>(n);
+    int *rowptr = mem.alloc<int>(n + 1);
+    CK(cudaMemsetAsync(count, 0, sizeof(int) * n, st));
+    if (m) {
+        launch(c, k_bsr_keys, dim3(std::min((m + 255) / 256, 1024)), dim3(256), 0, m, (const long long *)drows,
+               keys, vals, count);
+        const size_t tb = bsr_sort_temp_bytes(m);
+        void *tmp = mem.alloc<char>(tb);
+        int bits = 1;
+        while ((1 << bits) < n && bits < 31) ++bits;
+        CK(bsr_sort(tmp, tb, keys, skeys, vals, order, m, bits, st));
+        c->launches++;
+    }
+    launch(c, k_bsr_rowptr, dim3(1), dim3(1024), 0, n, (const int *)count, rowptr);
+    J.rowptr = rowptr;
+    J.order = order;
+    J.rhs = mem.upload(rhs, 3 * (size_t)n, st);
+    J.minv = mem.alloc<double>(9 * (size_t)n);
+    J.x = mem.alloc<double>(3 * (size_t)n); J.r = mem.alloc<double>(3 * (size_t)n);
+    J.z = mem.alloc<double>(3 * (size_t)n); J.p = mem.alloc<double>(3 * (size_t)n);
+    J.ap = mem.alloc<double>(3 * (size_t)n); J.best = mem.alloc<double>(3 * (size_t)n);
+    J.norms = mem.alloc<double>(LC_MAX_LOG);
+    J.info = mem.alloc<int>(4);
+    launch(c, k_pcg_bsr, dim3(1), dim3(1024), 0, J);
+    CK(cudaMemcpyAsync(x_out, J.best, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st));
+    int hinfo[4] = {0, 0, 0, 0};
+    double norms[LC_MAX_LOG];
+    CK(cudaMemcpyAsync(hinfo, J.info, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(norms, J.norms, sizeof(double) * LC_MAX_LOG, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (info) {
+        info->iterations = hinfo[0];
+        info->breakdown = hinfo[1];
+        for (int k = 0; k <= hinfo[0] && k < LC_MAX_LOG; ++k) info->residual_norms[k] = norms[k];
+    }
+    return last_launch_status();
+    API_END
+}
+
+extern "C" int lc_dense_solve(lc_ctx *c, int32_t n, const double *a, const double *b, double *x_out,
+                              lc_dense_info *info) {
+    API_BEGIN
+    require(c && a && b && x_out, "null argument");
+    require(n >= 1 && n <= 64, "dense solve supports 1 <= n <= 64");
+    for (int i = 0; i < n * n; ++i) require(std::isfinite(a[i]), "non-finite entries in normal system");
+    for (int i = 0; i < n; ++i) require(std::isfinite(b[i]), "non-finite entries in normal system");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DevArena m;
+    double *da = m.upload(a, (size_t)n * n, st), *db = m.upload(b, n, st);
+    double *dx = m.alloc<double>(n), *di = m.alloc<double>(2);
+    launch(c, k_dense_solve, dim3(1), dim3(256), 0, n, (const double *)da, (const double *)db, dx, di);
+    double hi[2];
+    CK(cudaMemcpyAsync(x_out, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hi, di, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (info) {
+        info->damped = hi[0] != 0.0;
+        info->damping = hi[1];
+    }
+    return last_launch_status();
+    API_END
+}

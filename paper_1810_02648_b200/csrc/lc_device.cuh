@@ -1,0 +1,265 @@
+// Device-side building blocks shared by the kernels.
+//
+// Everything here is fp64.  The library is compiled with --fmad=false so
+// `a*b + c` is never contracted: numpy and the numba kernels of the reference
+// evaluate it unfused, and several discrete decisions (raster coverage,
+// colour pruning, rim / inside tests, e1 <= e0) depend on the exact bits.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "lc_internal.h"
+
+#define LC_INF (__longlong_as_double(0x7ff0000000000000LL))
+
+struct V3 { double x, y, z; };
+
+__device__ __forceinline__ V3 v3(double x, double y, double z) { return V3{x, y, z}; }
+__device__ __forceinline__ V3 ld3(const double *p) { return V3{p[0], p[1], p[2]}; }
+__device__ __forceinline__ void st3(double *p, V3 v) { p[0] = v.x; p[1] = v.y; p[2] = v.z; }
+__device__ __forceinline__ V3 operator+(V3 a, V3 b) { return V3{a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ V3 operator-(V3 a, V3 b) { return V3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ V3 operator*(double s, V3 a) { return V3{s * a.x, s * a.y, s * a.z}; }
+__device__ __forceinline__ V3 operator*(V3 a, double s) { return V3{a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ V3 cross3(V3 a, V3 b) {
+    return V3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+// numpy add.reduce over a length-3 axis: (x0 + x1) + x2
+__device__ __forceinline__ double dot3(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ double norm3(V3 a) { return sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }
+
+// 3x3 row-major matrices
+__device__ __forceinline__ V3 mat_vec(const double *m, V3 v) {
+    return V3{m[0] * v.x + m[1] * v.y + m[2] * v.z, m[3] * v.x + m[4] * v.y + m[5] * v.z,
+              m[6] * v.x + m[7] * v.y + m[8] * v.z};
+}
+__device__ __forceinline__ void mat_mul(const double *a, const double *b, double *c) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            c[3 * i + j] = a[3 * i] * b[j] + a[3 * i + 1] * b[3 + j] + a[3 * i + 2] * b[6 + j];
+}
+
+// ---------------------------------------------------------------------------
+// camera (reference camera.py:45-83)
+
+__device__ __forceinline__ bool project(const CamDev &c, V3 p, double &px, double &py) {
+    const bool ok = p.z > 1e-9;
+    const double zs = ok ? p.z : 1.0;
+    px = ok ? c.fx * p.x / zs + c.cx : 0.0;
+    py = ok ? c.fy * p.y / zs + c.cy : 0.0;
+    return ok;
+}
+// rows of d(pix)/d(p): (a0, 0, a2) and (0, b1, b2); zero when invalid
+__device__ __forceinline__ void proj_jac(const CamDev &c, V3 p, double &a0, double &a2,
+                                         double &b1, double &b2) {
+    if (!(p.z > 1e-9)) { a0 = a2 = b1 = b2 = 0.0; return; }
+    const double zs = p.z;
+    a0 = c.fx / zs;
+    a2 = -c.fx * p.x / (zs * zs);
+    b1 = c.fy / zs;
+    b2 = -c.fy * p.y / (zs * zs);
+}
+
+// ---------------------------------------------------------------------------
+// quaternions (w, x, y, z)  (skinning.py:85-112)
+
+struct Q4 { double w, x, y, z; };
+__device__ __forceinline__ Q4 qmul(Q4 a, Q4 b) {
+    return Q4{a.w * b.w - a.x * b.x - a.y * b.y - a.z * b.z,
+              a.w * b.x + a.x * b.w + a.y * b.z - a.z * b.y,
+              a.w * b.y - a.x * b.z + a.y * b.w + a.z * b.x,
+              a.w * b.z + a.x * b.y - a.y * b.x + a.z * b.w};
+}
+__device__ __forceinline__ Q4 qconj(Q4 q) { return Q4{q.w, -q.x, -q.y, -q.z}; }
+__device__ __forceinline__ V3 qrot(Q4 q, V3 v) {
+    const V3 u{q.x, q.y, q.z};
+    const V3 t = 2.0 * cross3(u, v);
+    return v + q.w * t + cross3(u, t);
+}
+
+// ---------------------------------------------------------------------------
+// deterministic block reduction (fixed thread -> value mapping, fixed tree)
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x < 32) {
+        s = (l < NT / 32) ? red[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (l == 0) red[32] = s;
+    }
+    __syncthreads();
+    return red[32];
+}
+
+// several sums at once (M <= 8)
+template <int NT, int M>
+__device__ __forceinline__ void block_sums(double (&v)[M], double *red) {
+    for (int m = 0; m < M; ++m)
+        for (int o = 16; o > 0; o >>= 1) v[m] += __shfl_down_sync(0xffffffffu, v[m], o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0)
+        for (int m = 0; m < M; ++m) red[m * 32 + w] = v[m];
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        for (int m = 0; m < M; ++m) {
+            double s = (l < NT / 32) ? red[m * 32 + l] : 0.0;
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+            if (l == 0) red[8 * 32 + m] = s;
+        }
+    }
+    __syncthreads();
+    for (int m = 0; m < M; ++m) v[m] = red[8 * 32 + m];
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// exact nearest contour-pixel centre (DistanceField._nearest, imageproc.py:195-213)
+//
+// Uniform grid of LC_GRID_CELL-pixel cells with Chebyshev ring search.  Ties
+// on the squared distance break toward the lowest point index (argwhere
+// order).  Queries outside the grid fall back to a linear scan.
+
+__device__ __forceinline__ void nn_consider(const NnGridDev &g, int pid, double qx, double qy,
+                                            double &best, int &bi) {
+    const int2 p = g.pts[pid];
+    const double dx = qx - (double)p.x, dy = qy - (double)p.y;
+    const double d2 = dx * dx + dy * dy;
+    if (d2 < best || (d2 == best && pid < bi)) { best = d2; bi = pid; }
+}
+
+__device__ inline int nn_query(const NnGridDev &g, double qx, double qy, double &d2out) {
+    double best = LC_INF;
+    int bi = 0x7fffffff;
+    const double gx = (double)(g.ncx * LC_GRID_CELL), gy = (double)(g.ncy * LC_GRID_CELL);
+    if (!(qx >= 0.0 && qy >= 0.0 && qx < gx && qy < gy)) {
+        for (int k = 0; k < g.K; ++k) nn_consider(g, k, qx, qy, best, bi);
+        d2out = best;
+        return bi;
+    }
+    const int cx = (int)qx >> LC_GRID_SHIFT, cy = (int)qy >> LC_GRID_SHIFT;
+    const int rmax = max(max(cx, g.ncx - 1 - cx), max(cy, g.ncy - 1 - cy));
+    // after ring r every unvisited point is > r*CELL away (strictly), so the
+    // search may stop as soon as the best squared distance is <= (r*CELL)^2
+    for (int r = 0; r <= rmax; ++r) {
+        for (int yy = cy - r; yy <= cy + r; ++yy) {
+            if (yy < 0 || yy >= g.ncy) continue;
+            const bool full_row = (yy == cy - r) || (yy == cy + r);
+            const int stride = full_row ? 1 : 2 * r;
+            for (int xx = cx - r; xx <= cx + r; xx += stride) {
+                if (xx < 0 || xx >= g.ncx) continue;
+                const int c = yy * g.ncx + xx;
+                const int s = g.cell_start[c], e = g.cell_start[c + 1];
+                for (int k = s; k < e; ++k) nn_consider(g, g.cell_pts[k], qx, qy, best, bi);
+            }
+        }
+        const double lim = (double)(r * LC_GRID_CELL);
+        if (best <= lim * lim) break;
+    }
+    d2out = best;
+    return bi;
+}
+
+// continuous distance + unit direction away from the nearest contour point
+struct NnResult { double dist, vx, vy; bool clamped; };
+
+__device__ __forceinline__ NnResult field_nearest(const NnGridDev &g, double qx, double qy) {
+    NnResult r;
+    const bool fin = isfinite(qx) && isfinite(qy);
+    if (!fin) { qx = 0.0; qy = 0.0; }
+    double d2;
+    const int k = nn_query(g, qx, qy, d2);
+    if (k < 0 || k >= g.K) { r.dist = LC_INF; r.vx = r.vy = 0.0; r.clamped = true; return r; }
+    const double d = sqrt(d2);
+    const int2 p = g.pts[k];
+    const double safe = d > 1e-12 ? d : 1e-12;
+    const bool dirok = (d > 1e-12) && fin;
+    r.vx = dirok ? (qx - (double)p.x) / safe : 0.0;
+    r.vy = dirok ? (qy - (double)p.y) / safe : 0.0;
+    r.dist = fin ? d : 0.0;
+    r.clamped = !fin;
+    return r;
+}
+
+// C^1 interface residual (DistanceField.sample_residual, imageproc.py:225-243)
+__device__ __forceinline__ void field_residual(const NnResult &n, double &res, double &gx,
+                                               double &gy) {
+    const double lo = 0.5 - 0.15, hi = 0.5 + 0.15;
+    double t = n.dist - lo;
+    t = t < 0.0 ? 0.0 : (t > hi - lo ? hi - lo : t);
+    const bool far = n.dist >= hi;
+    res = far ? n.dist - 0.5 : t * t / (4.0 * 0.15);
+    const double slope = far ? 1.0 : t / (2.0 * 0.15);
+    gx = n.vx * slope;
+    gy = n.vy * slope;
+}
+
+__device__ __forceinline__ double field_interface(const NnResult &n) {
+    const double v = n.dist - 0.5;
+    return v > 0.0 ? v : 0.0;
+}
+
+// nearest-pixel foreground test (DistanceField.inside, imageproc.py:254-261); np.round == rint
+__device__ __forceinline__ bool field_inside(const NnGridDev &g, double x, double y) {
+    const double xr = rint(x), yr = rint(y);
+    if (!(xr >= 0.0 && xr < (double)g.W && yr >= 0.0 && yr < (double)g.H)) return false;
+    return g.mask[(int)yr * g.W + (int)xr] != 0;
+}
+
+// contour side sign (pose_stage.py:194-215): -1 iff inside and n . dir < 0
+__device__ __forceinline__ double side_sign(const NnGridDev &g, const NnResult &n, double px,
+                                            double py, double n2x, double n2y) {
+    if (!field_inside(g, px, py)) return 1.0;
+    return (n2x * n.vx + n2y * n.vy) < 0.0 ? -1.0 : 1.0;
+}
+
+// ---------------------------------------------------------------------------
+// bilinear sample of an (H,W,3) image with the analytic gradient
+// (sample_bilinear, imageproc.py:127-174)
+
+__device__ __forceinline__ bool bilinear3(const double *img, int W, int H, double x, double y,
+                                          double val[3], double gx[3], double gy[3]) {
+    const bool clamped = (x < 0) || (x > W - 1) || (y < 0) || (y > H - 1);
+    const double xc = fmin(fmax(x, 0.0), (double)(W - 1));
+    const double yc = fmin(fmax(y, 0.0), (double)(H - 1));
+    const int x0 = min((int)floor(xc), W - 2), y0 = min((int)floor(yc), H - 2);
+    const double fx = xc - x0, fy = yc - y0;
+    const double *p00 = img + ((size_t)y0 * W + x0) * 3;
+    const double *p10 = p00 + (size_t)W * 3;
+    const bool inx = (x >= 0) && (x <= W - 1), iny = (y >= 0) && (y <= H - 1);
+    for (int c = 0; c < 3; ++c) {
+        const double c00 = p00[c], c01 = p00[3 + c], c10 = p10[c], c11 = p10[3 + c];
+        const double top = c00 * (1 - fx) + c01 * fx;
+        const double bot = c10 * (1 - fx) + c11 * fx;
+        val[c] = top * (1 - fy) + bot * fy;
+        gx[c] = inx ? (c01 - c00) * (1 - fy) + (c11 - c10) * fy : 0.0;
+        gy[c] = iny ? bot - top : 0.0;
+    }
+    return clamped;
+}
+
+// ---------------------------------------------------------------------------
+// symmetric 3x3 inverse via the adjugate; s = (xx, xy, xz, yy, yz, zz)
+__device__ __forceinline__ bool sym3_inverse(const double s[6], double o[6]) {
+    const double a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5];
+    const double A = d * f - e * e, B = c * e - b * f, C = b * e - c * d;
+    const double det = a * A + b * B + c * C;
+    if (det == 0.0 || !isfinite(det)) return false;
+    const double id = 1.0 / det;
+    o[0] = A * id;
+    o[1] = B * id;
+    o[2] = C * id;
+    o[3] = (a * f - c * c) * id;
+    o[4] = (b * c - a * e) * id;
+    o[5] = (a * d - b * b) * id;
+    return true;
+}
+__device__ __forceinline__ V3 sym3_mul(const double s[6], V3 v) {
+    return V3{s[0] * v.x + s[1] * v.y + s[2] * v.z, s[1] * v.x + s[3] * v.y + s[4] * v.z,
+              s[2] * v.x + s[4] * v.y + s[5] * v.z};
+}

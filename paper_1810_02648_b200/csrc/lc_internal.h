@@ -1,0 +1,95 @@
+// Internal host/device layout of liblivecap (not part of the C-ABI).
+//
+// HBM layout (all fp64 AoS (.,3) like the reference's numpy arrays, int32
+// indices):
+//   actor tables   : uploaded once per actor, shared by every stream
+//   stream slots   : per capture stream, resident for the tracker's life
+//                    (pyramid, observed-contour grid, state, scratch)
+#pragma once
+#include <cstdint>
+
+#define LC_MAXJ 32
+#define LC_NDOF 27
+#define LC_NROT 30       // 3 root Euler + 27 joint angles
+#define LC_NP 36
+#define LC_GRID_CELL 16  // NN grid cell edge in pixels
+#define LC_GRID_SHIFT 4
+
+struct SkelDev {
+    int J, head, n_tree_levels;
+    int parents[LC_MAXJ];
+    double off[LC_MAXJ][3];
+    double rest[LC_MAXJ][3];
+    int dof_joint[LC_NDOF];
+    double dof_axes[LC_NDOF][3];
+    double tmin[LC_NDOF], tmax[LC_NDOF];
+    double marker[4][3];
+    unsigned moves_pos[LC_NDOF];    // bit j: dof k moves joint position j
+    unsigned moves_frame[LC_NDOF];  // bit j: dof k moves joint frame j
+    int dof_start[LC_MAXJ + 1];     // dofs of joint i: dof_list[dof_start[i]..dof_start[i+1])
+    int dof_list[LC_NDOF];
+    int level_start[LC_MAXJ + 1];   // FK schedule: joints grouped by tree depth
+    int level_joint[LC_MAXJ];
+    int group[LC_MAXJ];
+    int joint_part[LC_MAXJ];
+};
+
+struct ActorDev {
+    int N, T, E, J;
+    const double *rest;        // N*3
+    const int *tris;           // T*3
+    const double *colors;      // N*3
+    const int *edges;          // E*2
+    const int *edge_tris;      // E*2
+    const double *rest_len;    // E
+    const double *rest_dir;    // E*3 unit rest direction (degenerate-edge fallback)
+    const int *adj_ptr;        // N+1 : incident undirected edges per vertex, in the
+    const int *adj_edge;       //       reference's directed order (as src: forward
+    const int *adj_nbr;        //       edges asc., then reversed edges asc.)
+    const int *degrees;        // N
+    const double *w_dir;       // 2E directed material weights
+    const int *skin_idx;       // N*4 (-1 padding)
+    const double *skin_w;      // N*4
+    const int *dominant;       // N
+    const int *vt_ptr;         // N+1 : incident triangles in (slot, triangle) order
+    const int *vt_tri;
+    const double *rigidity;    // N (Table-1 class weight)
+    const int *vpart;          // N body part of the dominant joint
+    const SkelDev *skel;
+};
+
+struct CamDev {
+    double fx, fy, cx, cy;
+    int W, H;
+};
+
+// exact nearest-contour index over one mask
+struct NnGridDev {
+    int K;                 // contour pixels
+    int W, H, ncx, ncy;
+    const int2 *pts;       // K (x, y), np.argwhere row-major order
+    const int *cell_start; // ncx*ncy+1
+    const int *cell_pts;   // point ids grouped by cell
+    const uint8_t *mask;   // H*W, for inside()
+};
+
+// per-config constants of the surface energy
+struct EdgeConstDev {
+    const double *cs_f, *cs_r;  // E : sqrt(w_smooth s / deg(src)) forward / reversed half
+    const double *ce_f, *ce_r;  // E : sqrt(w_edge s / deg(src))
+    const double *alpha;        // E : cs_f^2 + cs_r^2
+    const double *beta;         // E : ce_f^2 + ce_r^2
+};
+
+struct PoseHyperDev {
+    double l2d, l3d, lsil, ltemp, lanat, face;
+    double tw[LC_MAXJ];   // lambda-free temporal group weight per joint
+    int gn, max_halvings;
+};
+
+struct SurfHyperDev {
+    double w_photo, w_sil, w_smooth, w_edge, w_vel, w_acc, tau;
+    int gn, pcg, max_halvings, n_levels, dilation;
+    double snap_step, snap_band;
+    int snap_max_steps;
+};

@@ -1,0 +1,104 @@
+// Kernel declarations and the per-stream job descriptors they consume.
+#pragma once
+#include "lc_kinematics.cuh"
+
+// ----- blur pyramid (imageproc.py:264-285) ---------------------------------
+struct PyrJob {
+    const double *src;   // H*W*C
+    double *tmp;         // H*W*C
+    double *dst;         // H*W*C
+};
+__global__ void k_blur_axis(const PyrJob *jobs, int H, int W, int C, const double *taps, int half,
+                            int axis);
+
+// ----- mask contour + NN grid (imageproc.py:34-49,186-193) -----------------
+struct GridJob {
+    const uint8_t *mask;   // H*W
+    int *row_count;        // H
+    int *row_start;        // H+1
+    int2 *pts;             // capacity H*W
+    int *cell_count;       // ncx*ncy
+    int *cell_start;       // ncx*ncy+1
+    int *cell_fill;        // ncx*ncy
+    int *cell_pts;         // capacity H*W
+    int *K;                // out: contour pixel count
+};
+__global__ void k_contour_rows(const GridJob *jobs, int H, int W);
+__global__ void k_contour_scan_rows(const GridJob *jobs, int H, int ncells);
+__global__ void k_contour_emit(const GridJob *jobs, int H, int W, int ncx);
+__global__ void k_contour_scan_cells(const GridJob *jobs, int ncells);
+__global__ void k_contour_fill(const GridJob *jobs, int ncx);
+
+// ----- rasterizer (rasterizer.py:18-120) -----------------------------------
+struct RasterJob {
+    const double *verts;        // N*3
+    unsigned long long *zbuf;   // H*W, fp64 bit patterns (+inf = empty)
+    int *tri_id;                // H*W, INT_MAX = empty
+    uint8_t *mask;              // H*W out (isfinite(zbuf)), may be null
+};
+__global__ void k_raster_clear(const RasterJob *jobs, int HW);
+__global__ void k_raster_depth(const RasterJob *jobs, CamDev cam, const int *tris, int T);
+__global__ void k_raster_winner(const RasterJob *jobs, CamDev cam, const int *tris, int T);
+__global__ void k_raster_mask(const RasterJob *jobs, int HW);
+__global__ void k_raster_resolve(const RasterJob *jobs, CamDev cam, const int *tris, int mode,
+                                 const double *attrs, int n_attr, const int *ids,
+                                 double bg_attr, long long bg_id, double *zout, double *aout,
+                                 long long *iout);
+
+// ----- kinematics / skinning (skinning.py:206-398) -------------------------
+struct FkJob {
+    const double *x;     // 36
+    FkState *fk;         // out
+    int active;
+};
+__global__ void k_fk(const FkJob *jobs, const SkelDev *sk);
+struct SkinJob {
+    const FkState *fk;
+    const double *rest;      // M*3 rest points (already gathered for subsets)
+    const double *disp;      // optional N*3 displacement added to rest (may be null)
+    const int *subset;       // optional M vertex ids (skinning rows); null = identity
+    double *pos;             // M*3 out
+    double *rot;             // M*4 out or null
+    double *jac;             // M*3*36 out or null
+    int M;
+    int active;
+};
+__global__ void k_skin(const SkinJob *jobs, ActorDev A);
+
+// ----- occluding contour + rim filter + part gating -------------------------
+struct ContourJob {
+    const double *verts;            // N*3
+    const unsigned long long *zbuf; // H*W
+    uint8_t *tri_front;             // T
+    double *tri_n;                  // T*3
+    uint8_t *vflag;                 // N
+    int *idx;                       // N capacity
+    double *n2d;                    // N*2
+    int *B;                         // out count
+    int *vis;                       // N capacity (visible_vertices), may be null
+    int *P;                         // out count
+    int active;
+};
+__global__ void k_tri_front(const ContourJob *jobs, ActorDev A);
+__global__ void k_sil_edges(const ContourJob *jobs, ActorDev A);
+__global__ void k_contour_compact(const ContourJob *jobs, ActorDev A, CamDev cam);
+
+struct RimJob {
+    const double *verts;       // N*3
+    const int *idx;            // B
+    const int *B;
+    NnGridDev own;             // own-mask field
+    const int *ownK;
+    uint8_t *keep;             // B out
+    int stage1;                // 1: thickness probes + rigidity gate
+    int active;
+    // stage-2 part gating
+    const int *tri_id;         // H*W winning triangle (Stage-II raster)
+    int part_gate;
+    int dilation;
+};
+__global__ void k_rim(const RimJob *jobs, ActorDev A, CamDev cam, const double *probe_offs);
+
+// ----- surface solve (nonrigid_stage.py:189-500) ---------------------------
+struct SurfJob;
+struct PoseJob;

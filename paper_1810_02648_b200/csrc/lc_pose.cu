@@ -1,0 +1,408 @@
+// Stage I: skeletal pose Gauss-Newton, one persistent CTA per stream.
+//
+// Reference: PoseProblem.evaluate (pose_stage.py:319-404) and solve_pose
+// (pose_stage.py:429-459).  Per evaluation: FK on one warp, the joint /
+// dual-quaternion Jacobian tables in shared memory, residual rows computed
+// NT at a time into a shared chunk, and J^T J / J^T F accumulated from the
+// chunk by 27 register-tiled tasks (21 upper 6x6 tiles + 6 rhs strips) per
+// row group.  The 36x36 system is solved in shared memory (lc_qr.cuh); the
+// halving line search re-evaluates energies only.  No host round trip.
+#include "livecap.h"
+#include "lc_kernels.cuh"
+#include "lc_qr.cuh"
+#include "lc_pose.cuh"
+
+namespace {
+
+constexpr int NT = 256;
+constexpr int G = NT / 32;  // row groups for the J^T J accumulation
+
+struct PoseSmem {
+    SkelDev sk;
+    FkState f;
+    QrSmem qr;
+    double A[LC_NP * LC_NP];
+    double rhs[LC_NP];
+    double x[LC_NP], xt[LC_NP], step[LC_NP];
+    double red[8 * 32 + 16];
+    double pix[LC_MAXJ + 4][2];
+    int okz[LC_MAXJ + 4];
+};
+
+struct PoseCtx {
+    const PoseJob *J;
+    PoseSmem *s;
+    double *jp;    // (J+4)*3*36
+    double *dqj;   // J*8*36
+    double *rows;  // NT*37
+    int B, n2, n3, nt, R;
+    CamDev cam;
+    ActorDev A;
+    NnGridDev obs;
+};
+
+// one residual row; writes the 36 Jacobian entries to `jr` when non-null.
+// Returns F and sets `term` (0 2d, 1 3d, 2 sil, 3 temporal, 4 anatomic).
+__device__ double pose_row(const PoseCtx &c, int r, double *jr, int &term, int &behind) {
+    const PoseSmem &s = *c.s;
+    const SkelDev &sk = s.sk;
+    const PoseJob &J = *c.J;
+    const PoseHyperDev &hp = J.hp;
+    const int nj = sk.J;
+    behind = 0;
+    if (r < c.n2) {                                      // 2D detections
+        term = 0;
+        const int n = r >> 1, comp = r & 1;
+        const double lam = n < nj ? hp.l2d : hp.l2d * hp.face;
+        const double w2 = (sqrt(lam) * (J.v2d[n] ? 1.0 : 0.0)) * (s.okz[n] ? 1.0 : 0.0);
+        const double F = (s.pix[n][comp] - J.j2d[2 * n + comp]) * w2;
+        if (jr) {
+            const V3 p = n < nj ? ld3(s.f.pos[n]) : ld3(s.f.markers[n - nj]);
+            double a0, a2, b1, b2;
+            proj_jac(c.cam, p, a0, a2, b1, b2);
+            const double d0 = comp == 0 ? a0 : 0.0, d1 = comp == 0 ? 0.0 : b1, d2 = comp == 0 ? a2 : b2;
+            const double *jn = c.jp + (size_t)n * 3 * LC_NP;
+            for (int q = 0; q < LC_NP; ++q)
+                jr[q] = (d0 * jn[q] + d1 * jn[LC_NP + q] + d2 * jn[2 * LC_NP + q]) * w2;
+        }
+        return F;
+    }
+    r -= c.n2;
+    if (r < c.n3) {                                      // 3D detections
+        term = 1;
+        const int i = r / 3, comp = r % 3;
+        const double w3 = sqrt(hp.l3d) * (J.v3d[i] ? 1.0 : 0.0);
+        const double F = ((s.f.pos[i][comp] - J.j3d[3 * i + comp]) - s.xt[33 + comp]) * w3;
+        if (jr) {
+            const double *jn = c.jp + ((size_t)i * 3 + comp) * LC_NP;
+            for (int q = 0; q < LC_NP; ++q) jr[q] = (jn[q] - (q == 33 + comp ? 1.0 : 0.0)) * w3;
+        }
+        return F;
+    }
+    r -= c.n3;
+    if (r < c.B) {                                       // silhouette
+        term = 2;
+        const int b = r;
+        const int v = J.cidx[b];
+        const V3 rest = J.crest ? ld3(J.crest + 3 * (size_t)b) : ld3(J.drest + 3 * (size_t)v);
+        Blend Bl;
+        struct SmemDq {
+            const FkState *f;
+            __device__ double operator()(int j, int k) const { return f->dq[j][k]; }
+        };
+        dq_blend(c.A.skin_idx + 4 * v, c.A.skin_w + 4 * v, c.A.dominant[v], SmemDq{&s.f}, Bl);
+        Q4 cr;
+        const V3 sp = dq_apply(Bl, rest, cr);
+        double px, py;
+        const bool cok = project(c.cam, sp, px, py);
+        behind = !cok;
+        NnResult nn;
+        double val = 0.0, gx = 0.0, gy = 0.0;
+        nn = field_nearest(c.obs, px, py);
+        field_residual(nn, val, gx, gy);
+        bool ok = cok && !nn.clamped;
+        if (J.enabled) ok = ok && J.enabled[b];
+        const double ws = sqrt(hp.lsil) * (ok ? 1.0 : 0.0);
+        const double F = val * ws;
+        if (jr) {
+            double a0, a2, b1, b2;
+            proj_jac(c.cam, sp, a0, a2, b1, b2);
+            const V3 g3 = v3(gx * a0, gy * b1, gx * a2 + gy * b2);
+            double dv[3][8];
+            dq_dtransform(Bl, rest, dv);
+            double h[8];
+            for (int k = 0; k < 8; ++k) h[k] = g3.x * dv[0][k] + g3.y * dv[1][k] + g3.z * dv[2][k];
+            const double sign = J.directional ? side_sign(c.obs, nn, px, py, J.n2d[2 * b], J.n2d[2 * b + 1]) : 1.0;
+            const double sc = ws * sign;
+            for (int q = 0; q < LC_NP; ++q) jr[q] = 0.0;
+            if (Bl.degenerate) {
+                const double *t = c.dqj + (size_t)Bl.dom * 8 * LC_NP;
+                for (int q = 0; q < LC_NP; ++q) {
+                    double a = 0.0;
+                    for (int k = 0; k < 8; ++k) a += h[k] * t[k * LC_NP + q];
+                    jr[q] = a;
+                }
+            } else {
+                for (int sl = 0; sl < 4; ++sl) {
+                    const double cf = Bl.coef[sl];
+                    if (cf == 0.0) continue;
+                    const double *t = c.dqj + (size_t)Bl.js[sl] * 8 * LC_NP;
+                    for (int q = 0; q < LC_NP; ++q) {
+                        double a = 0.0;
+                        for (int k = 0; k < 8; ++k) a += h[k] * t[k * LC_NP + q];
+                        jr[q] += cf * a;
+                    }
+                }
+            }
+            for (int q = 0; q < LC_NP; ++q) jr[q] *= sc;
+        }
+        return F;
+    }
+    r -= c.B;
+    if (r < c.nt) {                                      // temporal
+        term = 3;
+        const int i = r / 3, comp = r % 3;
+        const double wt = sqrt(hp.ltemp * hp.tw[i]);
+        const double F = (s.f.pos[i][comp] - J.prev_pos[3 * i + comp]) * wt;
+        if (jr) {
+            const double *jn = c.jp + ((size_t)i * 3 + comp) * LC_NP;
+            for (int q = 0; q < LC_NP; ++q) jr[q] = jn[q] * wt;
+        }
+        return F;
+    }
+    r -= c.nt;                                           // anatomic (27 rows)
+    term = 4;
+    const double th = s.xt[6 + r];
+    const bool hi = th > sk.tmax[r], lo = th < sk.tmin[r];
+    const double wa = sqrt(hp.lanat);
+    const double F = wa * ((hi ? th - sk.tmax[r] : 0.0) + (lo ? sk.tmin[r] - th : 0.0));
+    if (jr) {
+        for (int q = 0; q < LC_NP; ++q) jr[q] = 0.0;
+        jr[6 + r] = wa * ((hi ? 1.0 : 0.0) - (lo ? 1.0 : 0.0));
+    }
+    return F;
+}
+
+// evaluate at s.xt; with_jac fills s.A / s.rhs.  Returns the total energy,
+// per-term energies in terms[5], behind-camera count.
+__device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &behind_out) {
+    PoseSmem &s = *c.s;
+    const SkelDev &sk = s.sk;
+    const int nj = sk.J;
+    if (threadIdx.x < 32) fk_warp(sk, s.xt, s.f);
+    __syncthreads();
+    // projections of joints + markers
+    for (int n = threadIdx.x; n < nj + 4; n += NT) {
+        const V3 p = n < nj ? ld3(s.f.pos[n]) : ld3(s.f.markers[n - nj]);
+        double px, py;
+        s.okz[n] = project(c.cam, p, px, py);
+        s.pix[n][0] = px;
+        s.pix[n][1] = py;
+    }
+    if (with_jac) {
+        // joint/marker position Jacobian (J+4, 3, 36)
+        const int npos = (nj + 4) * 3 * LC_NP;
+        for (int e = threadIdx.x; e < npos; e += NT) {
+            const int q = e % LC_NP, comp = (e / LC_NP) % 3, pt = e / (3 * LC_NP);
+            double val;
+            if (q >= 3 && q < 6) val = (q - 3 == comp) ? 1.0 : 0.0;
+            else if (q >= 33) val = 0.0;
+            else {
+                const V3 sp = joint_spin(sk, s.f, pt, q < 3 ? q : q - 3);
+                val = comp == 0 ? sp.x : (comp == 1 ? sp.y : sp.z);
+            }
+            c.jp[e] = val;
+        }
+        // dual-quaternion Jacobian (J, 8, 36)
+        for (int e = threadIdx.x; e < nj * LC_NP; e += NT) {
+            const int j = e / LC_NP, q = e % LC_NP;
+            double o[8];
+            if (q >= 3 && q < 6) {
+                const Q4 d = dq_trans(s.f, j, q - 3);
+                o[0] = o[1] = o[2] = o[3] = 0.0;
+                o[4] = d.w; o[5] = d.x; o[6] = d.y; o[7] = d.z;
+            } else if (q >= 33) {
+                for (int k = 0; k < 8; ++k) o[k] = 0.0;
+            } else {
+                dq_spin(sk, s.f, j, q < 3 ? q : q - 3, o);
+            }
+            for (int k = 0; k < 8; ++k) c.dqj[((size_t)j * 8 + k) * LC_NP + q] = o[k];
+        }
+    }
+    __syncthreads();
+
+    double acc[5] = {0, 0, 0, 0, 0};
+    double total = 0.0;
+    int behind = 0;
+    // J^T J tiles: task = tid / G (27 tasks), group = tid % G
+    const int task = threadIdx.x / G, grp = threadIdx.x % G;
+    double tile[36];
+    for (int k = 0; k < 36; ++k) tile[k] = 0.0;
+    int ta = 0, tb = 0;
+    bool is_rhs = false;
+    if (task < 21) {
+        int t = task;
+        for (ta = 0; ta < 6; ++ta) {
+            if (t < 6 - ta) { tb = ta + t; break; }
+            t -= 6 - ta;
+        }
+    } else if (task < 27) {
+        is_rhs = true;
+        ta = task - 21;
+    }
+    for (int r0 = 0; r0 < c.R; r0 += NT) {
+        const int r = r0 + threadIdx.x;
+        if (r < c.R) {
+            int term, bh;
+            double *jr = with_jac ? c.rows + (size_t)threadIdx.x * 37 : nullptr;
+            const double F = pose_row(c, r, jr, term, bh);
+            if (jr) jr[36] = F;
+            acc[term] += F * F;
+            behind += bh;
+        }
+        if (with_jac) {
+            __syncthreads();
+            const int nr = min(NT, c.R - r0);
+            if (task < 27) {
+                for (int rr = grp; rr < nr; rr += G) {
+                    const double *row = c.rows + (size_t)rr * 37;
+                    if (is_rhs) {
+                        const double F = row[36];
+                        for (int i = 0; i < 6; ++i) tile[i] += row[6 * ta + i] * F;
+                    } else {
+                        double a[6], b[6];
+                        for (int i = 0; i < 6; ++i) { a[i] = row[6 * ta + i]; b[i] = row[6 * tb + i]; }
+                        for (int i = 0; i < 6; ++i)
+                            for (int j = 0; j < 6; ++j) tile[6 * i + j] += a[i] * b[j];
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // total energy = sum of F^2 over all rows (pose_stage.py:279-281)
+    {
+        double v8[8] = {acc[0], acc[1], acc[2], acc[3], acc[4], (double)behind, 0.0, 0.0};
+        block_sums<NT, 8>(v8, s.red);
+        for (int k = 0; k < 5; ++k) terms[k] = v8[k];
+        behind_out = (int)v8[5];
+        total = (((v8[0] + v8[1]) + v8[2]) + v8[3]) + v8[4];
+    }
+    if (with_jac) {
+        // partial tiles -> shared (reuse the row chunk), then reduce over groups
+        double *part = c.rows;
+        const int per_group = 21 * 36 + 6 * 6;
+        if (task < 27) {
+            double *dst = part + (size_t)grp * per_group + (is_rhs ? 21 * 36 + 6 * ta : 36 * task);
+            const int cnt = is_rhs ? 6 : 36;
+            for (int k = 0; k < cnt; ++k) dst[k] = tile[k];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < per_group; e += NT) {
+            double sum = part[e];
+            for (int g = 1; g < G; ++g) sum += part[(size_t)g * per_group + e];
+            if (e < 21 * 36) {
+                int t = e / 36, k = e % 36, a = 0, b = 0;
+                for (a = 0; a < 6; ++a) {
+                    if (t < 6 - a) { b = a + t; break; }
+                    t -= 6 - a;
+                }
+                const int i = 6 * a + k / 6, j = 6 * b + k % 6;
+                s.A[i * LC_NP + j] = sum;
+                s.A[j * LC_NP + i] = sum;
+            } else {
+                const int i = e - 21 * 36;
+                s.rhs[i] = -sum;
+            }
+        }
+        __syncthreads();
+    }
+    return total;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(NT, 1) k_pose_solve(const PoseJob *jobs, const SkelDev *skg,
+                                                      ActorDev A, CamDev cam) {
+    const PoseJob &J = jobs[blockIdx.x];
+    if (!J.active) return;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    PoseSmem &s = *reinterpret_cast<PoseSmem *>(dsm);
+    double *tail = reinterpret_cast<double *>(dsm + ((sizeof(PoseSmem) + 15) & ~size_t(15)));
+    {
+        const int *src = reinterpret_cast<const int *>(skg);
+        int *dst = reinterpret_cast<int *>(&s.sk);
+        for (int i = threadIdx.x; i < (int)(sizeof(SkelDev) / sizeof(int)); i += NT) dst[i] = src[i];
+    }
+    __syncthreads();
+    PoseCtx c;
+    c.J = &J;
+    c.s = &s;
+    c.cam = cam;
+    c.A = A;
+    const int nj = s.sk.J;
+    c.jp = tail;
+    c.dqj = c.jp + (size_t)(nj + 4) * 3 * LC_NP;
+    c.rows = c.dqj + (size_t)nj * 8 * LC_NP;
+    c.obs = J.obs;
+    c.obs.K = J.obs_K ? *J.obs_K : 0;
+    c.B = (J.has_field && c.obs.K > 0 && J.B) ? *J.B : 0;
+    c.n2 = 2 * (nj + 4);
+    c.n3 = 3 * nj;
+    c.nt = J.prev_pos ? 3 * nj : 0;
+    c.R = c.n2 + c.n3 + c.B + c.nt + 27;
+    for (int i = threadIdx.x; i < LC_NP; i += NT) s.x[i] = J.x0[i];
+    __syncthreads();
+
+    lc_pose_report *rep = J.report;
+    int log0 = J.log_offset;
+    int behind_total = 0, gimbal = 0;
+    for (int it = 0; it < J.hp.gn; ++it) {
+        for (int i = threadIdx.x; i < LC_NP; i += NT) s.xt[i] = s.x[i];
+        __syncthreads();
+        double terms[5];
+        int behind;
+        const double e0 = pose_eval(c, true, terms, behind);
+        behind_total += behind;
+        gimbal |= s.f.gimbal;
+        double damping;
+        const bool damped = dense_solve_block<NT>(s.qr, s.A, s.rhs, LC_NP, damping);
+        for (int i = threadIdx.x; i < LC_NP; i += NT) s.step[i] = s.qr.x[i];
+        __syncthreads();
+        int halv = 0;
+        bool rejected = false;
+        double e1;
+        for (;;) {
+            for (int i = threadIdx.x; i < LC_NP; i += NT) s.xt[i] = s.x[i] + s.step[i];
+            __syncthreads();
+            double tt[5];
+            int bh;
+            e1 = pose_eval(c, false, tt, bh);
+            if (e1 <= e0) {
+                for (int i = threadIdx.x; i < LC_NP; i += NT) s.x[i] = s.xt[i];
+                __syncthreads();
+                break;
+            }
+            if (halv >= J.hp.max_halvings) {
+                rejected = true;
+                e1 = e0;
+                break;
+            }
+            for (int i = threadIdx.x; i < LC_NP; i += NT) s.step[i] = 0.5 * s.step[i];
+            __syncthreads();
+            ++halv;
+        }
+        if (threadIdx.x == 0 && rep) {
+            const int k = log0 + it;
+            if (k < LC_MAX_LOG) {
+                rep->energy_before[k] = e0;
+                rep->energy_after[k] = e1;
+                double sn = 0.0;
+                for (int i = 0; i < LC_NP; ++i) sn += s.step[i] * s.step[i];
+                rep->step_norm[k] = sqrt(sn);
+                for (int t = 0; t < 5; ++t) rep->terms[k][t] = terms[t];
+                rep->halvings[k] = halv;
+                rep->rejected[k] = rejected;
+                rep->damped[k] = damped;
+            }
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < LC_NP; i += NT) J.x_out[i] = s.x[i];
+    if (threadIdx.x == 0 && rep) {
+        rep->n_iterations = log0 + J.hp.gn;
+        rep->behind_camera += behind_total;
+        rep->gimbal = rep->gimbal || gimbal;
+        rep->n_contour = c.B;
+        rep->has_temporal = J.prev_pos != nullptr;
+    }
+}
+
+size_t pose_smem_bytes(int n_joints) {
+    const size_t head = (sizeof(PoseSmem) + 15) & ~size_t(15);
+    const size_t tables = (size_t)(n_joints + 4) * 3 * LC_NP + (size_t)n_joints * 8 * LC_NP;
+    const size_t rows = (size_t)NT * 37;
+    return head + (tables + rows) * sizeof(double);
+}
+
+int pose_block_threads() { return NT; }

@@ -1,0 +1,61 @@
+// Job descriptors of the two persistent stage solvers.
+#pragma once
+#include "livecap.h"
+#include "lc_kernels.cuh"
+
+struct PoseJob {
+    int active;
+    const double *x0;
+    double *x_out;
+    NnGridDev obs;            // observed-silhouette field (K read from obs_K)
+    const int *obs_K;
+    int has_field;
+    const int *B;             // contour count (device)
+    const int *cidx;          // B contour vertex ids
+    const double *n2d;        // B*2
+    const double *crest;      // B*3 gathered rest points, or null -> drest[cidx]
+    const double *drest;      // N*3 displaced rest
+    const uint8_t *enabled;   // B or null
+    const double *j2d, *j3d;  // detections (j3d rescaled)
+    const uint8_t *v2d, *v3d;
+    const double *prev_pos;   // J*3 or null
+    PoseHyperDev hp;
+    int directional;
+    lc_pose_report *report;
+    int log_offset;
+};
+
+struct SurfJob {
+    int active;
+    int do_solve, do_snap;
+    const double *v0;         // N*3 start
+    double *v;                // N*3 result
+    const double *vs;         // N*3 skinned V^S
+    const double *pyr;        // levels*H*W*3
+    NnGridDev obs;
+    const int *obs_K;
+    int has_field;
+    const int *vis;           // P visible ids
+    const int *P;
+    const int *bidx;          // B boundary ids
+    const int *B;
+    const double *n2d;        // B*2
+    const uint8_t *enabled;   // B
+    const double *prev, *prev2;
+    int directional, enable_photo, enable_sil;
+    // scratch
+    double *diag, *minv;      // N*6 (sym: xx xy xz yy yz zz)
+    double *rhs, *x, *r, *z, *p, *ap, *best;   // N*3
+    double *edir, *eg;        // E*3
+    double *off0, *off1;      // N*3 snap offsets
+    uint8_t *hold;            // N
+    lc_nonrigid_report *report;
+};
+
+__global__ void k_pose_solve(const PoseJob *jobs, const SkelDev *skg, ActorDev A, CamDev cam);
+size_t pose_smem_bytes(int n_joints);
+int pose_block_threads();
+
+__global__ void k_surface_solve(const SurfJob *jobs, ActorDev A, CamDev cam, EdgeConstDev ec,
+                                SurfHyperDev hp, int H, int W);
+int surface_block_threads();

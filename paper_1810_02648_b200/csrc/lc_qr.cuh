@@ -1,0 +1,111 @@
+// Dense normal-equation solve (dense_solve, reference solvers.py:41-56):
+// Householder QR of A, rank test min|R_ii| < 1e-10 max|R_ii|, Tikhonov
+// damping 1e-6 tr(A)/n (or 1e-6) and a second QR, back substitution.
+//
+// Block-cooperative, everything in shared memory: one warp owns each column
+// (rows over lanes), so a Householder step is one broadcast of v and one
+// column update per warp.  n <= 64.
+#pragma once
+#include "lc_device.cuh"
+
+#define LC_QR_MAXN 64
+
+struct QrSmem {
+    double a[LC_QR_MAXN][LC_QR_MAXN + 1];   // augmented [A | b], row-major
+    double v[LC_QR_MAXN];
+    double rdiag[LC_QR_MAXN];
+    double x[LC_QR_MAXN];
+    double tau;
+    int skip;
+};
+
+// Householder on columns 0..n-1 of the augmented (n x n+1) matrix
+template <int NT>
+__device__ void qr_factor(QrSmem &s, int n) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int k = 0; k < n; ++k) {
+        if (w == 0) {
+            double ss = 0.0;
+            for (int i = k + lane; i < n; i += 32) ss += s.a[i][k] * s.a[i][k];
+            for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+            const double akk = s.a[k][k];
+            const double nrm = sqrt(ss);
+            const double alpha = akk >= 0.0 ? -nrm : nrm;
+            const double v0 = akk - alpha;
+            const double vn2 = ss - akk * akk + v0 * v0;
+            for (int i = k + lane; i < n; i += 32) s.v[i] = i == k ? v0 : s.a[i][k];
+            if (lane == 0) {
+                s.skip = !(nrm > 0.0) || !(vn2 > 0.0);
+                s.tau = s.skip ? 0.0 : 2.0 / vn2;
+                s.rdiag[k] = s.skip ? akk : alpha;
+            }
+        }
+        __syncthreads();
+        if (!s.skip) {
+            for (int j = k + 1 + w; j <= n; j += NT / 32) {
+                double d = 0.0;
+                for (int i = k + lane; i < n; i += 32) d += s.v[i] * s.a[i][j];
+                for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+                const double f = s.tau * d;
+                for (int i = k + lane; i < n; i += 32) s.a[i][j] -= f * s.v[i];
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s.a[k][k] = s.rdiag[k];
+        __syncthreads();
+    }
+}
+
+// back substitution R x = (Q^T b) on warp 0 (column n holds Q^T b)
+__device__ inline void qr_backsolve(QrSmem &s, int n) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    for (int k = n - 1; k >= 0; --k) {
+        double acc = 0.0;
+        for (int j = k + 1 + lane; j < n; j += 32) acc += s.a[k][j] * s.x[j];
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) s.x[k] = (s.a[k][n] - acc) / s.a[k][k];
+        __syncwarp();
+    }
+}
+
+// Solve with the reference's rank test / damping.  A is read from `A` (n*n
+// row-major, symmetric) and `b`; result in s.x.  Returns damped flag.
+template <int NT>
+__device__ bool dense_solve_block(QrSmem &s, const double *A, const double *b, int n,
+                                  double &damping) {
+    for (int i = threadIdx.x; i < n * n; i += NT) s.a[i / n][i % n] = A[i];
+    for (int i = threadIdx.x; i < n; i += NT) s.a[i][n] = b[i];
+    __syncthreads();
+    qr_factor<NT>(s, n);
+    __shared__ int damped_flag;
+    __shared__ double lam;
+    if (threadIdx.x == 0) {
+        double mx = 0.0, mn = LC_INF;
+        for (int i = 0; i < n; ++i) {
+            const double d = fabs(s.rdiag[i]);
+            mx = fmax(mx, d);
+            mn = fmin(mn, d);
+        }
+        damped_flag = mn < 1e-10 * fmax(mx, 1e-300);
+        double tr = 0.0;
+        for (int i = 0; i < n; ++i) tr += A[i * n + i];
+        double l = 1e-6 * tr / n;
+        if (l <= 0.0) l = 1e-6;
+        lam = damped_flag ? l : 0.0;
+    }
+    __syncthreads();
+    if (damped_flag) {
+        for (int i = threadIdx.x; i < n * n; i += NT) {
+            const int r = i / n, c = i % n;
+            s.a[r][c] = r == c ? A[i] + lam : A[i];
+        }
+        for (int i = threadIdx.x; i < n; i += NT) s.a[i][n] = b[i];
+        __syncthreads();
+        qr_factor<NT>(s, n);
+    }
+    qr_backsolve(s, n);
+    __syncthreads();
+    damping = lam;
+    return damped_flag != 0;
+}

@@ -1,0 +1,129 @@
+// Host-side runtime objects behind the C-ABI handles.
+#pragma once
+#include <cuda_runtime.h>
+#include <string>
+#include <vector>
+#include "livecap.h"
+#include "lc_pose.cuh"
+#include "lc_bsr.cuh"
+
+struct lc_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    long long launches = 0;
+    struct Slot *call_slot = nullptr;          // scratch slot for single-call entry points
+    const lc_actor *call_actor = nullptr;
+    int call_w = 0, call_h = 0;
+};
+
+// device allocation list owned by an object
+struct DevArena {
+    std::vector<void *> ptrs;
+    template <typename T>
+    T *alloc(size_t count) {
+        void *p = nullptr;
+        if (count == 0) count = 1;
+        if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) throw std::bad_alloc();
+        ptrs.push_back(p);
+        return static_cast<T *>(p);
+    }
+    template <typename T>
+    T *upload(const T *host, size_t count, cudaStream_t st) {
+        T *d = alloc<T>(count);
+        if (count) cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, st);
+        return d;
+    }
+    void release() {
+        for (void *p : ptrs) cudaFree(p);
+        ptrs.clear();
+    }
+    ~DevArena() { release(); }
+};
+
+struct lc_actor {
+    lc_ctx *ctx = nullptr;
+    DevArena mem;
+    ActorDev dev{};
+    SkelDev skel{};
+    SkelDev *skel_dev = nullptr;
+    std::vector<int> host_edges;      // E*2
+    std::vector<int> host_degrees;    // N
+    std::vector<double> host_wdir;    // 2E
+};
+
+// NN grid buffers for one mask
+struct GridBufs {
+    int *row_count, *row_start, *cell_count, *cell_start, *cell_fill, *cell_pts, *K;
+    int2 *pts;
+};
+
+// per-stream device state + scratch
+struct Slot {
+    DevArena mem;
+    int N = 0, T = 0, E = 0, H = 0, W = 0, levels = 0;
+    // frame inputs
+    double *image = nullptr;          // H*W*3 (own copy)
+    const double *image_src = nullptr; // resident source (own copy or caller's device pointer)
+    uint8_t *mask = nullptr;          // H*W
+    const uint8_t *mask_src = nullptr;
+    double *pyr = nullptr, *blur_tmp = nullptr;
+    GridBufs obs{}, own{};
+    uint8_t *own_mask = nullptr;
+    // detections
+    double *j2d, *j3d_raw, *j3d;
+    uint8_t *v2d, *v3d;
+    int *fallbacks;
+    // state (TrackState)
+    double *x_prev, *x_prev2, *joints_prev, *disp, *v_prev, *v_prev2;
+    bool has_prev = false, has_prev2 = false, has_vprev = false, has_vprev2 = false, has_disp = false;
+    // per-frame
+    double *x, *x0, *drest, *model, *vs, *rot, *vinit, *v;
+    FkState *fk;
+    unsigned long long *zbuf;
+    int *tri_id;
+    uint8_t *tri_front, *vflag, *enabled;
+    double *tri_n, *n2d, *crest;
+    int *cidx, *B, *vis, *P;
+    // surface scratch
+    double *diag, *minv, *rhs, *sx, *sr, *sz, *sp, *sap, *sbest, *edir, *eg, *off0, *off1;
+    uint8_t *hold;
+    // reports (device)
+    lc_pose_report *pose_rep;
+    lc_nonrigid_report *nr_rep;
+    void allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J);
+};
+
+struct lc_field {
+    lc_ctx *ctx = nullptr;
+    DevArena mem;
+    int H = 0, W = 0;
+    uint8_t *mask = nullptr;
+    GridBufs g{};
+    int K = 0;
+};
+
+struct ConfigDev {
+    DevArena mem;
+    EdgeConstDev ec{};
+    SurfHyperDev shp{};
+    PoseHyperDev php{};
+    double *taps = nullptr;   // levels * 32
+    int half[4] = {0, 0, 0, 0};
+    double *probe = nullptr;  // 128*2
+};
+
+struct lc_tracker {
+    lc_ctx *ctx = nullptr;
+    const lc_actor *actor = nullptr;
+    lc_camera cam{};
+    lc_config cfg{};
+    int S = 0;
+    std::vector<Slot *> slots;
+    ConfigDev conf;
+    DevArena mem;
+    // device job arrays (rebuilt when needed)
+    void *jobs_dev = nullptr;
+    size_t jobs_bytes = 0;
+    int frame_counter = 0;
+};

@@ -1,0 +1,575 @@
+// Per-frame setup kernels: blur pyramid, mask contour + NN grid, two-pass
+// rasterizer, FK / DQ skinning, occluding contour vertices, rim filter and
+// body-part gating.  All batched over streams with blockIdx.y (or one CTA per
+// stream where a CTA-wide ordered scan is needed).
+#include <climits>
+#include "lc_kernels.cuh"
+
+// ===========================================================================
+// separable Gaussian, mode "nearest" (scipy.ndimage.convolve1d order: centre
+// tap first, then symmetric pairs from the outermost inward -- verified
+// bit-exact against scipy 1.18.1).  imageproc.py:276-285
+
+__global__ void k_blur_axis(const PyrJob *jobs, int H, int W, int C, const double *taps, int half,
+                            int axis) {
+    const PyrJob J = jobs[blockIdx.y];
+    const double *in = axis == 0 ? J.src : J.tmp;
+    double *out = axis == 0 ? J.tmp : J.dst;
+    const long long n = (long long)H * W * C;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(i % C);
+        const long long pix = i / C;
+        const int x = (int)(pix % W), y = (int)(pix / W);
+        double acc = in[i] * taps[half];
+        if (axis == 0) {
+            for (int j = half; j >= 1; --j) {
+                const int ya = max(y - j, 0), yb = min(y + j, H - 1);
+                acc = acc + (in[((long long)ya * W + x) * C + c] + in[((long long)yb * W + x) * C + c])
+                                * taps[half + j];
+            }
+        } else {
+            for (int j = half; j >= 1; --j) {
+                const int xa = max(x - j, 0), xb = min(x + j, W - 1);
+                acc = acc + (in[((long long)y * W + xa) * C + c] + in[((long long)y * W + xb) * C + c])
+                                * taps[half + j];
+            }
+        }
+        out[i] = acc;
+    }
+}
+
+// ===========================================================================
+// contour pixels of a mask in np.argwhere (row-major) order, then a uniform
+// cell grid over them.  imageproc.py:34-49
+
+__device__ __forceinline__ bool is_contour(const uint8_t *m, int H, int W, int x, int y) {
+    if (!m[y * W + x]) return false;
+    const bool up = y > 0 && m[(y - 1) * W + x];
+    const bool dn = y < H - 1 && m[(y + 1) * W + x];
+    const bool lf = x > 0 && m[y * W + x - 1];
+    const bool rt = x < W - 1 && m[y * W + x + 1];
+    return !(up && dn && lf && rt);
+}
+
+// one block per row: row_count[y]
+__global__ void k_contour_rows(const GridJob *jobs, int H, int W) {
+    const GridJob J = jobs[blockIdx.y];
+    __shared__ int cnt;
+    for (int y = blockIdx.x; y < H; y += gridDim.x) {
+        if (threadIdx.x == 0) cnt = 0;
+        __syncthreads();
+        int local = 0;
+        for (int x = threadIdx.x; x < W; x += blockDim.x) local += is_contour(J.mask, H, W, x, y);
+        for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+        if ((threadIdx.x & 31) == 0 && local) atomicAdd(&cnt, local);
+        __syncthreads();
+        if (threadIdx.x == 0) J.row_count[y] = cnt;
+        __syncthreads();
+    }
+}
+
+// block-wide exclusive scan of n ints (single CTA); returns the total
+template <int NT>
+__device__ int block_exclusive_scan(const int *in, int *out, int n) {
+    __shared__ int warp_tot[NT / 32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n; base += NT) {
+        const int i = base + threadIdx.x;
+        const int v = i < n ? in[i] : 0;
+        int s = v;
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += t;
+        }
+        if (lane == 31) warp_tot[w] = s;
+        __syncthreads();
+        if (w == 0) {
+            int t = lane < NT / 32 ? warp_tot[lane] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += u;
+            }
+            if (lane < NT / 32) warp_tot[lane] = t;
+        }
+        __syncthreads();
+        const int before = (w > 0 ? warp_tot[w - 1] : 0) + carry;
+        if (i < n) out[i] = before + s - v;
+        __syncthreads();
+        if (threadIdx.x == NT - 1) carry = before + s;
+        __syncthreads();
+    }
+    return carry;
+}
+
+__global__ void k_contour_scan_rows(const GridJob *jobs, int H, int ncells) {
+    const GridJob J = jobs[blockIdx.x];
+    const int total = block_exclusive_scan<1024>(J.row_count, J.row_start, H);
+    if (threadIdx.x == 0) {
+        J.row_start[H] = total;
+        *J.K = total;
+    }
+    for (int c = threadIdx.x; c < ncells; c += blockDim.x) {
+        J.cell_count[c] = 0;
+        J.cell_fill[c] = 0;
+    }
+}
+
+// one block per row: ordered emission of (x, y) + per-cell counts
+__global__ void k_contour_emit(const GridJob *jobs, int H, int W, int ncx) {
+    const GridJob J = jobs[blockIdx.y];
+    __shared__ int wsum[32];
+    __shared__ int carry;
+    for (int y = blockIdx.x; y < H; y += gridDim.x) {
+        if (threadIdx.x == 0) carry = J.row_start[y];
+        __syncthreads();
+        for (int base = 0; base < W; base += blockDim.x) {
+            const int x = base + threadIdx.x;
+            const bool f = x < W && is_contour(J.mask, H, W, x, y);
+            const unsigned bal = __ballot_sync(0xffffffffu, f);
+            const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+            if (lane == 0) wsum[w] = __popc(bal);
+            __syncthreads();
+            int before = carry;
+            for (int k = 0; k < w; ++k) before += wsum[k];
+            if (f) {
+                const int slot = before + __popc(bal & ((1u << lane) - 1u));
+                J.pts[slot] = make_int2(x, y);
+                atomicAdd(&J.cell_count[(y >> LC_GRID_SHIFT) * ncx + (x >> LC_GRID_SHIFT)], 1);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int t = 0;
+                for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += wsum[k];
+                carry += t;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void k_contour_scan_cells(const GridJob *jobs, int ncells) {
+    const GridJob J = jobs[blockIdx.x];
+    const int total = block_exclusive_scan<1024>(J.cell_count, J.cell_start, ncells);
+    if (threadIdx.x == 0) J.cell_start[ncells] = total;
+}
+
+__global__ void k_contour_fill(const GridJob *jobs, int ncx) {
+    const GridJob J = jobs[blockIdx.y];
+    const int K = *J.K;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
+        const int2 p = J.pts[k];
+        const int c = (p.y >> LC_GRID_SHIFT) * ncx + (p.x >> LC_GRID_SHIFT);
+        const int s = atomicAdd(&J.cell_fill[c], 1);
+        J.cell_pts[J.cell_start[c] + s] = k;
+    }
+}
+
+// ===========================================================================
+// rasterizer.  The reference draws triangles sequentially and keeps the first
+// strictly-smaller depth (rasterizer.py:46-58).  Pass 1 finds the minimum
+// depth per pixel (atomicMin on the fp64 bit pattern: depths are positive);
+// pass 2 picks the lowest triangle index attaining it; the resolve pass
+// recomputes that triangle's barycentrics.  Same arithmetic, same order.
+
+__device__ __forceinline__ bool tri_setup(CamDev cam, const double *V, const int *tris, int t,
+                                          double P[3][2], double D[3], double &inv, int bb[4]) {
+    const int ids[3] = {tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]};
+    for (int k = 0; k < 3; ++k) {
+        const V3 p = ld3(V + 3 * (size_t)ids[k]);
+        double px, py;
+        const bool ok = project(cam, p, px, py);
+        P[k][0] = px;
+        P[k][1] = py;
+        D[k] = ok ? p.z : -1.0;
+    }
+    if (D[0] <= 0.0 || D[1] <= 0.0 || D[2] <= 0.0) return false;
+    const double area = (P[1][0] - P[0][0]) * (P[2][1] - P[0][1]) - (P[2][0] - P[0][0]) * (P[1][1] - P[0][1]);
+    if (area > -1e-12 && area < 1e-12) return false;
+    inv = 1.0 / area;
+    const double lx = fmin(P[0][0], fmin(P[1][0], P[2][0])), hx = fmax(P[0][0], fmax(P[1][0], P[2][0]));
+    const double ly = fmin(P[0][1], fmin(P[1][1], P[2][1])), hy = fmax(P[0][1], fmax(P[1][1], P[2][1]));
+    double x0 = floor(lx), x1 = ceil(hx), y0 = floor(ly), y1 = ceil(hy);
+    x0 = fmax(x0, 0.0); y0 = fmax(y0, 0.0);
+    x1 = fmin(x1, (double)(cam.W - 1)); y1 = fmin(y1, (double)(cam.H - 1));
+    if (!(x0 <= x1 && y0 <= y1)) return false;
+    bb[0] = (int)x0; bb[1] = (int)x1; bb[2] = (int)y0; bb[3] = (int)y1;
+    return true;
+}
+
+__device__ __forceinline__ bool bary(const double P[3][2], double inv, int ix, int iy, double &l0,
+                                     double &l1, double &l2) {
+    const double px = (double)ix, py = (double)iy;
+    l0 = ((P[1][0] - px) * (P[2][1] - py) - (P[2][0] - px) * (P[1][1] - py)) * inv;
+    l1 = ((px - P[0][0]) * (P[2][1] - P[0][1]) - (P[2][0] - P[0][0]) * (py - P[0][1])) * inv;
+    l2 = 1.0 - l0 - l1;
+    return !(l0 < 0.0 || l1 < 0.0 || l2 < 0.0);
+}
+
+__global__ void k_raster_clear(const RasterJob *jobs, int HW) {
+    const RasterJob J = jobs[blockIdx.y];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += gridDim.x * blockDim.x) {
+        J.zbuf[i] = 0x7ff0000000000000ULL;
+        J.tri_id[i] = INT_MAX;
+    }
+}
+
+__global__ void k_raster_depth(const RasterJob *jobs, CamDev cam, const int *tris, int T) {
+    const RasterJob J = jobs[blockIdx.y];
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    double P[3][2], D[3], inv;
+    int bb[4];
+    if (!tri_setup(cam, J.verts, tris, t, P, D, inv, bb)) return;
+    for (int y = bb[2]; y <= bb[3]; ++y)
+        for (int x = bb[0]; x <= bb[1]; ++x) {
+            double l0, l1, l2;
+            if (!bary(P, inv, x, y, l0, l1, l2)) continue;
+            const double z = l0 * D[0] + l1 * D[1] + l2 * D[2];
+            const unsigned long long zb = (unsigned long long)__double_as_longlong(z);
+            unsigned long long *dst = J.zbuf + (size_t)y * cam.W + x;
+            if (zb < *dst) atomicMin(dst, zb);
+        }
+}
+
+__global__ void k_raster_winner(const RasterJob *jobs, CamDev cam, const int *tris, int T) {
+    const RasterJob J = jobs[blockIdx.y];
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    double P[3][2], D[3], inv;
+    int bb[4];
+    if (!tri_setup(cam, J.verts, tris, t, P, D, inv, bb)) return;
+    for (int y = bb[2]; y <= bb[3]; ++y)
+        for (int x = bb[0]; x <= bb[1]; ++x) {
+            double l0, l1, l2;
+            if (!bary(P, inv, x, y, l0, l1, l2)) continue;
+            const double z = l0 * D[0] + l1 * D[1] + l2 * D[2];
+            const size_t pi = (size_t)y * cam.W + x;
+            if ((unsigned long long)__double_as_longlong(z) == J.zbuf[pi] && t < J.tri_id[pi])
+                atomicMin(J.tri_id + pi, t);
+        }
+}
+
+__global__ void k_raster_mask(const RasterJob *jobs, int HW) {
+    const RasterJob J = jobs[blockIdx.y];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += gridDim.x * blockDim.x)
+        J.mask[i] = J.zbuf[i] != 0x7ff0000000000000ULL;
+}
+
+// attributes / ids of the winning triangle (mode 1 / 2, rasterizer.py:58-68)
+__device__ __forceinline__ int id_pick(double l0, double l1, double l2) {
+    if (l0 >= l1 && l0 >= l2) return 0;
+    if (l1 >= l2) return 1;
+    return 2;
+}
+
+__global__ void k_raster_resolve(const RasterJob *jobs, CamDev cam, const int *tris, int mode,
+                                 const double *attrs, int n_attr, const int *ids, double bg_attr,
+                                 long long bg_id, double *zout, double *aout, long long *iout) {
+    const RasterJob J = jobs[blockIdx.y];
+    const int HW = cam.W * cam.H;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += gridDim.x * blockDim.x) {
+        zout[i] = __longlong_as_double((long long)J.zbuf[i]);
+        const int t = J.tri_id[i];
+        if (mode == 0) continue;
+        if (t == INT_MAX) {
+            if (mode == 1)
+                for (int k = 0; k < n_attr; ++k) aout[(size_t)i * n_attr + k] = bg_attr;
+            else
+                iout[i] = bg_id;
+            continue;
+        }
+        double P[3][2], D[3], inv;
+        int bb[4];
+        tri_setup(cam, J.verts, tris, t, P, D, inv, bb);
+        double l0, l1, l2;
+        bary(P, inv, i % cam.W, i / cam.W, l0, l1, l2);
+        const int v0 = tris[3 * t], v1 = tris[3 * t + 1], v2 = tris[3 * t + 2];
+        if (mode == 1) {
+            for (int k = 0; k < n_attr; ++k)
+                aout[(size_t)i * n_attr + k] = l0 * attrs[(size_t)v0 * n_attr + k]
+                                             + l1 * attrs[(size_t)v1 * n_attr + k]
+                                             + l2 * attrs[(size_t)v2 * n_attr + k];
+        } else {
+            const int w = id_pick(l0, l1, l2);
+            iout[i] = ids[w == 0 ? v0 : (w == 1 ? v1 : v2)];
+        }
+    }
+}
+
+// ===========================================================================
+// kinematics / skinning
+
+__global__ void k_fk(const FkJob *jobs, const SkelDev *sk) {
+    const FkJob J = jobs[blockIdx.x];
+    if (!J.active) return;
+    __shared__ FkState f;
+    fk_warp(*sk, J.x, f);
+    // copy out (plain struct of doubles/ints)
+    const double *src = reinterpret_cast<const double *>(&f);
+    double *dst = reinterpret_cast<double *>(J.fk);
+    const int nd = (int)(sizeof(FkState) / sizeof(double));
+    for (int i = threadIdx.x; i < nd; i += blockDim.x) dst[i] = src[i];
+}
+
+struct GlobalDq {
+    const FkState *f;
+    __device__ __forceinline__ double operator()(int j, int k) const { return f->dq[j][k]; }
+};
+
+__global__ void k_skin(const SkinJob *jobs, ActorDev A) {
+    const SkinJob J = jobs[blockIdx.y];
+    if (!J.active) return;
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= J.M) return;
+    const int v = J.subset ? J.subset[m] : m;
+    V3 r = ld3(J.rest + 3 * (size_t)m);
+    if (J.disp) r = r + ld3(J.disp + 3 * (size_t)m);
+    Blend B;
+    dq_blend(A.skin_idx + 4 * v, A.skin_w + 4 * v, A.dominant[v], GlobalDq{J.fk}, B);
+    Q4 cr;
+    const V3 p = dq_apply(B, r, cr);
+    st3(J.pos + 3 * (size_t)m, p);
+    if (J.rot) {
+        double *q = J.rot + 4 * (size_t)m;
+        q[0] = cr.w; q[1] = cr.x; q[2] = cr.y; q[3] = cr.z;
+    }
+}
+
+// ===========================================================================
+// occluding contour vertices (extract_contour_vertices, pose_stage.py:151-191)
+
+__global__ void k_tri_front(const ContourJob *jobs, ActorDev A) {
+    const ContourJob J = jobs[blockIdx.y];
+    if (!J.active) return;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < A.T; t += gridDim.x * blockDim.x) {
+        const V3 p0 = ld3(J.verts + 3 * (size_t)A.tris[3 * t]);
+        const V3 p1 = ld3(J.verts + 3 * (size_t)A.tris[3 * t + 1]);
+        const V3 p2 = ld3(J.verts + 3 * (size_t)A.tris[3 * t + 2]);
+        const V3 n = cross3(p1 - p0, p2 - p0);
+        const V3 c = v3(((p0.x + p1.x) + p2.x) / 3.0, ((p0.y + p1.y) + p2.y) / 3.0,
+                        ((p0.z + p1.z) + p2.z) / 3.0);
+        J.tri_front[t] = dot3(n, c) < 0.0;
+        st3(J.tri_n + 3 * (size_t)t, n);
+    }
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < A.N; v += gridDim.x * blockDim.x)
+        J.vflag[v] = 0;
+}
+
+__global__ void k_sil_edges(const ContourJob *jobs, ActorDev A) {
+    const ContourJob J = jobs[blockIdx.y];
+    if (!J.active) return;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < A.E; e += gridDim.x * blockDim.x) {
+        const int ta = A.edge_tris[2 * e], tb = A.edge_tris[2 * e + 1];
+        const bool sil = tb < 0 ? J.tri_front[ta] != 0 : (J.tri_front[ta] != J.tri_front[tb]);
+        if (sil) {
+            J.vflag[A.edges[2 * e]] = 1;
+            J.vflag[A.edges[2 * e + 1]] = 1;
+        }
+    }
+}
+
+// z <= zbuf[rint(pix)] + 0.01 z  with in-image test (pose_stage.py:175-181,
+// nonrigid_stage.py:93-99)
+__device__ __forceinline__ bool depth_visible(CamDev cam, const unsigned long long *zbuf, V3 p) {
+    double px, py;
+    const bool ok = project(cam, p, px, py);
+    const double xr = fmin(fmax(rint(px), 0.0), (double)(cam.W - 1));
+    const double yr = fmin(fmax(rint(py), 0.0), (double)(cam.H - 1));
+    const bool inimg = px >= -0.5 && px <= cam.W - 0.5 && py >= -0.5 && py <= cam.H - 0.5;
+    const double zb = __longlong_as_double((long long)zbuf[(size_t)yr * cam.W + (size_t)xr]);
+    return ok && inimg && (p.z <= zb + 0.01 * p.z);
+}
+
+// one CTA per stream: ordered compaction of contour candidates (np.unique
+// order = ascending vertex id) and, optionally, of visible vertices; then the
+// image-plane normals of the contour vertices.
+__global__ void __launch_bounds__(1024) k_contour_compact(const ContourJob *jobs, ActorDev A,
+                                                          CamDev cam) {
+    const ContourJob J = jobs[blockIdx.x];
+    if (!J.active) return;
+    __shared__ int wsum[32];
+    __shared__ int carry[2];
+    if (threadIdx.x == 0) carry[0] = carry[1] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int base = 0; base < A.N; base += blockDim.x) {
+        const int v = base + threadIdx.x;
+        bool vis = false;
+        if (v < A.N) vis = depth_visible(cam, J.zbuf, ld3(J.verts + 3 * (size_t)v));
+        for (int list = 0; list < 2; ++list) {
+            if (list == 1 && !J.vis) break;
+            const bool f = v < A.N && vis && (list == 1 || J.vflag[v]);
+            const unsigned bal = __ballot_sync(0xffffffffu, f);
+            if (lane == 0) wsum[w] = __popc(bal);
+            __syncthreads();
+            int before = carry[list];
+            for (int k = 0; k < w; ++k) before += wsum[k];
+            if (f) {
+                const int slot = before + __popc(bal & ((1u << lane) - 1u));
+                (list == 0 ? J.idx : J.vis)[slot] = v;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int t = 0;
+                for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += wsum[k];
+                carry[list] += t;
+            }
+            __syncthreads();
+        }
+    }
+    const int B = carry[0];
+    if (threadIdx.x == 0) {
+        *J.B = B;
+        if (J.P) *J.P = carry[1];
+    }
+    // vertex normals: area-weighted, accumulated in np.add.at slot order
+    // (pose_stage.py:139-148), projected with d(pix)/d(p), normalized
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+        const int v = J.idx[b];
+        V3 n = v3(0, 0, 0);
+        for (int k = A.vt_ptr[v]; k < A.vt_ptr[v + 1]; ++k) n = n + ld3(J.tri_n + 3 * (size_t)A.vt_tri[k]);
+        double nn = norm3(n);
+        if (nn < 1e-12) nn = 1.0;
+        n = v3(n.x / nn, n.y / nn, n.z / nn);
+        double a0, a2, b1, b2;
+        proj_jac(cam, ld3(J.verts + 3 * (size_t)v), a0, a2, b1, b2);
+        double u = a0 * n.x + 0.0 * n.y + a2 * n.z;
+        double q = 0.0 * n.x + b1 * n.y + b2 * n.z;
+        const double l = sqrt(u * u + q * q);
+        if (l > 1e-12) { u = u / l; q = q / l; } else { u = 0.0; q = 0.0; }
+        J.n2d[2 * b] = u;
+        J.n2d[2 * b + 1] = q;
+    }
+}
+
+// ===========================================================================
+// outer-rim filter (outer_rim_mask, pose_stage.py:218-264) and, for Stage II,
+// the body-part gate (pipeline.py:241-249 with build_body_part_mask,
+// nonrigid_stage.py:102-128).  One warp per contour vertex.
+
+#define LC_MAX_PARTS 16
+
+// part id of the max-barycentric vertex of the winning triangle at (x, y); 0 = background
+__device__ __forceinline__ int part_at(const ActorDev &A, CamDev cam, const double *verts,
+                                       const int *tri_id, int x, int y) {
+    const int t = tri_id[(size_t)y * cam.W + x];
+    if (t == INT_MAX) return 0;
+    double P[3][2], D[3], inv;
+    int bb[4];
+    tri_setup(cam, verts, A.tris, t, P, D, inv, bb);
+    double l0, l1, l2;
+    bary(P, inv, x, y, l0, l1, l2);
+    const int w = id_pick(l0, l1, l2);
+    return A.vpart[A.tris[3 * t + w]];
+}
+
+__global__ void k_rim(const RimJob *jobs, ActorDev A, CamDev cam, const double *probe_offs) {
+    const RimJob J = jobs[blockIdx.y];
+    if (!J.active) return;
+    const int B = *J.B;
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    NnGridDev own = J.own;
+    own.K = *J.ownK;
+    for (int b = blockIdx.x * wpb + (threadIdx.x >> 5); b < B; b += gridDim.x * wpb) {
+        const int v = J.idx[b];
+        const V3 p = ld3(J.verts + 3 * (size_t)v);
+        double px, py;
+        const bool ok = project(cam, p, px, py);
+        bool keep = false;
+        if (own.K > 0) {
+            const NnResult n = field_nearest(own, px, py);
+            keep = ok && !n.clamped && n.dist <= 1.5;
+        }
+        if (J.stage1) {
+            if (keep) {
+                // 16 directions x radii 1..8: depth = max over interior probes
+                double deep = 0.0;
+                for (int k = lane; k < 128; k += 32) {
+                    const double qx = px + probe_offs[2 * k], qy = py + probe_offs[2 * k + 1];
+                    const NnResult n = field_nearest(own, qx, qy);
+                    const double d = field_inside(own, qx, qy) ? n.dist : 0.0;
+                    deep = fmax(deep, d);
+                }
+                for (int o = 16; o > 0; o >>= 1) deep = fmax(deep, __shfl_xor_sync(0xffffffffu, deep, o));
+                keep = 2.0 * deep >= 12.0;
+            }
+            keep = keep && A.rigidity[v] >= 2.0;
+        } else if (J.part_gate) {
+            // label image value at rint(pix) clipped into the image
+            const int xi = (int)fmin(fmax(rint(px), 0.0), (double)(cam.W - 1));
+            const int yi = (int)fmin(fmax(rint(py), 0.0), (double)(cam.H - 1));
+            int label = part_at(A, cam, J.verts, J.tri_id, xi, yi);
+            if (label == 0) {
+                // bounded dilation: nearest part pixel per part within `dilation`
+                const int R = J.dilation;
+                int best[LC_MAX_PARTS];
+                for (int q = 0; q < LC_MAX_PARTS; ++q) best[q] = INT_MAX;
+                const int side = 2 * R + 1;
+                for (int k = lane; k < side * side; k += 32) {
+                    const int dx = k % side - R, dy = k / side - R;
+                    const int x = xi + dx, y = yi + dy;
+                    if (x < 0 || y < 0 || x >= cam.W || y >= cam.H) continue;
+                    const int d2 = dx * dx + dy * dy;
+                    if (d2 > R * R) continue;
+                    const int pp = part_at(A, cam, J.verts, J.tri_id, x, y);
+                    if (pp > 0 && pp < LC_MAX_PARTS && d2 < best[pp]) best[pp] = d2;
+                }
+                for (int q = 1; q < LC_MAX_PARTS; ++q)
+                    for (int o = 16; o > 0; o >>= 1)
+                        best[q] = min(best[q], __shfl_xor_sync(0xffffffffu, best[q], o));
+                int arg = 0, bd = INT_MAX;
+                for (int q = 1; q < LC_MAX_PARTS; ++q)
+                    if (best[q] < bd) { bd = best[q]; arg = q; }   // lowest id on ties
+                label = arg;
+                if (best[1] != INT_MAX) label = 1;                // torso override (TORSO_PART = 1)
+            }
+            keep = keep && ok && (label == 0 || label == A.vpart[v]);
+        }
+        if (lane == 0) J.keep[b] = keep;
+    }
+}
+
+// (M,3,36) skinning Jacobian for the lc_skin_points seam (skin_points with
+// dq_jacobian, skinning.py:391-397); the per-joint DQ Jacobian columns are
+// recomputed from the FK state on the fly.
+__global__ void k_skin_jac(const FkState *fk, const SkelDev *skg, ActorDev A, int M, const double *rest,
+                           const int *subset, double *jac) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    const SkelDev &sk = *skg;
+    const int v = subset ? subset[m] : m;
+    const V3 r = ld3(rest + 3 * (size_t)m);
+    Blend B;
+    dq_blend(A.skin_idx + 4 * v, A.skin_w + 4 * v, A.dominant[v], GlobalDq{fk}, B);
+    double dv[3][8];
+    dq_dtransform(B, r, dv);
+    for (int q = 0; q < LC_NP; ++q) {
+        double db[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const int nsl = B.degenerate ? 1 : 4;
+        for (int sl = 0; sl < nsl; ++sl) {
+            const int j = B.degenerate ? B.dom : B.js[sl];
+            const double cf = B.degenerate ? 1.0 : B.coef[sl];
+            double col[8];
+            if (q >= 3 && q < 6) {
+                const Q4 d = dq_trans(*fk, j, q - 3);
+                col[0] = col[1] = col[2] = col[3] = 0.0;
+                col[4] = d.w; col[5] = d.x; col[6] = d.y; col[7] = d.z;
+            } else if (q >= 33) {
+                for (int k = 0; k < 8; ++k) col[k] = 0.0;
+            } else {
+                dq_spin(sk, *fk, j, q < 3 ? q : q - 3, col);
+            }
+            for (int k = 0; k < 8; ++k) db[k] += cf * col[k];
+        }
+        for (int i = 0; i < 3; ++i) {
+            double a = 0.0;
+            for (int k = 0; k < 8; ++k) a += dv[i][k] * db[k];
+            jac[((size_t)m * 3 + i) * LC_NP + q] = a;
+        }
+    }
+}

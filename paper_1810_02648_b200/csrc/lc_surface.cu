@@ -1,0 +1,493 @@
+// Stage II: per-vertex non-rigid Gauss-Newton, one persistent CTA per stream.
+//
+// Reference: NonrigidProblem.evaluate / normal_system (nonrigid_stage.py:
+// 189-304), pcg_solve (solvers.py:104-145), solve_nonrigid (:372-403) and
+// snap_vertices (:417-500).
+//
+// The normal system is kept in compact matrix-free form:
+//   diag_i  = Jp_i^T Jp_i + g_i g_i^T + sum_{e ni i} (a_e I + b_e d_e d_e^T) + (cv^2+ca^2) I
+//   A_ij    = -(a_e I + b_e d_e d_e^T)           for every mesh edge e = {i, j}
+// with a_e = cs_fwd^2 + cs_rev^2 and b_e = ce_fwd^2 + ce_rev^2 per-config
+// constants and d_e the current unit edge direction.  Every CTA-wide sum is a
+// fixed-order tree (deterministic); there are no atomics.
+#include "lc_pose.cuh"
+
+namespace {
+
+constexpr int NT = 512;
+
+struct SurfCtx {
+    const SurfJob *J;
+    NnGridDev obs;
+    ActorDev A;
+    CamDev cam;
+    EdgeConstDev ec;
+    SurfHyperDev hp;
+    int H, W, P, B, N, E;
+    bool has_prev;
+    bool sil_on;
+    double *red;
+};
+
+__device__ __forceinline__ V3 trial_pos(const double *v, const double *step, int i) {
+    const V3 a = ld3(v + 3 * (size_t)i);
+    if (!step) return a;
+    return a + ld3(step + 3 * (size_t)i);
+}
+
+// photometric row of visible vertex i at position p (nonrigid_stage.py:196-213)
+struct PhotoRow { double r[3], J[3][3]; bool behind, pruned; };
+
+__device__ __forceinline__ void photo_row(const SurfCtx &c, const double *img, int i, V3 p,
+                                          bool with_jac, PhotoRow &o) {
+    double px, py;
+    const bool ok = project(c.cam, p, px, py);
+    double val[3], gx[3], gy[3];
+    const bool cl = bilinear3(img, c.W, c.H, px, py, val, gx, gy);
+    const double *col = c.A.colors + 3 * (size_t)i;
+    const double d0 = val[0] - col[0], d1 = val[1] - col[1], d2 = val[2] - col[2];
+    const bool prune = sqrt(d0 * d0 + d1 * d1 + d2 * d2) > c.hp.tau;
+    o.pruned = prune && ok && !cl;
+    o.behind = !ok;
+    const double w = sqrt(c.hp.w_photo) * ((ok && !cl && !prune) ? 1.0 : 0.0);
+    o.r[0] = d0 * w; o.r[1] = d1 * w; o.r[2] = d2 * w;
+    if (with_jac) {
+        double a0, a2, b1, b2;
+        proj_jac(c.cam, p, a0, a2, b1, b2);
+        for (int ch = 0; ch < 3; ++ch) {
+            o.J[ch][0] = (gx[ch] * a0 + gy[ch] * 0.0) * w;
+            o.J[ch][1] = (gx[ch] * 0.0 + gy[ch] * b1) * w;
+            o.J[ch][2] = (gx[ch] * a2 + gy[ch] * b2) * w;
+        }
+    }
+}
+
+// silhouette row of boundary slot b (nonrigid_stage.py:215-233)
+struct SilRow { double r, g[3]; bool behind; };
+
+__device__ __forceinline__ void sil_row(const SurfCtx &c, int b, V3 p, bool with_jac, SilRow &o) {
+    const SurfJob &J = *c.J;
+    double px, py;
+    const bool ok = project(c.cam, p, px, py);
+    o.behind = !ok;
+    const NnResult nn = field_nearest(c.obs, px, py);
+    double val, gx, gy;
+    field_residual(nn, val, gx, gy);
+    const double w = sqrt(c.hp.w_sil) * ((ok && !nn.clamped && J.enabled[b]) ? 1.0 : 0.0);
+    o.r = val * w;
+    if (with_jac) {
+        double a0, a2, b1, b2;
+        proj_jac(c.cam, p, a0, a2, b1, b2);
+        const double sign = J.directional ? side_sign(c.obs, nn, px, py, J.n2d[2 * b], J.n2d[2 * b + 1]) : 1.0;
+        const double sc = w * sign;
+        o.g[0] = (gx * a0 + gy * 0.0) * sc;
+        o.g[1] = (gx * 0.0 + gy * b1) * sc;
+        o.g[2] = (gx * a2 + gy * b2) * sc;
+    }
+}
+
+// per-edge quantities at the (trial) positions
+struct EdgeQ { V3 u, d; double len_err; bool degenerate; double e_smooth, e_edge; };
+
+__device__ __forceinline__ void edge_q(const SurfCtx &c, int e, const double *v, const double *step,
+                                       EdgeQ &q) {
+    const int a = c.A.edges[2 * e], b = c.A.edges[2 * e + 1];
+    const V3 ev = trial_pos(v, step, a) - trial_pos(v, step, b);
+    const V3 sd = ld3(c.J->vs + 3 * (size_t)a) - ld3(c.J->vs + 3 * (size_t)b);
+    q.u = ev - sd;
+    const double len = norm3(ev);
+    q.degenerate = len < 1e-9;
+    if (q.degenerate) q.d = ld3(c.A.rest_dir + 3 * (size_t)e);
+    else {
+        const double l = fmax(len, 1e-300);
+        q.d = v3(ev.x / l, ev.y / l, ev.z / l);
+    }
+    q.len_err = len - c.A.rest_len[e];
+    const double sf = c.ec.cs_f[e], sr = c.ec.cs_r[e], ef = c.ec.ce_f[e], er = c.ec.ce_r[e];
+    const double ux = q.u.x, uy = q.u.y, uz = q.u.z;
+    q.e_smooth = (ux * sf) * (ux * sf) + (uy * sf) * (uy * sf) + (uz * sf) * (uz * sf)
+               + (ux * sr) * (ux * sr) + (uy * sr) * (uy * sr) + (uz * sr) * (uz * sr);
+    q.e_edge = (q.len_err * ef) * (q.len_err * ef) + (q.len_err * er) * (q.len_err * er);
+}
+
+// energies at v (+ step): photo, sil, smooth, edge, vel, acc
+__device__ void surf_energy(const SurfCtx &c, int level, const double *v, const double *step,
+                            double en[6]) {
+    const SurfJob &J = *c.J;
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const double *img = J.pyr + (size_t)level * c.H * c.W * 3;
+    if (J.enable_photo)
+        for (int k = threadIdx.x; k < c.P; k += NT) {
+            const int i = J.vis[k];
+            PhotoRow o;
+            photo_row(c, img, i, trial_pos(v, step, i), false, o);
+            acc[0] += o.r[0] * o.r[0] + o.r[1] * o.r[1] + o.r[2] * o.r[2];
+        }
+    if (c.sil_on)
+        for (int b = threadIdx.x; b < c.B; b += NT) {
+            SilRow o;
+            sil_row(c, b, trial_pos(v, step, J.bidx[b]), false, o);
+            acc[1] += o.r * o.r;
+        }
+    for (int e = threadIdx.x; e < c.E; e += NT) {
+        EdgeQ q;
+        edge_q(c, e, v, step, q);
+        acc[2] += q.e_smooth;
+        acc[3] += q.e_edge;
+    }
+    if (c.has_prev) {
+        const double cv = sqrt(c.hp.w_vel), ca = sqrt(c.hp.w_acc);
+        for (int i = threadIdx.x; i < c.N; i += NT) {
+            const V3 p = trial_pos(v, step, i);
+            const V3 q1 = ld3(J.prev + 3 * (size_t)i);
+            const V3 q2 = J.prev2 ? ld3(J.prev2 + 3 * (size_t)i) : q1;
+            const V3 vr = (p - q1) * cv;
+            const V3 ar = ((p - 2.0 * q1) + q2) * ca;
+            acc[4] += vr.x * vr.x + vr.y * vr.y + vr.z * vr.z;
+            acc[5] += ar.x * ar.x + ar.y * ar.y + ar.z * ar.z;
+        }
+    }
+    block_sums<NT, 8>(acc, c.red);
+    for (int k = 0; k < 6; ++k) en[k] = acc[k];
+}
+
+__device__ __forceinline__ double total_energy(const double en[6], bool has_prev) {
+    double t = ((en[0] + en[1]) + en[2]) + en[3];
+    if (has_prev) t = (t + en[4]) + en[5];
+    return t;
+}
+
+// GN evaluation with the normal system (diag, minv, rhs, edir); returns energies + counters
+__device__ void surf_assemble(const SurfCtx &c, int level, const double *v, double en[6],
+                              int counts[3]) {
+    const SurfJob &J = *c.J;
+    const double cv = sqrt(c.hp.w_vel), ca = sqrt(c.hp.w_acc);
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // 6 energies, pruned, behind
+    double degen = 0.0;
+    // P0: clear data blocks; per-edge direction + gradient contribution
+    for (int i = threadIdx.x; i < c.N; i += NT) {
+        double *dg = J.diag + 6 * (size_t)i;
+        for (int k = 0; k < 6; ++k) dg[k] = 0.0;
+        st3(J.rhs + 3 * (size_t)i, v3(0, 0, 0));
+    }
+    for (int e = threadIdx.x; e < c.E; e += NT) {
+        EdgeQ q;
+        edge_q(c, e, v, nullptr, q);
+        acc[2] += q.e_smooth;
+        acc[3] += q.e_edge;
+        degen += q.degenerate ? 2.0 : 0.0;
+        st3(J.edir + 3 * (size_t)e, q.d);
+        const double al = c.ec.alpha[e], be = c.ec.beta[e];
+        st3(J.eg + 3 * (size_t)e, al * q.u + be * (q.len_err * q.d));
+    }
+    __syncthreads();
+    // P1: photometric data blocks (visible ids are unique)
+    const double *img = J.pyr + (size_t)level * c.H * c.W * 3;
+    if (J.enable_photo)
+        for (int k = threadIdx.x; k < c.P; k += NT) {
+            const int i = J.vis[k];
+            PhotoRow o;
+            photo_row(c, img, i, ld3(v + 3 * (size_t)i), true, o);
+            acc[0] += o.r[0] * o.r[0] + o.r[1] * o.r[1] + o.r[2] * o.r[2];
+            acc[6] += o.pruned ? 1.0 : 0.0;
+            acc[7] += o.behind ? 1.0 : 0.0;
+            double *dg = J.diag + 6 * (size_t)i;
+            const int map[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+            for (int m = 0; m < 6; ++m) {
+                const int a = map[m][0], b = map[m][1];
+                dg[m] = o.J[0][a] * o.J[0][b] + o.J[1][a] * o.J[1][b] + o.J[2][a] * o.J[2][b];
+            }
+            double *rh = J.rhs + 3 * (size_t)i;
+            for (int a = 0; a < 3; ++a)
+                rh[a] = -(o.J[0][a] * o.r[0] + o.J[1][a] * o.r[1] + o.J[2][a] * o.r[2]);
+        }
+    __syncthreads();
+    // P2: silhouette rank-1 blocks (boundary ids are unique)
+    if (c.sil_on)
+        for (int b = threadIdx.x; b < c.B; b += NT) {
+            const int i = J.bidx[b];
+            SilRow o;
+            sil_row(c, b, ld3(v + 3 * (size_t)i), true, o);
+            acc[1] += o.r * o.r;
+            acc[7] += o.behind ? 1.0 : 0.0;
+            double *dg = J.diag + 6 * (size_t)i;
+            dg[0] += o.g[0] * o.g[0]; dg[1] += o.g[0] * o.g[1]; dg[2] += o.g[0] * o.g[2];
+            dg[3] += o.g[1] * o.g[1]; dg[4] += o.g[1] * o.g[2]; dg[5] += o.g[2] * o.g[2];
+            double *rh = J.rhs + 3 * (size_t)i;
+            rh[0] += -o.g[0] * o.r; rh[1] += -o.g[1] * o.r; rh[2] += -o.g[2] * o.r;
+        }
+    __syncthreads();
+    // P3: full diagonal blocks, rhs, Jacobi preconditioner, temporal energies
+    for (int i = threadIdx.x; i < c.N; i += NT) {
+        double dg[6];
+        for (int k = 0; k < 6; ++k) dg[k] = J.diag[6 * (size_t)i + k];
+        V3 rh = ld3(J.rhs + 3 * (size_t)i);
+        for (int k = c.A.adj_ptr[i]; k < c.A.adj_ptr[i + 1]; ++k) {
+            const int e = c.A.adj_edge[k];
+            const V3 d = ld3(J.edir + 3 * (size_t)e);
+            const double al = c.ec.alpha[e], be = c.ec.beta[e];
+            dg[0] += al + be * (d.x * d.x); dg[1] += be * (d.x * d.y); dg[2] += be * (d.x * d.z);
+            dg[3] += al + be * (d.y * d.y); dg[4] += be * (d.y * d.z); dg[5] += al + be * (d.z * d.z);
+            const V3 g = ld3(J.eg + 3 * (size_t)e);
+            rh = (c.A.edges[2 * e] == i) ? rh - g : rh + g;
+        }
+        if (c.has_prev) {
+            const double cc = cv * cv + ca * ca;
+            dg[0] += cc; dg[3] += cc; dg[5] += cc;
+            const V3 p = ld3(v + 3 * (size_t)i);
+            const V3 q1 = ld3(J.prev + 3 * (size_t)i);
+            const V3 q2 = J.prev2 ? ld3(J.prev2 + 3 * (size_t)i) : q1;
+            const V3 vr = (p - q1) * cv;
+            const V3 ar = ((p - 2.0 * q1) + q2) * ca;
+            acc[4] += vr.x * vr.x + vr.y * vr.y + vr.z * vr.z;
+            acc[5] += ar.x * ar.x + ar.y * ar.y + ar.z * ar.z;
+            rh = rh - (cv * vr + ca * ar);
+        }
+        for (int k = 0; k < 6; ++k) J.diag[6 * (size_t)i + k] = dg[k];
+        st3(J.rhs + 3 * (size_t)i, rh);
+        double mi[6];
+        if (!sym3_inverse(dg, mi))
+            for (int k = 0; k < 6; ++k) mi[k] = 0.0;  // pinv of an all-zero block
+        for (int k = 0; k < 6; ++k) J.minv[6 * (size_t)i + k] = mi[k];
+    }
+    block_sums<NT, 8>(acc, c.red);
+    for (int k = 0; k < 6; ++k) en[k] = acc[k];
+    counts[0] = (int)acc[6];
+    counts[2] = (int)acc[7];
+    double dd[1] = {degen};
+    block_sums<NT, 1>(dd, c.red);
+    counts[1] = (int)dd[0];
+}
+
+// block-Jacobi PCG from zero, best-residual iterate (solvers.py:104-145)
+__device__ bool surf_pcg(const SurfCtx &c, int iters) {
+    const SurfJob &J = *c.J;
+    double part[2] = {0, 0};
+    for (int i = threadIdx.x; i < c.N; i += NT) {
+        const V3 r = ld3(J.rhs + 3 * (size_t)i);
+        const V3 z = sym3_mul(J.minv + 6 * (size_t)i, r);
+        st3(J.x + 3 * (size_t)i, v3(0, 0, 0));
+        st3(J.best + 3 * (size_t)i, v3(0, 0, 0));
+        st3(J.r + 3 * (size_t)i, r);
+        st3(J.z + 3 * (size_t)i, z);
+        st3(J.p + 3 * (size_t)i, z);
+        part[0] += r.x * z.x + r.y * z.y + r.z * z.z;
+        part[1] += r.x * r.x + r.y * r.y + r.z * r.z;
+    }
+    block_sums<NT, 2>(part, c.red);
+    double rz = part[0];
+    double best_norm = sqrt(part[1]);
+    bool breakdown = false;
+    for (int it = 0; it < iters; ++it) {
+        double s1[2] = {0, 0};
+        for (int i = threadIdx.x; i < c.N; i += NT) {
+            const V3 pi = ld3(J.p + 3 * (size_t)i);
+            V3 y = sym3_mul(J.diag + 6 * (size_t)i, pi);
+            for (int k = c.A.adj_ptr[i]; k < c.A.adj_ptr[i + 1]; ++k) {
+                const int e = c.A.adj_edge[k];
+                const V3 pj = ld3(J.p + 3 * (size_t)c.A.adj_nbr[k]);
+                const V3 d = ld3(J.edir + 3 * (size_t)e);
+                y = y - (c.ec.alpha[e] * pj + (c.ec.beta[e] * dot3(d, pj)) * d);
+            }
+            st3(J.ap + 3 * (size_t)i, y);
+            s1[0] += pi.x * y.x + pi.y * y.y + pi.z * y.z;
+            s1[1] += pi.x * pi.x + pi.y * pi.y + pi.z * pi.z;
+        }
+        block_sums<NT, 2>(s1, c.red);
+        const double pap = s1[0];
+        if (pap <= 1e-14 * fmax(s1[1], 1e-300)) { breakdown = true; break; }
+        const double alpha = rz / pap;
+        double s2[2] = {0, 0};
+        for (int i = threadIdx.x; i < c.N; i += NT) {
+            const V3 x = ld3(J.x + 3 * (size_t)i) + alpha * ld3(J.p + 3 * (size_t)i);
+            const V3 r = ld3(J.r + 3 * (size_t)i) - alpha * ld3(J.ap + 3 * (size_t)i);
+            const V3 z = sym3_mul(J.minv + 6 * (size_t)i, r);
+            st3(J.x + 3 * (size_t)i, x);
+            st3(J.r + 3 * (size_t)i, r);
+            st3(J.z + 3 * (size_t)i, z);
+            s2[0] += r.x * z.x + r.y * z.y + r.z * z.z;
+            s2[1] += r.x * r.x + r.y * r.y + r.z * r.z;
+        }
+        block_sums<NT, 2>(s2, c.red);
+        const double nrm = sqrt(s2[1]);
+        const bool better = nrm < best_norm;
+        if (better) best_norm = nrm;
+        const bool stop = rz <= 0.0;
+        const double beta = stop ? 0.0 : s2[0] / rz;
+        for (int i = threadIdx.x; i < c.N; i += NT) {
+            if (better) st3(J.best + 3 * (size_t)i, ld3(J.x + 3 * (size_t)i));
+            if (!stop)
+                st3(J.p + 3 * (size_t)i, ld3(J.z + 3 * (size_t)i) + beta * ld3(J.p + 3 * (size_t)i));
+        }
+        __syncthreads();
+        if (stop) { breakdown = true; break; }
+        rz = s2[0];
+    }
+    return breakdown;
+}
+
+// silhouette snapping (snap_vertices, nonrigid_stage.py:417-500)
+__device__ void surf_snap(const SurfCtx &c, double *v) {
+    const SurfJob &J = *c.J;
+    const SurfHyperDev &hp = c.hp;
+    double cnt[4] = {0, 0, 0, 0};  // walked, reached, stuck, moved
+    for (int i = threadIdx.x; i < c.N; i += NT) {
+        st3(J.off0 + 3 * (size_t)i, v3(0, 0, 0));
+        J.hold[i] = 0;
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < c.B; b += NT) {
+        const int i = J.bidx[b];
+        J.hold[i] = 1;
+        const V3 p = ld3(v + 3 * (size_t)i);
+        double px, py;
+        const bool ok = project(c.cam, p, px, py);
+        const bool en = J.enabled[b] && ok;
+        const NnResult n0 = field_nearest(c.obs, px, py);
+        const double sign = side_sign(c.obs, n0, px, py, J.n2d[2 * b], J.n2d[2 * b + 1]);
+        double val = field_interface(n0);
+        double qx = px, qy = py;
+        bool active = en && val > hp.snap_band;
+        bool stuck = false;
+        for (int s = 0; s < hp.snap_max_steps && active; ++s) {
+            const NnResult g = field_nearest(c.obs, qx, qy);
+            const double gn = sqrt(g.vx * g.vx + g.vy * g.vy);
+            const bool good = gn > 1e-9;
+            const double gd = fmax(gn, 1e-300);
+            const double dx = (-sign * g.vx) / gd, dy = (-sign * g.vy) / gd;
+            double step = hp.snap_step;
+            const double cur = val;
+            double nx = qx, ny = qy, nv = cur;
+            bool pending = good;
+            for (int h = 0; h < 3 && pending; ++h) {
+                const double tx = qx + step * dx, ty = qy + step * dy;
+                const double tv = field_interface(field_nearest(c.obs, tx, ty));
+                if (tv < cur) { nx = tx; ny = ty; nv = tv; pending = false; }
+                step *= 0.5;
+            }
+            if (!pending && good) { qx = nx; qy = ny; val = nv; }
+            if (pending || !good) { stuck = true; active = false; }
+            active = active && val > hp.snap_band;
+        }
+        cnt[0] += en ? 1.0 : 0.0;
+        cnt[1] += (en && val <= hp.snap_band) ? 1.0 : 0.0;
+        cnt[2] += (stuck && en) ? 1.0 : 0.0;
+        if (en) {
+            const double z = p.z;
+            const V3 landed = v3((qx - c.cam.cx) * z / c.cam.fx, (qy - c.cam.cy) * z / c.cam.fy, z);
+            st3(J.off0 + 3 * (size_t)i, landed - p);
+        }
+    }
+    __syncthreads();
+    // two uniform-Laplacian diffusion steps with the boundary held
+    double *src = J.off0, *dst = J.off1;
+    for (int round = 0; round < 2; ++round) {
+        for (int i = threadIdx.x; i < c.N; i += NT) {
+            if (J.hold[i]) { st3(dst + 3 * (size_t)i, ld3(src + 3 * (size_t)i)); continue; }
+            V3 a = v3(0, 0, 0);
+            for (int k = c.A.adj_ptr[i]; k < c.A.adj_ptr[i + 1]; ++k)
+                a = a + ld3(src + 3 * (size_t)c.A.adj_nbr[k]);
+            const double dg = (double)c.A.degrees[i];
+            st3(dst + 3 * (size_t)i, v3(a.x / dg, a.y / dg, a.z / dg));
+        }
+        __syncthreads();
+        double *t = src; src = dst; dst = t;
+    }
+    for (int i = threadIdx.x; i < c.N; i += NT) {
+        const V3 o = ld3(src + 3 * (size_t)i);
+        st3(v + 3 * (size_t)i, ld3(v + 3 * (size_t)i) + o);
+        cnt[3] += (o.x != 0.0 || o.y != 0.0 || o.z != 0.0) ? 1.0 : 0.0;
+    }
+    block_sums<NT, 4>(cnt, c.red);
+    if (threadIdx.x == 0 && J.report) {
+        J.report->snapped = 1;
+        J.report->snap_walked = (int)cnt[0];
+        J.report->snap_reached = (int)cnt[1];
+        J.report->snap_stuck = (int)cnt[2];
+        J.report->snap_moved = (int)cnt[3];
+    }
+    __syncthreads();
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(NT, 1) k_surface_solve(const SurfJob *jobs, ActorDev A, CamDev cam,
+                                                         EdgeConstDev ec, SurfHyperDev hp, int H,
+                                                         int W) {
+    const SurfJob &J = jobs[blockIdx.x];
+    if (!J.active) return;
+    __shared__ double red[8 * 32 + 16];
+    SurfCtx c;
+    c.J = &J;
+    c.obs = J.obs;
+    c.obs.K = J.obs_K ? *J.obs_K : 0;
+    c.A = A;
+    c.cam = cam;
+    c.ec = ec;
+    c.hp = hp;
+    c.H = H;
+    c.W = W;
+    c.P = J.P ? *J.P : 0;
+    c.B = J.B ? *J.B : 0;
+    c.N = A.N;
+    c.E = A.E;
+    c.has_prev = J.prev != nullptr;
+    c.red = red;
+    const bool has_field = J.has_field && c.obs.K > 0;
+    c.sil_on = J.enable_sil && has_field;
+    double *v = J.v;
+    for (int i = threadIdx.x; i < c.N * 3; i += NT) v[i] = J.v0[i];
+    __syncthreads();
+    lc_nonrigid_report *rep = J.report;
+    if (J.do_solve) {
+        const int levels = min(hp.gn, hp.n_levels);
+        int tot[3] = {0, 0, 0};
+        for (int it = 0; it < hp.gn; ++it) {
+            const int level = min(it, levels - 1);
+            double en[6];
+            int counts[3];
+            surf_assemble(c, level, v, en, counts);
+            for (int k = 0; k < 3; ++k) tot[k] += counts[k];
+            const bool breakdown = surf_pcg(c, hp.pcg);
+            const double e0 = total_energy(en, c.has_prev);
+            int halv = 0;
+            bool rejected = false;
+            double e1;
+            for (;;) {
+                double et[6];
+                surf_energy(c, level, v, J.best, et);
+                e1 = total_energy(et, c.has_prev);
+                if (e1 <= e0) {
+                    for (int i = threadIdx.x; i < c.N * 3; i += NT) v[i] = v[i] + J.best[i];
+                    __syncthreads();
+                    break;
+                }
+                if (halv >= hp.max_halvings) { rejected = true; e1 = e0; break; }
+                for (int i = threadIdx.x; i < c.N * 3; i += NT) J.best[i] = 0.5 * J.best[i];
+                __syncthreads();
+                ++halv;
+            }
+            if (threadIdx.x == 0 && rep && it < LC_MAX_LOG) {
+                rep->level[it] = level;
+                rep->energy_before[it] = e0;
+                rep->energy_after[it] = e1;
+                for (int k = 0; k < 6; ++k) rep->terms[it][k] = en[k];
+                rep->halvings[it] = halv;
+                rep->rejected[it] = rejected;
+                rep->pcg_breakdown[it] = breakdown;
+            }
+        }
+        if (threadIdx.x == 0 && rep) {
+            rep->n_iterations = hp.gn;
+            rep->pruned = tot[0];
+            rep->degenerate_edges = tot[1];
+            rep->behind_camera = tot[2];
+            rep->has_temporal = c.has_prev;
+            rep->n_visible = c.P;
+            rep->n_boundary = c.B;
+        }
+    }
+    if (J.do_snap && has_field && c.B > 0) surf_snap(c, v);
+}
+
+int surface_block_threads() { return NT; }

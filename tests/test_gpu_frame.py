@@ -1,0 +1,78 @@
+"""Frame-level parity of the batched device tracker (solve_frame,
+pipeline.py:263-302) against the oracle, teacher-forced per frame: every
+frame starts from the oracle's TrackState (the free-running
+tracker is chaotic, so only per-call / teacher-forced parity is defined)."""
+
+import numpy as np
+import pytest
+
+from helpers import bbox_diag, scene
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_state_to_mirror(st):
+    from paper_1810_02648_b200.config import TrackState
+    return TrackState(st.x_prev, st.x_prev2, st.joints_prev, st.disp_rest, st.v_prev, st.v_prev2)
+
+
+def _run(preset, res, n, directional, mode="full", streams=1):
+    from oracle import frame as OF
+    from paper_1810_02648_b200.config import SequenceConfig
+    from paper_1810_02648_b200.device import Tracker
+    actor, cam, frames = scene(preset, res, n)
+    cfg = SequenceConfig(directional=directional, mode=mode)
+    tr = Tracker(actor, cam, cfg, streams)
+    st = OF.State()
+    diag = bbox_diag(actor)
+    errs = []
+    for fr in frames:
+        prep = OF.prepare(fr.image, fr.mask, fr.detections, actor, cfg)
+        for s in range(streams):
+            tr.set_state(s, _oracle_state_to_mirror(st))
+            tr.set_frame(s, fr.image, fr.mask, fr.detections)
+        tr.step()
+        xo, vo, vso, st_new, plogs, slogs = OF.solve_frame(prep, actor, cam, cfg, st)
+        for s in range(streams):
+            x, v, vs, rep = tr.result(s)
+            errs.append((fr.index, s, np.abs(x - xo).max(), np.abs(v - vo).max() / diag))
+            assert rep.pose.n_iterations == len(plogs)
+            for k, o in enumerate(plogs):
+                assert rep.pose.halvings[k] == o["halvings"], (fr.index, k)
+                assert rep.pose.rejected[k] == o["rejected"], (fr.index, k)
+            if mode == "full":
+                for k, o in enumerate(slogs):
+                    assert rep.nonrigid.halvings[k] == o["halvings"], (fr.index, k)
+                    e = rep.nonrigid.energy_before[k]
+                    assert abs(e - o["energy_before"]) <= 1e-4 * o["energy_before"]
+            assert np.abs(v - vo).max() <= 1e-4 * diag, (fr.index, s, errs[-1])
+        st = st_new
+    return errs
+
+
+@pytest.mark.parametrize("preset,res", [("small", 128), ("standard", 256)])
+def test_tracker_teacher_forced(preset, res):
+    _run(preset, res, 3, directional=False)
+
+
+def test_tracker_pose_only():
+    _run("small", 128, 3, directional=False, mode="pose_only")
+
+
+def test_tracker_directional_stable_frames():
+    # frames 0 and 1 are stable under the self-jitter screen
+    _run("small", 128, 2, directional=True)
+
+
+def test_tracker_batched_streams_identical():
+    errs = _run("small", 128, 2, directional=False, streams=3)
+    by_frame = {}
+    for f, s, dx, dv in errs:
+        by_frame.setdefault(f, []).append(dv)
+    for f, v in by_frame.items():
+        assert max(v) == min(v), "streams fed identical inputs must agree exactly"
+
+
+@pytest.mark.slow
+def test_tracker_x5k_frame0():
+    _run("x5k", 1024, 2, directional=False)
