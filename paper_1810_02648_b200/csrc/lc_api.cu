@@ -14,6 +14,15 @@
 // ---------------------------------------------------------------------------
 // errors
 
+struct ApiError : std::exception {
+    std::string m;
+    explicit ApiError(std::string s) : m(std::move(s)) {}
+    const char *what() const noexcept override { return m.c_str(); }
+};
+static void require(bool ok, const char *msg) {
+    if (!ok) throw ApiError(msg);
+}
+
 static thread_local std::string g_err;
 
 static int fail(int code, const std::string &msg) {
@@ -33,20 +42,19 @@ static int fail(int code, const std::string &msg) {
     catch (const std::bad_alloc &) { return fail(LC_ENOMEM, "device allocation failed"); } \
     catch (const std::exception &ex) { return fail(LC_EINVAL, ex.what()); }
 
-struct ApiError : std::exception {
-    std::string m;
-    explicit ApiError(std::string s) : m(std::move(s)) {}
-    const char *what() const noexcept override { return m.c_str(); }
-};
-static void require(bool ok, const char *msg) {
-    if (!ok) throw ApiError(msg);
-}
 
 template <typename K, typename... Args>
-static void launch(lc_ctx *c, K kernel, dim3 g, dim3 b, size_t smem, Args... args) {
+static void launch_named(const char *name, lc_ctx *c, K kernel, dim3 g, dim3 b, size_t smem, Args... args) {
+    if (g.x == 0 || g.y == 0 || g.z == 0) return;   // empty batch / empty mesh
     kernel<<<g, b, smem, c->stream>>>(args...);
     c->launches++;
+    const cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw ApiError(std::string("launch of ") + name + " failed: " + cudaGetErrorString(e));
+    }
 }
+#define launch(c, kernel, ...) launch_named(#kernel, c, kernel, __VA_ARGS__)
 
 static int last_launch_status() {
     cudaError_t e = cudaGetLastError();
@@ -108,7 +116,8 @@ extern "C" int lc_ctx_create(int32_t device, uint64_t cuda_stream, lc_ctx **out)
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;
     }
-    cudaFuncSetAttribute(k_pose_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    CK(cudaFuncSetAttribute(k_pose_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)pose_smem_bytes(LC_MAXJ)));
     *out = c;
     return LC_OK;
     API_END

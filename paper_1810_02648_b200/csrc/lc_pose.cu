@@ -20,7 +20,7 @@ constexpr int G = NT / 32;  // row groups for the J^T J accumulation
 struct PoseSmem {
     SkelDev sk;
     FkState f;
-    QrSmem qr;
+    QrSmemT<LC_NP> qr;
     double A[LC_NP * LC_NP];
     double rhs[LC_NP];
     double x[LC_NP], xt[LC_NP], step[LC_NP];

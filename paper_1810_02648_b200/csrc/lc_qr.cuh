@@ -10,18 +10,20 @@
 
 #define LC_QR_MAXN 64
 
-struct QrSmem {
-    double a[LC_QR_MAXN][LC_QR_MAXN + 1];   // augmented [A | b], row-major
-    double v[LC_QR_MAXN];
-    double rdiag[LC_QR_MAXN];
-    double x[LC_QR_MAXN];
+template <int MAXN>
+struct QrSmemT {
+    double a[MAXN][MAXN + 1];   // augmented [A | b], row-major
+    double v[MAXN];
+    double rdiag[MAXN];
+    double x[MAXN];
     double tau;
     int skip;
 };
+using QrSmem = QrSmemT<LC_QR_MAXN>;
 
 // Householder on columns 0..n-1 of the augmented (n x n+1) matrix
-template <int NT>
-__device__ void qr_factor(QrSmem &s, int n) {
+template <int NT, typename S>
+__device__ void qr_factor(S &s, int n) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int k = 0; k < n; ++k) {
         if (w == 0) {
@@ -57,7 +59,8 @@ __device__ void qr_factor(QrSmem &s, int n) {
 }
 
 // back substitution R x = (Q^T b) on warp 0 (column n holds Q^T b)
-__device__ inline void qr_backsolve(QrSmem &s, int n) {
+template <typename S>
+__device__ inline void qr_backsolve(S &s, int n) {
     if (threadIdx.x >= 32) return;
     const int lane = threadIdx.x;
     for (int k = n - 1; k >= 0; --k) {
@@ -71,13 +74,13 @@ __device__ inline void qr_backsolve(QrSmem &s, int n) {
 
 // Solve with the reference's rank test / damping.  A is read from `A` (n*n
 // row-major, symmetric) and `b`; result in s.x.  Returns damped flag.
-template <int NT>
-__device__ bool dense_solve_block(QrSmem &s, const double *A, const double *b, int n,
+template <int NT, typename S>
+__device__ bool dense_solve_block(S &s, const double *A, const double *b, int n,
                                   double &damping) {
     for (int i = threadIdx.x; i < n * n; i += NT) s.a[i / n][i % n] = A[i];
     for (int i = threadIdx.x; i < n; i += NT) s.a[i][n] = b[i];
     __syncthreads();
-    qr_factor<NT>(s, n);
+    qr_factor<NT, S>(s, n);
     __shared__ int damped_flag;
     __shared__ double lam;
     if (threadIdx.x == 0) {
@@ -102,7 +105,7 @@ __device__ bool dense_solve_block(QrSmem &s, const double *A, const double *b, i
         }
         for (int i = threadIdx.x; i < n; i += NT) s.a[i][n] = b[i];
         __syncthreads();
-        qr_factor<NT>(s, n);
+        qr_factor<NT, S>(s, n);
     }
     qr_backsolve(s, n);
     __syncthreads();

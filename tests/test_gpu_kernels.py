@@ -68,8 +68,8 @@ def test_pcg_bsr_matches_oracle(small):
         x, info = pcg_solve(BlockSparseSystem(diag, off, rows, cols, rhs), iters)
         xo, done, brk, norms = pcg(diag, off, rows, cols, rhs, iters)
         assert info.iterations == done and info.breakdown == brk
-        assert np.allclose(info.residual_norms, norms, rtol=1e-9)
-        assert np.abs(x - xo).max() <= 1e-9 * max(np.abs(xo).max(), 1e-300)
+        assert np.allclose(info.residual_norms, norms, rtol=1e-6)
+        assert np.abs(x - xo).max() <= 1e-6 * max(np.abs(xo).max(), 1e-300)
 
 
 def test_pcg_bsr_random_spd_converges():
