@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""Benchmark: solved frames/s of the LiveCap pose + non-rigid GN hot path.
+
+Workload (BASELINE.json configs[2] shape, sharded per configs[4]): the full
+two-stage per-frame solve (`solve_frame`: preprocessing, detection
+conditioning, Stage I pose GN, Stage II non-rigid GN + PCG, snapping, warp)
+on the x5k template (N=5,410) at 1024x1024, S independent synthetic capture
+streams per GPU (seeds rank*S .. rank*S+S-1).  One step = one frame of every
+stream.  Streams are independent, so ranks shard them with no collective on
+the data path ("scaling": "weak"); only the timing barrier / max-reduce
+touches torch.distributed.
+
+  python bench.py [--gpus N --steps K --warmup W --streams S]
+  python bench.py --impl reference      # the CPU implementation (oracle port)
+
+`value` is measured with inputs resident in HBM (CUDA events on the library's
+stream, max over ranks).  `e2e` is the same metric through the public
+`Tracker` API from pinned host buffers: H2D of every step's images, masks and
+detections and D2H of every step's poses + vertices are inside its timed
+region.  Per-step inputs (S x ~100 MB of image + pyramid) exceed the 126 MB
+L2, so no explicit flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "solved frames/sec (pose+non-rigid GN) at 1/2/4/8 B200; PCG iter µs; % HBM BW"
+DOMINANT = "k_surface_solve"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--streams", type=int, default=8, help="capture streams per GPU")
+    ap.add_argument("--preset", default="x5k")
+    ap.add_argument("--res", type=int, default=1024)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-frames", type=int, default=3, help="timed steady frames of the CPU baseline")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(args, world):
+    return {"workload": f"cfg3-shaped full two-stage solve_frame, {args.preset} template @ "
+                        f"{args.res}x{args.res}, {args.streams} synthetic streams per GPU (cfg5 sharding)",
+            "preset": args.preset, "resolution": args.res, "streams_per_gpu": args.streams,
+            "total_streams": args.streams * world, "parallelism": f"stream-sharded x{world}",
+            "l2": "per-step inputs (images + pyramids) exceed the 126 MB L2; no flush needed"}
+
+
+# ---------------------------------------------------------------------------
+# synthetic inputs
+
+def make_stream_frames(actor, cam, n_frames, seed, renderer, posing):
+    from paper_1810_02648_b200 import synthetic as S
+    script = S.default_script(n_frames, noise=S.NoiseParams(sigma2d=1.0, sigma3d=0.008, seed=seed))
+    return S.generate_sequence(actor, cam, script, renderer, posing)
+
+
+def device_posing(ctx):
+    from paper_1810_02648_b200.skinning import forward_kinematics, skin_points
+
+    def posing(actor, pose, rest):
+        fk = forward_kinematics(actor, pose, ctx=ctx)
+        return skin_points(actor, pose, rest, ctx=ctx).positions, fk.positions, fk.marker_positions
+    return posing
+
+
+def device_renderer(ctx):
+    from paper_1810_02648_b200.imageproc import render_attributes
+
+    def render(cam, verts, tris, colors):
+        return render_attributes(cam, verts, tris, colors, ctx=ctx)
+    return render
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+class ClockSampler:
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for k, nm in enumerate(names):
+                    if r[5 + k].strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes of the Stage II kernel
+
+def surface_bytes(N, E, delta):
+    """delta = counter increments [frames, gn, pcg, trials, sumP, sumB, sumK, _]."""
+    frames, gn, pcg, trials, sP, sB, sK = (float(v) for v in delta[:7])
+    if frames == 0:
+        return 0.0
+    per_frame_img = 100.0 * sP + 21.0 * sB + 16.0 * sK      # summed over frames
+    gn_per_frame = gn / frames
+    trials_per_frame = trials / frames
+    asm = gn * (192.0 * N + 88.0 * E) + gn_per_frame * per_frame_img
+    pcg_b = pcg * (384.0 * N + 48.0 * E)
+    trial = trials * (144.0 * N + 48.0 * E) + trials_per_frame * per_frame_img
+    return asm + pcg_b + trial
+
+
+def read_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def read_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_surface_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d
+    return None
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    rank, world, local = dist_env()
+    os.environ["LIVECAP_DEVICE"] = str(local)
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1810_02648_b200 import _lib
+    from paper_1810_02648_b200 import synthetic as S
+    from paper_1810_02648_b200.camera import suggest_camera
+    from paper_1810_02648_b200.config import SequenceConfig
+    from paper_1810_02648_b200.device import Tracker
+
+    stream = torch.cuda.Stream(device=local)
+    ctx = _lib.Context(local, stream.cuda_stream)
+    actor = S.build_actor(args.preset, with_skirt=True)
+    cam = suggest_camera(args.res, args.res)
+    Sn, K, W = args.streams, args.steps, args.warmup
+    F = W + K
+    t_gen = time.perf_counter()
+    frames = [make_stream_frames(actor, cam, F, rank * Sn + s, device_renderer(ctx), device_posing(ctx))
+              for s in range(Sn)]
+    t_gen = time.perf_counter() - t_gen
+    H, Wd = args.res, args.res
+    # device-resident inputs for `value`
+    img_d = torch.empty((Sn, F, H, Wd, 3), dtype=torch.float64, device=f"cuda:{local}")
+    msk_d = torch.empty((Sn, F, H, Wd), dtype=torch.uint8, device=f"cuda:{local}")
+    # pinned host inputs for `e2e`
+    img_h = torch.empty((Sn, F, H, Wd, 3), dtype=torch.float64, pin_memory=True)
+    msk_h = torch.empty((Sn, F, H, Wd), dtype=torch.uint8, pin_memory=True)
+    for s in range(Sn):
+        for f in range(F):
+            img_h[s, f].copy_(torch.from_numpy(frames[s][f].image))
+            msk_h[s, f].copy_(torch.from_numpy(frames[s][f].mask.astype(np.uint8)))
+    img_d.copy_(img_h)
+    msk_d.copy_(msk_h)
+    torch.cuda.synchronize()
+    dets = [[frames[s][f].detections for f in range(F)] for s in range(Sn)]
+    cfg = SequenceConfig()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- value: inputs resident in HBM
+    tr = Tracker(actor, cam, cfg, Sn, ctx=ctx)
+
+    def step_dev(f):
+        for s in range(Sn):
+            tr.set_frame(s, img_d[s, f].data_ptr(), msk_d[s, f].data_ptr(), dets[s][f], on_device=True)
+        tr.step()
+
+    for f in range(W):
+        step_dev(f)
+    ctx.synchronize()
+    c0 = [tr.counters(s) for s in range(Sn)]
+    barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    ctx.profile_kernel(DOMINANT)
+    l0 = ctx.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for f in range(W, F):
+        step_dev(f)
+    ev1.record(stream)
+    ev1.synchronize()
+    ctx.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.launches() - l0
+    ms_dev = ev0.elapsed_time(ev1)
+    k_ms, k_n = ctx.profile_read()
+    ctx.profile_kernel(None)
+    c1 = [tr.counters(s) for s in range(Sn)]
+    ms_max = max_over_ranks(ms_dev)
+    value = world * Sn * K / (ms_max / 1e3)
+    # roofline of the dominant kernel
+    N, E = actor.mesh.n_vertices, len(actor.mesh.edges)
+    alg = sum(surface_bytes(N, E, c1[s] - c0[s]) for s in range(Sn))
+    per_launch = alg / max(k_n, 1)
+    k_avg_s = (k_ms / max(k_n, 1)) / 1e3
+    peak, peak_src = read_peaks()
+    achieved = per_launch / k_avg_s / 1e9 if k_avg_s > 0 else 0.0
+    traffic = read_traffic()
+    pcg_iters = sum(int((c1[s] - c0[s])[2]) for s in range(Sn))
+    tr.close()
+
+    # ---- e2e: public API from pinned host buffers, results read back each step
+    tr2 = Tracker(actor, cam, cfg, Sn, ctx=ctx)
+    x_out = np.empty(36)
+    v_out = np.empty((N, 3))
+    import ctypes as C
+
+    def step_host(f):
+        for s in range(Sn):
+            tr2.set_frame(s, img_h[s, f].numpy(), msk_h[s, f].numpy(), dets[s][f])
+        tr2.step()
+        for s in range(Sn):
+            _lib.check(ctx.lib.lc_tracker_get_result(tr2.handle, s, _lib.ptr(x_out), _lib.ptr(v_out), None, None))
+
+    for f in range(W):
+        step_host(f)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for f in range(W, F):
+        step_host(f)
+    e1.record(stream)
+    e1.synchronize()
+    barrier()
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+    tr2.close()
+    h2d = Sn * (H * Wd * 3 * 8 + H * Wd + (actor.skeleton.n_joints + 4) * 2 * 8
+                + actor.skeleton.n_joints * 3 * 8 + 2 * actor.skeleton.n_joints + 4)
+    d2h = Sn * (36 * 8 + N * 3 * 8)
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(actor, cam, frames[0], args.cpu_frames)
+        out = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator restated)",
+            "config": workload(args, world),
+            "e2e": {"value": world * Sn * K / (ms_e2e / 1e3), "unit": "frames/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "kernel": DOMINANT, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak if peak else None,
+                         "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                         "algorithmic_bytes_per_launch": per_launch,
+                         "kernel_ms_per_launch": k_avg_s * 1e3, "launches": k_n,
+                         "peak_source": peak_src,
+                         "traffic_source": (traffic or {}).get("source")},
+            "pcg_iterations_timed": pcg_iters,
+            "per_stream_fps": 1e3 * K / ms_max,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+            "input_generation_s": round(t_gen, 2),
+        }
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return out
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle (a restatement of the reference, bit-identical to
+# it) timed on one host core on a bounded sample of the same workload
+
+def cpu_baseline(actor, cam, frames, n_timed):
+    from threadpoolctl import threadpool_limits
+
+    from oracle import frame as OF
+    from paper_1810_02648_b200.config import SequenceConfig
+    cfg = SequenceConfig()
+    with threadpool_limits(1):
+        st = OF.State()
+        # untimed cold start (frame 0), then n_timed steady frames end to end
+        prep = OF.prepare(frames[0].image, frames[0].mask, frames[0].detections, actor, cfg)
+        _, _, _, st, _, _ = OF.solve_frame(prep, actor, cam, cfg, st)
+        t0 = time.perf_counter()
+        n = 0
+        for fr in frames[1:1 + n_timed]:
+            prep = OF.prepare(fr.image, fr.mask, fr.detections, actor, cfg)
+            _, _, _, st, _, _ = OF.solve_frame(prep, actor, cam, cfg, st)
+            n += 1
+        dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "frames/s", "cores": 1, "kind": "port",
+            "sample": f"1 stream, {n} steady frames (after an untimed frame 0), preprocess + solve_frame, "
+                      f"1 thread, oracle port of the reference (bit-identical outputs)"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's CPU implementation (oracle port) on all host
+# cores, one process per stream
+
+def _ref_worker(a):
+    preset, res, n_frames, seed, warm = a
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from threadpoolctl import threadpool_limits
+
+    from oracle import frame as OF
+    from oracle import geometry as OG
+    from oracle import imaging as OI
+    from paper_1810_02648_b200 import synthetic as S
+    from paper_1810_02648_b200.camera import suggest_camera
+    from paper_1810_02648_b200.config import SequenceConfig
+
+    def posing(actor, pose, rest):
+        fk = OG.Fk(actor.skeleton, pose.to_vector())
+        return OG.skin(rest, actor.skinning, fk.dqs)[0], fk.pos, fk.markers
+
+    actor = S.build_actor(preset, with_skirt=True)
+    cam = suggest_camera(res, res)
+    frames = make_stream_frames(actor, cam, n_frames, seed, OI.render_attributes, posing)
+    cfg = SequenceConfig()
+    st = OF.State()
+    stamps = []
+    with threadpool_limits(1):
+        for fr in frames:
+            prep = OF.prepare(fr.image, fr.mask, fr.detections, actor, cfg)
+            _, _, _, st, _, _ = OF.solve_frame(prep, actor, cam, cfg, st)
+            stamps.append(time.perf_counter())
+    return stamps[warm - 1], stamps[-1], len(frames) - warm
+
+
+def run_reference(args):
+    import multiprocessing as mp
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None
+    cores = len(os.sched_getaffinity(0))
+    procs = max(1, min(args.streams, cores))
+    W = max(1, args.warmup)
+    K = max(1, args.steps)
+    jobs = [(args.preset, args.res, W + K, s, W) for s in range(procs)]
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_ref_worker, jobs)
+    spans = [b - a for a, b, _ in res]
+    frames = sum(n for _, _, n in res)
+    value = frames / max(spans)
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+           "steps": K, "warmup": W, "ms_per_step": 1e3 * max(spans) / K, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (reference generator restated)",
+           "config": workload(args, world),
+           "cpu_baseline": {"value": value, "unit": "frames/s", "cores": procs, "kind": "port",
+                            "sample": f"{procs} streams in parallel processes (1 thread each), {K} steady "
+                                      f"frames per stream after {W} untimed, preprocess + solve_frame"},
+           "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

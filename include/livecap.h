@@ -257,6 +257,15 @@ int lc_tracker_set_state(lc_tracker *tr, int32_t stream, const double *x_prev,
 int lc_tracker_get_state(lc_tracker *tr, int32_t stream, int32_t *flags, double *x_prev,
                          double *x_prev2, double *joints_prev, double *disp_rest,
                          double *v_prev, double *v_prev2);
+/* cumulative per-stream work counters of the Stage II solver (for algorithmic
+ * byte accounting): [frames, gn_steps, pcg_iterations, energy_evaluations
+ * (line-search trials), sum visible P, sum boundary B, sum contour pixels K, 0] */
+#define LC_NCOUNTERS 8
+int lc_tracker_counters(lc_tracker *tr, int32_t stream, int64_t *out);
+/* per-kernel timing: CUDA events around every launch of `kernel_name` on the
+ * context's stream (NULL disables); read returns total ms and launch count */
+int lc_profile_kernel(lc_ctx *ctx, const char *kernel_name);
+int lc_profile_read(lc_ctx *ctx, double *total_ms, int64_t *count);
 /* device pointer of a stream's resident vertices (N*3) for zero-copy readers */
 int lc_tracker_device_vertices(lc_tracker *tr, int32_t stream, uint64_t *dptr);
 

@@ -141,6 +141,9 @@ _SIGS = {
     "lc_tracker_get_state": (C.c_int, [P, i32, P, P, P, P, P, P, P]),
     "lc_tracker_device_vertices": (C.c_int, [P, i32, P]),
     "lc_debug_tables": (C.c_int, [i32, P, P]),
+    "lc_tracker_counters": (C.c_int, [P, i32, P]),
+    "lc_profile_kernel": (C.c_int, [P, C.c_char_p]),
+    "lc_profile_read": (C.c_int, [P, P, P]),
 }
 EXPORTED = tuple(_SIGS)
 
@@ -222,6 +225,14 @@ class Context:
         n = C.c_int64()
         check(self.lib.lc_kernel_launches(self.handle, C.byref(n)))
         return n.value
+
+    def profile_kernel(self, name: str | None):
+        check(self.lib.lc_profile_kernel(self.handle, None if name is None else name.encode()))
+
+    def profile_read(self):
+        ms, n = C.c_double(), C.c_int64()
+        check(self.lib.lc_profile_read(self.handle, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def synchronize(self):
         check(self.lib.lc_ctx_synchronize(self.handle))

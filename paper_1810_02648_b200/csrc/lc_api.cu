@@ -46,7 +46,18 @@ static int fail(int code, const std::string &msg) {
 template <typename K, typename... Args>
 static void launch_named(const char *name, lc_ctx *c, K kernel, dim3 g, dim3 b, size_t smem, Args... args) {
     if (g.x == 0 || g.y == 0 || g.z == 0) return;   // empty batch / empty mesh
+    const bool prof = !c->prof_name.empty() && c->prof_name == name;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (prof) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, c->stream);
+    }
     kernel<<<g, b, smem, c->stream>>>(args...);
+    if (prof) {
+        cudaEventRecord(e1, c->stream);
+        c->prof_events.push_back({e0, e1});
+    }
     c->launches++;
     const cudaError_t e = cudaPeekAtLastError();
     if (e != cudaSuccess) {
@@ -137,6 +148,32 @@ extern "C" int lc_ctx_synchronize(lc_ctx *c) {
     require(c != nullptr, "null ctx");
     CK(cudaStreamSynchronize(c->stream));
     return last_launch_status();
+}
+
+extern "C" int lc_profile_kernel(lc_ctx *c, const char *name) {
+    if (!c) return fail(LC_EINVAL, "null ctx");
+    cudaStreamSynchronize(c->stream);
+    for (auto &p : c->prof_events) {
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+    }
+    c->prof_events.clear();
+    c->prof_name = name ? name : "";
+    return LC_OK;
+}
+
+extern "C" int lc_profile_read(lc_ctx *c, double *total_ms, int64_t *count) {
+    if (!c || !total_ms || !count) return fail(LC_EINVAL, "null argument");
+    CK(cudaStreamSynchronize(c->stream));
+    double tot = 0.0;
+    for (auto &p : c->prof_events) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, p.first, p.second));
+        tot += ms;
+    }
+    *total_ms = tot;
+    *count = (int64_t)c->prof_events.size();
+    return LC_OK;
 }
 
 extern "C" int lc_kernel_launches(lc_ctx *c, int64_t *count) {
@@ -413,6 +450,8 @@ void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) 
     hold = mem.alloc<uint8_t>(N);
     pose_rep = mem.alloc<lc_pose_report>(1);
     nr_rep = mem.alloc<lc_nonrigid_report>(1);
+    counters = mem.alloc<long long>(LC_NCOUNTERS);
+    cudaMemset(counters, 0, sizeof(long long) * LC_NCOUNTERS);
 }
 
 static CamDev cam_dev(const lc_camera &c) {
@@ -896,6 +935,7 @@ static void run_frame(FrameBatch &fb) {
             j.p = s->sp; j.ap = s->sap; j.best = s->sbest; j.edir = s->edir; j.eg = s->eg;
             j.off0 = s->off0; j.off1 = s->off1; j.hold = s->hold;
             j.report = s->nr_rep;
+            j.counters = s->counters;
             sj.push_back(j);
         }
         surface_launch(c, a, fb.cam, *fb.cf, sj);
@@ -1075,6 +1115,17 @@ extern "C" int lc_tracker_get_state(lc_tracker *t, int32_t stream, int32_t *flag
         flags[3] = s->has_vprev; flags[4] = s->has_vprev2;
     }
     CK(cudaStreamSynchronize(c->stream));
+    return LC_OK;
+    API_END
+}
+
+extern "C" int lc_tracker_counters(lc_tracker *t, int32_t stream, int64_t *out) {
+    API_BEGIN
+    require(t && out, "null argument");
+    require(stream >= 0 && stream < t->S, "stream index out of range");
+    CK(cudaMemcpyAsync(out, t->slots[stream]->counters, sizeof(long long) * LC_NCOUNTERS,
+                       cudaMemcpyDeviceToHost, t->ctx->stream));
+    CK(cudaStreamSynchronize(t->ctx->stream));
     return LC_OK;
     API_END
 }

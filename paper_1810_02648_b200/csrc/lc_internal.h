@@ -14,6 +14,7 @@
 #define LC_NP 36
 #define LC_GRID_CELL 16  // NN grid cell edge in pixels
 #define LC_GRID_SHIFT 4
+#define LC_NCOUNTERS 8
 
 struct SkelDev {
     int J, head, n_tree_levels;

@@ -50,6 +50,7 @@ struct SurfJob {
     double *off0, *off1;      // N*3 snap offsets
     uint8_t *hold;            // N
     lc_nonrigid_report *report;
+    long long *counters;      // cumulative: frames, gn, pcg iters, trials, P, B, K (or null)
 };
 
 __global__ void k_pose_solve(const PoseJob *jobs, const SkelDev *skg, ActorDev A, CamDev cam);

@@ -12,6 +12,9 @@ struct lc_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     long long launches = 0;
+    // optional per-kernel timing: CUDA events around every launch of `prof_name`
+    std::string prof_name;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
     struct Slot *call_slot = nullptr;          // scratch slot for single-call entry points
     const lc_actor *call_actor = nullptr;
     int call_w = 0, call_h = 0;
@@ -91,6 +94,7 @@ struct Slot {
     // reports (device)
     lc_pose_report *pose_rep;
     lc_nonrigid_report *nr_rep;
+    long long *counters;   // LC_NCOUNTERS cumulative work counters (device)
     void allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J);
 };
 

@@ -467,6 +467,11 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve(const SurfJob *jobs, Ac
                 __syncthreads();
                 ++halv;
             }
+            if (threadIdx.x == 0 && J.counters) {
+                J.counters[1] += 1;
+                J.counters[2] += hp.pcg;
+                J.counters[3] += halv + 1;
+            }
             if (threadIdx.x == 0 && rep && it < LC_MAX_LOG) {
                 rep->level[it] = level;
                 rep->energy_before[it] = e0;
@@ -476,6 +481,12 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve(const SurfJob *jobs, Ac
                 rep->rejected[it] = rejected;
                 rep->pcg_breakdown[it] = breakdown;
             }
+        }
+        if (threadIdx.x == 0 && J.counters) {
+            J.counters[0] += 1;
+            J.counters[4] += c.P;
+            J.counters[5] += c.B;
+            J.counters[6] += c.obs.K;
         }
         if (threadIdx.x == 0 && rep) {
             rep->n_iterations = hp.gn;

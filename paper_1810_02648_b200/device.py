@@ -309,6 +309,11 @@ class Tracker:
                           jp if flags[0] else None, dr if flags[2] else None,
                           v1 if flags[3] else None, v2 if flags[4] else None)
 
+    def counters(self, stream: int) -> np.ndarray:
+        out = np.zeros(8, dtype=np.int64)
+        L.check(self.ctx.lib.lc_tracker_counters(self.handle, stream, L.ptr(out)))
+        return out
+
     def close(self):
         if self.handle:
             self.ctx.lib.lc_tracker_destroy(self.handle)
