@@ -79,15 +79,25 @@ extern "C" int lc_version(void) { return 1; }
 // ---------------------------------------------------------------------------
 // job staging: small per-launch descriptor arrays copied H2D in stream order
 
+// Pinned host ring + device ring: descriptors are memcpy'd into pinned
+// memory and copied with a truly asynchronous cudaMemcpyAsync (a pageable
+// source would synchronize the stream on every launch).  Before the ring
+// wraps, the stream is drained so no in-flight copy still reads a slot.
 struct JobRing {
     char *dev = nullptr;
+    char *host = nullptr;
     size_t cap = 0, off = 0;
-    void *put(cudaStream_t st, const void *host, size_t bytes) {
-        bytes = (bytes + 255) & ~size_t(255);
-        if (off + bytes > cap) off = 0;
-        void *d = dev + off;
-        cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, st);
-        off += bytes;
+    void *put(cudaStream_t st, const void *src, size_t bytes, void *dst = nullptr) {
+        const size_t padded = (bytes + 255) & ~size_t(255);
+        if (padded > cap) throw ApiError("job descriptor larger than the staging ring");
+        if (off + padded > cap) {
+            cudaStreamSynchronize(st);
+            off = 0;
+        }
+        std::memcpy(host + off, src, bytes);
+        void *d = dst ? dst : dev + off;
+        cudaMemcpyAsync(d, host + off, bytes, cudaMemcpyHostToDevice, st);
+        off += padded;
         return d;
     }
 };
@@ -96,17 +106,19 @@ static JobRing &ring_of(lc_ctx *c) {
     for (auto &r : rings)
         if (r.first == c) return r.second;
     JobRing jr;
-    jr.cap = 8 << 20;
+    jr.cap = 16 << 20;
     if (cudaMalloc(&jr.dev, jr.cap) != cudaSuccess) throw std::bad_alloc();
+    if (cudaMallocHost(&jr.host, jr.cap) != cudaSuccess) throw std::bad_alloc();
     rings.push_back({c, jr});
     return rings.back().second;
 }
 template <typename T>
 static const T *stage(lc_ctx *c, const std::vector<T> &v) {
-    // pad to 256 B so ring slices stay aligned
-    std::vector<char> buf(((v.size() * sizeof(T)) + 255) & ~size_t(255));
-    std::memcpy(buf.data(), v.data(), v.size() * sizeof(T));
-    return static_cast<const T *>(ring_of(c).put(c->stream, buf.data(), buf.size()));
+    return static_cast<const T *>(ring_of(c).put(c->stream, v.data(), v.size() * sizeof(T)));
+}
+// small host array -> existing device buffer, asynchronously via the pinned ring
+static void stage_to(lc_ctx *c, void *dst, const void *src, size_t bytes) {
+    if (bytes) ring_of(c).put(c->stream, src, bytes, dst);
 }
 
 // ---------------------------------------------------------------------------
@@ -387,6 +399,10 @@ static void alloc_grid(DevArena &m, GridBufs &g, int H, int W) {
     g.pts = m.alloc<int2>((size_t)H * W);
     g.cell_pts = m.alloc<int>((size_t)H * W);
     g.K = m.alloc<int>(1);
+    g.cand_cnt = m.alloc<int>(ncx * ncy);
+    g.cand_range = m.alloc<int2>(ncx * ncy);
+    g.cand_pts = m.alloc<int>((size_t)ncx * ncy * LC_CAND_PER_CELL);
+    g.cand_total = m.alloc<int>(1);
 }
 
 void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) {
@@ -424,6 +440,8 @@ void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) 
     fk = mem.alloc<FkState>(1);
     zbuf = mem.alloc<unsigned long long>(HW);
     tri_id = mem.alloc<int>(HW);
+    big = mem.alloc<int>(std::max(T, 1));
+    n_big = mem.alloc<int>(1);
     tri_front = mem.alloc<uint8_t>(T);
     vflag = mem.alloc<uint8_t>(N);
     enabled = mem.alloc<uint8_t>(N);
@@ -470,6 +488,8 @@ static NnGridDev grid_dev(const GridBufs &g, const uint8_t *mask, int H, int W) 
     d.cell_start = g.cell_start;
     d.cell_pts = g.cell_pts;
     d.mask = mask;
+    d.cand_range = g.cand_range;
+    d.cand_pts = g.cand_pts;
     return d;
 }
 
@@ -484,6 +504,8 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
         j.row_count = p.first->row_count; j.row_start = p.first->row_start;
         j.pts = p.first->pts; j.cell_count = p.first->cell_count; j.cell_start = p.first->cell_start;
         j.cell_fill = p.first->cell_fill; j.cell_pts = p.first->cell_pts; j.K = p.first->K;
+        j.cand_cnt = p.first->cand_cnt; j.cand_range = p.first->cand_range;
+        j.cand_pts = p.first->cand_pts; j.cand_total = p.first->cand_total;
         jobs.push_back(j);
     }
     const GridJob *dj = stage(c, jobs);
@@ -495,6 +517,9 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
     launch(c, k_contour_emit, dim3(rows_grid, S), dim3(256), 0, dj, H, W, ncx);
     launch(c, k_contour_scan_cells, dim3(S), dim3(1024), 0, dj, ncx * ncy);
     launch(c, k_contour_fill, dim3(64, S), dim3(256), 0, dj, ncx);
+    launch(c, k_cand_count, dim3((ncx * ncy + 7) / 8, S), dim3(256), 0, dj, H, W);
+    launch(c, k_cand_scan, dim3(S), dim3(1024), 0, dj, ncx * ncy);
+    launch(c, k_cand_fill, dim3((ncx * ncy + 7) / 8, S), dim3(256), 0, dj, H, W);
 }
 
 static void raster(lc_ctx *c, const lc_actor *a, const lc_camera &cam, std::vector<RasterJob> jobs,
@@ -507,7 +532,11 @@ static void raster(lc_ctx *c, const lc_actor *a, const lc_camera &cam, std::vect
     const int T = a->dev.T;
     launch(c, k_raster_clear, dim3(592, S), dim3(256), 0, dj, HW);
     launch(c, k_raster_depth, dim3((T + 127) / 128, S), dim3(128), 0, dj, cd, a->dev.tris, T);
-    if (winner) launch(c, k_raster_winner, dim3((T + 127) / 128, S), dim3(128), 0, dj, cd, a->dev.tris, T);
+    launch(c, k_raster_depth_big, dim3(64, S), dim3(256), 0, dj, cd, a->dev.tris);
+    if (winner) {
+        launch(c, k_raster_winner, dim3((T + 127) / 128, S), dim3(128), 0, dj, cd, a->dev.tris, T);
+        launch(c, k_raster_winner_big, dim3(64, S), dim3(256), 0, dj, cd, a->dev.tris);
+    }
     if (mask) launch(c, k_raster_mask, dim3(592, S), dim3(256), 0, dj, HW);
 }
 
@@ -777,7 +806,7 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
     const lc_actor *a = fb.a;
     const int H = fb.cam.height, W = fb.cam.width;
     std::vector<RasterJob> rj;
-    for (Slot *s : ss) rj.push_back(RasterJob{s->*verts, s->zbuf, s->tri_id, s->own_mask});
+    for (Slot *s : ss) rj.push_back(RasterJob{s->*verts, s->zbuf, s->tri_id, s->own_mask, s->big, s->n_big});
     raster(c, a, fb.cam, rj, !stage1 && fb.cfg->enable_part_mask, true);
     std::vector<std::pair<const GridBufs *, const uint8_t *>> gs;
     for (Slot *s : ss) gs.push_back({&s->own, s->own_mask});
@@ -1001,10 +1030,10 @@ extern "C" int lc_tracker_destroy(lc_tracker *t) {
 }
 
 static void upload_dets(lc_ctx *c, Slot *s, const lc_detections *d, int J) {
-    cudaMemcpyAsync(s->j2d, d->joints2d, sizeof(double) * 2 * (J + 4), cudaMemcpyHostToDevice, c->stream);
-    cudaMemcpyAsync(s->j3d_raw, d->joints3d, sizeof(double) * 3 * J, cudaMemcpyHostToDevice, c->stream);
-    cudaMemcpyAsync(s->v2d, d->valid2d, J + 4, cudaMemcpyHostToDevice, c->stream);
-    cudaMemcpyAsync(s->v3d, d->valid3d, J, cudaMemcpyHostToDevice, c->stream);
+    stage_to(c, s->j2d, d->joints2d, sizeof(double) * 2 * (J + 4));
+    stage_to(c, s->j3d_raw, d->joints3d, sizeof(double) * 3 * J);
+    stage_to(c, s->v2d, d->valid2d, J + 4);
+    stage_to(c, s->v3d, d->valid3d, J);
 }
 
 extern "C" int lc_tracker_set_frame(lc_tracker *t, int32_t stream, const double *image, const uint8_t *mask,
@@ -1362,7 +1391,7 @@ extern "C" int lc_contour_vertices(lc_ctx *c, const lc_actor *a, const lc_camera
     Slot *s = call_slot(c, a, H, W, 1);
     cudaStream_t st = c->stream;
     CK(cudaMemcpyAsync(s->model, verts, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
-    raster(c, a, *cam, {RasterJob{s->model, s->zbuf, s->tri_id, nullptr}}, false, false);
+    raster(c, a, *cam, {RasterJob{s->model, s->zbuf, s->tri_id, nullptr, s->big, s->n_big}}, false, false);
     ContourJob j{};
     j.verts = s->model; j.zbuf = s->zbuf; j.tri_front = s->tri_front; j.tri_n = s->tri_n; j.vflag = s->vflag;
     j.idx = s->cidx; j.n2d = s->n2d; j.B = s->B; j.vis = nullptr; j.P = nullptr; j.active = 1;
@@ -1425,11 +1454,16 @@ extern "C" int lc_render(lc_ctx *c, const lc_camera *cam, int32_t n, const doubl
         di = m.upload(ii.data(), ii.size(), st);
         io = m.alloc<long long>(HW);
     }
-    const RasterJob *dj = stage(c, std::vector<RasterJob>{RasterJob{dv, zb, tid, nullptr}});
+    int *big = m.alloc<int>(std::max(t, 1)), *nbig = m.alloc<int>(1);
+    const RasterJob *dj = stage(c, std::vector<RasterJob>{RasterJob{dv, zb, tid, nullptr, big, nbig}});
     const CamDev cd = cam_dev(*cam);
     launch(c, k_raster_clear, dim3(592), dim3(256), 0, dj, (int)HW);
     launch(c, k_raster_depth, dim3((t + 127) / 128), dim3(128), 0, dj, cd, (const int *)dt, t);
-    if (mode) launch(c, k_raster_winner, dim3((t + 127) / 128), dim3(128), 0, dj, cd, (const int *)dt, t);
+    launch(c, k_raster_depth_big, dim3(64), dim3(256), 0, dj, cd, (const int *)dt);
+    if (mode) {
+        launch(c, k_raster_winner, dim3((t + 127) / 128), dim3(128), 0, dj, cd, (const int *)dt, t);
+        launch(c, k_raster_winner_big, dim3(64), dim3(256), 0, dj, cd, (const int *)dt);
+    }
     launch(c, k_raster_resolve, dim3(592), dim3(256), 0, dj, cd, (const int *)dt, mode, (const double *)da,
            n_attr, (const int *)di, bg_attr, (long long)bg_id, za, ao, io);
     CK(cudaMemcpyAsync(zbuf_out, za, HW * sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -143,6 +143,14 @@ __device__ inline int nn_query(const NnGridDev &g, double qx, double qy, double 
         return bi;
     }
     const int cx = (int)qx >> LC_GRID_SHIFT, cy = (int)qy >> LC_GRID_SHIFT;
+    if (g.cand_range) {
+        const int2 rg = g.cand_range[cy * g.ncx + cx];
+        if (rg.y >= 0) {
+            for (int k = rg.x; k < rg.x + rg.y; ++k) nn_consider(g, g.cand_pts[k], qx, qy, best, bi);
+            d2out = best;
+            return bi;
+        }
+    }
     const int rmax = max(max(cx, g.ncx - 1 - cx), max(cy, g.ncy - 1 - cy));
     // after ring r every unvisited point is > r*CELL away (strictly), so the
     // search may stop as soon as the best squared distance is <= (r*CELL)^2
@@ -163,6 +171,45 @@ __device__ inline int nn_query(const NnGridDev &g, double qx, double qy, double 
     }
     d2out = best;
     return bi;
+}
+
+// ---- per-cell candidate lists (built once per mask) ----------------------
+// squared farthest / nearest distance from cell c's square to point p
+__device__ __forceinline__ double cell_far2(int cx, int cy, int2 p) {
+    const double x0 = (double)(cx * LC_GRID_CELL), y0 = (double)(cy * LC_GRID_CELL);
+    const double x1 = x0 + LC_GRID_CELL, y1 = y0 + LC_GRID_CELL;
+    const double dx = fmax(fabs(p.x - x0), fabs(p.x - x1)), dy = fmax(fabs(p.y - y0), fabs(p.y - y1));
+    return dx * dx + dy * dy;
+}
+__device__ __forceinline__ double cell_near2(int cx, int cy, int2 p) {
+    const double x0 = (double)(cx * LC_GRID_CELL), y0 = (double)(cy * LC_GRID_CELL);
+    const double x1 = x0 + LC_GRID_CELL, y1 = y0 + LC_GRID_CELL;
+    const double dx = p.x < x0 ? x0 - p.x : (p.x > x1 ? p.x - x1 : 0.0);
+    const double dy = p.y < y0 ? y0 - p.y : (p.y > y1 ? p.y - y1 : 0.0);
+    return dx * dx + dy * dy;
+}
+
+// Visit every grid point within Chebyshev cell-rings [0, rmax] of (cx, cy),
+// lanes striding over the cells of each ring.  Returns when `done(r)` after ring r.
+template <typename F, typename D>
+__device__ __forceinline__ void ring_visit_warp(const NnGridDev &g, int cx, int cy, F &&f, D &&done) {
+    const int lane = threadIdx.x & 31;
+    const int rmax = max(max(cx, g.ncx - 1 - cx), max(cy, g.ncy - 1 - cy));
+    for (int r = 0; r <= rmax; ++r) {
+        const int side = 2 * r + 1;
+        const int ncell = r == 0 ? 1 : 8 * r;
+        for (int k = lane; k < ncell; k += 32) {
+            int xx, yy;
+            if (r == 0) { xx = cx; yy = cy; }
+            else if (k < side) { xx = cx - r + k; yy = cy - r; }
+            else if (k < 2 * side) { xx = cx - r + (k - side); yy = cy + r; }
+            else { const int m = k - 2 * side; xx = (m & 1) ? cx + r : cx - r; yy = cy - r + 1 + (m >> 1); }
+            if (xx < 0 || yy < 0 || xx >= g.ncx || yy >= g.ncy) continue;
+            const int c = yy * g.ncx + xx;
+            for (int q = g.cell_start[c]; q < g.cell_start[c + 1]; ++q) f(g.cell_pts[q]);
+        }
+        if (done(r)) return;
+    }
 }
 
 // continuous distance + unit direction away from the nearest contour point

@@ -72,7 +72,13 @@ struct NnGridDev {
     const int *cell_start; // ncx*ncy+1
     const int *cell_pts;   // point ids grouped by cell
     const uint8_t *mask;   // H*W, for inside()
+    // exact per-cell candidate lists (null -> ring search): cand_range[c] =
+    // (start, count); count < 0 marks an overflowed cell (ring search there)
+    const int2 *cand_range; // ncx*ncy
+    const int *cand_pts;
 };
+#define LC_CAND_PER_CELL 128   // average candidate capacity per cell
+#define LC_CAND_MAX 1024       // per-cell cap before falling back to the ring search
 
 // per-config constants of the surface energy
 struct EdgeConstDev {

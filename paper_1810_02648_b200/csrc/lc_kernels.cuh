@@ -22,12 +22,19 @@ struct GridJob {
     int *cell_fill;        // ncx*ncy
     int *cell_pts;         // capacity H*W
     int *K;                // out: contour pixel count
+    int *cand_cnt;         // ncells
+    int2 *cand_range;      // ncells
+    int *cand_pts;         // capacity ncells * LC_CAND_PER_CELL
+    int *cand_total;       // 1
 };
 __global__ void k_contour_rows(const GridJob *jobs, int H, int W);
 __global__ void k_contour_scan_rows(const GridJob *jobs, int H, int ncells);
 __global__ void k_contour_emit(const GridJob *jobs, int H, int W, int ncx);
 __global__ void k_contour_scan_cells(const GridJob *jobs, int ncells);
 __global__ void k_contour_fill(const GridJob *jobs, int ncx);
+__global__ void k_cand_count(const GridJob *jobs, int H, int W);
+__global__ void k_cand_scan(const GridJob *jobs, int ncells);
+__global__ void k_cand_fill(const GridJob *jobs, int H, int W);
 
 // ----- rasterizer (rasterizer.py:18-120) -----------------------------------
 struct RasterJob {
@@ -35,10 +42,15 @@ struct RasterJob {
     unsigned long long *zbuf;   // H*W, fp64 bit patterns (+inf = empty)
     int *tri_id;                // H*W, INT_MAX = empty
     uint8_t *mask;              // H*W out (isfinite(zbuf)), may be null
+    int *big;                   // T capacity: triangles whose clipped bbox is large
+    int *n_big;                 // count (reset by k_raster_clear)
 };
+#define LC_RASTER_SMALL 256     // bbox pixels handled by one thread; larger -> one CTA
 __global__ void k_raster_clear(const RasterJob *jobs, int HW);
 __global__ void k_raster_depth(const RasterJob *jobs, CamDev cam, const int *tris, int T);
 __global__ void k_raster_winner(const RasterJob *jobs, CamDev cam, const int *tris, int T);
+__global__ void k_raster_depth_big(const RasterJob *jobs, CamDev cam, const int *tris);
+__global__ void k_raster_winner_big(const RasterJob *jobs, CamDev cam, const int *tris);
 __global__ void k_raster_mask(const RasterJob *jobs, int HW);
 __global__ void k_raster_resolve(const RasterJob *jobs, CamDev cam, const int *tris, int mode,
                                  const double *attrs, int n_attr, const int *ids,

@@ -59,6 +59,8 @@ struct lc_actor {
 struct GridBufs {
     int *row_count, *row_start, *cell_count, *cell_start, *cell_fill, *cell_pts, *K;
     int2 *pts;
+    int *cand_cnt, *cand_pts, *cand_total;
+    int2 *cand_range;
 };
 
 // per-stream device state + scratch
@@ -85,6 +87,7 @@ struct Slot {
     FkState *fk;
     unsigned long long *zbuf;
     int *tri_id;
+    int *big, *n_big;
     uint8_t *tri_front, *vflag, *enabled;
     double *tri_n, *n2d, *crest;
     int *cidx, *B, *vis, *P;

@@ -168,6 +168,115 @@ __global__ void k_contour_fill(const GridJob *jobs, int ncx) {
     }
 }
 
+// ---- exact per-cell candidate lists (see NnGridDev) -----------------------
+
+__device__ __forceinline__ NnGridDev grid_of(const GridJob &J, int H, int W) {
+    NnGridDev g{};
+    g.K = *J.K;
+    g.W = W; g.H = H;
+    g.ncx = (W + LC_GRID_CELL - 1) / LC_GRID_CELL;
+    g.ncy = (H + LC_GRID_CELL - 1) / LC_GRID_CELL;
+    g.pts = J.pts; g.cell_start = J.cell_start; g.cell_pts = J.cell_pts;
+    return g;
+}
+
+// U2 = min over sites of the squared farthest distance from cell c
+__device__ double cell_bound_warp(const NnGridDev &g, int cx, int cy) {
+    double u2 = LC_INF;
+    ring_visit_warp(g, cx, cy, [&](int pid) { u2 = fmin(u2, cell_far2(cx, cy, g.pts[pid])); },
+                    [&](int r) {
+                        for (int o = 16; o > 0; o >>= 1) u2 = fmin(u2, __shfl_xor_sync(0xffffffffu, u2, o));
+                        const double lim = (double)(r * LC_GRID_CELL);
+                        return u2 <= lim * lim;
+                    });
+    return u2;
+}
+
+__global__ void k_cand_count(const GridJob *jobs, int H, int W) {
+    const GridJob J = jobs[blockIdx.y];
+    const NnGridDev g = grid_of(J, H, W);
+    const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    for (int c = blockIdx.x * wpb + (threadIdx.x >> 5); c < g.ncx * g.ncy; c += gridDim.x * wpb) {
+        const int cx = c % g.ncx, cy = c / g.ncx;
+        int cnt = 0;
+        if (g.K > 0) {
+            const double u2 = cell_bound_warp(g, cx, cy);
+            ring_visit_warp(g, cx, cy, [&](int pid) { cnt += cell_near2(cx, cy, g.pts[pid]) <= u2; },
+                            [&](int r) {
+                                const double lim = (double)(r * LC_GRID_CELL);
+                                return lim * lim > u2;
+                            });
+            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        }
+        if (lane == 0) J.cand_cnt[c] = cnt > LC_CAND_MAX ? -1 : cnt;
+    }
+}
+
+__global__ void k_cand_scan(const GridJob *jobs, int ncells) {
+    const GridJob J = jobs[blockIdx.x];
+    // exclusive scan of max(count, 0) into cand_range[].x (count kept in .y)
+    __shared__ int wt[32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < ncells; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const int raw = i < ncells ? J.cand_cnt[i] : 0;
+        const int v = raw > 0 ? raw : 0;
+        int s = v;
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += t;
+        }
+        if (lane == 31) wt[w] = s;
+        __syncthreads();
+        if (w == 0) {
+            int t = lane < (int)(blockDim.x >> 5) ? wt[lane] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += u;
+            }
+            if (lane < (int)(blockDim.x >> 5)) wt[lane] = t;
+        }
+        __syncthreads();
+        const int before = (w > 0 ? wt[w - 1] : 0) + carry;
+        if (i < ncells) {
+            const int start = before + s - v;
+            // lists past the buffer capacity fall back to the ring search
+            const bool fits = start + v <= ncells * LC_CAND_PER_CELL;
+            J.cand_range[i] = make_int2(start, (raw >= 0 && fits) ? raw : -1);
+            J.cell_fill[i] = 0;   // reused as the per-cell append counter by k_cand_fill
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = before + s;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *J.cand_total = carry;
+}
+
+__global__ void k_cand_fill(const GridJob *jobs, int H, int W) {
+    const GridJob J = jobs[blockIdx.y];
+    const NnGridDev g = grid_of(J, H, W);
+    const int wpb = blockDim.x >> 5;
+    for (int c = blockIdx.x * wpb + (threadIdx.x >> 5); c < g.ncx * g.ncy; c += gridDim.x * wpb) {
+        const int2 rg = J.cand_range[c];
+        if (rg.y <= 0 || g.K == 0) continue;
+        const int cx = c % g.ncx, cy = c / g.ncx;
+        const double u2 = cell_bound_warp(g, cx, cy);
+        // append order inside a list is irrelevant: ties break on the point index
+        ring_visit_warp(g, cx, cy,
+                        [&](int pid) {
+                            if (cell_near2(cx, cy, g.pts[pid]) <= u2)
+                                J.cand_pts[rg.x + atomicAdd(&J.cell_fill[c], 1)] = pid;
+                        },
+                        [&](int r) {
+                            const double lim = (double)(r * LC_GRID_CELL);
+                            return lim * lim > u2;
+                        });
+    }
+}
+
 // ===========================================================================
 // rasterizer.  The reference draws triangles sequentially and keeps the first
 // strictly-smaller depth (rasterizer.py:46-58).  Pass 1 finds the minimum
@@ -211,12 +320,40 @@ __device__ __forceinline__ bool bary(const double P[3][2], double inv, int ix, i
 
 __global__ void k_raster_clear(const RasterJob *jobs, int HW) {
     const RasterJob J = jobs[blockIdx.y];
+    if (blockIdx.x == 0 && threadIdx.x == 0) *J.n_big = 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += gridDim.x * blockDim.x) {
         J.zbuf[i] = 0x7ff0000000000000ULL;
         J.tri_id[i] = INT_MAX;
     }
 }
 
+__device__ __forceinline__ void depth_pixel(const RasterJob &J, CamDev cam, const double P[3][2],
+                                            const double D[3], double inv, int x, int y) {
+    double l0, l1, l2;
+    if (!bary(P, inv, x, y, l0, l1, l2)) return;
+    const double z = l0 * D[0] + l1 * D[1] + l2 * D[2];
+    const unsigned long long zb = (unsigned long long)__double_as_longlong(z);
+    unsigned long long *dst = J.zbuf + (size_t)y * cam.W + x;
+    if (zb < *dst) atomicMin(dst, zb);
+}
+
+__device__ __forceinline__ void winner_pixel(const RasterJob &J, CamDev cam, const double P[3][2],
+                                             const double D[3], double inv, int x, int y, int t) {
+    double l0, l1, l2;
+    if (!bary(P, inv, x, y, l0, l1, l2)) return;
+    const double z = l0 * D[0] + l1 * D[1] + l2 * D[2];
+    const size_t pi = (size_t)y * cam.W + x;
+    if ((unsigned long long)__double_as_longlong(z) == J.zbuf[pi] && t < J.tri_id[pi])
+        atomicMin(J.tri_id + pi, t);
+}
+
+__device__ __forceinline__ long long bbox_pixels(const int bb[4]) {
+    return (long long)(bb[1] - bb[0] + 1) * (long long)(bb[3] - bb[2] + 1);
+}
+
+// one thread per small triangle; large (clipped) triangles are deferred to
+// the one-CTA-per-triangle pass so no thread walks a megapixel bbox (the
+// reference's own trackers produce such triangles once they lose track)
 __global__ void k_raster_depth(const RasterJob *jobs, CamDev cam, const int *tris, int T) {
     const RasterJob J = jobs[blockIdx.y];
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -224,15 +361,12 @@ __global__ void k_raster_depth(const RasterJob *jobs, CamDev cam, const int *tri
     double P[3][2], D[3], inv;
     int bb[4];
     if (!tri_setup(cam, J.verts, tris, t, P, D, inv, bb)) return;
+    if (bbox_pixels(bb) > LC_RASTER_SMALL) {
+        J.big[atomicAdd(J.n_big, 1)] = t;
+        return;
+    }
     for (int y = bb[2]; y <= bb[3]; ++y)
-        for (int x = bb[0]; x <= bb[1]; ++x) {
-            double l0, l1, l2;
-            if (!bary(P, inv, x, y, l0, l1, l2)) continue;
-            const double z = l0 * D[0] + l1 * D[1] + l2 * D[2];
-            const unsigned long long zb = (unsigned long long)__double_as_longlong(z);
-            unsigned long long *dst = J.zbuf + (size_t)y * cam.W + x;
-            if (zb < *dst) atomicMin(dst, zb);
-        }
+        for (int x = bb[0]; x <= bb[1]; ++x) depth_pixel(J, cam, P, D, inv, x, y);
 }
 
 __global__ void k_raster_winner(const RasterJob *jobs, CamDev cam, const int *tris, int T) {
@@ -242,15 +376,39 @@ __global__ void k_raster_winner(const RasterJob *jobs, CamDev cam, const int *tr
     double P[3][2], D[3], inv;
     int bb[4];
     if (!tri_setup(cam, J.verts, tris, t, P, D, inv, bb)) return;
+    if (bbox_pixels(bb) > LC_RASTER_SMALL) return;
     for (int y = bb[2]; y <= bb[3]; ++y)
-        for (int x = bb[0]; x <= bb[1]; ++x) {
-            double l0, l1, l2;
-            if (!bary(P, inv, x, y, l0, l1, l2)) continue;
-            const double z = l0 * D[0] + l1 * D[1] + l2 * D[2];
-            const size_t pi = (size_t)y * cam.W + x;
-            if ((unsigned long long)__double_as_longlong(z) == J.zbuf[pi] && t < J.tri_id[pi])
-                atomicMin(J.tri_id + pi, t);
-        }
+        for (int x = bb[0]; x <= bb[1]; ++x) winner_pixel(J, cam, P, D, inv, x, y, t);
+}
+
+__global__ void k_raster_depth_big(const RasterJob *jobs, CamDev cam, const int *tris) {
+    const RasterJob J = jobs[blockIdx.y];
+    const int nb = *J.n_big;
+    for (int k = blockIdx.x; k < nb; k += gridDim.x) {
+        const int t = J.big[k];
+        double P[3][2], D[3], inv;
+        int bb[4];
+        tri_setup(cam, J.verts, tris, t, P, D, inv, bb);
+        const int w = bb[1] - bb[0] + 1;
+        const long long n = bbox_pixels(bb);
+        for (long long i = threadIdx.x; i < n; i += blockDim.x)
+            depth_pixel(J, cam, P, D, inv, bb[0] + (int)(i % w), bb[2] + (int)(i / w));
+    }
+}
+
+__global__ void k_raster_winner_big(const RasterJob *jobs, CamDev cam, const int *tris) {
+    const RasterJob J = jobs[blockIdx.y];
+    const int nb = *J.n_big;
+    for (int k = blockIdx.x; k < nb; k += gridDim.x) {
+        const int t = J.big[k];
+        double P[3][2], D[3], inv;
+        int bb[4];
+        tri_setup(cam, J.verts, tris, t, P, D, inv, bb);
+        const int w = bb[1] - bb[0] + 1;
+        const long long n = bbox_pixels(bb);
+        for (long long i = threadIdx.x; i < n; i += blockDim.x)
+            winner_pixel(J, cam, P, D, inv, bb[0] + (int)(i % w), bb[2] + (int)(i / w), t);
+    }
 }
 
 __global__ void k_raster_mask(const RasterJob *jobs, int HW) {

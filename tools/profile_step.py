@@ -1,0 +1,47 @@
+"""Run the bench workload's tracker for a few frames (for ncu captures).
+
+  python tools/profile_step.py --streams 8 --frames 4
+Input generation (device renders) happens first: ncu filters should skip the
+8*frames mode-1 renders when targeting raster kernels.
+"""
+import argparse
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--streams", type=int, default=8)
+    ap.add_argument("--frames", type=int, default=4)
+    ap.add_argument("--preset", default="x5k")
+    ap.add_argument("--res", type=int, default=1024)
+    a = ap.parse_args()
+    from paper_1810_02648_b200 import _lib
+    from paper_1810_02648_b200 import synthetic as S
+    from paper_1810_02648_b200.camera import suggest_camera
+    from paper_1810_02648_b200.config import SequenceConfig
+    from paper_1810_02648_b200.device import Tracker
+    ctx = _lib.default_context()
+    actor = S.build_actor(a.preset, with_skirt=True)
+    cam = suggest_camera(a.res, a.res)
+    frames = [bench.make_stream_frames(actor, cam, a.frames, s, bench.device_renderer(ctx),
+                                       bench.device_posing(ctx)) for s in range(a.streams)]
+    tr = Tracker(actor, cam, SequenceConfig(), a.streams, ctx=ctx)
+    for f in range(a.frames):
+        t0 = time.perf_counter()
+        for s in range(a.streams):
+            fr = frames[s][f]
+            tr.set_frame(s, fr.image, fr.mask, fr.detections)
+        tr.step()
+        ctx.synchronize()
+        print(f"frame {f}: {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
+
+
+if __name__ == "__main__":
+    main()
