@@ -67,6 +67,52 @@ static void launch_named(const char *name, lc_ctx *c, K kernel, dim3 g, dim3 b, 
 }
 #define launch(c, kernel, ...) launch_named(#kernel, c, kernel, __VA_ARGS__)
 
+// cluster launch: `streams` teams of `cs` CTAs (one thread-block cluster per stream)
+template <typename... KArgs, typename... Args>
+static void launch_cluster(const char *name, lc_ctx *c, void (*kernel)(KArgs...), int streams, int cs,
+                           dim3 block, size_t smem, Args... args) {
+    if (streams <= 0) return;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(streams * cs);
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const bool prof = !c->prof_name.empty() && c->prof_name == name;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (prof) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, c->stream);
+    }
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+    if (prof) {
+        cudaEventRecord(e1, c->stream);
+        c->prof_events.push_back({e0, e1});
+    }
+    c->launches++;
+    if (e == cudaSuccess) e = cudaPeekAtLastError();
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw ApiError(std::string("cluster launch of ") + name + " failed: " + cudaGetErrorString(e));
+    }
+}
+
+static int cluster_size() {
+    static int cs = [] {
+        const char *v = getenv("LIVECAP_CLUSTER");
+        int x = v ? atoi(v) : 8;
+        return (x == 1 || x == 4 || x == 8 || x == 16) ? x : 8;
+    }();
+    return cs;
+}
+
 static int last_launch_status() {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(LC_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
@@ -139,8 +185,15 @@ extern "C" int lc_ctx_create(int32_t device, uint64_t cuda_stream, lc_ctx **out)
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;
     }
-    CK(cudaFuncSetAttribute(k_pose_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)pose_smem_bytes(LC_MAXJ)));
+    {
+        const int sm = (int)pose_smem_bytes(LC_MAXJ);
+        CK(cudaFuncSetAttribute(k_pose_solve_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_pose_solve_t<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_pose_solve_t<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_pose_solve_t<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_pose_solve_t<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        CK(cudaFuncSetAttribute(k_surface_solve_t<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
     *out = c;
     return LC_OK;
     API_END
@@ -403,6 +456,7 @@ static void alloc_grid(DevArena &m, GridBufs &g, int H, int W) {
     g.cand_range = m.alloc<int2>(ncx * ncy);
     g.cand_pts = m.alloc<int>((size_t)ncx * ncy * LC_CAND_PER_CELL);
     g.cand_total = m.alloc<int>(1);
+    g.cand_u2 = m.alloc<double>(ncx * ncy);
 }
 
 void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) {
@@ -495,7 +549,7 @@ static NnGridDev grid_dev(const GridBufs &g, const uint8_t *mask, int H, int W) 
 
 // contour pixels + grid for a batch of masks
 static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *, const uint8_t *>> &gs,
-                        int H, int W) {
+                        int H, int W, int max_ring = 1 << 30) {
     if (gs.empty()) return;
     std::vector<GridJob> jobs;
     for (auto &p : gs) {
@@ -506,6 +560,7 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
         j.cell_fill = p.first->cell_fill; j.cell_pts = p.first->cell_pts; j.K = p.first->K;
         j.cand_cnt = p.first->cand_cnt; j.cand_range = p.first->cand_range;
         j.cand_pts = p.first->cand_pts; j.cand_total = p.first->cand_total;
+        j.cand_u2 = p.first->cand_u2; j.max_ring = max_ring;
         jobs.push_back(j);
     }
     const GridJob *dj = stage(c, jobs);
@@ -810,7 +865,7 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
     raster(c, a, fb.cam, rj, !stage1 && fb.cfg->enable_part_mask, true);
     std::vector<std::pair<const GridBufs *, const uint8_t *>> gs;
     for (Slot *s : ss) gs.push_back({&s->own, s->own_mask});
-    build_grids(c, gs, H, W);
+    build_grids(c, gs, H, W, 3);   // rim queries stay within a few pixels of the own contour
     std::vector<ContourJob> cj;
     for (Slot *s : ss) {
         ContourJob j{};
@@ -846,14 +901,20 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
 
 static void pose_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, const std::vector<PoseJob> &jobs) {
     const size_t smem = pose_smem_bytes(a->skel.J);
-    launch(c, k_pose_solve, dim3((unsigned)jobs.size()), dim3(pose_block_threads()), smem, stage(c, jobs),
-           (const SkelDev *)a->skel_dev, a->dev, cam_dev(cam));
+    const int cs = cluster_size();
+    auto k = cs == 1 ? k_pose_solve_t<1> : cs == 4 ? k_pose_solve_t<4> : cs == 8 ? k_pose_solve_t<8>
+                                                                           : k_pose_solve_t<16>;
+    launch_cluster("k_pose_solve", c, k, (int)jobs.size(), cs, dim3(pose_block_threads()), smem,
+                   stage(c, jobs), (const SkelDev *)a->skel_dev, a->dev, cam_dev(cam));
 }
 
 static void surface_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, const ConfigDev &cf,
                            const std::vector<SurfJob> &jobs) {
-    launch(c, k_surface_solve, dim3((unsigned)jobs.size()), dim3(surface_block_threads()), 0, stage(c, jobs),
-           a->dev, cam_dev(cam), cf.ec, cf.shp, cam.height, cam.width);
+    const int cs = cluster_size();
+    auto k = cs == 1 ? k_surface_solve_t<1> : cs == 4 ? k_surface_solve_t<4>
+             : cs == 8 ? k_surface_solve_t<8> : k_surface_solve_t<16>;
+    launch_cluster("k_surface_solve", c, k, (int)jobs.size(), cs, dim3(surface_block_threads()), 0,
+                   stage(c, jobs), a->dev, cam_dev(cam), cf.ec, cf.shp, cam.height, cam.width);
 }
 
 static void run_frame(FrameBatch &fb) {
@@ -1155,6 +1216,46 @@ extern "C" int lc_tracker_counters(lc_tracker *t, int32_t stream, int64_t *out) 
     CK(cudaMemcpyAsync(out, t->slots[stream]->counters, sizeof(long long) * LC_NCOUNTERS,
                        cudaMemcpyDeviceToHost, t->ctx->stream));
     CK(cudaStreamSynchronize(t->ctx->stream));
+    return LC_OK;
+    API_END
+}
+
+extern "C" int lc_tracker_inspect(lc_tracker *t, int32_t stream, int32_t what, void *out, int64_t cap,
+                                  int64_t *n_out) {
+    API_BEGIN
+    require(t && out && n_out, "null argument");
+    require(stream >= 0 && stream < t->S, "stream index out of range");
+    Slot *s = t->slots[stream];
+    cudaStream_t st = t->ctx->stream;
+    int B = 0, P = 0;
+    CK(cudaMemcpyAsync(&B, s->B, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&P, s->P, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const size_t N = s->N;
+    if (what == 0 || what == 2) {
+        const int n = what == 0 ? B : P;
+        require(n <= cap, "capacity too small");
+        std::vector<int> tmp(n);
+        if (n) CK(cudaMemcpy(tmp.data(), what == 0 ? s->cidx : s->vis, sizeof(int) * n, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < n; ++i) static_cast<int64_t *>(out)[i] = tmp[i];
+        *n_out = n;
+    } else if (what == 1) {
+        require(B <= cap, "capacity too small");
+        std::vector<uint8_t> tmp(B);
+        if (B) CK(cudaMemcpy(tmp.data(), s->enabled, B, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < B; ++i) static_cast<int64_t *>(out)[i] = tmp[i];
+        *n_out = B;
+    } else if (what == 3) {
+        require(2 * (int64_t)B <= cap, "capacity too small");
+        if (B) CK(cudaMemcpy(out, s->n2d, sizeof(double) * 2 * B, cudaMemcpyDeviceToHost));
+        *n_out = B;
+    } else if (what == 4 || what == 5) {
+        require((int64_t)(3 * N) <= cap, "capacity too small");
+        CK(cudaMemcpy(out, what == 4 ? s->vinit : s->vs, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost));
+        *n_out = (int64_t)N;
+    } else {
+        return fail(LC_EINVAL, "unknown inspect target");
+    }
     return LC_OK;
     API_END
 }

@@ -26,6 +26,8 @@ struct GridJob {
     int2 *cand_range;      // ncells
     int *cand_pts;         // capacity ncells * LC_CAND_PER_CELL
     int *cand_total;       // 1
+    double *cand_u2;       // ncells: per-cell bound U^2 (count -> fill)
+    int max_ring;          // cells with no site within this many rings use the ring search
 };
 __global__ void k_contour_rows(const GridJob *jobs, int H, int W);
 __global__ void k_contour_scan_rows(const GridJob *jobs, int H, int ncells);

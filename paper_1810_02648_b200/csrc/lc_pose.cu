@@ -11,6 +11,7 @@
 #include "lc_kernels.cuh"
 #include "lc_qr.cuh"
 #include "lc_pose.cuh"
+#include "lc_team.cuh"
 
 namespace {
 
@@ -24,7 +25,7 @@ struct PoseSmem {
     double A[LC_NP * LC_NP];
     double rhs[LC_NP];
     double x[LC_NP], xt[LC_NP], step[LC_NP];
-    double red[8 * 32 + 16];
+    double red[8 * 32 + 32];
     double pix[LC_MAXJ + 4][2];
     int okz[LC_MAXJ + 4];
 };
@@ -164,7 +165,9 @@ __device__ double pose_row(const PoseCtx &c, int r, double *jr, int &term, int &
 }
 
 // evaluate at s.xt; with_jac fills s.A / s.rhs.  Returns the total energy,
-// per-term energies in terms[5], behind-camera count.
+// per-term energies in terms[5], behind-camera count.  Rows are split over
+// the team's CTAs; every CTA ends with the same totals.
+template <typename T>
 __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &behind_out) {
     PoseSmem &s = *c.s;
     const SkelDev &sk = s.sk;
@@ -230,7 +233,7 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
         is_rhs = true;
         ta = task - 21;
     }
-    for (int r0 = 0; r0 < c.R; r0 += NT) {
+    for (int r0 = T::rank() * NT; r0 < c.R; r0 += T::size) {
         const int r = r0 + threadIdx.x;
         if (r < c.R) {
             int term, bh;
@@ -263,7 +266,7 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
     // total energy = sum of F^2 over all rows (pose_stage.py:279-281)
     {
         double v8[8] = {acc[0], acc[1], acc[2], acc[3], acc[4], (double)behind, 0.0, 0.0};
-        block_sums<NT, 8>(v8, s.red);
+        T::template sums<8>(v8, s.red);
         for (int k = 0; k < 5; ++k) terms[k] = v8[k];
         behind_out = (int)v8[5];
         total = (((v8[0] + v8[1]) + v8[2]) + v8[3]) + v8[4];
@@ -278,9 +281,18 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
             for (int k = 0; k < cnt; ++k) dst[k] = tile[k];
         }
         __syncthreads();
+        // groups -> this CTA's partial, then the team total in rank order
+        double *cta_part = part + (size_t)G * per_group;
+        double *team_tot = cta_part + per_group;
         for (int e = threadIdx.x; e < per_group; e += NT) {
             double sum = part[e];
             for (int g = 1; g < G; ++g) sum += part[(size_t)g * per_group + e];
+            cta_part[e] = sum;
+        }
+        __syncthreads();
+        T::sum_arrays(cta_part, team_tot, per_group);
+        for (int e = threadIdx.x; e < per_group; e += NT) {
+            const double sum = team_tot[e];
             if (e < 21 * 36) {
                 int t = e / 36, k = e % 36, a = 0, b = 0;
                 for (a = 0; a < 6; ++a) {
@@ -302,9 +314,11 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
 
 }  // namespace
 
-__global__ void __launch_bounds__(NT, 1) k_pose_solve(const PoseJob *jobs, const SkelDev *skg,
-                                                      ActorDev A, CamDev cam) {
-    const PoseJob &J = jobs[blockIdx.x];
+template <int CS>
+__global__ void __launch_bounds__(NT, 1) k_pose_solve_t(const PoseJob *jobs, const SkelDev *skg,
+                                                        ActorDev A, CamDev cam) {
+    using T = Team<CS, NT>;
+    const PoseJob &J = jobs[T::stream()];
     if (!J.active) return;
     extern __shared__ __align__(16) unsigned char dsm[];
     PoseSmem &s = *reinterpret_cast<PoseSmem *>(dsm);
@@ -342,7 +356,7 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve(const PoseJob *jobs, const
         __syncthreads();
         double terms[5];
         int behind;
-        const double e0 = pose_eval(c, true, terms, behind);
+        const double e0 = pose_eval<T>(c, true, terms, behind);
         behind_total += behind;
         gimbal |= s.f.gimbal;
         double damping;
@@ -357,7 +371,7 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve(const PoseJob *jobs, const
             __syncthreads();
             double tt[5];
             int bh;
-            e1 = pose_eval(c, false, tt, bh);
+            e1 = pose_eval<T>(c, false, tt, bh);
             if (e1 <= e0) {
                 for (int i = threadIdx.x; i < LC_NP; i += NT) s.x[i] = s.xt[i];
                 __syncthreads();
@@ -372,7 +386,7 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve(const PoseJob *jobs, const
             __syncthreads();
             ++halv;
         }
-        if (threadIdx.x == 0 && rep) {
+        if (T::tid() == 0 && rep) {
             const int k = log0 + it;
             if (k < LC_MAX_LOG) {
                 rep->energy_before[k] = e0;
@@ -388,8 +402,9 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve(const PoseJob *jobs, const
         }
         __syncthreads();
     }
-    for (int i = threadIdx.x; i < LC_NP; i += NT) J.x_out[i] = s.x[i];
-    if (threadIdx.x == 0 && rep) {
+    if (T::rank() == 0)
+        for (int i = threadIdx.x; i < LC_NP; i += NT) J.x_out[i] = s.x[i];
+    if (T::tid() == 0 && rep) {
         rep->n_iterations = log0 + J.hp.gn;
         rep->behind_camera += behind_total;
         rep->gimbal = rep->gimbal || gimbal;
@@ -397,6 +412,11 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve(const PoseJob *jobs, const
         rep->has_temporal = J.prev_pos != nullptr;
     }
 }
+
+template __global__ void k_pose_solve_t<1>(const PoseJob *, const SkelDev *, ActorDev, CamDev);
+template __global__ void k_pose_solve_t<4>(const PoseJob *, const SkelDev *, ActorDev, CamDev);
+template __global__ void k_pose_solve_t<8>(const PoseJob *, const SkelDev *, ActorDev, CamDev);
+template __global__ void k_pose_solve_t<16>(const PoseJob *, const SkelDev *, ActorDev, CamDev);
 
 size_t pose_smem_bytes(int n_joints) {
     const size_t head = (sizeof(PoseSmem) + 15) & ~size_t(15);

@@ -53,10 +53,12 @@ struct SurfJob {
     long long *counters;      // cumulative: frames, gn, pcg iters, trials, P, B, K (or null)
 };
 
-__global__ void k_pose_solve(const PoseJob *jobs, const SkelDev *skg, ActorDev A, CamDev cam);
+template <int CS>
+__global__ void k_pose_solve_t(const PoseJob *jobs, const SkelDev *skg, ActorDev A, CamDev cam);
 size_t pose_smem_bytes(int n_joints);
 int pose_block_threads();
 
-__global__ void k_surface_solve(const SurfJob *jobs, ActorDev A, CamDev cam, EdgeConstDev ec,
-                                SurfHyperDev hp, int H, int W);
+template <int CS>
+__global__ void k_surface_solve_t(const SurfJob *jobs, ActorDev A, CamDev cam, EdgeConstDev ec,
+                                  SurfHyperDev hp, int H, int W);
 int surface_block_threads();

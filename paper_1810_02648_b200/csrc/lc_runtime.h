@@ -61,6 +61,7 @@ struct GridBufs {
     int2 *pts;
     int *cand_cnt, *cand_pts, *cand_total;
     int2 *cand_range;
+    double *cand_u2;
 };
 
 // per-stream device state + scratch

@@ -180,16 +180,19 @@ __device__ __forceinline__ NnGridDev grid_of(const GridJob &J, int H, int W) {
     return g;
 }
 
-// U2 = min over sites of the squared farthest distance from cell c
-__device__ double cell_bound_warp(const NnGridDev &g, int cx, int cy) {
+// U2 = min over sites of the squared farthest distance from cell c; -1 when
+// no site lies within `max_ring` rings (the cell then keeps the ring search)
+__device__ double cell_bound_warp(const NnGridDev &g, int cx, int cy, int max_ring) {
     double u2 = LC_INF;
+    bool gave_up = false;
     ring_visit_warp(g, cx, cy, [&](int pid) { u2 = fmin(u2, cell_far2(cx, cy, g.pts[pid])); },
                     [&](int r) {
                         for (int o = 16; o > 0; o >>= 1) u2 = fmin(u2, __shfl_xor_sync(0xffffffffu, u2, o));
+                        if (r >= max_ring && u2 == LC_INF) { gave_up = true; return true; }
                         const double lim = (double)(r * LC_GRID_CELL);
                         return u2 <= lim * lim;
                     });
-    return u2;
+    return gave_up ? -1.0 : u2;
 }
 
 __global__ void k_cand_count(const GridJob *jobs, int H, int W) {
@@ -199,8 +202,9 @@ __global__ void k_cand_count(const GridJob *jobs, int H, int W) {
     for (int c = blockIdx.x * wpb + (threadIdx.x >> 5); c < g.ncx * g.ncy; c += gridDim.x * wpb) {
         const int cx = c % g.ncx, cy = c / g.ncx;
         int cnt = 0;
-        if (g.K > 0) {
-            const double u2 = cell_bound_warp(g, cx, cy);
+        double u2 = -1.0;
+        if (g.K > 0) u2 = cell_bound_warp(g, cx, cy, J.max_ring);
+        if (u2 >= 0.0) {
             ring_visit_warp(g, cx, cy, [&](int pid) { cnt += cell_near2(cx, cy, g.pts[pid]) <= u2; },
                             [&](int r) {
                                 const double lim = (double)(r * LC_GRID_CELL);
@@ -208,7 +212,10 @@ __global__ void k_cand_count(const GridJob *jobs, int H, int W) {
                             });
             for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         }
-        if (lane == 0) J.cand_cnt[c] = cnt > LC_CAND_MAX ? -1 : cnt;
+        if (lane == 0) {
+            J.cand_cnt[c] = (u2 < 0.0 || cnt > LC_CAND_MAX) ? -1 : cnt;
+            J.cand_u2[c] = u2;
+        }
     }
 }
 
@@ -263,7 +270,7 @@ __global__ void k_cand_fill(const GridJob *jobs, int H, int W) {
         const int2 rg = J.cand_range[c];
         if (rg.y <= 0 || g.K == 0) continue;
         const int cx = c % g.ncx, cy = c / g.ncx;
-        const double u2 = cell_bound_warp(g, cx, cy);
+        const double u2 = J.cand_u2[c];
         // append order inside a list is irrelevant: ties break on the point index
         ring_visit_warp(g, cx, cy,
                         [&](int pid) {

@@ -11,6 +11,7 @@
 // constants and d_e the current unit edge direction.  Every CTA-wide sum is a
 // fixed-order tree (deterministic); there are no atomics.
 #include "lc_pose.cuh"
+#include "lc_team.cuh"
 
 namespace {
 
@@ -111,25 +112,26 @@ __device__ __forceinline__ void edge_q(const SurfCtx &c, int e, const double *v,
 }
 
 // energies at v (+ step): photo, sil, smooth, edge, vel, acc
+template <typename T>
 __device__ void surf_energy(const SurfCtx &c, int level, const double *v, const double *step,
                             double en[6]) {
     const SurfJob &J = *c.J;
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const double *img = J.pyr + (size_t)level * c.H * c.W * 3;
     if (J.enable_photo)
-        for (int k = threadIdx.x; k < c.P; k += NT) {
+        for (int k = T::tid(); k < c.P; k += T::size) {
             const int i = J.vis[k];
             PhotoRow o;
             photo_row(c, img, i, trial_pos(v, step, i), false, o);
             acc[0] += o.r[0] * o.r[0] + o.r[1] * o.r[1] + o.r[2] * o.r[2];
         }
     if (c.sil_on)
-        for (int b = threadIdx.x; b < c.B; b += NT) {
+        for (int b = T::tid(); b < c.B; b += T::size) {
             SilRow o;
             sil_row(c, b, trial_pos(v, step, J.bidx[b]), false, o);
             acc[1] += o.r * o.r;
         }
-    for (int e = threadIdx.x; e < c.E; e += NT) {
+    for (int e = T::tid(); e < c.E; e += T::size) {
         EdgeQ q;
         edge_q(c, e, v, step, q);
         acc[2] += q.e_smooth;
@@ -137,7 +139,7 @@ __device__ void surf_energy(const SurfCtx &c, int level, const double *v, const 
     }
     if (c.has_prev) {
         const double cv = sqrt(c.hp.w_vel), ca = sqrt(c.hp.w_acc);
-        for (int i = threadIdx.x; i < c.N; i += NT) {
+        for (int i = T::tid(); i < c.N; i += T::size) {
             const V3 p = trial_pos(v, step, i);
             const V3 q1 = ld3(J.prev + 3 * (size_t)i);
             const V3 q2 = J.prev2 ? ld3(J.prev2 + 3 * (size_t)i) : q1;
@@ -147,7 +149,7 @@ __device__ void surf_energy(const SurfCtx &c, int level, const double *v, const 
             acc[5] += ar.x * ar.x + ar.y * ar.y + ar.z * ar.z;
         }
     }
-    block_sums<NT, 8>(acc, c.red);
+    T::template sums<8>(acc, c.red);
     for (int k = 0; k < 6; ++k) en[k] = acc[k];
 }
 
@@ -158,6 +160,7 @@ __device__ __forceinline__ double total_energy(const double en[6], bool has_prev
 }
 
 // GN evaluation with the normal system (diag, minv, rhs, edir); returns energies + counters
+template <typename T>
 __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, double en[6],
                               int counts[3]) {
     const SurfJob &J = *c.J;
@@ -165,12 +168,12 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // 6 energies, pruned, behind
     double degen = 0.0;
     // P0: clear data blocks; per-edge direction + gradient contribution
-    for (int i = threadIdx.x; i < c.N; i += NT) {
+    for (int i = T::tid(); i < c.N; i += T::size) {
         double *dg = J.diag + 6 * (size_t)i;
         for (int k = 0; k < 6; ++k) dg[k] = 0.0;
         st3(J.rhs + 3 * (size_t)i, v3(0, 0, 0));
     }
-    for (int e = threadIdx.x; e < c.E; e += NT) {
+    for (int e = T::tid(); e < c.E; e += T::size) {
         EdgeQ q;
         edge_q(c, e, v, nullptr, q);
         acc[2] += q.e_smooth;
@@ -180,11 +183,11 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
         const double al = c.ec.alpha[e], be = c.ec.beta[e];
         st3(J.eg + 3 * (size_t)e, al * q.u + be * (q.len_err * q.d));
     }
-    __syncthreads();
+    T::sync();
     // P1: photometric data blocks (visible ids are unique)
     const double *img = J.pyr + (size_t)level * c.H * c.W * 3;
     if (J.enable_photo)
-        for (int k = threadIdx.x; k < c.P; k += NT) {
+        for (int k = T::tid(); k < c.P; k += T::size) {
             const int i = J.vis[k];
             PhotoRow o;
             photo_row(c, img, i, ld3(v + 3 * (size_t)i), true, o);
@@ -201,10 +204,10 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
             for (int a = 0; a < 3; ++a)
                 rh[a] = -(o.J[0][a] * o.r[0] + o.J[1][a] * o.r[1] + o.J[2][a] * o.r[2]);
         }
-    __syncthreads();
+    T::sync();
     // P2: silhouette rank-1 blocks (boundary ids are unique)
     if (c.sil_on)
-        for (int b = threadIdx.x; b < c.B; b += NT) {
+        for (int b = T::tid(); b < c.B; b += T::size) {
             const int i = J.bidx[b];
             SilRow o;
             sil_row(c, b, ld3(v + 3 * (size_t)i), true, o);
@@ -216,9 +219,9 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
             double *rh = J.rhs + 3 * (size_t)i;
             rh[0] += -o.g[0] * o.r; rh[1] += -o.g[1] * o.r; rh[2] += -o.g[2] * o.r;
         }
-    __syncthreads();
+    T::sync();
     // P3: full diagonal blocks, rhs, Jacobi preconditioner, temporal energies
-    for (int i = threadIdx.x; i < c.N; i += NT) {
+    for (int i = T::tid(); i < c.N; i += T::size) {
         double dg[6];
         for (int k = 0; k < 6; ++k) dg[k] = J.diag[6 * (size_t)i + k];
         V3 rh = ld3(J.rhs + 3 * (size_t)i);
@@ -250,20 +253,21 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
             for (int k = 0; k < 6; ++k) mi[k] = 0.0;  // pinv of an all-zero block
         for (int k = 0; k < 6; ++k) J.minv[6 * (size_t)i + k] = mi[k];
     }
-    block_sums<NT, 8>(acc, c.red);
+    T::template sums<8>(acc, c.red);
     for (int k = 0; k < 6; ++k) en[k] = acc[k];
     counts[0] = (int)acc[6];
     counts[2] = (int)acc[7];
     double dd[1] = {degen};
-    block_sums<NT, 1>(dd, c.red);
+    T::template sums<1>(dd, c.red);
     counts[1] = (int)dd[0];
 }
 
 // block-Jacobi PCG from zero, best-residual iterate (solvers.py:104-145)
+template <typename T>
 __device__ bool surf_pcg(const SurfCtx &c, int iters) {
     const SurfJob &J = *c.J;
     double part[2] = {0, 0};
-    for (int i = threadIdx.x; i < c.N; i += NT) {
+    for (int i = T::tid(); i < c.N; i += T::size) {
         const V3 r = ld3(J.rhs + 3 * (size_t)i);
         const V3 z = sym3_mul(J.minv + 6 * (size_t)i, r);
         st3(J.x + 3 * (size_t)i, v3(0, 0, 0));
@@ -274,13 +278,13 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters) {
         part[0] += r.x * z.x + r.y * z.y + r.z * z.z;
         part[1] += r.x * r.x + r.y * r.y + r.z * r.z;
     }
-    block_sums<NT, 2>(part, c.red);
+    T::template sums<2>(part, c.red);
     double rz = part[0];
     double best_norm = sqrt(part[1]);
     bool breakdown = false;
     for (int it = 0; it < iters; ++it) {
         double s1[2] = {0, 0};
-        for (int i = threadIdx.x; i < c.N; i += NT) {
+        for (int i = T::tid(); i < c.N; i += T::size) {
             const V3 pi = ld3(J.p + 3 * (size_t)i);
             V3 y = sym3_mul(J.diag + 6 * (size_t)i, pi);
             for (int k = c.A.adj_ptr[i]; k < c.A.adj_ptr[i + 1]; ++k) {
@@ -293,12 +297,12 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters) {
             s1[0] += pi.x * y.x + pi.y * y.y + pi.z * y.z;
             s1[1] += pi.x * pi.x + pi.y * pi.y + pi.z * pi.z;
         }
-        block_sums<NT, 2>(s1, c.red);
+        T::template sums<2>(s1, c.red);
         const double pap = s1[0];
         if (pap <= 1e-14 * fmax(s1[1], 1e-300)) { breakdown = true; break; }
         const double alpha = rz / pap;
         double s2[2] = {0, 0};
-        for (int i = threadIdx.x; i < c.N; i += NT) {
+        for (int i = T::tid(); i < c.N; i += T::size) {
             const V3 x = ld3(J.x + 3 * (size_t)i) + alpha * ld3(J.p + 3 * (size_t)i);
             const V3 r = ld3(J.r + 3 * (size_t)i) - alpha * ld3(J.ap + 3 * (size_t)i);
             const V3 z = sym3_mul(J.minv + 6 * (size_t)i, r);
@@ -308,18 +312,18 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters) {
             s2[0] += r.x * z.x + r.y * z.y + r.z * z.z;
             s2[1] += r.x * r.x + r.y * r.y + r.z * r.z;
         }
-        block_sums<NT, 2>(s2, c.red);
+        T::template sums<2>(s2, c.red);
         const double nrm = sqrt(s2[1]);
         const bool better = nrm < best_norm;
         if (better) best_norm = nrm;
         const bool stop = rz <= 0.0;
         const double beta = stop ? 0.0 : s2[0] / rz;
-        for (int i = threadIdx.x; i < c.N; i += NT) {
+        for (int i = T::tid(); i < c.N; i += T::size) {
             if (better) st3(J.best + 3 * (size_t)i, ld3(J.x + 3 * (size_t)i));
             if (!stop)
                 st3(J.p + 3 * (size_t)i, ld3(J.z + 3 * (size_t)i) + beta * ld3(J.p + 3 * (size_t)i));
         }
-        __syncthreads();
+        T::sync();
         if (stop) { breakdown = true; break; }
         rz = s2[0];
     }
@@ -327,16 +331,17 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters) {
 }
 
 // silhouette snapping (snap_vertices, nonrigid_stage.py:417-500)
+template <typename T>
 __device__ void surf_snap(const SurfCtx &c, double *v) {
     const SurfJob &J = *c.J;
     const SurfHyperDev &hp = c.hp;
     double cnt[4] = {0, 0, 0, 0};  // walked, reached, stuck, moved
-    for (int i = threadIdx.x; i < c.N; i += NT) {
+    for (int i = T::tid(); i < c.N; i += T::size) {
         st3(J.off0 + 3 * (size_t)i, v3(0, 0, 0));
         J.hold[i] = 0;
     }
-    __syncthreads();
-    for (int b = threadIdx.x; b < c.B; b += NT) {
+    T::sync();
+    for (int b = T::tid(); b < c.B; b += T::size) {
         const int i = J.bidx[b];
         J.hold[i] = 1;
         const V3 p = ld3(v + 3 * (size_t)i);
@@ -378,11 +383,11 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
             st3(J.off0 + 3 * (size_t)i, landed - p);
         }
     }
-    __syncthreads();
+    T::sync();
     // two uniform-Laplacian diffusion steps with the boundary held
     double *src = J.off0, *dst = J.off1;
     for (int round = 0; round < 2; ++round) {
-        for (int i = threadIdx.x; i < c.N; i += NT) {
+        for (int i = T::tid(); i < c.N; i += T::size) {
             if (J.hold[i]) { st3(dst + 3 * (size_t)i, ld3(src + 3 * (size_t)i)); continue; }
             V3 a = v3(0, 0, 0);
             for (int k = c.A.adj_ptr[i]; k < c.A.adj_ptr[i + 1]; ++k)
@@ -390,33 +395,35 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
             const double dg = (double)c.A.degrees[i];
             st3(dst + 3 * (size_t)i, v3(a.x / dg, a.y / dg, a.z / dg));
         }
-        __syncthreads();
+        T::sync();
         double *t = src; src = dst; dst = t;
     }
-    for (int i = threadIdx.x; i < c.N; i += NT) {
+    for (int i = T::tid(); i < c.N; i += T::size) {
         const V3 o = ld3(src + 3 * (size_t)i);
         st3(v + 3 * (size_t)i, ld3(v + 3 * (size_t)i) + o);
         cnt[3] += (o.x != 0.0 || o.y != 0.0 || o.z != 0.0) ? 1.0 : 0.0;
     }
-    block_sums<NT, 4>(cnt, c.red);
-    if (threadIdx.x == 0 && J.report) {
+    T::template sums<4>(cnt, c.red);
+    if (T::tid() == 0 && J.report) {
         J.report->snapped = 1;
         J.report->snap_walked = (int)cnt[0];
         J.report->snap_reached = (int)cnt[1];
         J.report->snap_stuck = (int)cnt[2];
         J.report->snap_moved = (int)cnt[3];
     }
-    __syncthreads();
+    T::sync();
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(NT, 1) k_surface_solve(const SurfJob *jobs, ActorDev A, CamDev cam,
-                                                         EdgeConstDev ec, SurfHyperDev hp, int H,
-                                                         int W) {
-    const SurfJob &J = jobs[blockIdx.x];
+template <int CS>
+__global__ void __launch_bounds__(NT, 1) k_surface_solve_t(const SurfJob *jobs, ActorDev A, CamDev cam,
+                                                           EdgeConstDev ec, SurfHyperDev hp, int H,
+                                                           int W) {
+    using T = Team<CS, NT>;
+    const SurfJob &J = jobs[T::stream()];
     if (!J.active) return;
-    __shared__ double red[8 * 32 + 16];
+    __shared__ double red[8 * 32 + 32];
     SurfCtx c;
     c.J = &J;
     c.obs = J.obs;
@@ -436,8 +443,8 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve(const SurfJob *jobs, Ac
     const bool has_field = J.has_field && c.obs.K > 0;
     c.sil_on = J.enable_sil && has_field;
     double *v = J.v;
-    for (int i = threadIdx.x; i < c.N * 3; i += NT) v[i] = J.v0[i];
-    __syncthreads();
+    for (int i = T::tid(); i < c.N * 3; i += T::size) v[i] = J.v0[i];
+    T::sync();
     lc_nonrigid_report *rep = J.report;
     if (J.do_solve) {
         const int levels = min(hp.gn, hp.n_levels);
@@ -446,33 +453,33 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve(const SurfJob *jobs, Ac
             const int level = min(it, levels - 1);
             double en[6];
             int counts[3];
-            surf_assemble(c, level, v, en, counts);
+            surf_assemble<T>(c, level, v, en, counts);
             for (int k = 0; k < 3; ++k) tot[k] += counts[k];
-            const bool breakdown = surf_pcg(c, hp.pcg);
+            const bool breakdown = surf_pcg<T>(c, hp.pcg);
             const double e0 = total_energy(en, c.has_prev);
             int halv = 0;
             bool rejected = false;
             double e1;
             for (;;) {
                 double et[6];
-                surf_energy(c, level, v, J.best, et);
+                surf_energy<T>(c, level, v, J.best, et);
                 e1 = total_energy(et, c.has_prev);
                 if (e1 <= e0) {
-                    for (int i = threadIdx.x; i < c.N * 3; i += NT) v[i] = v[i] + J.best[i];
-                    __syncthreads();
+                    for (int i = T::tid(); i < c.N * 3; i += T::size) v[i] = v[i] + J.best[i];
+                    T::sync();
                     break;
                 }
                 if (halv >= hp.max_halvings) { rejected = true; e1 = e0; break; }
-                for (int i = threadIdx.x; i < c.N * 3; i += NT) J.best[i] = 0.5 * J.best[i];
-                __syncthreads();
+                for (int i = T::tid(); i < c.N * 3; i += T::size) J.best[i] = 0.5 * J.best[i];
+                T::sync();
                 ++halv;
             }
-            if (threadIdx.x == 0 && J.counters) {
+            if (T::tid() == 0 && J.counters) {
                 J.counters[1] += 1;
                 J.counters[2] += hp.pcg;
                 J.counters[3] += halv + 1;
             }
-            if (threadIdx.x == 0 && rep && it < LC_MAX_LOG) {
+            if (T::tid() == 0 && rep && it < LC_MAX_LOG) {
                 rep->level[it] = level;
                 rep->energy_before[it] = e0;
                 rep->energy_after[it] = e1;
@@ -482,13 +489,13 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve(const SurfJob *jobs, Ac
                 rep->pcg_breakdown[it] = breakdown;
             }
         }
-        if (threadIdx.x == 0 && J.counters) {
+        if (T::tid() == 0 && J.counters) {
             J.counters[0] += 1;
             J.counters[4] += c.P;
             J.counters[5] += c.B;
             J.counters[6] += c.obs.K;
         }
-        if (threadIdx.x == 0 && rep) {
+        if (T::tid() == 0 && rep) {
             rep->n_iterations = hp.gn;
             rep->pruned = tot[0];
             rep->degenerate_edges = tot[1];
@@ -498,7 +505,12 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve(const SurfJob *jobs, Ac
             rep->n_boundary = c.B;
         }
     }
-    if (J.do_snap && has_field && c.B > 0) surf_snap(c, v);
+    if (J.do_snap && has_field && c.B > 0) surf_snap<T>(c, v);
 }
+
+template __global__ void k_surface_solve_t<1>(const SurfJob *, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
+template __global__ void k_surface_solve_t<4>(const SurfJob *, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
+template __global__ void k_surface_solve_t<8>(const SurfJob *, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
+template __global__ void k_surface_solve_t<16>(const SurfJob *, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
 
 int surface_block_threads() { return NT; }

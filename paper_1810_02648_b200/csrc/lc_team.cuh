@@ -1,0 +1,86 @@
+// A "team" is the set of CTAs that cooperate on one capture stream: a thread
+// block cluster of CS CTAs (CS = 1: a single CTA).  Phases are separated by
+// cluster barriers (barrier.cluster arrive.release / wait.acquire, which also
+// order the global-memory writes of one phase before the reads of the next),
+// and reductions are deterministic: every CTA tree-reduces its threads, then
+// every CTA sums the per-CTA partials in rank order through distributed
+// shared memory, so all CTAs hold bit-identical totals whatever the timing.
+#pragma once
+#include <cooperative_groups.h>
+#include "lc_device.cuh"
+
+namespace cg = cooperative_groups;
+
+template <int CS, int NT>
+struct Team {
+    static constexpr int size = CS * NT;
+    static constexpr int ctas = CS;
+
+    __device__ __forceinline__ static int rank() {
+        if constexpr (CS == 1) return 0;
+        else return (int)cg::this_cluster().block_rank();
+    }
+    // stream index of this CTA (clusters are laid out contiguously along x)
+    __device__ __forceinline__ static int stream() { return blockIdx.x / CS; }
+    __device__ __forceinline__ static int tid() { return rank() * NT + (int)threadIdx.x; }
+
+    __device__ __forceinline__ static void sync() {
+        if constexpr (CS == 1) __syncthreads();
+        else cg::this_cluster().sync();
+    }
+
+    // M simultaneous sums over every thread of the team.  `red` is a shared
+    // buffer of at least 8*32 + 2*8 doubles at the same offset in every CTA.
+    template <int M>
+    __device__ static void sums(double (&v)[M], double *red) {
+        static_assert(M <= 8, "at most 8 sums at once");
+        for (int m = 0; m < M; ++m)
+            for (int o = 16; o > 0; o >>= 1) v[m] += __shfl_down_sync(0xffffffffu, v[m], o);
+        const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+        __syncthreads();
+        if (l == 0)
+            for (int m = 0; m < M; ++m) red[m * 32 + w] = v[m];
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            for (int m = 0; m < M; ++m) {
+                double s = (l < NT / 32) ? red[m * 32 + l] : 0.0;
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+                if (l == 0) red[8 * 32 + m] = s;       // this CTA's partial
+            }
+        }
+        if constexpr (CS == 1) {
+            __syncthreads();
+            for (int m = 0; m < M; ++m) v[m] = red[8 * 32 + m];
+            __syncthreads();
+        } else {
+            auto cl = cg::this_cluster();
+            cl.sync();
+            if (threadIdx.x < M) {
+                double s = 0.0;
+                for (int r = 0; r < CS; ++r) s += cl.map_shared_rank(red, r)[8 * 32 + threadIdx.x];
+                red[8 * 32 + 8 + threadIdx.x] = s;
+            }
+            cl.sync();   // partials may be overwritten only after every CTA read them
+            for (int m = 0; m < M; ++m) v[m] = red[8 * 32 + 8 + m];
+            __syncthreads();
+        }
+    }
+
+    // element-wise sum of a per-CTA shared array `part[n]` over the team, in
+    // rank order, into `out[n]` (shared, every CTA).  Caller syncs after.
+    __device__ static void sum_arrays(const double *part, double *out, int n) {
+        if constexpr (CS == 1) {
+            for (int e = threadIdx.x; e < n; e += NT) out[e] = part[e];
+            __syncthreads();
+        } else {
+            auto cl = cg::this_cluster();
+            cl.sync();
+            for (int e = threadIdx.x; e < n; e += NT) {
+                double s = 0.0;
+                for (int r = 0; r < CS; ++r) s += cl.map_shared_rank(part, r)[e];
+                out[e] = s;
+            }
+            cl.sync();
+        }
+    }
+};

@@ -309,6 +309,26 @@ class Tracker:
                           jp if flags[0] else None, dr if flags[2] else None,
                           v1 if flags[3] else None, v2 if flags[4] else None)
 
+    def inspect(self, stream: int) -> dict:
+        """Last Stage II setup of a stream: boundary ids, enabled flags, visible
+        ids, normals2d, v_init, V^S (for parity tests)."""
+        out = {}
+        n = C.c_int64()
+        cap = 3 * self.N
+        for what, key in ((0, "boundary"), (1, "enabled"), (2, "visible")):
+            buf = np.empty(cap, dtype=np.int64)
+            L.check(self.ctx.lib.lc_tracker_inspect(self.handle, stream, what, L.ptr(buf), cap, C.byref(n)))
+            out[key] = buf[:n.value].copy()
+        out["enabled"] = out["enabled"].astype(bool)
+        buf = np.empty(cap)
+        L.check(self.ctx.lib.lc_tracker_inspect(self.handle, stream, 3, L.ptr(buf), cap, C.byref(n)))
+        out["normals2d"] = buf[:2 * n.value].reshape(-1, 2).copy()
+        for what, key in ((4, "v_init"), (5, "skinned")):
+            buf = np.empty((self.N, 3))
+            L.check(self.ctx.lib.lc_tracker_inspect(self.handle, stream, what, L.ptr(buf), cap, C.byref(n)))
+            out[key] = buf
+        return out
+
     def counters(self, stream: int) -> np.ndarray:
         out = np.zeros(8, dtype=np.int64)
         L.check(self.ctx.lib.lc_tracker_counters(self.handle, stream, L.ptr(out)))

@@ -10,19 +10,39 @@ from test_oracle_golden import check_digest, gen, load
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name,stable_frames", [("ref_frames_small128_dir0.npz", 4),
-                                                ("ref_frames_standard256_dir0.npz", 3),
-                                                ("ref_frames_small128_dir1.npz", 2)])
-def test_tracker_against_reference_sequence(name, stable_frames):
+def golden_state(actor, g, k):
+    """TrackState entering frame k, rebuilt from the reference's outputs of
+    frames k-1, k-2 (pipeline.py:281-299): teacher forcing."""
+    from oracle.geometry import Fk, qconj, qrot, skin
+    from paper_1810_02648_b200.config import TrackState
+    if k == 0:
+        return TrackState()
+    x1 = g["poses"][k - 1]
+    fk = Fk(actor.skeleton, x1)
+    _, rot, _, _ = skin(actor.mesh.rest_vertices, actor.skinning, fk.dqs)
+    disp = qrot(qconj(rot), g["vertices"][k - 1] - g["skinned"][k - 1])
+    return TrackState(x1, g["poses"][k - 2] if k >= 2 else None, fk.pos, disp, g["vertices"][k - 1],
+                      g["vertices"][k - 2] if k >= 2 else None)
+
+
+@pytest.mark.parametrize("name", ["ref_frames_small128_dir0.npz", "ref_frames_standard256_dir0.npz",
+                                  "ref_frames_small128_dir1.npz"])
+def test_tracker_against_reference_sequence(name):
+    """Every frame teacher-forced from the reference's own previous outputs."""
     from paper_1810_02648_b200.config import SequenceConfig
     from paper_1810_02648_b200.device import Tracker
     g = load(name)
     preset, res, n, directional, seed = g["meta"]
+    directional = bool(int(directional))
     actor, cam, frames = gen(preset, int(res), int(n), int(seed))
     check_digest(g, frames)
-    tr = Tracker(actor, cam, SequenceConfig(directional=bool(int(directional))), 1)
+    tr = Tracker(actor, cam, SequenceConfig(directional=directional), 1)
     diag = bbox_diag(actor)
-    for k, fr in enumerate(frames[:stable_frames]):
+    # default-directional frames >= 2 fail the oracle's own self-jitter screen
+    # (SURVEY.md §8c); compare them only when directional is off
+    last = len(frames) if not directional else 2
+    for k, fr in enumerate(frames[:last]):
+        tr.set_state(0, golden_state(actor, g, k))
         tr.set_frame(0, fr.image, fr.mask, fr.detections)
         tr.step()
         x, v, vs, rep = tr.result(0)
@@ -32,6 +52,23 @@ def test_tracker_against_reference_sequence(name, stable_frames):
         assert [rep.nonrigid.halvings[i] for i in range(rep.nonrigid.n_iterations)] == list(g["nr_halv"][k])
         pe = [rep.pose.energy_before[i] for i in range(rep.pose.n_iterations)]
         assert np.allclose(pe, g["pose_e0"][k][:len(pe)], rtol=1e-4), k
+        assert [rep.pose.halvings[i] for i in range(rep.pose.n_iterations)] == \
+            list(g["pose_halv"][k][:len(pe)]), k
+
+
+def test_free_running_first_frames_match_reference():
+    """Free-running (no state injection): the frames before the recursion's
+    amplification of fp64 reordering noise (frames 0-1) match the reference."""
+    from paper_1810_02648_b200.config import SequenceConfig
+    from paper_1810_02648_b200.device import Tracker
+    g = load("ref_frames_small128_dir0.npz")
+    actor, cam, frames = gen("small", 128, 4, 0)
+    tr = Tracker(actor, cam, SequenceConfig(directional=False), 1)
+    for k, fr in enumerate(frames[:2]):
+        tr.set_frame(0, fr.image, fr.mask, fr.detections)
+        tr.step()
+        _, v, _, _ = tr.result(0)
+        assert np.abs(v - g["vertices"][k]).max() <= 1e-4 * bbox_diag(actor), k
 
 
 def test_kernels_against_reference():
