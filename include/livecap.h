@@ -272,6 +272,9 @@ int lc_profile_read(lc_ctx *ctx, double *total_ms, int64_t *count);
  * 5: V^S (N*3 f64).  n_out = element count written (rows for 0-3). */
 int lc_tracker_inspect(lc_tracker *tr, int32_t stream, int32_t what, void *out, int64_t capacity,
                        int64_t *n_out);
+/* %globaltimer stamps (ns) at the phase boundaries of the last pose / surface
+ * solve of a stream (64 slots each; profiling aid) */
+int lc_tracker_phase_times(lc_tracker *tr, int32_t stream, int64_t *pose_ns, int64_t *surf_ns);
 /* device pointer of a stream's resident vertices (N*3) for zero-copy readers */
 int lc_tracker_device_vertices(lc_tracker *tr, int32_t stream, uint64_t *dptr);
 

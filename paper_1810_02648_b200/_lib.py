@@ -143,6 +143,7 @@ _SIGS = {
     "lc_debug_tables": (C.c_int, [i32, P, P]),
     "lc_tracker_counters": (C.c_int, [P, i32, P]),
     "lc_tracker_inspect": (C.c_int, [P, i32, i32, P, i64, P]),
+    "lc_tracker_phase_times": (C.c_int, [P, i32, P, P]),
     "lc_profile_kernel": (C.c_int, [P, C.c_char_p]),
     "lc_profile_read": (C.c_int, [P, P, P]),
 }

@@ -454,9 +454,13 @@ static void alloc_grid(DevArena &m, GridBufs &g, int H, int W) {
     g.K = m.alloc<int>(1);
     g.cand_cnt = m.alloc<int>(ncx * ncy);
     g.cand_range = m.alloc<int2>(ncx * ncy);
-    g.cand_pts = m.alloc<int>((size_t)ncx * ncy * LC_CAND_PER_CELL);
+    g.cand_pts = m.alloc<int2>((size_t)ncx * ncy * LC_CAND_PER_CELL);
     g.cand_total = m.alloc<int>(1);
     g.cand_u2 = m.alloc<double>(ncx * ncy);
+    g.qP = 1;
+    g.qL = 0;
+    while (g.qP < std::max(ncx, ncy)) { g.qP *= 2; g.qL++; }
+    g.quad = m.alloc<int>(quad_off(g.qP, g.qL + 1));
 }
 
 void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) {
@@ -523,6 +527,10 @@ void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) 
     pose_rep = mem.alloc<lc_pose_report>(1);
     nr_rep = mem.alloc<lc_nonrigid_report>(1);
     counters = mem.alloc<long long>(LC_NCOUNTERS);
+    phase_pose = mem.alloc<long long>(LC_NPHASE);
+    phase_surf = mem.alloc<long long>(LC_NPHASE);
+    cudaMemset(phase_pose, 0, sizeof(long long) * LC_NPHASE);
+    cudaMemset(phase_surf, 0, sizeof(long long) * LC_NPHASE);
     cudaMemset(counters, 0, sizeof(long long) * LC_NCOUNTERS);
 }
 
@@ -544,6 +552,9 @@ static NnGridDev grid_dev(const GridBufs &g, const uint8_t *mask, int H, int W) 
     d.mask = mask;
     d.cand_range = g.cand_range;
     d.cand_pts = g.cand_pts;
+    d.quad = g.quad;
+    d.qP = g.qP;
+    d.qL = g.qL;
     return d;
 }
 
@@ -561,6 +572,7 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
         j.cand_cnt = p.first->cand_cnt; j.cand_range = p.first->cand_range;
         j.cand_pts = p.first->cand_pts; j.cand_total = p.first->cand_total;
         j.cand_u2 = p.first->cand_u2; j.max_ring = max_ring;
+        j.quad = p.first->quad; j.qP = p.first->qP; j.qL = p.first->qL;
         jobs.push_back(j);
     }
     const GridJob *dj = stage(c, jobs);
@@ -571,6 +583,7 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
     launch(c, k_contour_scan_rows, dim3(S), dim3(1024), 0, dj, H, ncx * ncy);
     launch(c, k_contour_emit, dim3(rows_grid, S), dim3(256), 0, dj, H, W, ncx);
     launch(c, k_contour_scan_cells, dim3(S), dim3(1024), 0, dj, ncx * ncy);
+    launch(c, k_quad_build, dim3(S), dim3(1024), 0, dj, ncx, ncy);
     launch(c, k_contour_fill, dim3(64, S), dim3(256), 0, dj, ncx);
     launch(c, k_cand_count, dim3((ncx * ncy + 7) / 8, S), dim3(256), 0, dj, H, W);
     launch(c, k_cand_scan, dim3(S), dim3(1024), 0, dj, ncx * ncy);
@@ -992,6 +1005,7 @@ static void run_frame(FrameBatch &fb) {
             p.directional = cfg.directional;
             p.report = s->pose_rep;
             p.log_offset = log_off[i];
+            p.phase = s->phase_pose;
             log_off[i] += h.gn_iterations;
             pj.push_back(p);
             ++k;
@@ -1026,6 +1040,7 @@ static void run_frame(FrameBatch &fb) {
             j.off0 = s->off0; j.off1 = s->off1; j.hold = s->hold;
             j.report = s->nr_rep;
             j.counters = s->counters;
+            j.phase = s->phase_surf;
             sj.push_back(j);
         }
         surface_launch(c, a, fb.cam, *fb.cf, sj);
@@ -1256,6 +1271,17 @@ extern "C" int lc_tracker_inspect(lc_tracker *t, int32_t stream, int32_t what, v
     } else {
         return fail(LC_EINVAL, "unknown inspect target");
     }
+    return LC_OK;
+    API_END
+}
+
+extern "C" int lc_tracker_phase_times(lc_tracker *t, int32_t stream, int64_t *pose_ns, int64_t *surf_ns) {
+    API_BEGIN
+    require(t != nullptr, "null tracker");
+    require(stream >= 0 && stream < t->S, "stream index out of range");
+    Slot *s = t->slots[stream];
+    if (pose_ns) CK(cudaMemcpy(pose_ns, s->phase_pose, sizeof(long long) * LC_NPHASE, cudaMemcpyDeviceToHost));
+    if (surf_ns) CK(cudaMemcpy(surf_ns, s->phase_surf, sizeof(long long) * LC_NPHASE, cudaMemcpyDeviceToHost));
     return LC_OK;
     API_END
 }

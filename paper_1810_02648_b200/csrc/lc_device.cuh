@@ -11,6 +11,14 @@
 
 #define LC_INF (__longlong_as_double(0x7ff0000000000000LL))
 
+// nanosecond device clock (phase timing of the persistent solvers)
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define LC_NPHASE 64
+
 struct V3 { double x, y, z; };
 
 __device__ __forceinline__ V3 v3(double x, double y, double z) { return V3{x, y, z}; }
@@ -133,42 +141,78 @@ __device__ __forceinline__ void nn_consider(const NnGridDev &g, int pid, double 
     if (d2 < best || (d2 == best && pid < bi)) { best = d2; bi = pid; }
 }
 
+// packed candidate: one 8-byte load carries the coordinates and the id
+__device__ __forceinline__ void nn_consider_packed(int2 c, double qx, double qy, double &best, int &bi) {
+    const double dx = qx - (double)(c.x & 0xffff), dy = qy - (double)(c.x >> 16);
+    const double d2 = dx * dx + dy * dy;
+    if (d2 < best || (d2 == best && c.y < bi)) { best = d2; bi = c.y; }
+}
+
+__device__ __forceinline__ double box_dist2(double qx, double qy, double x0, double y0, double s) {
+    const double dx = qx < x0 ? x0 - qx : (qx > x0 + s ? qx - (x0 + s) : 0.0);
+    const double dy = qy < y0 ? y0 - qy : (qy > y0 + s ? qy - (y0 + s) : 0.0);
+    return dx * dx + dy * dy;
+}
+
+// Exact best-first search of the site-count quadtree: a subtree is skipped
+// only when its box is strictly farther than the best distance so far, so
+// equidistant sites are still all seen and the lowest index wins.
+__device__ inline void nn_quadtree(const NnGridDev &g, double qx, double qy, double &best, int &bi) {
+    int stack[3 * 12 + 2];
+    int sp = 0;
+    stack[sp++] = g.qL << 24;                       // root: level qL, (0, 0)
+    while (sp > 0) {
+        const int e = stack[--sp];
+        const int l = e >> 24, ny = (e >> 12) & 0xfff, nx = e & 0xfff;
+        const int side = g.qP >> l;
+        if (g.quad[quad_off(g.qP, l) + ny * side + nx] == 0) continue;
+        const double s = (double)(LC_GRID_CELL << l);
+        if (box_dist2(qx, qy, nx * s, ny * s, s) > best) continue;
+        if (l == 0) {
+            if (nx < g.ncx && ny < g.ncy) {
+                const int c = ny * g.ncx + nx;
+                for (int k = g.cell_start[c]; k < g.cell_start[c + 1]; ++k) nn_consider(g, g.cell_pts[k], qx, qy, best, bi);
+            }
+            continue;
+        }
+        // push the 4 children, nearest last (popped first)
+        int ch[4];
+        double d[4];
+        const double cs = s * 0.5;
+        for (int k = 0; k < 4; ++k) {
+            const int cx = 2 * nx + (k & 1), cy = 2 * ny + (k >> 1);
+            ch[k] = ((l - 1) << 24) | (cy << 12) | cx;
+            d[k] = box_dist2(qx, qy, cx * cs, cy * cs, cs);
+        }
+        for (int i = 1; i < 4; ++i)      // sort descending by distance
+            for (int j = i; j > 0 && d[j] > d[j - 1]; --j) {
+                const double td = d[j]; d[j] = d[j - 1]; d[j - 1] = td;
+                const int tc = ch[j]; ch[j] = ch[j - 1]; ch[j - 1] = tc;
+            }
+        for (int k = 0; k < 4; ++k) stack[sp++] = ch[k];
+    }
+}
+
 __device__ inline int nn_query(const NnGridDev &g, double qx, double qy, double &d2out) {
     double best = LC_INF;
     int bi = 0x7fffffff;
     const double gx = (double)(g.ncx * LC_GRID_CELL), gy = (double)(g.ncy * LC_GRID_CELL);
-    if (!(qx >= 0.0 && qy >= 0.0 && qx < gx && qy < gy)) {
-        for (int k = 0; k < g.K; ++k) nn_consider(g, k, qx, qy, best, bi);
-        d2out = best;
-        return bi;
-    }
-    const int cx = (int)qx >> LC_GRID_SHIFT, cy = (int)qy >> LC_GRID_SHIFT;
-    if (g.cand_range) {
+    const bool in_grid = qx >= 0.0 && qy >= 0.0 && qx < gx && qy < gy;
+    if (in_grid && g.cand_range) {
+        const int cx = (int)qx >> LC_GRID_SHIFT, cy = (int)qy >> LC_GRID_SHIFT;
         const int2 rg = g.cand_range[cy * g.ncx + cx];
         if (rg.y >= 0) {
-            for (int k = rg.x; k < rg.x + rg.y; ++k) nn_consider(g, g.cand_pts[k], qx, qy, best, bi);
+            for (int k = rg.x; k < rg.x + rg.y; ++k) nn_consider_packed(g.cand_pts[k], qx, qy, best, bi);
             d2out = best;
             return bi;
         }
     }
-    const int rmax = max(max(cx, g.ncx - 1 - cx), max(cy, g.ncy - 1 - cy));
-    // after ring r every unvisited point is > r*CELL away (strictly), so the
-    // search may stop as soon as the best squared distance is <= (r*CELL)^2
-    for (int r = 0; r <= rmax; ++r) {
-        for (int yy = cy - r; yy <= cy + r; ++yy) {
-            if (yy < 0 || yy >= g.ncy) continue;
-            const bool full_row = (yy == cy - r) || (yy == cy + r);
-            const int stride = full_row ? 1 : 2 * r;
-            for (int xx = cx - r; xx <= cx + r; xx += stride) {
-                if (xx < 0 || xx >= g.ncx) continue;
-                const int c = yy * g.ncx + xx;
-                const int s = g.cell_start[c], e = g.cell_start[c + 1];
-                for (int k = s; k < e; ++k) nn_consider(g, g.cell_pts[k], qx, qy, best, bi);
-            }
-        }
-        const double lim = (double)(r * LC_GRID_CELL);
-        if (best <= lim * lim) break;
+    if (g.quad) {
+        nn_quadtree(g, qx, qy, best, bi);
+        d2out = best;
+        return bi;
     }
+    for (int k = 0; k < g.K; ++k) nn_consider(g, k, qx, qy, best, bi);
     d2out = best;
     return bi;
 }

@@ -75,8 +75,17 @@ struct NnGridDev {
     // exact per-cell candidate lists (null -> ring search): cand_range[c] =
     // (start, count); count < 0 marks an overflowed cell (ring search there)
     const int2 *cand_range; // ncx*ncy
-    const int *cand_pts;
+    const int2 *cand_pts;   // (x | y << 16, site id)
+    // site-count quadtree over the cells padded to qP x qP (qP = 2^qL):
+    // level l (leaves l = 0) stores (qP>>l)^2 counts at offset quad_off(l)
+    const int *quad;
+    int qP, qL;
 };
+__host__ __device__ __forceinline__ int quad_off(int P, int l) {
+    int o = 0;
+    for (int k = 0; k < l; ++k) o += (P >> k) * (P >> k);
+    return o;
+}
 #define LC_CAND_PER_CELL 128   // average candidate capacity per cell
 #define LC_CAND_MAX 1024       // per-cell cap before falling back to the ring search
 

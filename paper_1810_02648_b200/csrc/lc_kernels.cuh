@@ -24,9 +24,11 @@ struct GridJob {
     int *K;                // out: contour pixel count
     int *cand_cnt;         // ncells
     int2 *cand_range;      // ncells
-    int *cand_pts;         // capacity ncells * LC_CAND_PER_CELL
+    int2 *cand_pts;        // capacity ncells * LC_CAND_PER_CELL: (x | y << 16, id)
     int *cand_total;       // 1
     double *cand_u2;       // ncells: per-cell bound U^2 (count -> fill)
+    int *quad;             // site-count quadtree (see NnGridDev)
+    int qP, qL;
     int max_ring;          // cells with no site within this many rings use the ring search
 };
 __global__ void k_contour_rows(const GridJob *jobs, int H, int W);
@@ -35,6 +37,7 @@ __global__ void k_contour_emit(const GridJob *jobs, int H, int W, int ncx);
 __global__ void k_contour_scan_cells(const GridJob *jobs, int ncells);
 __global__ void k_contour_fill(const GridJob *jobs, int ncx);
 __global__ void k_cand_count(const GridJob *jobs, int H, int W);
+__global__ void k_quad_build(const GridJob *jobs, int ncx, int ncy);
 __global__ void k_cand_scan(const GridJob *jobs, int ncells);
 __global__ void k_cand_fill(const GridJob *jobs, int H, int W);
 

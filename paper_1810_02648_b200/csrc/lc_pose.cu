@@ -350,6 +350,12 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(const PoseJob *jobs, con
 
     lc_pose_report *rep = J.report;
     int log0 = J.log_offset;
+    int ph = 0;
+    auto stamp = [&]() {
+        if (J.phase && T::tid() == 0 && ph < LC_NPHASE) J.phase[ph] = gtimer();
+        ++ph;
+    };
+    stamp();
     int behind_total = 0, gimbal = 0;
     for (int it = 0; it < J.hp.gn; ++it) {
         for (int i = threadIdx.x; i < LC_NP; i += NT) s.xt[i] = s.x[i];
@@ -357,12 +363,14 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(const PoseJob *jobs, con
         double terms[5];
         int behind;
         const double e0 = pose_eval<T>(c, true, terms, behind);
+        stamp();
         behind_total += behind;
         gimbal |= s.f.gimbal;
         double damping;
         const bool damped = dense_solve_block<NT>(s.qr, s.A, s.rhs, LC_NP, damping);
         for (int i = threadIdx.x; i < LC_NP; i += NT) s.step[i] = s.qr.x[i];
         __syncthreads();
+        stamp();
         int halv = 0;
         bool rejected = false;
         double e1;
@@ -386,6 +394,7 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(const PoseJob *jobs, con
             __syncthreads();
             ++halv;
         }
+        stamp();
         if (T::tid() == 0 && rep) {
             const int k = log0 + it;
             if (k < LC_MAX_LOG) {

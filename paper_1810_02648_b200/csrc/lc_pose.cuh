@@ -23,6 +23,7 @@ struct PoseJob {
     int directional;
     lc_pose_report *report;
     int log_offset;
+    long long *phase;         // LC_NPHASE timestamps (or null)
 };
 
 struct SurfJob {
@@ -51,6 +52,7 @@ struct SurfJob {
     uint8_t *hold;            // N
     lc_nonrigid_report *report;
     long long *counters;      // cumulative: frames, gn, pcg iters, trials, P, B, K (or null)
+    long long *phase;         // LC_NPHASE timestamps (or null)
 };
 
 template <int CS>

@@ -59,9 +59,12 @@ struct lc_actor {
 struct GridBufs {
     int *row_count, *row_start, *cell_count, *cell_start, *cell_fill, *cell_pts, *K;
     int2 *pts;
-    int *cand_cnt, *cand_pts, *cand_total;
+    int *cand_cnt, *cand_total;
+    int2 *cand_pts;
     int2 *cand_range;
     double *cand_u2;
+    int *quad;
+    int qP, qL;
 };
 
 // per-stream device state + scratch
@@ -99,6 +102,7 @@ struct Slot {
     lc_pose_report *pose_rep;
     lc_nonrigid_report *nr_rep;
     long long *counters;   // LC_NCOUNTERS cumulative work counters (device)
+    long long *phase_pose, *phase_surf;   // LC_NPHASE timestamps of the last solves
     void allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J);
 };
 

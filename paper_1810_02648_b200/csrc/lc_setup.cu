@@ -168,6 +168,28 @@ __global__ void k_contour_fill(const GridJob *jobs, int ncx) {
     }
 }
 
+// ---- site-count quadtree over the cells (one CTA per stream) -------------
+__global__ void k_quad_build(const GridJob *jobs, int ncx, int ncy) {
+    const GridJob J = jobs[blockIdx.x];
+    const int P = J.qP;
+    for (int i = threadIdx.x; i < P * P; i += blockDim.x) {
+        const int cx = i % P, cy = i / P;
+        J.quad[i] = (cx < ncx && cy < ncy) ? J.cell_count[cy * ncx + cx] : 0;
+    }
+    __syncthreads();
+    for (int l = 1; l <= J.qL; ++l) {
+        const int side = P >> l, cside = side * 2;
+        const int o = quad_off(P, l), co = quad_off(P, l - 1);
+        for (int i = threadIdx.x; i < side * side; i += blockDim.x) {
+            const int x = i % side, y = i / side;
+            const int *c = J.quad + co;
+            J.quad[o + i] = c[(2 * y) * cside + 2 * x] + c[(2 * y) * cside + 2 * x + 1]
+                          + c[(2 * y + 1) * cside + 2 * x] + c[(2 * y + 1) * cside + 2 * x + 1];
+        }
+        __syncthreads();
+    }
+}
+
 // ---- exact per-cell candidate lists (see NnGridDev) -----------------------
 
 __device__ __forceinline__ NnGridDev grid_of(const GridJob &J, int H, int W) {
@@ -177,6 +199,7 @@ __device__ __forceinline__ NnGridDev grid_of(const GridJob &J, int H, int W) {
     g.ncx = (W + LC_GRID_CELL - 1) / LC_GRID_CELL;
     g.ncy = (H + LC_GRID_CELL - 1) / LC_GRID_CELL;
     g.pts = J.pts; g.cell_start = J.cell_start; g.cell_pts = J.cell_pts;
+    g.quad = J.quad; g.qP = J.qP; g.qL = J.qL;
     return g;
 }
 
@@ -274,8 +297,9 @@ __global__ void k_cand_fill(const GridJob *jobs, int H, int W) {
         // append order inside a list is irrelevant: ties break on the point index
         ring_visit_warp(g, cx, cy,
                         [&](int pid) {
-                            if (cell_near2(cx, cy, g.pts[pid]) <= u2)
-                                J.cand_pts[rg.x + atomicAdd(&J.cell_fill[c], 1)] = pid;
+                            const int2 p = g.pts[pid];
+                            if (cell_near2(cx, cy, p) <= u2)
+                                J.cand_pts[rg.x + atomicAdd(&J.cell_fill[c], 1)] = make_int2(p.x | (p.y << 16), pid);
                         },
                         [&](int r) {
                             const double lim = (double)(r * LC_GRID_CELL);

@@ -414,6 +414,12 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
     T::sync();
 }
 
+template <typename T>
+__device__ __forceinline__ void stamp(const SurfJob &J, int &k) {
+    if (J.phase && T::tid() == 0 && k < LC_NPHASE) J.phase[k] = gtimer();
+    ++k;
+}
+
 }  // namespace
 
 template <int CS>
@@ -446,6 +452,8 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve_t(const SurfJob *jobs, 
     for (int i = T::tid(); i < c.N * 3; i += T::size) v[i] = J.v0[i];
     T::sync();
     lc_nonrigid_report *rep = J.report;
+    int ph = 0;
+    stamp<T>(J, ph);
     if (J.do_solve) {
         const int levels = min(hp.gn, hp.n_levels);
         int tot[3] = {0, 0, 0};
@@ -454,8 +462,10 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve_t(const SurfJob *jobs, 
             double en[6];
             int counts[3];
             surf_assemble<T>(c, level, v, en, counts);
+            stamp<T>(J, ph);
             for (int k = 0; k < 3; ++k) tot[k] += counts[k];
             const bool breakdown = surf_pcg<T>(c, hp.pcg);
+            stamp<T>(J, ph);
             const double e0 = total_energy(en, c.has_prev);
             int halv = 0;
             bool rejected = false;
@@ -474,6 +484,7 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve_t(const SurfJob *jobs, 
                 T::sync();
                 ++halv;
             }
+            stamp<T>(J, ph);
             if (T::tid() == 0 && J.counters) {
                 J.counters[1] += 1;
                 J.counters[2] += hp.pcg;
@@ -506,6 +517,7 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve_t(const SurfJob *jobs, 
         }
     }
     if (J.do_snap && has_field && c.B > 0) surf_snap<T>(c, v);
+    stamp<T>(J, ph);
 }
 
 template __global__ void k_surface_solve_t<1>(const SurfJob *, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);

@@ -1,0 +1,51 @@
+"""CPU, world_size 2 over gloo: the stream-sharding host logic of bench.py
+(disjoint seeds per rank, max-over-ranks timing, whole-job aggregation)."""
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    seeds = bench.shard_seeds(rank, 4)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, seeds)
+    fake_ms = torch.tensor([100.0 + 50.0 * rank], dtype=torch.float64)
+    dist.all_reduce(fake_ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        out.put((gathered, float(fake_ms.item()), bench.aggregate_fps([fake_ms.item()], world, 4, 10)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharding_two_ranks():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    gathered, ms, fps = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert gathered[0] == [0, 1, 2, 3] and gathered[1] == [4, 5, 6, 7]
+    assert not set(gathered[0]) & set(gathered[1])
+    assert ms == 150.0
+    assert fps == pytest.approx(2 * 4 * 10 / 0.150)

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--frames", type=int, default=4)
     ap.add_argument("--preset", default="x5k")
     ap.add_argument("--res", type=int, default=1024)
+    ap.add_argument("--phases", action="store_true")
     a = ap.parse_args()
     from paper_1810_02648_b200 import _lib
     from paper_1810_02648_b200 import synthetic as S
@@ -41,6 +42,14 @@ def main():
         tr.step()
         ctx.synchronize()
         print(f"frame {f}: {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
+        if a.phases:
+            import numpy as np
+            pp, ss = np.zeros(64, dtype=np.int64), np.zeros(64, dtype=np.int64)
+            _lib.check(ctx.lib.lc_tracker_phase_times(tr.handle, 0, _lib.ptr(pp), _lib.ptr(ss)))
+            for name, arr in (("pose", pp), ("surface", ss)):
+                n = int(np.count_nonzero(arr))
+                d = np.diff(arr[:n]) / 1e3
+                print(f"   {name} phases (us): " + " ".join(f"{x:.0f}" for x in d) + f"  total {d.sum():.0f}")
 
 
 if __name__ == "__main__":
