@@ -193,6 +193,8 @@ extern "C" int lc_ctx_create(int32_t device, uint64_t cuda_stream, lc_ctx **out)
         CK(cudaFuncSetAttribute(k_pose_solve_t<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CK(cudaFuncSetAttribute(k_pose_solve_t<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         CK(cudaFuncSetAttribute(k_surface_solve_t<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        CK(cudaFuncSetAttribute(k_pyramid_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pyramid_fused_smem()));
     }
     *out = c;
     return LC_OK;
@@ -734,6 +736,18 @@ static void build_config(lc_ctx *c, const lc_actor *a, const lc_nonrigid_hyper *
 
 static void pyramid(lc_ctx *c, const ConfigDev &cf, const std::vector<Slot *> &slots, int levels) {
     if (slots.empty()) return;
+    bool fused = levels <= 4;
+    for (int l = 0; l < levels; ++l) fused = fused && cf.half[l] <= LC_PYR_HALO;
+    if (fused) {
+        const int H = slots[0]->H, W = slots[0]->W;
+        std::vector<PyrAllJob> jobs;
+        for (Slot *s : slots) jobs.push_back(PyrAllJob{s->image_src, s->pyr});
+        const int tiles = ((W + LC_PYR_TILE - 1) / LC_PYR_TILE) * ((H + LC_PYR_TILE - 1) / LC_PYR_TILE);
+        launch(c, k_pyramid_fused, dim3(tiles, (unsigned)slots.size()), dim3(256), pyramid_fused_smem(),
+               stage(c, jobs), H, W, levels, (const double *)cf.taps, cf.half[0], cf.half[1], cf.half[2],
+               cf.half[3]);
+        return;
+    }
     const int H = slots[0]->H, W = slots[0]->W;
     const long long n = (long long)H * W * 3;
     const int grid = (int)std::min<long long>((n + 255) / 256, 2368);
@@ -1615,6 +1629,25 @@ extern "C" int lc_gaussian_pyramid(lc_ctx *c, int32_t h, int32_t w, int32_t ch, 
     double *tmp = m.alloc<double>(n);
     double *dst = m.alloc<double>(n * n_levels);
     const int grid = (int)std::min<size_t>((n + 255) / 256, 2368);
+    bool fused = ch == 3 && n_levels <= 4 && given_taps;
+    for (int l = 0; l < n_levels && fused; ++l) fused = kernel_sizes[l] <= 2 * LC_PYR_HALO + 1;
+    if (fused) {
+        std::vector<double> taps(given_taps, given_taps + 32 * n_levels);
+        taps.resize(4 * 32, 0.0);
+        double *dt = m.upload(taps.data(), taps.size(), st);
+        int hs[4] = {0, 0, 0, 0};
+        for (int l = 0; l < n_levels; ++l) {
+            require(kernel_sizes[l] >= 1 && kernel_sizes[l] % 2 == 1, "kernel size must be odd and positive");
+            hs[l] = kernel_sizes[l] / 2;
+        }
+        const int tiles = ((w + LC_PYR_TILE - 1) / LC_PYR_TILE) * ((h + LC_PYR_TILE - 1) / LC_PYR_TILE);
+        const PyrAllJob *dj = stage(c, std::vector<PyrAllJob>{PyrAllJob{src, dst}});
+        launch(c, k_pyramid_fused, dim3(tiles), dim3(256), pyramid_fused_smem(), dj, h, w, n_levels,
+               (const double *)dt, hs[0], hs[1], hs[2], hs[3]);
+        CK(cudaMemcpyAsync(out, dst, n * n_levels * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return last_launch_status();
+    }
     for (int l = 0; l < n_levels; ++l) {
         const int k = kernel_sizes[l];
         require(k >= 1 && k % 2 == 1, "kernel size must be odd and positive");

@@ -202,7 +202,23 @@ __device__ inline int nn_query(const NnGridDev &g, double qx, double qy, double 
         const int cx = (int)qx >> LC_GRID_SHIFT, cy = (int)qy >> LC_GRID_SHIFT;
         const int2 rg = g.cand_range[cy * g.ncx + cx];
         if (rg.y >= 0) {
-            for (int k = rg.x; k < rg.x + rg.y; ++k) nn_consider_packed(g.cand_pts[k], qx, qy, best, bi);
+            // 4 independent (best, id) chains expose memory-level parallelism;
+            // merging keeps the minimum with the lowest id on ties (exact)
+            double b1 = LC_INF, b2 = LC_INF, b3 = LC_INF;
+            int i1 = 0x7fffffff, i2 = 0x7fffffff, i3 = 0x7fffffff;
+            const int2 *cp = g.cand_pts + rg.x;
+            int k = 0;
+            for (; k + 4 <= rg.y; k += 4) {
+                const int2 c0 = __ldg(cp + k), c1 = __ldg(cp + k + 1), c2 = __ldg(cp + k + 2), c3 = __ldg(cp + k + 3);
+                nn_consider_packed(c0, qx, qy, best, bi);
+                nn_consider_packed(c1, qx, qy, b1, i1);
+                nn_consider_packed(c2, qx, qy, b2, i2);
+                nn_consider_packed(c3, qx, qy, b3, i3);
+            }
+            for (; k < rg.y; ++k) nn_consider_packed(__ldg(cp + k), qx, qy, best, bi);
+            if (b1 < best || (b1 == best && i1 < bi)) { best = b1; bi = i1; }
+            if (b2 < best || (b2 == best && i2 < bi)) { best = b2; bi = i2; }
+            if (b3 < best || (b3 == best && i3 < bi)) { best = b3; bi = i3; }
             d2out = best;
             return bi;
         }

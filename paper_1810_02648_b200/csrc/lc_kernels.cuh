@@ -10,6 +10,16 @@ struct PyrJob {
 };
 __global__ void k_blur_axis(const PyrJob *jobs, int H, int W, int C, const double *taps, int half,
                             int axis);
+// all levels of an (H,W,3) image from one haloed tile per CTA (levels*H*W*3 out)
+#define LC_PYR_TILE 32
+#define LC_PYR_HALO 7
+struct PyrAllJob {
+    const double *src;   // H*W*3
+    double *dst;         // levels*H*W*3
+};
+__global__ void k_pyramid_fused(const PyrAllJob *jobs, int H, int W, int levels, const double *taps,
+                                int h0, int h1, int h2, int h3);
+size_t pyramid_fused_smem();
 
 // ----- mask contour + NN grid (imageproc.py:34-49,186-193) -----------------
 struct GridJob {

@@ -323,6 +323,7 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(const PoseJob *jobs, con
     extern __shared__ __align__(16) unsigned char dsm[];
     PoseSmem &s = *reinterpret_cast<PoseSmem *>(dsm);
     double *tail = reinterpret_cast<double *>(dsm + ((sizeof(PoseSmem) + 15) & ~size_t(15)));
+    if (threadIdx.x == 0) *reinterpret_cast<int *>(s.red + 8 * 32 + 24) = 0;   // Team::sums parity
     {
         const int *src = reinterpret_cast<const int *>(skg);
         int *dst = reinterpret_cast<int *>(&s.sk);

@@ -16,12 +16,16 @@ struct QrSmemT {
     double v[MAXN];
     double rdiag[MAXN];
     double x[MAXN];
+    double w[MAXN + 1];
     double tau;
     int skip;
 };
 using QrSmem = QrSmemT<LC_QR_MAXN>;
 
-// Householder on columns 0..n-1 of the augmented (n x n+1) matrix
+// Householder on columns 0..n-1 of the augmented (n x n+1) matrix.
+// Per column: warp 0 forms the reflector (shuffle-reduced norm), one thread
+// per trailing column forms w_j = v . a_j serially (no shuffle chains on the
+// critical path), then every thread updates the trailing block.
 template <int NT, typename S>
 __device__ void qr_factor(S &s, int n) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -43,19 +47,25 @@ __device__ void qr_factor(S &s, int n) {
             }
         }
         __syncthreads();
+        const int m = n - k;            // rows k..n-1
+        const int ncol = n - k;         // columns k+1..n (incl. the rhs column n)
         if (!s.skip) {
-            for (int j = k + 1 + w; j <= n; j += NT / 32) {
+            for (int jj = threadIdx.x; jj < ncol; jj += NT) {
+                const int j = k + 1 + jj;
                 double d = 0.0;
-                for (int i = k + lane; i < n; i += 32) d += s.v[i] * s.a[i][j];
-                for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-                const double f = s.tau * d;
-                for (int i = k + lane; i < n; i += 32) s.a[i][j] -= f * s.v[i];
+                for (int i = k; i < n; ++i) d += s.v[i] * s.a[i][j];
+                s.w[jj] = s.tau * d;
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < m * ncol; e += NT) {
+                const int i = k + e / ncol, jj = e % ncol;
+                s.a[i][k + 1 + jj] -= s.w[jj] * s.v[i];
             }
         }
         __syncthreads();
         if (threadIdx.x == 0) s.a[k][k] = s.rdiag[k];
-        __syncthreads();
     }
+    __syncthreads();
 }
 
 // back substitution R x = (Q^T b) on warp 0 (column n holds Q^T b)

@@ -39,6 +39,106 @@ __global__ void k_blur_axis(const PyrJob *jobs, int H, int W, int C, const doubl
     }
 }
 
+// One CTA per 32x32 output tile and stream: the haloed input tile is loaded
+// once (coordinates clamped = mode "nearest"), then for every level the
+// vertical pass fills a shared intermediate over the tile columns +- halo and
+// the horizontal pass writes the level.  Each output is the same expression
+// in the same order as the two-pass version, so results are bit-identical.
+size_t pyramid_fused_smem() {
+    const int T = LC_PYR_TILE, E = LC_PYR_TILE + 2 * LC_PYR_HALO;
+    return sizeof(double) * 3 * ((size_t)E * E + (size_t)T * E);
+}
+
+// Register-blocked passes: a thread owns RB consecutive outputs along the
+// filter axis and loads its (RB + 2*HH)-wide window once.  Each output is
+// still  w[c]*x[0] + (x[-h]+x[h])*w[h] + ... + (x[-1]+x[1])*w[1]  in that order.
+template <int HH>
+__device__ __forceinline__ void pyr_level(const double *__restrict__ in, double *__restrict__ mid,
+                                          double *__restrict__ out, const double *__restrict__ tp,
+                                          int tx0, int ty0, int H, int W) {
+    constexpr int T = LC_PYR_TILE, R = LC_PYR_HALO, E = T + 2 * R, RB = 8, NWIN = RB + 2 * HH;
+    double t[HH + 1];
+#pragma unroll
+    for (int j = 0; j <= HH; ++j) t[j] = tp[HH + j];
+    // vertical: unit = (tile column col in [0,3E), row block rb in [0,T/RB))
+    for (int u = threadIdx.x; u < 3 * E * (T / RB); u += blockDim.x) {
+        const int col = u % (3 * E), rb = u / (3 * E);
+        const double *p = in + (rb * RB + R - HH) * 3 * E + col;
+        double win[NWIN];
+#pragma unroll
+        for (int k = 0; k < NWIN; ++k) win[k] = p[k * 3 * E];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            double acc = win[r + HH] * t[0];
+#pragma unroll
+            for (int j = HH; j >= 1; --j) acc = acc + (win[r + HH - j] + win[r + HH + j]) * t[j];
+            mid[(rb * RB + r) * 3 * E + col] = acc;
+        }
+    }
+    __syncthreads();
+    // horizontal: unit = (row, channel, column block); mid holds clamped columns
+    for (int u = threadIdx.x; u < T * 3 * (T / RB); u += blockDim.x) {
+        const int cb = u % (T / RB), rc = u / (T / RB), c = rc % 3, row = rc / 3;
+        const int gy = ty0 + row;
+        if (gy >= H) continue;
+        const double *p = mid + row * 3 * E + (cb * RB + R - HH) * 3 + c;
+        double win[NWIN];
+#pragma unroll
+        for (int k = 0; k < NWIN; ++k) win[k] = p[3 * k];
+        double *o = out + ((size_t)gy * W + tx0 + cb * RB) * 3 + c;
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            double acc = win[r + HH] * t[0];
+#pragma unroll
+            for (int j = HH; j >= 1; --j) acc = acc + (win[r + HH - j] + win[r + HH + j]) * t[j];
+            if (tx0 + cb * RB + r < W) o[3 * r] = acc;
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_pyramid_fused(const PyrAllJob *jobs, int H, int W, int levels,
+                                                       const double *taps, int h0, int h1, int h2, int h3) {
+    const PyrAllJob J = jobs[blockIdx.y];
+    constexpr int T = LC_PYR_TILE, R = LC_PYR_HALO, E = T + 2 * R;
+    extern __shared__ double sm[];
+    double *in = sm;                 // E rows x 3E
+    double *mid = sm + E * E * 3;    // T rows x 3E
+    const int tiles_x = (W + T - 1) / T;
+    const int tx0 = (blockIdx.x % tiles_x) * T, ty0 = (blockIdx.x / tiles_x) * T;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // asynchronous tile copy (LDGSTS): every thread keeps ~25 loads in flight
+    for (int row = warp; row < E; row += nw) {
+        const int gy = min(max(ty0 + row - R, 0), H - 1);
+        const double *src = J.src + (size_t)gy * W * 3;
+        for (int col = lane; col < 3 * E; col += 32) {
+            const int x = col / 3;
+            const int gx = min(max(tx0 + x - R, 0), W - 1);
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(in + row * 3 * E + col);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                         "l"(src + gx * 3 + (col - 3 * x)));
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    const int hs[4] = {h0, h1, h2, h3};
+    for (int l = 0; l < levels; ++l) {
+        double *out = J.dst + (size_t)l * H * W * 3;
+        const double *tp = taps + 32 * l;
+        switch (hs[l]) {
+            case 0: pyr_level<0>(in, mid, out, tp, tx0, ty0, H, W); break;
+            case 1: pyr_level<1>(in, mid, out, tp, tx0, ty0, H, W); break;
+            case 2: pyr_level<2>(in, mid, out, tp, tx0, ty0, H, W); break;
+            case 3: pyr_level<3>(in, mid, out, tp, tx0, ty0, H, W); break;
+            case 4: pyr_level<4>(in, mid, out, tp, tx0, ty0, H, W); break;
+            case 5: pyr_level<5>(in, mid, out, tp, tx0, ty0, H, W); break;
+            case 6: pyr_level<6>(in, mid, out, tp, tx0, ty0, H, W); break;
+            default: pyr_level<7>(in, mid, out, tp, tx0, ty0, H, W); break;
+        }
+    }
+}
+
 // ===========================================================================
 // contour pixels of a mask in np.argwhere (row-major) order, then a uniform
 // cell grid over them.  imageproc.py:34-49

@@ -430,6 +430,8 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve_t(const SurfJob *jobs, 
     const SurfJob &J = jobs[T::stream()];
     if (!J.active) return;
     __shared__ double red[8 * 32 + 32];
+    if (threadIdx.x == 0) *reinterpret_cast<int *>(red + 8 * 32 + 24) = 0;   // Team::sums parity
+    __syncthreads();
     SurfCtx c;
     c.J = &J;
     c.obs = J.obs;

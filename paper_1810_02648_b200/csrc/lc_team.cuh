@@ -30,7 +30,11 @@ struct Team {
     }
 
     // M simultaneous sums over every thread of the team.  `red` is a shared
-    // buffer of at least 8*32 + 2*8 doubles at the same offset in every CTA.
+    // buffer of at least 8*32 + 32 doubles at the same offset in every CTA.
+    // Per-CTA partials alternate between two slots (`parity`, identical in
+    // every CTA because every CTA makes the same sequence of calls), so one
+    // cluster barrier suffices: a slot is rewritten two calls later, after
+    // an intermediate barrier that every reader must have reached.
     template <int M>
     __device__ static void sums(double (&v)[M], double *red) {
         static_assert(M <= 8, "at most 8 sums at once");
@@ -40,30 +44,35 @@ struct Team {
         __syncthreads();
         if (l == 0)
             for (int m = 0; m < M; ++m) red[m * 32 + w] = v[m];
+        int *par = reinterpret_cast<int *>(red + 8 * 32 + 24);
         __syncthreads();
+        const int parity = *par;
+        double *slot = red + 8 * 32 + 8 * parity;     // this CTA's partials
+        double *res = red + 8 * 32 + 16;              // local copy of the totals
         if (threadIdx.x < 32) {
             for (int m = 0; m < M; ++m) {
                 double s = (l < NT / 32) ? red[m * 32 + l] : 0.0;
                 for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-                if (l == 0) red[8 * 32 + m] = s;       // this CTA's partial
+                if (l == 0) {
+                    if constexpr (CS == 1) res[m] = s;
+                    else slot[m] = s;
+                }
             }
         }
         if constexpr (CS == 1) {
-            __syncthreads();
-            for (int m = 0; m < M; ++m) v[m] = red[8 * 32 + m];
             __syncthreads();
         } else {
             auto cl = cg::this_cluster();
             cl.sync();
             if (threadIdx.x < M) {
                 double s = 0.0;
-                for (int r = 0; r < CS; ++r) s += cl.map_shared_rank(red, r)[8 * 32 + threadIdx.x];
-                red[8 * 32 + 8 + threadIdx.x] = s;
+                for (int r = 0; r < CS; ++r) s += cl.map_shared_rank(slot, r)[threadIdx.x];
+                res[threadIdx.x] = s;
             }
-            cl.sync();   // partials may be overwritten only after every CTA read them
-            for (int m = 0; m < M; ++m) v[m] = red[8 * 32 + 8 + m];
+            if (threadIdx.x == 0) *par = parity ^ 1;
             __syncthreads();
         }
+        for (int m = 0; m < M; ++m) v[m] = res[m];
     }
 
     // element-wise sum of a per-CTA shared array `part[n]` over the team, in
