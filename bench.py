@@ -41,7 +41,7 @@ DOMINANT = "k_surface_solve"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--streams", type=int, default=8, help="capture streams per GPU")
@@ -116,7 +116,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.p = None
@@ -248,13 +248,13 @@ def run_ours(args):
             tr.set_frame(s, img_d[s, f].data_ptr(), msk_d[s, f].data_ptr(), dets[s][f], on_device=True)
         tr.step()
 
+    clocks = ClockSampler(local)     # sampling spans warm-up + the timed region
     for f in range(W):
         step_dev(f)
     ctx.synchronize()
     c0 = [tr.counters(s) for s in range(Sn)]
     barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
     ctx.profile_kernel(DOMINANT)
     l0 = ctx.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -329,7 +329,8 @@ def run_ours(args):
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "kernel": DOMINANT, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak if peak else None,
-                         "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                         "traffic": ((traffic or {}).get("dram_bytes_per_launch")
+                                     if (traffic or {}).get("streams") == Sn else None),
                          "algorithmic_bytes_per_launch": per_launch,
                          "kernel_ms_per_launch": k_avg_s * 1e3, "launches": k_n,
                          "peak_source": peak_src,

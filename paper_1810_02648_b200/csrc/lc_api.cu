@@ -509,6 +509,7 @@ void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) 
     n2d = mem.alloc<double>(2 * (size_t)N);
     crest = mem.alloc<double>(3 * (size_t)N);
     cidx = mem.alloc<int>(N);
+    nn_hint = mem.alloc<int>(N);
     B = mem.alloc<int>(1);
     vis = mem.alloc<int>(N);
     P = mem.alloc<int>(1);
@@ -561,8 +562,10 @@ static NnGridDev grid_dev(const GridBufs &g, const uint8_t *mask, int H, int W) 
 }
 
 // contour pixels + grid for a batch of masks
+// candidate lists only for cells within `max_ring` cell rings of a contour
+// pixel; farther queries take the exact quadtree search
 static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *, const uint8_t *>> &gs,
-                        int H, int W, int max_ring = 1 << 30) {
+                        int H, int W, int max_ring = 3) {
     if (gs.empty()) return;
     std::vector<GridJob> jobs;
     for (auto &p : gs) {
@@ -587,9 +590,9 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
     launch(c, k_contour_scan_cells, dim3(S), dim3(1024), 0, dj, ncx * ncy);
     launch(c, k_quad_build, dim3(S), dim3(1024), 0, dj, ncx, ncy);
     launch(c, k_contour_fill, dim3(64, S), dim3(256), 0, dj, ncx);
-    launch(c, k_cand_count, dim3((ncx * ncy + 7) / 8, S), dim3(256), 0, dj, H, W);
+    launch(c, k_cand_count, dim3((ncx * ncy + 127) / 128, S), dim3(128), 0, dj, H, W);
     launch(c, k_cand_scan, dim3(S), dim3(1024), 0, dj, ncx * ncy);
-    launch(c, k_cand_fill, dim3((ncx * ncy + 7) / 8, S), dim3(256), 0, dj, H, W);
+    launch(c, k_cand_fill, dim3((ncx * ncy + 127) / 128, S), dim3(128), 0, dj, H, W);
 }
 
 static void raster(lc_ctx *c, const lc_actor *a, const lc_camera &cam, std::vector<RasterJob> jobs,
@@ -1020,6 +1023,7 @@ static void run_frame(FrameBatch &fb) {
             p.report = s->pose_rep;
             p.log_offset = log_off[i];
             p.phase = s->phase_pose;
+            p.nn_hint = s->nn_hint;
             log_off[i] += h.gn_iterations;
             pj.push_back(p);
             ++k;
@@ -1053,6 +1057,7 @@ static void run_frame(FrameBatch &fb) {
             j.p = s->sp; j.ap = s->sap; j.best = s->sbest; j.edir = s->edir; j.eg = s->eg;
             j.off0 = s->off0; j.off1 = s->off1; j.hold = s->hold;
             j.report = s->nr_rep;
+            j.nn_hint = s->nn_hint;
             j.counters = s->counters;
             j.phase = s->phase_surf;
             sj.push_back(j);
@@ -1373,6 +1378,7 @@ extern "C" int lc_pose_solve(lc_ctx *c, const lc_actor *a, const lc_camera *cam,
     p.directional = pb->directional;
     p.report = s->pose_rep;
     p.log_offset = 0;
+    p.nn_hint = s->nn_hint;
     require(pb->hyper.gn_iterations <= LC_MAX_LOG, "too many GN iterations for the report");
     pose_launch(c, a, *cam, {p});
     CK(cudaMemcpyAsync(x_out, s->x, sizeof(double) * LC_NP, cudaMemcpyDeviceToHost, st));
@@ -1443,6 +1449,7 @@ extern "C" int lc_nonrigid_solve(lc_ctx *c, const lc_actor *a, const lc_camera *
     j.p = s->sp; j.ap = s->sap; j.best = s->sbest; j.edir = s->edir; j.eg = s->eg;
     j.off0 = s->off0; j.off1 = s->off1; j.hold = s->hold;
     j.report = s->nr_rep;
+    j.nn_hint = s->nn_hint;
     surface_launch(c, a, *cam, cf, {j});
     CK(cudaMemcpyAsync(v_out, s->v, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost, st));
     if (report) CK(cudaMemcpyAsync(report, s->nr_rep, sizeof(lc_nonrigid_report), cudaMemcpyDeviceToHost, st));

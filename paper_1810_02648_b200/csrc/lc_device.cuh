@@ -193,9 +193,12 @@ __device__ inline void nn_quadtree(const NnGridDev &g, double qx, double qy, dou
     }
 }
 
-__device__ inline int nn_query(const NnGridDev &g, double qx, double qy, double &d2out) {
+// `hint` (a site id or -1) only seeds the search bound: the result is the
+// exact nearest site with the lowest-index tie break whatever the hint.
+__device__ inline int nn_query(const NnGridDev &g, double qx, double qy, double &d2out, int hint = -1) {
     double best = LC_INF;
     int bi = 0x7fffffff;
+    if (hint >= 0 && hint < g.K) nn_consider(g, hint, qx, qy, best, bi);
     const double gx = (double)(g.ncx * LC_GRID_CELL), gy = (double)(g.ncy * LC_GRID_CELL);
     const bool in_grid = qx >= 0.0 && qy >= 0.0 && qx < gx && qy < gy;
     if (in_grid && g.cand_range) {
@@ -275,12 +278,14 @@ __device__ __forceinline__ void ring_visit_warp(const NnGridDev &g, int cx, int 
 // continuous distance + unit direction away from the nearest contour point
 struct NnResult { double dist, vx, vy; bool clamped; };
 
-__device__ __forceinline__ NnResult field_nearest(const NnGridDev &g, double qx, double qy) {
+__device__ __forceinline__ NnResult field_nearest(const NnGridDev &g, double qx, double qy,
+                                                  int *hint = nullptr) {
     NnResult r;
     const bool fin = isfinite(qx) && isfinite(qy);
     if (!fin) { qx = 0.0; qy = 0.0; }
     double d2;
-    const int k = nn_query(g, qx, qy, d2);
+    const int k = nn_query(g, qx, qy, d2, hint ? *hint : -1);
+    if (hint && k >= 0 && k < g.K) *hint = k;
     if (k < 0 || k >= g.K) { r.dist = LC_INF; r.vx = r.vy = 0.0; r.clamped = true; return r; }
     const double d = sqrt(d2);
     const int2 p = g.pts[k];

@@ -86,7 +86,7 @@ __host__ __device__ __forceinline__ int quad_off(int P, int l) {
     for (int k = 0; k < l; ++k) o += (P >> k) * (P >> k);
     return o;
 }
-#define LC_CAND_PER_CELL 128   // average candidate capacity per cell
+#define LC_CAND_PER_CELL 384   // average candidate capacity per cell
 #define LC_CAND_MAX 1024       // per-cell cap before falling back to the ring search
 
 // per-config constants of the surface energy

@@ -99,7 +99,7 @@ __device__ double pose_row(const PoseCtx &c, int r, double *jr, int &term, int &
         behind = !cok;
         NnResult nn;
         double val = 0.0, gx = 0.0, gy = 0.0;
-        nn = field_nearest(c.obs, px, py);
+        nn = field_nearest(c.obs, px, py, J.nn_hint ? J.nn_hint + b : nullptr);
         field_residual(nn, val, gx, gy);
         bool ok = cok && !nn.clamped;
         if (J.enabled) ok = ok && J.enabled[b];
@@ -347,7 +347,9 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(const PoseJob *jobs, con
     c.nt = J.prev_pos ? 3 * nj : 0;
     c.R = c.n2 + c.n3 + c.B + c.nt + 27;
     for (int i = threadIdx.x; i < LC_NP; i += NT) s.x[i] = J.x0[i];
-    __syncthreads();
+    if (J.nn_hint)
+        for (int b = T::tid(); b < c.B; b += T::size) J.nn_hint[b] = -1;
+    T::sync();
 
     lc_pose_report *rep = J.report;
     int log0 = J.log_offset;

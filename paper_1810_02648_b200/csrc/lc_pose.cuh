@@ -24,6 +24,7 @@ struct PoseJob {
     lc_pose_report *report;
     int log_offset;
     long long *phase;         // LC_NPHASE timestamps (or null)
+    int *nn_hint;             // B: last nearest contour pixel per silhouette row (or null)
 };
 
 struct SurfJob {
@@ -51,6 +52,7 @@ struct SurfJob {
     double *off0, *off1;      // N*3 snap offsets
     uint8_t *hold;            // N
     lc_nonrigid_report *report;
+    int *nn_hint;             // B: last nearest contour pixel per boundary row (or null)
     long long *counters;      // cumulative: frames, gn, pcg iters, trials, P, B, K (or null)
     long long *phase;         // LC_NPHASE timestamps (or null)
 };

@@ -95,6 +95,7 @@ struct Slot {
     uint8_t *tri_front, *vflag, *enabled;
     double *tri_n, *n2d, *crest;
     int *cidx, *B, *vis, *P;
+    int *nn_hint;
     // surface scratch
     double *diag, *minv, *rhs, *sx, *sr, *sz, *sp, *sap, *sbest, *edir, *eg, *off0, *off1;
     uint8_t *hold;

@@ -303,42 +303,81 @@ __device__ __forceinline__ NnGridDev grid_of(const GridJob &J, int H, int W) {
     return g;
 }
 
-// U2 = min over sites of the squared farthest distance from cell c; -1 when
-// no site lies within `max_ring` rings (the cell then keeps the ring search)
-__device__ double cell_bound_warp(const NnGridDev &g, int cx, int cy, int max_ring) {
-    double u2 = LC_INF;
-    bool gave_up = false;
-    ring_visit_warp(g, cx, cy, [&](int pid) { u2 = fmin(u2, cell_far2(cx, cy, g.pts[pid])); },
-                    [&](int r) {
-                        for (int o = 16; o > 0; o >>= 1) u2 = fmin(u2, __shfl_xor_sync(0xffffffffu, u2, o));
-                        if (r >= max_ring && u2 == LC_INF) { gave_up = true; return true; }
-                        const double lim = (double)(r * LC_GRID_CELL);
-                        return u2 <= lim * lim;
-                    });
-    return gave_up ? -1.0 : u2;
+// Per-cell candidate sets from the site-count quadtree (thread per cell).
+// U2 = min over sites of the squared distance from the cell's farthest point;
+// candidates = sites whose squared distance to the cell is <= U2.  Any query
+// inside the cell has its nearest site (and every site tied with it) in the set.
+struct CellBox { double x0, y0, x1, y1; };
+
+__device__ __forceinline__ double near2_box(const CellBox &c, double bx0, double by0, double bx1, double by1) {
+    const double dx = fmax(0.0, fmax(bx0 - c.x1, c.x0 - bx1));
+    const double dy = fmax(0.0, fmax(by0 - c.y1, c.y0 - by1));
+    return dx * dx + dy * dy;
+}
+
+// visit sites of nodes passing `keep(near2)`; F(pid, int2 p)
+template <typename K, typename F>
+__device__ __forceinline__ void quad_walk(const NnGridDev &g, const CellBox &cb, K &&keep, F &&f) {
+    int stack[3 * 12 + 2];
+    int sp = 0;
+    stack[sp++] = g.qL << 24;
+    while (sp > 0) {
+        const int e = stack[--sp];
+        const int l = e >> 24, ny = (e >> 12) & 0xfff, nx = e & 0xfff;
+        const int side = g.qP >> l;
+        if (g.quad[quad_off(g.qP, l) + ny * side + nx] == 0) continue;
+        const double s = (double)(LC_GRID_CELL << l);
+        if (!keep(near2_box(cb, nx * s, ny * s, nx * s + s - 1.0, ny * s + s - 1.0))) continue;
+        if (l == 0) {
+            if (nx < g.ncx && ny < g.ncy) {
+                const int c = ny * g.ncx + nx;
+                for (int k = g.cell_start[c]; k < g.cell_start[c + 1]; ++k) {
+                    const int pid = g.cell_pts[k];
+                    f(pid, g.pts[pid]);
+                }
+            }
+            continue;
+        }
+        // children: nearest pushed last
+        int ch[4];
+        double d[4];
+        const double cs = s * 0.5;
+        for (int k = 0; k < 4; ++k) {
+            const int cx = 2 * nx + (k & 1), cy = 2 * ny + (k >> 1);
+            ch[k] = ((l - 1) << 24) | (cy << 12) | cx;
+            d[k] = near2_box(cb, cx * cs, cy * cs, cx * cs + cs - 1.0, cy * cs + cs - 1.0);
+        }
+        for (int i = 1; i < 4; ++i)
+            for (int j = i; j > 0 && d[j] > d[j - 1]; --j) {
+                const double td = d[j]; d[j] = d[j - 1]; d[j - 1] = td;
+                const int tc = ch[j]; ch[j] = ch[j - 1]; ch[j - 1] = tc;
+            }
+        for (int k = 0; k < 4; ++k) stack[sp++] = ch[k];
+    }
+}
+
+__device__ __forceinline__ CellBox cell_box(int cx, int cy) {
+    return CellBox{(double)(cx * LC_GRID_CELL), (double)(cy * LC_GRID_CELL),
+                   (double)(cx * LC_GRID_CELL + LC_GRID_CELL), (double)(cy * LC_GRID_CELL + LC_GRID_CELL)};
 }
 
 __global__ void k_cand_count(const GridJob *jobs, int H, int W) {
     const GridJob J = jobs[blockIdx.y];
     const NnGridDev g = grid_of(J, H, W);
-    const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-    for (int c = blockIdx.x * wpb + (threadIdx.x >> 5); c < g.ncx * g.ncy; c += gridDim.x * wpb) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < g.ncx * g.ncy; c += gridDim.x * blockDim.x) {
         const int cx = c % g.ncx, cy = c / g.ncx;
         int cnt = 0;
         double u2 = -1.0;
-        if (g.K > 0) u2 = cell_bound_warp(g, cx, cy, J.max_ring);
-        if (u2 >= 0.0) {
-            ring_visit_warp(g, cx, cy, [&](int pid) { cnt += cell_near2(cx, cy, g.pts[pid]) <= u2; },
-                            [&](int r) {
-                                const double lim = (double)(r * LC_GRID_CELL);
-                                return lim * lim > u2;
-                            });
-            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (g.K > 0) {
+            const CellBox cb = cell_box(cx, cy);
+            u2 = LC_INF;
+            quad_walk(g, cb, [&](double n2) { return n2 < u2; },
+                      [&](int, int2 p) { u2 = fmin(u2, cell_far2(cx, cy, p)); });
+            quad_walk(g, cb, [&](double n2) { return n2 <= u2; },
+                      [&](int, int2 p) { cnt += cell_near2(cx, cy, p) <= u2; });
         }
-        if (lane == 0) {
-            J.cand_cnt[c] = (u2 < 0.0 || cnt > LC_CAND_MAX) ? -1 : cnt;
-            J.cand_u2[c] = u2;
-        }
+        J.cand_cnt[c] = (u2 < 0.0 || cnt > LC_CAND_MAX) ? -1 : cnt;
+        J.cand_u2[c] = u2;
     }
 }
 
@@ -388,23 +427,16 @@ __global__ void k_cand_scan(const GridJob *jobs, int ncells) {
 __global__ void k_cand_fill(const GridJob *jobs, int H, int W) {
     const GridJob J = jobs[blockIdx.y];
     const NnGridDev g = grid_of(J, H, W);
-    const int wpb = blockDim.x >> 5;
-    for (int c = blockIdx.x * wpb + (threadIdx.x >> 5); c < g.ncx * g.ncy; c += gridDim.x * wpb) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < g.ncx * g.ncy; c += gridDim.x * blockDim.x) {
         const int2 rg = J.cand_range[c];
         if (rg.y <= 0 || g.K == 0) continue;
         const int cx = c % g.ncx, cy = c / g.ncx;
         const double u2 = J.cand_u2[c];
-        // append order inside a list is irrelevant: ties break on the point index
-        ring_visit_warp(g, cx, cy,
-                        [&](int pid) {
-                            const int2 p = g.pts[pid];
-                            if (cell_near2(cx, cy, p) <= u2)
-                                J.cand_pts[rg.x + atomicAdd(&J.cell_fill[c], 1)] = make_int2(p.x | (p.y << 16), pid);
-                        },
-                        [&](int r) {
-                            const double lim = (double)(r * LC_GRID_CELL);
-                            return lim * lim > u2;
-                        });
+        int k = 0;
+        quad_walk(g, cell_box(cx, cy), [&](double n2) { return n2 <= u2; },
+                  [&](int pid, int2 p) {
+                      if (cell_near2(cx, cy, p) <= u2) J.cand_pts[rg.x + k++] = make_int2(p.x | (p.y << 16), pid);
+                  });
     }
 }
 
@@ -463,9 +495,8 @@ __device__ __forceinline__ void depth_pixel(const RasterJob &J, CamDev cam, cons
     double l0, l1, l2;
     if (!bary(P, inv, x, y, l0, l1, l2)) return;
     const double z = l0 * D[0] + l1 * D[1] + l2 * D[2];
-    const unsigned long long zb = (unsigned long long)__double_as_longlong(z);
-    unsigned long long *dst = J.zbuf + (size_t)y * cam.W + x;
-    if (zb < *dst) atomicMin(dst, zb);
+    // result unused -> compiled to a fire-and-forget RED.MIN (no load latency on the path)
+    atomicMin(J.zbuf + (size_t)y * cam.W + x, (unsigned long long)__double_as_longlong(z));
 }
 
 __device__ __forceinline__ void winner_pixel(const RasterJob &J, CamDev cam, const double P[3][2],

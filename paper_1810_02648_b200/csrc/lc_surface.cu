@@ -71,7 +71,7 @@ __device__ __forceinline__ void sil_row(const SurfCtx &c, int b, V3 p, bool with
     double px, py;
     const bool ok = project(c.cam, p, px, py);
     o.behind = !ok;
-    const NnResult nn = field_nearest(c.obs, px, py);
+    const NnResult nn = field_nearest(c.obs, px, py, J.nn_hint ? J.nn_hint + b : nullptr);
     double val, gx, gy;
     field_residual(nn, val, gx, gy);
     const double w = sqrt(c.hp.w_sil) * ((ok && !nn.clamped && J.enabled[b]) ? 1.0 : 0.0);
@@ -348,14 +348,15 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
         double px, py;
         const bool ok = project(c.cam, p, px, py);
         const bool en = J.enabled[b] && ok;
-        const NnResult n0 = field_nearest(c.obs, px, py);
+        int hint = J.nn_hint ? J.nn_hint[b] : -1;
+        const NnResult n0 = field_nearest(c.obs, px, py, &hint);
         const double sign = side_sign(c.obs, n0, px, py, J.n2d[2 * b], J.n2d[2 * b + 1]);
         double val = field_interface(n0);
         double qx = px, qy = py;
         bool active = en && val > hp.snap_band;
         bool stuck = false;
         for (int s = 0; s < hp.snap_max_steps && active; ++s) {
-            const NnResult g = field_nearest(c.obs, qx, qy);
+            const NnResult g = field_nearest(c.obs, qx, qy, &hint);
             const double gn = sqrt(g.vx * g.vx + g.vy * g.vy);
             const bool good = gn > 1e-9;
             const double gd = fmax(gn, 1e-300);
@@ -366,7 +367,8 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
             bool pending = good;
             for (int h = 0; h < 3 && pending; ++h) {
                 const double tx = qx + step * dx, ty = qy + step * dy;
-                const double tv = field_interface(field_nearest(c.obs, tx, ty));
+                int th = hint;
+                const double tv = field_interface(field_nearest(c.obs, tx, ty, &th));
                 if (tv < cur) { nx = tx; ny = ty; nv = tv; pending = false; }
                 step *= 0.5;
             }
@@ -452,6 +454,8 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve_t(const SurfJob *jobs, 
     c.sil_on = J.enable_sil && has_field;
     double *v = J.v;
     for (int i = T::tid(); i < c.N * 3; i += T::size) v[i] = J.v0[i];
+    if (J.nn_hint)
+        for (int b = T::tid(); b < c.B; b += T::size) J.nn_hint[b] = -1;
     T::sync();
     lc_nonrigid_report *rep = J.report;
     int ph = 0;

@@ -44,12 +44,18 @@ def main():
         print(f"frame {f}: {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
         if a.phases:
             import numpy as np
-            pp, ss = np.zeros(64, dtype=np.int64), np.zeros(64, dtype=np.int64)
-            _lib.check(ctx.lib.lc_tracker_phase_times(tr.handle, 0, _lib.ptr(pp), _lib.ptr(ss)))
-            for name, arr in (("pose", pp), ("surface", ss)):
-                n = int(np.count_nonzero(arr))
-                d = np.diff(arr[:n]) / 1e3
-                print(f"   {name} phases (us): " + " ".join(f"{x:.0f}" for x in d) + f"  total {d.sum():.0f}")
+            worst = {}
+            for st in range(a.streams):
+                pp, ss = np.zeros(64, dtype=np.int64), np.zeros(64, dtype=np.int64)
+                _lib.check(ctx.lib.lc_tracker_phase_times(tr.handle, st, _lib.ptr(pp), _lib.ptr(ss)))
+                for name, arr, n in (("pose", pp, 19), ("surface", ss, 11)):
+                    d = np.diff(arr[:n]) / 1e3
+                    if d.min() < 0:
+                        continue
+                    if name not in worst or d.sum() > worst[name][1].sum():
+                        worst[name] = (st, d)
+            for name, (st, d) in worst.items():
+                print(f"   slowest {name} stream {st} (us): " + " ".join(f"{x:.0f}" for x in d) + f"  total {d.sum():.0f}")
 
 
 if __name__ == "__main__":
