@@ -67,6 +67,14 @@ static void launch_named(const char *name, lc_ctx *c, K kernel, dim3 g, dim3 b, 
 }
 #define launch(c, kernel, ...) launch_named(#kernel, c, kernel, __VA_ARGS__)
 
+// temporarily route a context's launches to another stream
+struct OnStream {
+    lc_ctx *c;
+    cudaStream_t saved;
+    OnStream(lc_ctx *c_, cudaStream_t s) : c(c_), saved(c_->stream) { c->stream = s; }
+    ~OnStream() { c->stream = saved; }
+};
+
 // cluster launch: `streams` teams of `cs` CTAs (one thread-block cluster per stream)
 template <typename... KArgs, typename... Args>
 static void launch_cluster(const char *name, lc_ctx *c, void (*kernel)(KArgs...), int streams, int cs,
@@ -133,11 +141,13 @@ struct JobRing {
     char *dev = nullptr;
     char *host = nullptr;
     size_t cap = 0, off = 0;
+    cudaStream_t aux = nullptr;
     void *put(cudaStream_t st, const void *src, size_t bytes, void *dst = nullptr) {
         const size_t padded = (bytes + 255) & ~size_t(255);
         if (padded > cap) throw ApiError("job descriptor larger than the staging ring");
         if (off + padded > cap) {
             cudaStreamSynchronize(st);
+            if (aux) cudaStreamSynchronize(aux);
             off = 0;
         }
         std::memcpy(host + off, src, bytes);
@@ -153,6 +163,7 @@ static JobRing &ring_of(lc_ctx *c) {
         if (r.first == c) return r.second;
     JobRing jr;
     jr.cap = 16 << 20;
+    jr.aux = c->aux;
     if (cudaMalloc(&jr.dev, jr.cap) != cudaSuccess) throw std::bad_alloc();
     if (cudaMallocHost(&jr.host, jr.cap) != cudaSuccess) throw std::bad_alloc();
     rings.push_back({c, jr});
@@ -185,6 +196,10 @@ extern "C" int lc_ctx_create(int32_t device, uint64_t cuda_stream, lc_ctx **out)
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;
     }
+    CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_obs, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_pyr, cudaEventDisableTiming));
     {
         const int sm = (int)pose_smem_bytes(LC_MAXJ);
         CK(cudaFuncSetAttribute(k_pose_solve_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -206,6 +221,11 @@ extern "C" int lc_ctx_destroy(lc_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     delete c->call_slot;
+    cudaStreamSynchronize(c->aux);
+    cudaStreamDestroy(c->aux);
+    cudaEventDestroy(c->ev_fork);
+    cudaEventDestroy(c->ev_obs);
+    cudaEventDestroy(c->ev_pyr);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
     return LC_OK;
@@ -459,6 +479,7 @@ static void alloc_grid(DevArena &m, GridBufs &g, int H, int W) {
     g.cand_pts = m.alloc<int2>((size_t)ncx * ncy * LC_CAND_PER_CELL);
     g.cand_total = m.alloc<int>(1);
     g.cand_u2 = m.alloc<double>(ncx * ncy);
+    g.cell_seed = m.alloc<int>(ncx * ncy);
     g.qP = 1;
     g.qL = 0;
     while (g.qP < std::max(ncx, ncy)) { g.qP *= 2; g.qL++; }
@@ -565,7 +586,7 @@ static NnGridDev grid_dev(const GridBufs &g, const uint8_t *mask, int H, int W) 
 // candidate lists only for cells within `max_ring` cell rings of a contour
 // pixel; farther queries take the exact quadtree search
 static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *, const uint8_t *>> &gs,
-                        int H, int W, int max_ring = 3) {
+                        int H, int W, double max_u = 1e30, bool lists = true) {
     if (gs.empty()) return;
     std::vector<GridJob> jobs;
     for (auto &p : gs) {
@@ -576,8 +597,9 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
         j.cell_fill = p.first->cell_fill; j.cell_pts = p.first->cell_pts; j.K = p.first->K;
         j.cand_cnt = p.first->cand_cnt; j.cand_range = p.first->cand_range;
         j.cand_pts = p.first->cand_pts; j.cand_total = p.first->cand_total;
-        j.cand_u2 = p.first->cand_u2; j.max_ring = max_ring;
+        j.cand_u2 = p.first->cand_u2; j.max_ring = 0; j.max_u2 = max_u * max_u;
         j.quad = p.first->quad; j.qP = p.first->qP; j.qL = p.first->qL;
+        j.cell_seed = p.first->cell_seed;
         jobs.push_back(j);
     }
     const GridJob *dj = stage(c, jobs);
@@ -590,9 +612,11 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
     launch(c, k_contour_scan_cells, dim3(S), dim3(1024), 0, dj, ncx * ncy);
     launch(c, k_quad_build, dim3(S), dim3(1024), 0, dj, ncx, ncy);
     launch(c, k_contour_fill, dim3(64, S), dim3(256), 0, dj, ncx);
-    launch(c, k_cand_count, dim3((ncx * ncy + 127) / 128, S), dim3(128), 0, dj, H, W);
+    if (!lists) return;
+    launch(c, k_cell_jfa, dim3(S), dim3(1024), sizeof(int) * 2 * ncx * ncy, dj, ncx, ncy);
+    launch(c, k_cand_count, dim3((ncx * ncy + 7) / 8, S), dim3(256), 0, dj, H, W);
     launch(c, k_cand_scan, dim3(S), dim3(1024), 0, dj, ncx * ncy);
-    launch(c, k_cand_fill, dim3((ncx * ncy + 127) / 128, S), dim3(128), 0, dj, H, W);
+    launch(c, k_cand_fill, dim3((ncx * ncy + 7) / 8, S), dim3(256), 0, dj, H, W);
 }
 
 static void raster(lc_ctx *c, const lc_actor *a, const lc_camera &cam, std::vector<RasterJob> jobs,
@@ -895,7 +919,7 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
     raster(c, a, fb.cam, rj, !stage1 && fb.cfg->enable_part_mask, true);
     std::vector<std::pair<const GridBufs *, const uint8_t *>> gs;
     for (Slot *s : ss) gs.push_back({&s->own, s->own_mask});
-    build_grids(c, gs, H, W, 3);   // rim queries stay within a few pixels of the own contour
+    build_grids(c, gs, H, W, 0.0, false);   // rim queries stay near the own contour: quadtree only
     std::vector<ContourJob> cj;
     for (Slot *s : ss) {
         ContourJob j{};
@@ -916,6 +940,7 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
         RimJob r{};
         r.verts = s->*verts; r.idx = s->cidx; r.B = s->B;
         r.own = grid_dev(s->own, s->own_mask, H, W);
+        r.own.cand_range = nullptr;                       // no per-cell lists for own-mask grids
         r.ownK = s->own.K;
         r.keep = s->enabled;
         r.stage1 = stage1;
@@ -954,12 +979,20 @@ static void run_frame(FrameBatch &fb) {
     const int H = fb.cam.height, W = fb.cam.width;
     auto &ss = fb.slots;
     const unsigned S = (unsigned)ss.size();
-    // ---- preprocess (pipeline.py:156-162): pyramid + observed contour grid
-    if (cfg.mode == 0) pyramid(c, *fb.cf, ss, cfg.nonrigid.n_levels);
+    // ---- preprocess (pipeline.py:156-162) on the auxiliary stream, concurrent
+    // with Stage I's own setup: observed contour grid (joined before the pose
+    // solve), blur pyramid (joined before the surface solve).  Descriptors are
+    // staged on the main stream before the fork.
+    cudaEventRecord(c->ev_fork, c->stream);
+    cudaStreamWaitEvent(c->aux, c->ev_fork, 0);
     {
+        OnStream on(c, c->aux);
         std::vector<std::pair<const GridBufs *, const uint8_t *>> gs;
         for (Slot *s : ss) gs.push_back({&s->obs, s->mask_src});
         build_grids(c, gs, H, W);
+        cudaEventRecord(c->ev_obs, c->aux);
+        if (cfg.mode == 0) pyramid(c, *fb.cf, ss, cfg.nonrigid.n_levels);
+        cudaEventRecord(c->ev_pyr, c->aux);
     }
     // ---- condition (pipeline.py:165-170) + displaced rest + initial pose
     {
@@ -1028,6 +1061,7 @@ static void run_frame(FrameBatch &fb) {
             pj.push_back(p);
             ++k;
         }
+        if (r == 0) cudaStreamWaitEvent(c->stream, c->ev_obs, 0);
         pose_launch(c, a, fb.cam, pj);
     }
     // ---- Stage II (pipeline.py:227-260) or the pose-only surface
@@ -1062,8 +1096,10 @@ static void run_frame(FrameBatch &fb) {
             j.phase = s->phase_surf;
             sj.push_back(j);
         }
+        cudaStreamWaitEvent(c->stream, c->ev_pyr, 0);
         surface_launch(c, a, fb.cam, *fb.cf, sj);
     }
+    cudaStreamWaitEvent(c->stream, c->ev_pyr, 0);   // join the aux stream in every mode
     // ---- state update (pipeline.py:281-299)
     std::vector<FinishJob> fj;
     for (Slot *s : ss) {

@@ -39,7 +39,9 @@ struct GridJob {
     double *cand_u2;       // ncells: per-cell bound U^2 (count -> fill)
     int *quad;             // site-count quadtree (see NnGridDev)
     int qP, qL;
-    int max_ring;          // cells with no site within this many rings use the ring search
+    int max_ring;          // unused (ring-search builder)
+    double max_u2;         // cells whose bound U^2 exceeds this keep the quadtree search
+    int *cell_seed;        // ncells: a nearby site per cell (jump flooding), -1 = none
 };
 __global__ void k_contour_rows(const GridJob *jobs, int H, int W);
 __global__ void k_contour_scan_rows(const GridJob *jobs, int H, int ncells);
@@ -47,6 +49,7 @@ __global__ void k_contour_emit(const GridJob *jobs, int H, int W, int ncx);
 __global__ void k_contour_scan_cells(const GridJob *jobs, int ncells);
 __global__ void k_contour_fill(const GridJob *jobs, int ncx);
 __global__ void k_cand_count(const GridJob *jobs, int H, int W);
+__global__ void k_cell_jfa(const GridJob *jobs, int ncx, int ncy);
 __global__ void k_quad_build(const GridJob *jobs, int ncx, int ncy);
 __global__ void k_cand_scan(const GridJob *jobs, int ncells);
 __global__ void k_cand_fill(const GridJob *jobs, int H, int W);

@@ -11,6 +11,9 @@ struct lc_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // auxiliary stream for work independent of Stage I (pyramid, observed grid)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_obs = nullptr, ev_pyr = nullptr;
     long long launches = 0;
     // optional per-kernel timing: CUDA events around every launch of `prof_name`
     std::string prof_name;
@@ -63,6 +66,7 @@ struct GridBufs {
     int2 *cand_pts;
     int2 *cand_range;
     double *cand_u2;
+    int *cell_seed;
     int *quad;
     int qP, qL;
 };

@@ -315,9 +315,13 @@ __device__ __forceinline__ double near2_box(const CellBox &c, double bx0, double
     return dx * dx + dy * dy;
 }
 
-// visit sites of nodes passing `keep(near2)`; F(pid, int2 p)
-template <typename K, typename F>
-__device__ __forceinline__ void quad_walk(const NnGridDev &g, const CellBox &cb, K &&keep, F &&f) {
+// Warp-cooperative walk of the site quadtree: the traversal is warp-uniform
+// (node tests use warp-uniform bounds), the sites of each visited leaf are
+// split over the lanes: leaf(k0) is called by every lane, which handles
+// sites k0 + lane, k0 + lane + 32, ...; `after_leaf()` re-synchronizes bounds.
+template <typename K, typename L, typename A>
+__device__ __forceinline__ void quad_walk_warp(const NnGridDev &g, const CellBox &cb, K &&keep, L &&leaf,
+                                               A &&after_leaf) {
     int stack[3 * 12 + 2];
     int sp = 0;
     stack[sp++] = g.qL << 24;
@@ -331,14 +335,11 @@ __device__ __forceinline__ void quad_walk(const NnGridDev &g, const CellBox &cb,
         if (l == 0) {
             if (nx < g.ncx && ny < g.ncy) {
                 const int c = ny * g.ncx + nx;
-                for (int k = g.cell_start[c]; k < g.cell_start[c + 1]; ++k) {
-                    const int pid = g.cell_pts[k];
-                    f(pid, g.pts[pid]);
-                }
+                leaf(g.cell_start[c], g.cell_start[c + 1]);
+                after_leaf();
             }
             continue;
         }
-        // children: nearest pushed last
         int ch[4];
         double d[4];
         const double cs = s * 0.5;
@@ -361,23 +362,82 @@ __device__ __forceinline__ CellBox cell_box(int cx, int cy) {
                    (double)(cx * LC_GRID_CELL + LC_GRID_CELL), (double)(cy * LC_GRID_CELL + LC_GRID_CELL)};
 }
 
+// Jump flooding over the cell grid (one CTA per stream): every cell gets a
+// site near its centre.  Only used as an upper bound for the candidate band
+// (any real site bounds the nearest distance), so JFA's rare misses cost
+// list length, never exactness.
+__global__ void k_cell_jfa(const GridJob *jobs, int ncx, int ncy) {
+    const GridJob J = jobs[blockIdx.x];
+    extern __shared__ int seeds[];   // 2 * ncells ping-pong
+    const int nc = ncx * ncy;
+    int *a = seeds, *b = seeds + nc;
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+        const int s0 = J.cell_start[c], s1 = J.cell_start[c + 1];
+        a[c] = s1 > s0 ? J.cell_pts[s0] : -1;
+    }
+    __syncthreads();
+    int step = 1;
+    while (step * 2 < max(ncx, ncy)) step *= 2;
+    auto pass = [&](int k) {
+        for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+            const int cx = c % ncx, cy = c / ncx;
+            const double qx = cx * LC_GRID_CELL + 0.5 * LC_GRID_CELL, qy = cy * LC_GRID_CELL + 0.5 * LC_GRID_CELL;
+            int best = a[c];
+            double bd = LC_INF;
+            if (best >= 0) {
+                const int2 p = J.pts[best];
+                bd = (qx - p.x) * (qx - p.x) + (qy - p.y) * (qy - p.y);
+            }
+            for (int dy = -k; dy <= k; dy += k)
+                for (int dx = -k; dx <= k; dx += k) {
+                    const int nx = cx + dx, ny = cy + dy;
+                    if ((dx == 0 && dy == 0) || nx < 0 || ny < 0 || nx >= ncx || ny >= ncy) continue;
+                    const int sd = a[ny * ncx + nx];
+                    if (sd < 0) continue;
+                    const int2 p = J.pts[sd];
+                    const double d = (qx - p.x) * (qx - p.x) + (qy - p.y) * (qy - p.y);
+                    if (d < bd) { bd = d; best = sd; }
+                }
+            b[c] = best;
+        }
+        __syncthreads();
+        int *t = a; a = b; b = t;
+    };
+    for (int k = step; k >= 1; k >>= 1) pass(k);
+    pass(1);
+    pass(1);
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) J.cell_seed[c] = a[c];
+}
+
+// warp per cell: bound U^2 (warp min), then the candidate count (warp sum)
 __global__ void k_cand_count(const GridJob *jobs, int H, int W) {
     const GridJob J = jobs[blockIdx.y];
     const NnGridDev g = grid_of(J, H, W);
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < g.ncx * g.ncy; c += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    for (int c = blockIdx.x * wpb + (threadIdx.x >> 5); c < g.ncx * g.ncy; c += gridDim.x * wpb) {
         const int cx = c % g.ncx, cy = c / g.ncx;
         int cnt = 0;
         double u2 = -1.0;
         if (g.K > 0) {
             const CellBox cb = cell_box(cx, cy);
-            u2 = LC_INF;
-            quad_walk(g, cb, [&](double n2) { return n2 < u2; },
-                      [&](int, int2 p) { u2 = fmin(u2, cell_far2(cx, cy, p)); });
-            quad_walk(g, cb, [&](double n2) { return n2 <= u2; },
-                      [&](int, int2 p) { cnt += cell_near2(cx, cy, p) <= u2; });
+            const int seed = J.cell_seed[c];
+            // upper bound of the cell's farthest-point nearest distance
+            u2 = seed >= 0 ? cell_far2(cx, cy, g.pts[seed]) : LC_INF;
+            if (u2 > J.max_u2) u2 = -1.0;      // far cell: queries use the quadtree
+            else {
+                quad_walk_warp(g, cb, [&](double n2) { return n2 <= u2; },
+                               [&](int k0, int k1) {
+                                   for (int k = k0 + lane; k < k1; k += 32)
+                                       cnt += cell_near2(cx, cy, g.pts[g.cell_pts[k]]) <= u2;
+                               },
+                               [&]() {});
+                for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            }
         }
-        J.cand_cnt[c] = (u2 < 0.0 || cnt > LC_CAND_MAX) ? -1 : cnt;
-        J.cand_u2[c] = u2;
+        if (lane == 0) {
+            J.cand_cnt[c] = (u2 < 0.0 || cnt > LC_CAND_MAX) ? -1 : cnt;
+            J.cand_u2[c] = u2;
+        }
     }
 }
 
@@ -427,16 +487,33 @@ __global__ void k_cand_scan(const GridJob *jobs, int ncells) {
 __global__ void k_cand_fill(const GridJob *jobs, int H, int W) {
     const GridJob J = jobs[blockIdx.y];
     const NnGridDev g = grid_of(J, H, W);
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < g.ncx * g.ncy; c += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    for (int c = blockIdx.x * wpb + (threadIdx.x >> 5); c < g.ncx * g.ncy; c += gridDim.x * wpb) {
         const int2 rg = J.cand_range[c];
         if (rg.y <= 0 || g.K == 0) continue;
         const int cx = c % g.ncx, cy = c / g.ncx;
         const double u2 = J.cand_u2[c];
-        int k = 0;
-        quad_walk(g, cell_box(cx, cy), [&](double n2) { return n2 <= u2; },
-                  [&](int pid, int2 p) {
-                      if (cell_near2(cx, cy, p) <= u2) J.cand_pts[rg.x + k++] = make_int2(p.x | (p.y << 16), pid);
-                  });
+        int base = rg.x;
+        quad_walk_warp(g, cell_box(cx, cy), [&](double n2) { return n2 <= u2; },
+                       [&](int k0, int k1) {
+                           for (int k = k0; k < k1; k += 32) {
+                               const int kk = k + lane;
+                               bool take = false;
+                               int2 p = make_int2(0, 0);
+                               int pid = 0;
+                               if (kk < k1) {
+                                   pid = g.cell_pts[kk];
+                                   p = g.pts[pid];
+                                   take = cell_near2(cx, cy, p) <= u2;
+                               }
+                               const unsigned bal = __ballot_sync(0xffffffffu, take);
+                               if (take)
+                                   J.cand_pts[base + __popc(bal & ((1u << lane) - 1u))] =
+                                       make_int2(p.x | (p.y << 16), pid);
+                               base += __popc(bal);
+                           }
+                       },
+                       [&]() {});
     }
 }
 
@@ -801,17 +878,23 @@ __global__ void k_rim(const RimJob *jobs, ActorDev A, CamDev cam, const double *
         double px, py;
         const bool ok = project(cam, p, px, py);
         bool keep = false;
+        int hint0 = -1;
         if (own.K > 0) {
-            const NnResult n = field_nearest(own, px, py);
+            const NnResult n = field_nearest(own, px, py, &hint0);
             keep = ok && !n.clamped && n.dist <= 1.5;
         }
         if (J.stage1) {
             if (keep) {
-                // 16 directions x radii 1..8: depth = max over interior probes
+                // 16 directions x radii 1..8: depth = max over interior probes.
+                // Lane = (direction, half of the radii); walking outward, each
+                // probe seeds its neighbour search with the previous site.
                 double deep = 0.0;
-                for (int k = lane; k < 128; k += 32) {
+                const int dir = lane >> 1, r0 = (lane & 1) * 4;
+                int hint = hint0;
+                for (int r = r0; r < r0 + 4; ++r) {
+                    const int k = dir * 8 + r;
                     const double qx = px + probe_offs[2 * k], qy = py + probe_offs[2 * k + 1];
-                    const NnResult n = field_nearest(own, qx, qy);
+                    const NnResult n = field_nearest(own, qx, qy, &hint);
                     const double d = field_inside(own, qx, qy) ? n.dist : 0.0;
                     deep = fmax(deep, d);
                 }
