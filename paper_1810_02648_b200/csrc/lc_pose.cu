@@ -25,9 +25,27 @@ struct PoseSmem {
     double A[LC_NP * LC_NP];
     double rhs[LC_NP];
     double x[LC_NP], xt[LC_NP], step[LC_NP];
-    double red[8 * 32 + 32];
+    double red[Team<1, NT>::red_doubles];
     double pix[LC_MAXJ + 4][2];
     int okz[LC_MAXJ + 4];
+};
+
+// one evaluation point: FK state, parameters and joint/marker projections
+struct PoseView {
+    FkState *f;
+    double *xt;
+    double (*pix)[2];
+    int *okz;
+};
+
+// line-search trial points evaluated together (aliases the Jacobian tables,
+// which only the with-Jacobian evaluation uses)
+constexpr int kTrials = 4;
+struct TrialSmem {
+    FkState f[kTrials];
+    double xt[kTrials][LC_NP];
+    double pix[kTrials][LC_MAXJ + 4][2];
+    int okz[kTrials][LC_MAXJ + 4];
 };
 
 struct PoseCtx {
@@ -44,9 +62,10 @@ struct PoseCtx {
 
 // one residual row; writes the 36 Jacobian entries to `jr` when non-null.
 // Returns F and sets `term` (0 2d, 1 3d, 2 sil, 3 temporal, 4 anatomic).
-__device__ double pose_row(const PoseCtx &c, int r, double *jr, int &term, int &behind) {
+__device__ double pose_row(const PoseCtx &c, const PoseView &pv, int r, double *jr, int &term, int &behind) {
     const PoseSmem &s = *c.s;
     const SkelDev &sk = s.sk;
+    const FkState &f = *pv.f;
     const PoseJob &J = *c.J;
     const PoseHyperDev &hp = J.hp;
     const int nj = sk.J;
@@ -55,10 +74,10 @@ __device__ double pose_row(const PoseCtx &c, int r, double *jr, int &term, int &
         term = 0;
         const int n = r >> 1, comp = r & 1;
         const double lam = n < nj ? hp.l2d : hp.l2d * hp.face;
-        const double w2 = (sqrt(lam) * (J.v2d[n] ? 1.0 : 0.0)) * (s.okz[n] ? 1.0 : 0.0);
-        const double F = (s.pix[n][comp] - J.j2d[2 * n + comp]) * w2;
+        const double w2 = (sqrt(lam) * (J.v2d[n] ? 1.0 : 0.0)) * (pv.okz[n] ? 1.0 : 0.0);
+        const double F = (pv.pix[n][comp] - J.j2d[2 * n + comp]) * w2;
         if (jr) {
-            const V3 p = n < nj ? ld3(s.f.pos[n]) : ld3(s.f.markers[n - nj]);
+            const V3 p = n < nj ? ld3(f.pos[n]) : ld3(f.markers[n - nj]);
             double a0, a2, b1, b2;
             proj_jac(c.cam, p, a0, a2, b1, b2);
             const double d0 = comp == 0 ? a0 : 0.0, d1 = comp == 0 ? 0.0 : b1, d2 = comp == 0 ? a2 : b2;
@@ -73,7 +92,7 @@ __device__ double pose_row(const PoseCtx &c, int r, double *jr, int &term, int &
         term = 1;
         const int i = r / 3, comp = r % 3;
         const double w3 = sqrt(hp.l3d) * (J.v3d[i] ? 1.0 : 0.0);
-        const double F = ((s.f.pos[i][comp] - J.j3d[3 * i + comp]) - s.xt[33 + comp]) * w3;
+        const double F = ((f.pos[i][comp] - J.j3d[3 * i + comp]) - pv.xt[33 + comp]) * w3;
         if (jr) {
             const double *jn = c.jp + ((size_t)i * 3 + comp) * LC_NP;
             for (int q = 0; q < LC_NP; ++q) jr[q] = (jn[q] - (q == 33 + comp ? 1.0 : 0.0)) * w3;
@@ -91,7 +110,7 @@ __device__ double pose_row(const PoseCtx &c, int r, double *jr, int &term, int &
             const FkState *f;
             __device__ double operator()(int j, int k) const { return f->dq[j][k]; }
         };
-        dq_blend(c.A.skin_idx + 4 * v, c.A.skin_w + 4 * v, c.A.dominant[v], SmemDq{&s.f}, Bl);
+        dq_blend(c.A.skin_idx + 4 * v, c.A.skin_w + 4 * v, c.A.dominant[v], SmemDq{&f}, Bl);
         Q4 cr;
         const V3 sp = dq_apply(Bl, rest, cr);
         double px, py;
@@ -144,7 +163,7 @@ __device__ double pose_row(const PoseCtx &c, int r, double *jr, int &term, int &
         term = 3;
         const int i = r / 3, comp = r % 3;
         const double wt = sqrt(hp.ltemp * hp.tw[i]);
-        const double F = (s.f.pos[i][comp] - J.prev_pos[3 * i + comp]) * wt;
+        const double F = (f.pos[i][comp] - J.prev_pos[3 * i + comp]) * wt;
         if (jr) {
             const double *jn = c.jp + ((size_t)i * 3 + comp) * LC_NP;
             for (int q = 0; q < LC_NP; ++q) jr[q] = jn[q] * wt;
@@ -153,7 +172,7 @@ __device__ double pose_row(const PoseCtx &c, int r, double *jr, int &term, int &
     }
     r -= c.nt;                                           // anatomic (27 rows)
     term = 4;
-    const double th = s.xt[6 + r];
+    const double th = pv.xt[6 + r];
     const bool hi = th > sk.tmax[r], lo = th < sk.tmin[r];
     const double wa = sqrt(hp.lanat);
     const double F = wa * ((hi ? th - sk.tmax[r] : 0.0) + (lo ? sk.tmin[r] - th : 0.0));
@@ -168,12 +187,18 @@ __device__ double pose_row(const PoseCtx &c, int r, double *jr, int &term, int &
 // per-term energies in terms[5], behind-camera count.  Rows are split over
 // the team's CTAs; every CTA ends with the same totals.
 template <typename T>
-__device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &behind_out) {
+__device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &behind_out, int fine = -1) {
     PoseSmem &s = *c.s;
+    auto fst = [&](int k) {
+        if (fine >= 0 && c.J->phase && T::tid() == 0) c.J->phase[fine + k] = gtimer();
+    };
+    fst(0);
     const SkelDev &sk = s.sk;
     const int nj = sk.J;
+    const PoseView pv{&s.f, s.xt, s.pix, s.okz};
     if (threadIdx.x < 32) fk_warp(sk, s.xt, s.f);
     __syncthreads();
+    fst(1);
     // projections of joints + markers
     for (int n = threadIdx.x; n < nj + 4; n += NT) {
         const V3 p = n < nj ? ld3(s.f.pos[n]) : ld3(s.f.markers[n - nj]);
@@ -213,6 +238,7 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
         }
     }
     __syncthreads();
+    fst(2);
 
     double acc[5] = {0, 0, 0, 0, 0};
     double total = 0.0;
@@ -238,7 +264,7 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
         if (r < c.R) {
             int term, bh;
             double *jr = with_jac ? c.rows + (size_t)threadIdx.x * 37 : nullptr;
-            const double F = pose_row(c, r, jr, term, bh);
+            const double F = pose_row(c, pv, r, jr, term, bh);
             if (jr) jr[36] = F;
             acc[term] += F * F;
             behind += bh;
@@ -263,6 +289,7 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
             __syncthreads();
         }
     }
+    fst(3);
     // total energy = sum of F^2 over all rows (pose_stage.py:279-281)
     {
         double v8[8] = {acc[0], acc[1], acc[2], acc[3], acc[4], (double)behind, 0.0, 0.0};
@@ -271,6 +298,7 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
         behind_out = (int)v8[5];
         total = (((v8[0] + v8[1]) + v8[2]) + v8[3]) + v8[4];
     }
+    fst(4);
     if (with_jac) {
         // partial tiles -> shared (reuse the row chunk), then reduce over groups
         double *part = c.rows;
@@ -309,7 +337,55 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
         }
         __syncthreads();
     }
+    fst(5);
     return total;
+}
+
+// Energies of nt line-search trial points at once (ts.xt[h], h < nt): FK on
+// warp h, then the nt*R residual rows spread over the team, one team
+// reduction of the nt x 5 term sums.  e[h] is summed in the same term order
+// as the single-point evaluation (pose_stage.py:279-281).
+template <typename T>
+__device__ void pose_trials(PoseCtx &c, TrialSmem &ts, int nt, double e[kTrials], int fine = -1) {
+    PoseSmem &s = *c.s;
+    auto fst = [&](int k) {
+        if (fine >= 0 && c.J->phase && T::tid() == 0) c.J->phase[fine + k] = gtimer();
+    };
+    fst(0);
+    const SkelDev &sk = s.sk;
+    const int nj = sk.J;
+    const int w = threadIdx.x >> 5;
+    if (w < nt) fk_warp(sk, ts.xt[w], ts.f[w]);
+    __syncthreads();
+    fst(1);
+    for (int k = threadIdx.x; k < nt * (nj + 4); k += NT) {
+        const int h = k / (nj + 4), n = k - h * (nj + 4);
+        const V3 p = n < nj ? ld3(ts.f[h].pos[n]) : ld3(ts.f[h].markers[n - nj]);
+        double px, py;
+        ts.okz[h][n] = project(c.cam, p, px, py);
+        ts.pix[h][n][0] = px;
+        ts.pix[h][n][1] = py;
+    }
+    __syncthreads();
+    fst(2);
+    double acc[kTrials * 5];
+    for (int k = 0; k < kTrials * 5; ++k) acc[k] = 0.0;
+    for (int rr = T::tid(); rr < nt * c.R; rr += T::size) {
+        const int h = rr / c.R, r = rr - h * c.R;
+        const PoseView pv{&ts.f[h], ts.xt[h], ts.pix[h], ts.okz[h]};
+        int term, bh;
+        const double F = pose_row(c, pv, r, nullptr, term, bh);
+        const double f2 = F * F;
+        const int slot = h * 5 + term;
+#pragma unroll
+        for (int k = 0; k < kTrials * 5; ++k)
+            if (k == slot) acc[k] += f2;
+    }
+    fst(3);
+    T::template sums<kTrials * 5>(acc, s.red);
+    fst(4);
+    for (int h = 0; h < kTrials; ++h)
+        e[h] = (((acc[5 * h] + acc[5 * h + 1]) + acc[5 * h + 2]) + acc[5 * h + 3]) + acc[5 * h + 4];
 }
 
 }  // namespace
@@ -323,7 +399,7 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(const PoseJob *jobs, con
     extern __shared__ __align__(16) unsigned char dsm[];
     PoseSmem &s = *reinterpret_cast<PoseSmem *>(dsm);
     double *tail = reinterpret_cast<double *>(dsm + ((sizeof(PoseSmem) + 15) & ~size_t(15)));
-    if (threadIdx.x == 0) *reinterpret_cast<int *>(s.red + 8 * 32 + 24) = 0;   // Team::sums parity
+    T::init_red(s.red);
     {
         const int *src = reinterpret_cast<const int *>(skg);
         int *dst = reinterpret_cast<int *>(&s.sk);
@@ -365,7 +441,7 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(const PoseJob *jobs, con
         __syncthreads();
         double terms[5];
         int behind;
-        const double e0 = pose_eval<T>(c, true, terms, behind);
+        const double e0 = pose_eval<T>(c, true, terms, behind, it == 1 ? 32 : -1);
         stamp();
         behind_total += behind;
         gimbal |= s.f.gimbal;
@@ -374,28 +450,40 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(const PoseJob *jobs, con
         for (int i = threadIdx.x; i < LC_NP; i += NT) s.step[i] = s.qr.x[i];
         __syncthreads();
         stamp();
+        // halving line search (pose_stage.py:441-453): accept the first
+        // trial step * 0.5^h with e1 <= e0, h <= max_halvings, else reject.
+        // Trials are evaluated kTrials at a time; halving is exact, so every
+        // trial point has the bits of the sequential search.
+        TrialSmem &ts = *reinterpret_cast<TrialSmem *>(c.jp);
         int halv = 0;
         bool rejected = false;
-        double e1;
-        for (;;) {
-            for (int i = threadIdx.x; i < LC_NP; i += NT) s.xt[i] = s.x[i] + s.step[i];
-            __syncthreads();
-            double tt[5];
-            int bh;
-            e1 = pose_eval<T>(c, false, tt, bh);
-            if (e1 <= e0) {
-                for (int i = threadIdx.x; i < LC_NP; i += NT) s.x[i] = s.xt[i];
-                __syncthreads();
-                break;
+        double e1 = e0;
+        for (int base = 0;; base += kTrials) {
+            const int nt = min(kTrials, J.hp.max_halvings + 1 - base);
+            for (int i = threadIdx.x; i < LC_NP; i += NT) {
+                double st = s.step[i];
+                for (int h = 0; h < nt; ++h) {
+                    ts.xt[h][i] = s.x[i] + st;
+                    st = 0.5 * st;
+                }
             }
-            if (halv >= J.hp.max_halvings) {
-                rejected = true;
-                e1 = e0;
-                break;
-            }
-            for (int i = threadIdx.x; i < LC_NP; i += NT) s.step[i] = 0.5 * s.step[i];
             __syncthreads();
-            ++halv;
+            double et[kTrials];
+            pose_trials<T>(c, ts, nt, et, (it == 1 && base == 0) ? 40 : -1);
+            int hit = -1;
+            for (int h = 0; h < nt; ++h)
+                if (et[h] <= e0) { hit = h; break; }
+            const bool last = base + nt > J.hp.max_halvings;
+            const int nh = hit >= 0 ? hit : (last ? nt - 1 : nt);   // halvings applied to s.step
+            for (int i = threadIdx.x; i < LC_NP; i += NT) {
+                double st = s.step[i];
+                for (int h = 0; h < nh; ++h) st = 0.5 * st;
+                s.step[i] = st;
+                if (hit >= 0) s.x[i] = ts.xt[hit][i];
+            }
+            __syncthreads();
+            if (hit >= 0) { halv = base + hit; e1 = et[hit]; break; }
+            if (last) { halv = J.hp.max_halvings; rejected = true; e1 = e0; break; }
         }
         stamp();
         if (T::tid() == 0 && rep) {
@@ -432,7 +520,9 @@ template __global__ void k_pose_solve_t<16>(const PoseJob *, const SkelDev *, Ac
 
 size_t pose_smem_bytes(int n_joints) {
     const size_t head = (sizeof(PoseSmem) + 15) & ~size_t(15);
-    const size_t tables = (size_t)(n_joints + 4) * 3 * LC_NP + (size_t)n_joints * 8 * LC_NP;
+    size_t tables = (size_t)(n_joints + 4) * 3 * LC_NP + (size_t)n_joints * 8 * LC_NP;
+    const size_t trial = (sizeof(TrialSmem) + sizeof(double) - 1) / sizeof(double);
+    if (tables < trial) tables = trial;
     const size_t rows = (size_t)NT * 37;
     return head + (tables + rows) * sizeof(double);
 }

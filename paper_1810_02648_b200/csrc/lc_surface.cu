@@ -162,8 +162,11 @@ __device__ __forceinline__ double total_energy(const double en[6], bool has_prev
 // GN evaluation with the normal system (diag, minv, rhs, edir); returns energies + counters
 template <typename T>
 __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, double en[6],
-                              int counts[3]) {
+                              int counts[3], int fine = -1) {
     const SurfJob &J = *c.J;
+    auto fst = [&](int k) {
+        if (fine >= 0 && J.phase && T::tid() == 0) J.phase[fine + k] = gtimer();
+    };
     const double cv = sqrt(c.hp.w_vel), ca = sqrt(c.hp.w_acc);
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // 6 energies, pruned, behind
     double degen = 0.0;
@@ -184,6 +187,7 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
         st3(J.eg + 3 * (size_t)e, al * q.u + be * (q.len_err * q.d));
     }
     T::sync();
+    fst(0);
     // P1: photometric data blocks (visible ids are unique)
     const double *img = J.pyr + (size_t)level * c.H * c.W * 3;
     if (J.enable_photo)
@@ -205,6 +209,7 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
                 rh[a] = -(o.J[0][a] * o.r[0] + o.J[1][a] * o.r[1] + o.J[2][a] * o.r[2]);
         }
     T::sync();
+    fst(1);
     // P2: silhouette rank-1 blocks (boundary ids are unique)
     if (c.sil_on)
         for (int b = T::tid(); b < c.B; b += T::size) {
@@ -220,6 +225,7 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
             rh[0] += -o.g[0] * o.r; rh[1] += -o.g[1] * o.r; rh[2] += -o.g[2] * o.r;
         }
     T::sync();
+    fst(2);
     // P3: full diagonal blocks, rhs, Jacobi preconditioner, temporal energies
     for (int i = T::tid(); i < c.N; i += T::size) {
         double dg[6];
@@ -253,7 +259,9 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
             for (int k = 0; k < 6; ++k) mi[k] = 0.0;  // pinv of an all-zero block
         for (int k = 0; k < 6; ++k) J.minv[6 * (size_t)i + k] = mi[k];
     }
+    fst(3);
     T::template sums<8>(acc, c.red);
+    fst(4);
     for (int k = 0; k < 6; ++k) en[k] = acc[k];
     counts[0] = (int)acc[6];
     counts[2] = (int)acc[7];
@@ -335,12 +343,17 @@ template <typename T>
 __device__ void surf_snap(const SurfCtx &c, double *v) {
     const SurfJob &J = *c.J;
     const SurfHyperDev &hp = c.hp;
+    auto fst = [&](int k) {
+        if (J.phase && T::tid() == 0) J.phase[24 + k] = gtimer();
+    };
+    fst(0);
     double cnt[4] = {0, 0, 0, 0};  // walked, reached, stuck, moved
     for (int i = T::tid(); i < c.N; i += T::size) {
         st3(J.off0 + 3 * (size_t)i, v3(0, 0, 0));
         J.hold[i] = 0;
     }
     T::sync();
+    fst(1);
     for (int b = T::tid(); b < c.B; b += T::size) {
         const int i = J.bidx[b];
         J.hold[i] = 1;
@@ -386,6 +399,7 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
         }
     }
     T::sync();
+    fst(2);
     // two uniform-Laplacian diffusion steps with the boundary held
     double *src = J.off0, *dst = J.off1;
     for (int round = 0; round < 2; ++round) {
@@ -398,6 +412,7 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
             st3(dst + 3 * (size_t)i, v3(a.x / dg, a.y / dg, a.z / dg));
         }
         T::sync();
+    fst(3);
         double *t = src; src = dst; dst = t;
     }
     for (int i = T::tid(); i < c.N; i += T::size) {
@@ -414,6 +429,7 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
         J.report->snap_moved = (int)cnt[3];
     }
     T::sync();
+    fst(4);
 }
 
 template <typename T>
@@ -431,8 +447,8 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve_t(const SurfJob *jobs, 
     using T = Team<CS, NT>;
     const SurfJob &J = jobs[T::stream()];
     if (!J.active) return;
-    __shared__ double red[8 * 32 + 32];
-    if (threadIdx.x == 0) *reinterpret_cast<int *>(red + 8 * 32 + 24) = 0;   // Team::sums parity
+    __shared__ double red[T::red_doubles];
+    T::init_red(red);
     __syncthreads();
     SurfCtx c;
     c.J = &J;
@@ -467,7 +483,7 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve_t(const SurfJob *jobs, 
             const int level = min(it, levels - 1);
             double en[6];
             int counts[3];
-            surf_assemble<T>(c, level, v, en, counts);
+            surf_assemble<T>(c, level, v, en, counts, it == 1 ? 16 : -1);
             stamp<T>(J, ph);
             for (int k = 0; k < 3; ++k) tot[k] += counts[k];
             const bool breakdown = surf_pcg<T>(c, hp.pcg);

@@ -29,34 +29,48 @@ struct Team {
         else cg::this_cluster().sync();
     }
 
-    // M simultaneous sums over every thread of the team.  `red` is a shared
-    // buffer of at least 8*32 + 32 doubles at the same offset in every CTA.
-    // Per-CTA partials alternate between two slots (`parity`, identical in
-    // every CTA because every CTA makes the same sequence of calls), so one
-    // cluster barrier suffices: a slot is rewritten two calls later, after
-    // an intermediate barrier that every reader must have reached.
+    // Layout of the shared reduction buffer (the same offsets in every CTA):
+    // per-warp partials [kMaxSums][32], two parity slots of per-CTA partials,
+    // the totals, and the parity flag.
+    static constexpr int kMaxSums = 24;
+    static constexpr int kSlot = kMaxSums * 32;
+    static constexpr int kRes = kSlot + 2 * kMaxSums;
+    static constexpr int kPar = kRes + kMaxSums;
+    static constexpr int red_doubles = kPar + 2;
+
+    __device__ __forceinline__ static void init_red(double *red) {
+        if (threadIdx.x == 0) *reinterpret_cast<int *>(red + kPar) = 0;
+    }
+
+    // M simultaneous sums over every thread of the team.  Per-warp shuffle
+    // trees, then warp m' sums partial m over the CTA's warps (fixed order),
+    // then every CTA adds the per-CTA partials in rank order through DSMEM,
+    // so every CTA holds bit-identical totals.  Per-CTA partials alternate
+    // between two slots (`parity`, identical in every CTA because every CTA
+    // makes the same sequence of calls), so one cluster barrier suffices: a
+    // slot is rewritten two calls later, after an intermediate barrier that
+    // every reader must have reached.
     template <int M>
     __device__ static void sums(double (&v)[M], double *red) {
-        static_assert(M <= 8, "at most 8 sums at once");
+        static_assert(M <= kMaxSums, "too many simultaneous sums");
+        constexpr int NW = NT / 32;
         for (int m = 0; m < M; ++m)
             for (int o = 16; o > 0; o >>= 1) v[m] += __shfl_down_sync(0xffffffffu, v[m], o);
         const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
         __syncthreads();
         if (l == 0)
             for (int m = 0; m < M; ++m) red[m * 32 + w] = v[m];
-        int *par = reinterpret_cast<int *>(red + 8 * 32 + 24);
+        int *par = reinterpret_cast<int *>(red + kPar);
         __syncthreads();
         const int parity = *par;
-        double *slot = red + 8 * 32 + 8 * parity;     // this CTA's partials
-        double *res = red + 8 * 32 + 16;              // local copy of the totals
-        if (threadIdx.x < 32) {
-            for (int m = 0; m < M; ++m) {
-                double s = (l < NT / 32) ? red[m * 32 + l] : 0.0;
-                for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-                if (l == 0) {
-                    if constexpr (CS == 1) res[m] = s;
-                    else slot[m] = s;
-                }
+        double *slot = red + kSlot + kMaxSums * parity;   // this CTA's partials
+        double *res = red + kRes;                          // local copy of the totals
+        for (int m = w; m < M; m += NW) {
+            double s = (l < NW) ? red[m * 32 + l] : 0.0;
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+            if (l == 0) {
+                if constexpr (CS == 1) res[m] = s;
+                else slot[m] = s;
             }
         }
         if constexpr (CS == 1) {

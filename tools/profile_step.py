@@ -56,6 +56,14 @@ def main():
                         worst[name] = (st, d)
             for name, (st, d) in worst.items():
                 print(f"   slowest {name} stream {st} (us): " + " ".join(f"{x:.0f}" for x in d) + f"  total {d.sum():.0f}")
+            # fine sub-phase stamps (GN iteration 1): pose eval+J [32..37], pose trial [40..45],
+            # surface assembly [16..21], snap [24..29]
+            pp, ss = np.zeros(64, dtype=np.int64), np.zeros(64, dtype=np.int64)
+            _lib.check(ctx.lib.lc_tracker_phase_times(tr.handle, 0, _lib.ptr(pp), _lib.ptr(ss)))
+            for name, arr, a0, n in (("pose evalJ", pp, 32, 6), ("pose trial", pp, 40, 6),
+                                     ("surf asm", ss, 16, 5), ("surf snap", ss, 24, 5)):
+                d = np.diff(arr[a0:a0 + n]) / 1e3
+                print(f"   stream0 {name} (us): " + " ".join(f"{x:.1f}" for x in d))
 
 
 if __name__ == "__main__":
