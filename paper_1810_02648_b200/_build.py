@@ -21,6 +21,8 @@ LIB = os.path.join(HERE, "liblivecap.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+# developer-only extra defines (e.g. LIVECAP_NVCC_EXTRA=-DLC_NN_STATS for query statistics)
+FLAGS += os.environ.get("LIVECAP_NVCC_EXTRA", "").split()
 
 
 def _nvcc() -> str:

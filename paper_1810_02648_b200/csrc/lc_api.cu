@@ -476,7 +476,8 @@ static void alloc_grid(DevArena &m, GridBufs &g, int H, int W) {
     g.K = m.alloc<int>(1);
     g.cand_cnt = m.alloc<int>(ncx * ncy);
     g.cand_range = m.alloc<int2>(ncx * ncy);
-    g.cand_pts = m.alloc<int2>((size_t)ncx * ncy * LC_CAND_PER_CELL);
+    g.cand_pts = m.alloc<int>((size_t)ncx * ncy * LC_CAND_PER_CELL);
+    g.cand_blk = m.alloc<int>((size_t)ncx * ncy * 32);
     g.cand_total = m.alloc<int>(1);
     g.cand_u2 = m.alloc<double>(ncx * ncy);
     g.cell_seed = m.alloc<int>(ncx * ncy);
@@ -576,6 +577,7 @@ static NnGridDev grid_dev(const GridBufs &g, const uint8_t *mask, int H, int W) 
     d.mask = mask;
     d.cand_range = g.cand_range;
     d.cand_pts = g.cand_pts;
+    d.cand_blk = g.cand_blk;
     d.quad = g.quad;
     d.qP = g.qP;
     d.qL = g.qL;
@@ -585,6 +587,18 @@ static NnGridDev grid_dev(const GridBufs &g, const uint8_t *mask, int H, int W) 
 // contour pixels + grid for a batch of masks
 // candidate lists only for cells within `max_ring` cell rings of a contour
 // pixel; farther queries take the exact quadtree search
+// Candidate lists are built for cells whose bound U (the farthest point of
+// the cell to a nearby site) is at most this many pixels; queries in farther
+// cells take the exact quadtree search.  Far cells have long lists and are
+// rarely queried, so listing them costs more build time than it saves.
+static double obs_list_radius() {
+    static double r = [] {
+        const char *v = getenv("LIVECAP_LIST_RADIUS");
+        return v ? atof(v) : 1e30;
+    }();
+    return r;
+}
+
 static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *, const uint8_t *>> &gs,
                         int H, int W, double max_u = 1e30, bool lists = true) {
     if (gs.empty()) return;
@@ -597,6 +611,7 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
         j.cell_fill = p.first->cell_fill; j.cell_pts = p.first->cell_pts; j.K = p.first->K;
         j.cand_cnt = p.first->cand_cnt; j.cand_range = p.first->cand_range;
         j.cand_pts = p.first->cand_pts; j.cand_total = p.first->cand_total;
+        j.cand_blk = p.first->cand_blk;
         j.cand_u2 = p.first->cand_u2; j.max_ring = 0; j.max_u2 = max_u * max_u;
         j.quad = p.first->quad; j.qP = p.first->qP; j.qL = p.first->qL;
         j.cell_seed = p.first->cell_seed;
@@ -616,7 +631,7 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
     launch(c, k_cell_jfa, dim3(S), dim3(1024), sizeof(int) * 2 * ncx * ncy, dj, ncx, ncy);
     launch(c, k_cand_count, dim3((ncx * ncy + 7) / 8, S), dim3(256), 0, dj, H, W);
     launch(c, k_cand_scan, dim3(S), dim3(1024), 0, dj, ncx * ncy);
-    launch(c, k_cand_fill, dim3((ncx * ncy + 7) / 8, S), dim3(256), 0, dj, H, W);
+    launch(c, k_cand_fill, dim3((ncx * ncy + 3) / 4, S), dim3(128), 0, dj, H, W);
 }
 
 static void raster(lc_ctx *c, const lc_actor *a, const lc_camera &cam, std::vector<RasterJob> jobs,
@@ -941,6 +956,7 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
         r.verts = s->*verts; r.idx = s->cidx; r.B = s->B;
         r.own = grid_dev(s->own, s->own_mask, H, W);
         r.own.cand_range = nullptr;                       // no per-cell lists for own-mask grids
+        r.own.cand_blk = nullptr;
         r.ownK = s->own.K;
         r.keep = s->enabled;
         r.stage1 = stage1;
@@ -989,7 +1005,7 @@ static void run_frame(FrameBatch &fb) {
         OnStream on(c, c->aux);
         std::vector<std::pair<const GridBufs *, const uint8_t *>> gs;
         for (Slot *s : ss) gs.push_back({&s->obs, s->mask_src});
-        build_grids(c, gs, H, W);
+        build_grids(c, gs, H, W, obs_list_radius());
         cudaEventRecord(c->ev_obs, c->aux);
         if (cfg.mode == 0) pyramid(c, *fb.cf, ss, cfg.nonrigid.n_levels);
         cudaEventRecord(c->ev_pyr, c->aux);

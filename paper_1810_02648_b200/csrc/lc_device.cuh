@@ -133,19 +133,21 @@ __device__ __forceinline__ void block_sums(double (&v)[M], double *red) {
 // on the squared distance break toward the lowest point index (argwhere
 // order).  Queries outside the grid fall back to a linear scan.
 
-__device__ __forceinline__ void nn_consider(const NnGridDev &g, int pid, double qx, double qy,
-                                            double &best, int &bi) {
-    const int2 p = g.pts[pid];
-    const double dx = qx - (double)p.x, dy = qy - (double)p.y;
+// A site is identified by its key y << 16 | x.  Contour pixels are indexed
+// in np.argwhere (row-major) order, so ascending keys are ascending indices
+// and the lowest-index tie break is the lowest-key tie break.
+__device__ __forceinline__ int site_key(int2 p) { return (p.y << 16) | p.x; }
+__device__ __forceinline__ int2 site_xy(int key) { return make_int2(key & 0xffff, key >> 16); }
+
+__device__ __forceinline__ void nn_consider_key(int key, double qx, double qy, double &best, int &bk) {
+    const double dx = qx - (double)(key & 0xffff), dy = qy - (double)(key >> 16);
     const double d2 = dx * dx + dy * dy;
-    if (d2 < best || (d2 == best && pid < bi)) { best = d2; bi = pid; }
+    if (d2 < best || (d2 == best && key < bk)) { best = d2; bk = key; }
 }
 
-// packed candidate: one 8-byte load carries the coordinates and the id
-__device__ __forceinline__ void nn_consider_packed(int2 c, double qx, double qy, double &best, int &bi) {
-    const double dx = qx - (double)(c.x & 0xffff), dy = qy - (double)(c.x >> 16);
-    const double d2 = dx * dx + dy * dy;
-    if (d2 < best || (d2 == best && c.y < bi)) { best = d2; bi = c.y; }
+__device__ __forceinline__ void nn_consider(const NnGridDev &g, int pid, double qx, double qy,
+                                            double &best, int &bk) {
+    nn_consider_key(site_key(g.pts[pid]), qx, qy, best, bk);
 }
 
 __device__ __forceinline__ double box_dist2(double qx, double qy, double x0, double y0, double s) {
@@ -193,47 +195,125 @@ __device__ inline void nn_quadtree(const NnGridDev &g, double qx, double qy, dou
     }
 }
 
-// `hint` (a site id or -1) only seeds the search bound: the result is the
-// exact nearest site with the lowest-index tie break whatever the hint.
+#ifdef LC_NN_STATS
+__device__ unsigned long long g_nn_stats[16];   // queries, list entries read, quadtree queries, hinted, max walk cycles, its steps, max steps, total steps
+#endif
+
+// Up to 16 keys of a sorted candidate list at once.  A single-precision
+// pass (no serial chain through the running best; fp32 issues far faster
+// than fp64) bounds the batch: with |q| < 2^11 the float distance is within
+// 1e-3 px of the exact one, so only keys whose float squared distance is
+// within thr = m (1 + 1e-5) + 1e-2 of the smaller of the batch's float
+// minimum and the running best can win or tie, and only those are measured
+// exactly in fp64 (the reference's arithmetic) and merged into (best, bk)
+// in (distance, key) order.  `stop` is set when the batch's last key is
+// farther from the cell than best: every later key of the sorted list is
+// then strictly farther than the answer.  Exact and order-independent.
+__device__ __forceinline__ void nn_batch16(const int *e, int n, int x0, int y0, double qx, double qy,
+                                           float qxf, float qyf, double &best, int &bk, bool &stop) {
+    float df[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        const float dx = qxf - (float)(e[u] & 0xffff), dy = qyf - (float)(e[u] >> 16);
+        df[u] = u < n ? fmaf(dx, dx, dy * dy) : __int_as_float(0x7f800000);
+    }
+    float m = df[0];
+#pragma unroll
+    for (int u = 1; u < 16; ++u) m = fminf(m, df[u]);
+    const float lim = fminf(m, (float)best);
+    const float thr = fmaf(lim, 1e-5f, lim) + 1e-2f;
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+        if (df[u] <= thr) nn_consider_key(e[u], qx, qy, best, bk);
+    int last = e[0];
+#pragma unroll
+    for (int u = 1; u < 16; ++u) if (u < n) last = e[u];
+    const int px = last & 0xffff, py = last >> 16;
+    const int ex = px < x0 ? x0 - px : (px > x0 + LC_GRID_CELL ? px - (x0 + LC_GRID_CELL) : 0);
+    const int ey = py < y0 ? y0 - py : (py > y0 + LC_GRID_CELL ? py - (y0 + LC_GRID_CELL) : 0);
+    if ((double)(ex * ex + ey * ey) > best) stop = true;
+}
+
+// Returns the key of the nearest site (INT_MAX if there is none).  `hint`
+// (a site key of this grid, or -1) only seeds the search bound: the result
+// is the exact nearest site with the lowest-key tie break whatever the hint.
 __device__ inline int nn_query(const NnGridDev &g, double qx, double qy, double &d2out, int hint = -1) {
     double best = LC_INF;
-    int bi = 0x7fffffff;
-    if (hint >= 0 && hint < g.K) nn_consider(g, hint, qx, qy, best, bi);
+    int bk = 0x7fffffff;
+    if (hint >= 0) nn_consider_key(hint, qx, qy, best, bk);
     const double gx = (double)(g.ncx * LC_GRID_CELL), gy = (double)(g.ncy * LC_GRID_CELL);
     const bool in_grid = qx >= 0.0 && qy >= 0.0 && qx < gx && qy < gy;
-    if (in_grid && g.cand_range) {
+    if (in_grid && g.cand_blk) {
+        // One 128 B line holds the cell's list range and the first
+        // LC_CAND_HEAD keys.  The list is sorted by (cell distance, key):
+        // stop at the first entry whose distance to the cell exceeds the
+        // best squared distance (it and every later entry are strictly
+        // farther, so ties are still all seen).
         const int cx = (int)qx >> LC_GRID_SHIFT, cy = (int)qy >> LC_GRID_SHIFT;
-        const int2 rg = g.cand_range[cy * g.ncx + cx];
-        if (rg.y >= 0) {
-            // 4 independent (best, id) chains expose memory-level parallelism;
-            // merging keeps the minimum with the lowest id on ties (exact)
-            double b1 = LC_INF, b2 = LC_INF, b3 = LC_INF;
-            int i1 = 0x7fffffff, i2 = 0x7fffffff, i3 = 0x7fffffff;
-            const int2 *cp = g.cand_pts + rg.x;
-            int k = 0;
-            for (; k + 4 <= rg.y; k += 4) {
-                const int2 c0 = __ldg(cp + k), c1 = __ldg(cp + k + 1), c2 = __ldg(cp + k + 2), c3 = __ldg(cp + k + 3);
-                nn_consider_packed(c0, qx, qy, best, bi);
-                nn_consider_packed(c1, qx, qy, b1, i1);
-                nn_consider_packed(c2, qx, qy, b2, i2);
-                nn_consider_packed(c3, qx, qy, b3, i3);
+        const int4 *blk = reinterpret_cast<const int4 *>(g.cand_blk) + 8 * (size_t)(cy * g.ncx + cx);
+        int4 h4[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) h4[u] = __ldg(blk + u);
+        const int start = h4[0].x, cnt = h4[0].y;
+        if (cnt >= 0) {
+            const int x0 = cx << LC_GRID_SHIFT, y0 = cy << LC_GRID_SHIFT;
+            const float qxf = (float)qx, qyf = (float)qy;
+            const int head[32] = {h4[0].z, h4[0].w, h4[1].x, h4[1].y, h4[1].z, h4[1].w, h4[2].x, h4[2].y,
+                                  h4[2].z, h4[2].w, h4[3].x, h4[3].y, h4[3].z, h4[3].w, h4[4].x, h4[4].y,
+                                  h4[4].z, h4[4].w, h4[5].x, h4[5].y, h4[5].z, h4[5].w, h4[6].x, h4[6].y,
+                                  h4[6].z, h4[6].w, h4[7].x, h4[7].y, h4[7].z, h4[7].w, -1, -1};
+            // long lists: put every line of the tail in flight now (L1
+            // prefetch, no registers), so the batches below mostly hit L1
+            // instead of paying one L2 round trip per 128 B line in turn
+            if (cnt > LC_CAND_HEAD) {
+                const uintptr_t l0 = reinterpret_cast<uintptr_t>(g.cand_pts + start + LC_CAND_HEAD - 2) & ~uintptr_t(127);
+                const uintptr_t l1 = reinterpret_cast<uintptr_t>(g.cand_pts + start + cnt - 1);
+                for (uintptr_t l = l0; l <= l1; l += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(l));
             }
-            for (; k < rg.y; ++k) nn_consider_packed(__ldg(cp + k), qx, qy, best, bi);
-            if (b1 < best || (b1 == best && i1 < bi)) { best = b1; bi = i1; }
-            if (b2 < best || (b2 == best && i2 < bi)) { best = b2; bi = i2; }
-            if (b3 < best || (b3 == best && i3 < bi)) { best = b3; bi = i3; }
+            bool stop = false;
+            nn_batch16(head, min(cnt, 16), x0, y0, qx, qy, qxf, qyf, best, bk, stop);
+            if (!stop && cnt > 16) nn_batch16(head + 16, min(cnt, LC_CAND_HEAD) - 16, x0, y0, qx, qy, qxf, qyf, best, bk, stop);
+#ifdef LC_NN_STATS
+            int scanned = min(cnt, stop ? 16 : LC_CAND_HEAD);
+#endif
+            // the tail, 16 keys (4 x 128-bit loads) at a time; it restarts
+            // at the aligned index 28 (re-visiting two head keys is harmless)
+            const int4 *cp = reinterpret_cast<const int4 *>(g.cand_pts + start);
+            for (int k = LC_CAND_HEAD - 2; k < cnt && !stop; k += 16) {
+#ifdef LC_NN_STATS
+                scanned += min(16, cnt - k);
+#endif
+                int4 e4[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    e4[u] = k + 4 * u < cnt ? __ldg(cp + (k >> 2) + u) : make_int4(-1, -1, -1, -1);
+                const int e[16] = {e4[0].x, e4[0].y, e4[0].z, e4[0].w, e4[1].x, e4[1].y, e4[1].z, e4[1].w,
+                                   e4[2].x, e4[2].y, e4[2].z, e4[2].w, e4[3].x, e4[3].y, e4[3].z, e4[3].w};
+                nn_batch16(e, min(16, cnt - k), x0, y0, qx, qy, qxf, qyf, best, bk, stop);
+            }
+#ifdef LC_NN_STATS
+            atomicAdd(&g_nn_stats[0], 1ull);
+            atomicAdd(&g_nn_stats[1], (unsigned long long)scanned);
+            atomicMax(&g_nn_stats[8], (unsigned long long)scanned);
+            atomicMax(&g_nn_stats[9], (unsigned long long)cnt);
+            atomicAdd(&g_nn_stats[10 + min(5, scanned / 64)], 1ull);
+            if (hint >= 0) atomicAdd(&g_nn_stats[3], 1ull);
+#endif
             d2out = best;
-            return bi;
+            return bk;
         }
     }
+#ifdef LC_NN_STATS
+    atomicAdd(&g_nn_stats[2], 1ull);
+#endif
     if (g.quad) {
-        nn_quadtree(g, qx, qy, best, bi);
+        nn_quadtree(g, qx, qy, best, bk);
         d2out = best;
-        return bi;
+        return bk;
     }
-    for (int k = 0; k < g.K; ++k) nn_consider(g, k, qx, qy, best, bi);
+    for (int k = 0; k < g.K; ++k) nn_consider(g, k, qx, qy, best, bk);
     d2out = best;
-    return bi;
+    return bk;
 }
 
 // ---- per-cell candidate lists (built once per mask) ----------------------
@@ -242,6 +322,13 @@ __device__ __forceinline__ double cell_far2(int cx, int cy, int2 p) {
     const double x0 = (double)(cx * LC_GRID_CELL), y0 = (double)(cy * LC_GRID_CELL);
     const double x1 = x0 + LC_GRID_CELL, y1 = y0 + LC_GRID_CELL;
     const double dx = fmax(fabs(p.x - x0), fabs(p.x - x1)), dy = fmax(fabs(p.y - y0), fabs(p.y - y1));
+    return dx * dx + dy * dy;
+}
+__device__ __forceinline__ int cell_near2_int(int cx, int cy, int2 p) {
+    const int x0 = cx * LC_GRID_CELL, y0 = cy * LC_GRID_CELL;
+    const int x1 = x0 + LC_GRID_CELL, y1 = y0 + LC_GRID_CELL;
+    const int dx = p.x < x0 ? x0 - p.x : (p.x > x1 ? p.x - x1 : 0);
+    const int dy = p.y < y0 ? y0 - p.y : (p.y > y1 ? p.y - y1 : 0);
     return dx * dx + dy * dy;
 }
 __device__ __forceinline__ double cell_near2(int cx, int cy, int2 p) {
@@ -275,6 +362,32 @@ __device__ __forceinline__ void ring_visit_warp(const NnGridDev &g, int cx, int 
     }
 }
 
+// Bounded exact query: the squared distance to the nearest site when some
+// site lies within R of (qx, qy), else +inf.  Only the cells overlapping the
+// square of half-side R around the query are scanned (any site within R
+// lies in one of them), so no search structure beyond the cell buckets is
+// needed.  Threshold tests of the reference (rim distance <= 1.5 px,
+// thickness probes >= 6 px) are decided exactly by it.
+__device__ inline double nn_within2(const NnGridDev &g, double qx, double qy, double R) {
+    double best = LC_INF;
+    if (!(isfinite(qx) && isfinite(qy))) return best;
+    const int cx0 = max(0, (int)floor((qx - R) / LC_GRID_CELL));
+    const int cx1 = min(g.ncx - 1, (int)floor((qx + R) / LC_GRID_CELL));
+    const int cy0 = max(0, (int)floor((qy - R) / LC_GRID_CELL));
+    const int cy1 = min(g.ncy - 1, (int)floor((qy + R) / LC_GRID_CELL));
+    for (int cy = cy0; cy <= cy1; ++cy)
+        for (int cx = cx0; cx <= cx1; ++cx) {
+            const int c = cy * g.ncx + cx;
+            const int k0 = g.cell_start[c], k1 = g.cell_start[c + 1];
+            for (int k = k0; k < k1; ++k) {
+                const int2 p = g.pts[g.cell_pts[k]];
+                const double dx = qx - (double)p.x, dy = qy - (double)p.y;
+                best = fmin(best, dx * dx + dy * dy);
+            }
+        }
+    return best <= R * R ? best : LC_INF;
+}
+
 // continuous distance + unit direction away from the nearest contour point
 struct NnResult { double dist, vx, vy; bool clamped; };
 
@@ -285,10 +398,10 @@ __device__ __forceinline__ NnResult field_nearest(const NnGridDev &g, double qx,
     if (!fin) { qx = 0.0; qy = 0.0; }
     double d2;
     const int k = nn_query(g, qx, qy, d2, hint ? *hint : -1);
-    if (hint && k >= 0 && k < g.K) *hint = k;
-    if (k < 0 || k >= g.K) { r.dist = LC_INF; r.vx = r.vy = 0.0; r.clamped = true; return r; }
+    if (k == 0x7fffffff) { r.dist = LC_INF; r.vx = r.vy = 0.0; r.clamped = true; return r; }
+    if (hint) *hint = k;
     const double d = sqrt(d2);
-    const int2 p = g.pts[k];
+    const int2 p = site_xy(k);
     const double safe = d > 1e-12 ? d : 1e-12;
     const bool dirok = (d > 1e-12) && fin;
     r.vx = dirok ? (qx - (double)p.x) / safe : 0.0;

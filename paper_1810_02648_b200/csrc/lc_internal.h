@@ -75,7 +75,10 @@ struct NnGridDev {
     // exact per-cell candidate lists (null -> ring search): cand_range[c] =
     // (start, count); count < 0 marks an overflowed cell (ring search there)
     const int2 *cand_range; // ncx*ncy
-    const int2 *cand_pts;   // (x | y << 16, site id)
+    const int *cand_pts;    // per-cell lists of site keys y << 16 | x (16 B aligned)
+    // per-cell 128 B blocks: {list start, list count, first LC_CAND_HEAD keys}
+    // so a query gets its cell's range and the head of its list in one line
+    const int *cand_blk;
     // site-count quadtree over the cells padded to qP x qP (qP = 2^qL):
     // level l (leaves l = 0) stores (qP>>l)^2 counts at offset quad_off(l)
     const int *quad;
@@ -88,6 +91,7 @@ __host__ __device__ __forceinline__ int quad_off(int P, int l) {
 }
 #define LC_CAND_PER_CELL 384   // average candidate capacity per cell
 #define LC_CAND_MAX 1024       // per-cell cap before falling back to the ring search
+#define LC_CAND_HEAD 30        // keys stored inline in each cell's 128 B block
 
 // per-config constants of the surface energy
 struct EdgeConstDev {

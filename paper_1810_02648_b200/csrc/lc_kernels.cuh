@@ -34,7 +34,8 @@ struct GridJob {
     int *K;                // out: contour pixel count
     int *cand_cnt;         // ncells
     int2 *cand_range;      // ncells
-    int2 *cand_pts;        // capacity ncells * LC_CAND_PER_CELL: (x | y << 16, id)
+    int *cand_pts;         // capacity ncells * LC_CAND_PER_CELL: site keys y << 16 | x, lists 16 B aligned
+    int *cand_blk;         // ncells * 32: {start, count, LC_CAND_HEAD keys}
     int *cand_total;       // 1
     double *cand_u2;       // ncells: per-cell bound U^2 (count -> fill)
     int *quad;             // site-count quadtree (see NnGridDev)

@@ -528,3 +528,14 @@ size_t pose_smem_bytes(int n_joints) {
 }
 
 int pose_block_threads() { return NT; }
+
+#ifdef LC_NN_STATS
+extern "C" int lc_debug_nn_stats_pose(unsigned long long *o, int reset) {
+    cudaMemcpyFromSymbol(o, g_nn_stats, sizeof(unsigned long long) * 16);
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_nn_stats, z, sizeof z);
+    }
+    return 0;
+}
+#endif

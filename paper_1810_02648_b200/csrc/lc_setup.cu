@@ -451,7 +451,7 @@ __global__ void k_cand_scan(const GridJob *jobs, int ncells) {
     for (int base = 0; base < ncells; base += blockDim.x) {
         const int i = base + threadIdx.x;
         const int raw = i < ncells ? J.cand_cnt[i] : 0;
-        const int v = raw > 0 ? raw : 0;
+        const int v = raw > 0 ? (raw + 3) & ~3 : 0;   // lists start 16 B aligned
         int s = v;
         const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
         for (int o = 1; o < 32; o <<= 1) {
@@ -474,7 +474,10 @@ __global__ void k_cand_scan(const GridJob *jobs, int ncells) {
             const int start = before + s - v;
             // lists past the buffer capacity fall back to the ring search
             const bool fits = start + v <= ncells * LC_CAND_PER_CELL;
-            J.cand_range[i] = make_int2(start, (raw >= 0 && fits) ? raw : -1);
+            const int cnt = (raw >= 0 && fits) ? raw : -1;
+            J.cand_range[i] = make_int2(start, cnt);
+            J.cand_blk[32 * (size_t)i] = start;
+            J.cand_blk[32 * (size_t)i + 1] = cnt;
             J.cell_fill[i] = 0;   // reused as the per-cell append counter by k_cand_fill
         }
         __syncthreads();
@@ -484,23 +487,31 @@ __global__ void k_cand_scan(const GridJob *jobs, int ncells) {
     if (threadIdx.x == 0) *J.cand_total = carry;
 }
 
-__global__ void k_cand_fill(const GridJob *jobs, int H, int W) {
+// Candidate lists are emitted by the quadtree walk, then sorted per cell by
+// (squared distance from the cell's square, site key): a query scans its
+// cell's list in that order and stops at the first entry whose cell
+// distance exceeds its best distance so far (nn_query), so only the head of
+// the list is read.  Sort: warp-local bitonic network in shared memory over
+// 64-bit keys (near2 << 32 | id); lists are capped at LC_CAND_MAX.
+__global__ void __launch_bounds__(128) k_cand_fill(const GridJob *jobs, int H, int W) {
     const GridJob J = jobs[blockIdx.y];
     const NnGridDev g = grid_of(J, H, W);
     const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    __shared__ unsigned long long keys_all[4][LC_CAND_MAX];
+    unsigned long long *key = keys_all[threadIdx.x >> 5];
     for (int c = blockIdx.x * wpb + (threadIdx.x >> 5); c < g.ncx * g.ncy; c += gridDim.x * wpb) {
         const int2 rg = J.cand_range[c];
         if (rg.y <= 0 || g.K == 0) continue;
         const int cx = c % g.ncx, cy = c / g.ncx;
         const double u2 = J.cand_u2[c];
-        int base = rg.x;
+        int n = 0;
         quad_walk_warp(g, cell_box(cx, cy), [&](double n2) { return n2 <= u2; },
                        [&](int k0, int k1) {
                            for (int k = k0; k < k1; k += 32) {
                                const int kk = k + lane;
                                bool take = false;
-                               int2 p = make_int2(0, 0);
                                int pid = 0;
+                               int2 p = make_int2(0, 0);
                                if (kk < k1) {
                                    pid = g.cell_pts[kk];
                                    p = g.pts[pid];
@@ -508,12 +519,34 @@ __global__ void k_cand_fill(const GridJob *jobs, int H, int W) {
                                }
                                const unsigned bal = __ballot_sync(0xffffffffu, take);
                                if (take)
-                                   J.cand_pts[base + __popc(bal & ((1u << lane) - 1u))] =
-                                       make_int2(p.x | (p.y << 16), pid);
-                               base += __popc(bal);
+                                   key[n + __popc(bal & ((1u << lane) - 1u))] =
+                                       ((unsigned long long)cell_near2_int(cx, cy, p) << 32) | (unsigned)pid;
+                               n += __popc(bal);
                            }
                        },
                        [&]() {});
+        int P = 1;
+        while (P < n) P <<= 1;
+        for (int i = n + lane; i < P; i += 32) key[i] = ~0ull;
+        __syncwarp();
+        for (int k = 2; k <= P; k <<= 1)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = lane; i < P; i += 32) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const unsigned long long a = key[i], b = key[ixj];
+                        if ((a > b) == ((i & k) == 0)) { key[i] = b; key[ixj] = a; }
+                    }
+                }
+                __syncwarp();
+            }
+        for (int i = lane; i < n; i += 32) {
+            const int pid = (int)(unsigned)(key[i] & 0xffffffffu);
+            const int k = site_key(g.pts[pid]);
+            J.cand_pts[rg.x + i] = k;
+            if (i < LC_CAND_HEAD) J.cand_blk[32 * (size_t)c + 2 + i] = k;
+        }
+        __syncwarp();
     }
 }
 
@@ -877,26 +910,27 @@ __global__ void k_rim(const RimJob *jobs, ActorDev A, CamDev cam, const double *
         const V3 p = ld3(J.verts + 3 * (size_t)v);
         double px, py;
         const bool ok = project(cam, p, px, py);
+        // outer_rim_mask (pose_stage.py:218-264): keep iff the own-mask
+        // contour is within 1.5 px, and in Stage I some interior probe is at
+        // least 6 px (2 * depth >= 12) from it.  Both are threshold tests, so
+        // bounded exact searches decide them (nn_within2).
         bool keep = false;
-        int hint0 = -1;
-        if (own.K > 0) {
-            const NnResult n = field_nearest(own, px, py, &hint0);
-            keep = ok && !n.clamped && n.dist <= 1.5;
+        if (own.K > 0 && ok) {
+            const double d2 = nn_within2(own, px, py, 2.0);
+            keep = d2 != LC_INF && sqrt(d2) <= 1.5;
         }
         if (J.stage1) {
             if (keep) {
-                // 16 directions x radii 1..8: depth = max over interior probes.
-                // Lane = (direction, half of the radii); walking outward, each
-                // probe seeds its neighbour search with the previous site.
+                // 16 directions x radii 1..8: depth = max over interior probes;
+                // lane = (direction, half of the radii)
                 double deep = 0.0;
                 const int dir = lane >> 1, r0 = (lane & 1) * 4;
-                int hint = hint0;
                 for (int r = r0; r < r0 + 4; ++r) {
                     const int k = dir * 8 + r;
                     const double qx = px + probe_offs[2 * k], qy = py + probe_offs[2 * k + 1];
-                    const NnResult n = field_nearest(own, qx, qy, &hint);
-                    const double d = field_inside(own, qx, qy) ? n.dist : 0.0;
-                    deep = fmax(deep, d);
+                    if (!field_inside(own, qx, qy)) continue;
+                    const double d2 = nn_within2(own, qx, qy, 7.0);
+                    deep = fmax(deep, d2 == LC_INF ? 7.0 : sqrt(d2));   // > 7 px: any value >= 6 decides
                 }
                 for (int o = 16; o > 0; o >>= 1) deep = fmax(deep, __shfl_xor_sync(0xffffffffu, deep, o));
                 keep = 2.0 * deep >= 12.0;

@@ -354,48 +354,111 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
     }
     T::sync();
     fst(1);
-    for (int b = T::tid(); b < c.B; b += T::size) {
-        const int i = J.bidx[b];
-        J.hold[i] = 1;
-        const V3 p = ld3(v + 3 * (size_t)i);
-        double px, py;
-        const bool ok = project(c.cam, p, px, py);
-        const bool en = J.enabled[b] && ok;
-        int hint = J.nn_hint ? J.nn_hint[b] : -1;
-        const NnResult n0 = field_nearest(c.obs, px, py, &hint);
-        const double sign = side_sign(c.obs, n0, px, py, J.n2d[2 * b], J.n2d[2 * b + 1]);
-        double val = field_interface(n0);
-        double qx = px, qy = py;
-        bool active = en && val > hp.snap_band;
-        bool stuck = false;
-        for (int s = 0; s < hp.snap_max_steps && active; ++s) {
-            const NnResult g = field_nearest(c.obs, qx, qy, &hint);
-            const double gn = sqrt(g.vx * g.vx + g.vy * g.vy);
-            const bool good = gn > 1e-9;
-            const double gd = fmax(gn, 1e-300);
-            const double dx = (-sign * g.vx) / gd, dy = (-sign * g.vy) / gd;
-            double step = hp.snap_step;
-            const double cur = val;
-            double nx = qx, ny = qy, nv = cur;
-            bool pending = good;
-            for (int h = 0; h < 3 && pending; ++h) {
-                const double tx = qx + step * dx, ty = qy + step * dy;
-                int th = hint;
-                const double tv = field_interface(field_nearest(c.obs, tx, ty, &th));
-                if (tv < cur) { nx = tx; ny = ty; nv = tv; pending = false; }
-                step *= 0.5;
+    // One quad of threads per boundary vertex.  A walk step's three halving
+    // trials (step, step/2, step/4 along the gradient) only depend on the
+    // current point, so quad lanes 0..2 query them concurrently and the
+    // first trial that lowers the interface distance is taken, exactly as
+    // the sequential search would; the accepted trial's query is the next
+    // step's gradient query (same point, same exact answer), so one round
+    // of concurrent queries per step replaces up to four dependent ones.
+    // Loops are warp-uniform (inactive quads idle through the shuffles).
+    {
+        const int lane = threadIdx.x & 31, r = lane & 3;
+        const unsigned qmask = 0xfu << (lane & ~3);
+        const int qbase = lane & ~3;
+        constexpr int QPT = T::size / 4;   // quads per team
+        for (int b0 = 0; b0 < c.B; b0 += QPT) {
+            const int b = b0 + T::tid() / 4;
+            const bool valid = b < c.B;
+            int i = 0;
+            V3 p = v3(0, 0, 0);
+            bool en = false;
+            double px = 0.0, py = 0.0;
+            int hint = -1;
+            NnResult g{LC_INF, 0.0, 0.0, true};
+            double sign = 1.0, val = 0.0;
+            if (valid) {
+                i = J.bidx[b];
+                if (r == 0) J.hold[i] = 1;
+                p = ld3(v + 3 * (size_t)i);
+                const bool ok = project(c.cam, p, px, py);
+                en = J.enabled[b] && ok;
+                hint = J.nn_hint ? J.nn_hint[b] : -1;
+                g = field_nearest(c.obs, px, py, &hint);
+                sign = side_sign(c.obs, g, px, py, J.n2d[2 * b], J.n2d[2 * b + 1]);
+                val = field_interface(g);
             }
-            if (!pending && good) { qx = nx; qy = ny; val = nv; }
-            if (pending || !good) { stuck = true; active = false; }
-            active = active && val > hp.snap_band;
-        }
-        cnt[0] += en ? 1.0 : 0.0;
-        cnt[1] += (en && val <= hp.snap_band) ? 1.0 : 0.0;
-        cnt[2] += (stuck && en) ? 1.0 : 0.0;
-        if (en) {
-            const double z = p.z;
-            const V3 landed = v3((qx - c.cam.cx) * z / c.cam.fx, (qy - c.cam.cy) * z / c.cam.fy, z);
-            st3(J.off0 + 3 * (size_t)i, landed - p);
+            double qx = px, qy = py;
+            bool active = valid && en && val > hp.snap_band;
+            bool stuck = false;
+#ifdef LC_NN_STATS
+            const long long w0 = clock64();
+            int nsteps = 0;
+#endif
+            for (int s = 0; s < hp.snap_max_steps; ++s) {
+                if (!__any_sync(0xffffffffu, active)) break;
+#ifdef LC_NN_STATS
+                nsteps += active ? 1 : 0;
+#endif
+                const double gn = sqrt(g.vx * g.vx + g.vy * g.vy);
+                const bool good = gn > 1e-9;
+                const double gd = fmax(gn, 1e-300);
+                const double dx = (-sign * g.vx) / gd, dy = (-sign * g.vy) / gd;
+                // lane r < 3 tries step * 0.5^r (exact halvings)
+                double step = hp.snap_step;
+                for (int h = 0; h < r && h < 2; ++h) step *= 0.5;
+                const double tx = qx + step * dx, ty = qy + step * dy;
+                NnResult t{LC_INF, 0.0, 0.0, true};
+                int th = hint;
+                double tv = LC_INF;
+                if (active && good && r < 3) {
+                    t = field_nearest(c.obs, tx, ty, &th);
+                    tv = field_interface(t);
+                }
+                const double tv0 = __shfl_sync(0xffffffffu, tv, qbase);
+                const double tv1 = __shfl_sync(0xffffffffu, tv, qbase + 1);
+                const double tv2 = __shfl_sync(0xffffffffu, tv, qbase + 2);
+                const double cur = val;
+                const int hit = tv0 < cur ? 0 : (tv1 < cur ? 1 : (tv2 < cur ? 2 : -1));
+                const int src = qbase + (hit < 0 ? 0 : hit);
+                const double nx = __shfl_sync(0xffffffffu, tx, src), ny = __shfl_sync(0xffffffffu, ty, src);
+                const double nvx = __shfl_sync(0xffffffffu, t.vx, src), nvy = __shfl_sync(0xffffffffu, t.vy, src);
+                const double ndist = __shfl_sync(0xffffffffu, t.dist, src);
+                const int nclamp = __shfl_sync(0xffffffffu, (int)t.clamped, src);
+                const int nth = __shfl_sync(0xffffffffu, th, src);
+                if (active) {
+                    if (good && hit >= 0) {
+                        qx = nx; qy = ny;
+                        val = hit == 0 ? tv0 : (hit == 1 ? tv1 : tv2);
+                        g = NnResult{ndist, nvx, nvy, nclamp != 0};
+                        hint = nth;
+                    } else {
+                        stuck = true;
+                        active = false;
+                    }
+                    active = active && val > hp.snap_band;
+                }
+            }
+            (void)qmask;
+#ifdef LC_NN_STATS
+            if (valid && r == 0) {
+                const unsigned long long cyc = (unsigned long long)(clock64() - w0);
+                const unsigned long long prev = atomicMax(&g_nn_stats[4], cyc);
+                if (cyc > prev) g_nn_stats[5] = (unsigned long long)nsteps;
+                atomicMax(&g_nn_stats[6], (unsigned long long)nsteps);
+                atomicAdd(&g_nn_stats[7], (unsigned long long)nsteps);
+            }
+#endif
+            if (valid && r == 0) {
+                cnt[0] += en ? 1.0 : 0.0;
+                cnt[1] += (en && val <= hp.snap_band) ? 1.0 : 0.0;
+                cnt[2] += (stuck && en) ? 1.0 : 0.0;
+                if (en) {
+                    const double z = p.z;
+                    const V3 landed = v3((qx - c.cam.cx) * z / c.cam.fx, (qy - c.cam.cy) * z / c.cam.fy, z);
+                    st3(J.off0 + 3 * (size_t)i, landed - p);
+                }
+            }
         }
     }
     T::sync();
@@ -548,3 +611,14 @@ template __global__ void k_surface_solve_t<8>(const SurfJob *, ActorDev, CamDev,
 template __global__ void k_surface_solve_t<16>(const SurfJob *, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
 
 int surface_block_threads() { return NT; }
+
+#ifdef LC_NN_STATS
+extern "C" int lc_debug_nn_stats_surface(unsigned long long *o, int reset) {
+    cudaMemcpyFromSymbol(o, g_nn_stats, sizeof(unsigned long long) * 16);
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_nn_stats, z, sizeof z);
+    }
+    return 0;
+}
+#endif

@@ -34,6 +34,13 @@ def main():
     frames = [bench.make_stream_frames(actor, cam, a.frames, s, bench.device_renderer(ctx),
                                        bench.device_posing(ctx)) for s in range(a.streams)]
     tr = Tracker(actor, cam, SequenceConfig(), a.streams, ctx=ctx)
+    stats = hasattr(ctx.lib, "lc_debug_nn_stats_pose") if False else None
+    try:
+        import ctypes
+        raw = ctypes.CDLL(_lib.LIB_PATH)
+        stats = [getattr(raw, "lc_debug_nn_stats_" + k) for k in ("pose", "surface")]
+    except (AttributeError, OSError):
+        stats = None
     for f in range(a.frames):
         t0 = time.perf_counter()
         for s in range(a.streams):
@@ -42,6 +49,17 @@ def main():
         tr.step()
         ctx.synchronize()
         print(f"frame {f}: {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
+        if stats:
+            import numpy as np
+            for k, fn in zip(("pose", "surface"), stats):
+                o = np.zeros(16, dtype=np.uint64)
+                fn(o.ctypes.data, 1)
+                q = max(int(o[0]), 1)
+                print(f"   nn {k}: list queries {int(o[0])} entries/query {int(o[1]) / q:.1f} "
+                      f"quadtree {int(o[2])} hinted {int(o[3])}"
+                      + (f" | snap: slowest walk {int(o[4])} cyc / {int(o[5])} steps, max steps {int(o[6])}, "
+                         f"total steps {int(o[7])}" if k == "surface" else "")
+                      + f" | max scanned {int(o[8])} max list {int(o[9])} hist/64 {[int(x) for x in o[10:16]]}")
         if a.phases:
             import numpy as np
             worst = {}
