@@ -190,13 +190,18 @@ extern "C" int lc_ctx_create(int32_t device, uint64_t cuda_stream, lc_ctx **out)
     CK(cudaSetDevice(device));
     lc_ctx *c = new lc_ctx();
     c->device = device;
+    // the solve stream gets the highest priority and the preprocessing
+    // (auxiliary) stream the lowest, so queued-frame preprocessing fills the
+    // SMs the solve leaves idle instead of delaying its cluster launches
+    int prio_lo = 0, prio_hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     if (cuda_stream) {
         c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
     } else {
-        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
         c->own_stream = true;
     }
-    CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio_lo));
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_obs, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_pyr, cudaEventDisableTiming));
@@ -234,6 +239,7 @@ extern "C" int lc_ctx_destroy(lc_ctx *c) {
 extern "C" int lc_ctx_synchronize(lc_ctx *c) {
     require(c != nullptr, "null ctx");
     CK(cudaStreamSynchronize(c->stream));
+    CK(cudaStreamSynchronize(c->aux));
     return last_launch_status();
 }
 
@@ -559,6 +565,44 @@ void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) 
     cudaMemset(counters, 0, sizeof(long long) * LC_NCOUNTERS);
 }
 
+// second input buffer + events of a tracker stream; in[0] is the slot's own
+void Slot::allocate_queue() {
+    const size_t HW = (size_t)H * W;
+    FrameIn &a = in[0];
+    a.image = image; a.mask = mask; a.image_src = image; a.mask_src = mask;
+    a.pyr = pyr; a.obs = obs; a.j2d = j2d; a.j3d_raw = j3d_raw; a.v2d = v2d; a.v3d = v3d;
+    FrameIn &b = in[1];
+    b.image = mem.alloc<double>(HW * 3);
+    b.mask = mem.alloc<uint8_t>(HW);
+    b.image_src = b.image; b.mask_src = b.mask;
+    b.pyr = mem.alloc<double>(HW * 3 * std::max(levels, 1));
+    alloc_grid(mem, b.obs, H, W);
+    b.j2d = mem.alloc<double>(2 * (LC_MAXJ + 4));
+    b.j3d_raw = mem.alloc<double>(3 * LC_MAXJ);
+    b.v2d = mem.alloc<uint8_t>(LC_MAXJ + 4);
+    b.v3d = mem.alloc<uint8_t>(LC_MAXJ);
+    a.tmp = b.tmp = blur_tmp;
+    for (FrameIn &f : in) {
+        cudaEventCreateWithFlags(&f.ready_obs, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&f.ready, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&f.freed, cudaEventDisableTiming);
+    }
+}
+
+// point the slot's per-frame input fields at queued frame `f`
+void Slot::view(const FrameIn &f) {
+    image_src = f.image_src; mask_src = f.mask_src; pyr = f.pyr; obs = f.obs;
+    j2d = f.j2d; j3d_raw = f.j3d_raw; v2d = f.v2d; v3d = f.v3d;
+}
+
+Slot::~Slot() {
+    for (FrameIn &f : in) {
+        if (f.ready_obs) cudaEventDestroy(f.ready_obs);
+        if (f.ready) cudaEventDestroy(f.ready);
+        if (f.freed) cudaEventDestroy(f.freed);
+    }
+}
+
 static CamDev cam_dev(const lc_camera &c) {
     CamDev d;
     d.fx = c.fx; d.fy = c.fy; d.cx = c.cx; d.cy = c.cy; d.W = c.width; d.H = c.height;
@@ -776,32 +820,40 @@ static void build_config(lc_ctx *c, const lc_actor *a, const lc_nonrigid_hyper *
     cf.probe = cf.mem.upload(pr.data(), pr.size(), st);
 }
 
-static void pyramid(lc_ctx *c, const ConfigDev &cf, const std::vector<Slot *> &slots, int levels) {
-    if (slots.empty()) return;
+// gaussian_pyramid (imageproc.py:276-285) of a batch of images
+struct PyrTarget { const double *src; double *dst; double *tmp; };
+
+static void pyramid(lc_ctx *c, const ConfigDev &cf, const std::vector<PyrTarget> &ts, int H, int W, int levels) {
+    if (ts.empty()) return;
     bool fused = levels <= 4;
     for (int l = 0; l < levels; ++l) fused = fused && cf.half[l] <= LC_PYR_HALO;
     if (fused) {
-        const int H = slots[0]->H, W = slots[0]->W;
         std::vector<PyrAllJob> jobs;
-        for (Slot *s : slots) jobs.push_back(PyrAllJob{s->image_src, s->pyr});
+        for (const PyrTarget &t : ts) jobs.push_back(PyrAllJob{t.src, t.dst});
         const int tiles = ((W + LC_PYR_TILE - 1) / LC_PYR_TILE) * ((H + LC_PYR_TILE - 1) / LC_PYR_TILE);
-        launch(c, k_pyramid_fused, dim3(tiles, (unsigned)slots.size()), dim3(256), pyramid_fused_smem(),
+        launch(c, k_pyramid_fused, dim3(tiles, (unsigned)ts.size()), dim3(256), pyramid_fused_smem(),
                stage(c, jobs), H, W, levels, (const double *)cf.taps, cf.half[0], cf.half[1], cf.half[2],
                cf.half[3]);
         return;
     }
-    const int H = slots[0]->H, W = slots[0]->W;
     const long long n = (long long)H * W * 3;
     const int grid = (int)std::min<long long>((n + 255) / 256, 2368);
     for (int l = 0; l < levels; ++l) {
         std::vector<PyrJob> jobs;
-        for (Slot *s : slots) jobs.push_back(PyrJob{s->image_src, s->blur_tmp, s->pyr + (size_t)l * n});
+        for (const PyrTarget &t : ts) jobs.push_back(PyrJob{t.src, t.tmp, t.dst + (size_t)l * n});
         const PyrJob *dj = stage(c, jobs);
-        launch(c, k_blur_axis, dim3(grid, (unsigned)slots.size()), dim3(256), 0, dj, H, W, 3,
+        launch(c, k_blur_axis, dim3(grid, (unsigned)ts.size()), dim3(256), 0, dj, H, W, 3,
                (const double *)(cf.taps + 32 * l), cf.half[l], 0);
-        launch(c, k_blur_axis, dim3(grid, (unsigned)slots.size()), dim3(256), 0, dj, H, W, 3,
+        launch(c, k_blur_axis, dim3(grid, (unsigned)ts.size()), dim3(256), 0, dj, H, W, 3,
                (const double *)(cf.taps + 32 * l), cf.half[l], 1);
     }
+}
+
+static void pyramid(lc_ctx *c, const ConfigDev &cf, const std::vector<Slot *> &slots, int levels) {
+    if (slots.empty()) return;
+    std::vector<PyrTarget> ts;
+    for (Slot *s : slots) ts.push_back(PyrTarget{s->image_src, s->pyr, s->blur_tmp});
+    pyramid(c, cf, ts, slots[0]->H, slots[0]->W, levels);
 }
 
 // ---------------------------------------------------------------------------
@@ -900,7 +952,34 @@ struct FrameBatch {
     const lc_config *cfg;
     ConfigDev *cf;
     std::vector<Slot *> slots;
+    std::vector<FrameIn *> in;    // the frame each slot solves (its preprocessing is launched)
 };
+
+// Preprocessing of queued frames (pipeline.py:156-162) on the auxiliary
+// stream: observed-silhouette contour + NN grid, then the blur pyramid.  A
+// buffer is rebuilt only after the solve that last read it has finished.
+static void launch_preprocess(lc_ctx *c, const ConfigDev &cf, const lc_config &cfg,
+                              const std::vector<FrameIn *> &fs, int H, int W) {
+    if (fs.empty()) return;
+    cudaEventRecord(c->ev_fork, c->stream);
+    cudaStreamWaitEvent(c->aux, c->ev_fork, 0);
+    for (FrameIn *f : fs)
+        if (f->used) cudaStreamWaitEvent(c->aux, f->freed, 0);
+    OnStream on(c, c->aux);
+    std::vector<std::pair<const GridBufs *, const uint8_t *>> gs;
+    for (FrameIn *f : fs) gs.push_back({&f->obs, f->mask_src});
+    build_grids(c, gs, H, W, obs_list_radius());
+    for (FrameIn *f : fs) cudaEventRecord(f->ready_obs, c->aux);
+    if (cfg.mode == 0) {
+        std::vector<PyrTarget> ts;
+        for (FrameIn *f : fs) ts.push_back(PyrTarget{f->image_src, f->pyr, f->tmp});
+        pyramid(c, cf, ts, H, W, cfg.nonrigid.n_levels);
+    }
+    for (FrameIn *f : fs) {
+        cudaEventRecord(f->ready, c->aux);
+        f->state = 2;
+    }
+}
 
 // FK of each slot's pose (optional) then DQ skinning of the actor rest shape
 // (use_drest = false) or the slot's displaced rest shape (use_drest = true)
@@ -995,21 +1074,10 @@ static void run_frame(FrameBatch &fb) {
     const int H = fb.cam.height, W = fb.cam.width;
     auto &ss = fb.slots;
     const unsigned S = (unsigned)ss.size();
-    // ---- preprocess (pipeline.py:156-162) on the auxiliary stream, concurrent
-    // with Stage I's own setup: observed contour grid (joined before the pose
-    // solve), blur pyramid (joined before the surface solve).  Descriptors are
-    // staged on the main stream before the fork.
-    cudaEventRecord(c->ev_fork, c->stream);
-    cudaStreamWaitEvent(c->aux, c->ev_fork, 0);
-    {
-        OnStream on(c, c->aux);
-        std::vector<std::pair<const GridBufs *, const uint8_t *>> gs;
-        for (Slot *s : ss) gs.push_back({&s->obs, s->mask_src});
-        build_grids(c, gs, H, W, obs_list_radius());
-        cudaEventRecord(c->ev_obs, c->aux);
-        if (cfg.mode == 0) pyramid(c, *fb.cf, ss, cfg.nonrigid.n_levels);
-        cudaEventRecord(c->ev_pyr, c->aux);
-    }
+    // ---- preprocessing (pipeline.py:156-162) was launched on the auxiliary
+    // stream by lc_tracker_step (possibly during the previous frame's solve);
+    // the observed grid is joined before the pose solve, the pyramid before
+    // the surface solve.
     // ---- condition (pipeline.py:165-170) + displaced rest + initial pose
     {
         std::vector<PrepJob> pj;
@@ -1077,7 +1145,8 @@ static void run_frame(FrameBatch &fb) {
             pj.push_back(p);
             ++k;
         }
-        if (r == 0) cudaStreamWaitEvent(c->stream, c->ev_obs, 0);
+        if (r == 0)
+            for (FrameIn *f : fb.in) cudaStreamWaitEvent(c->stream, f->ready_obs, 0);
         pose_launch(c, a, fb.cam, pj);
     }
     // ---- Stage II (pipeline.py:227-260) or the pose-only surface
@@ -1112,10 +1181,10 @@ static void run_frame(FrameBatch &fb) {
             j.phase = s->phase_surf;
             sj.push_back(j);
         }
-        cudaStreamWaitEvent(c->stream, c->ev_pyr, 0);
+        for (FrameIn *f : fb.in) cudaStreamWaitEvent(c->stream, f->ready, 0);
         surface_launch(c, a, fb.cam, *fb.cf, sj);
     }
-    cudaStreamWaitEvent(c->stream, c->ev_pyr, 0);   // join the aux stream in every mode
+    for (FrameIn *f : fb.in) cudaStreamWaitEvent(c->stream, f->ready, 0);   // join the aux stream in every mode
     // ---- state update (pipeline.py:281-299)
     std::vector<FinishJob> fj;
     for (Slot *s : ss) {
@@ -1160,6 +1229,7 @@ extern "C" int lc_tracker_create(lc_ctx *c, const lc_actor *a, const lc_camera *
     for (int i = 0; i < S; ++i) {
         Slot *s = new Slot();
         s->allocate(a->dev.N, a->dev.T, a->dev.E, cam->height, cam->width, cfg->nonrigid.n_levels, a->skel.J);
+        s->allocate_queue();
         t->slots.push_back(s);
     }
     CK(cudaStreamSynchronize(c->stream));
@@ -1171,36 +1241,45 @@ extern "C" int lc_tracker_create(lc_ctx *c, const lc_actor *a, const lc_camera *
 extern "C" int lc_tracker_destroy(lc_tracker *t) {
     if (!t) return LC_OK;
     cudaStreamSynchronize(t->ctx->stream);
+    cudaStreamSynchronize(t->ctx->aux);   // queued frames may still be preprocessing
     for (Slot *s : t->slots) delete s;
     delete t;
     return LC_OK;
 }
 
-static void upload_dets(lc_ctx *c, Slot *s, const lc_detections *d, int J) {
-    stage_to(c, s->j2d, d->joints2d, sizeof(double) * 2 * (J + 4));
-    stage_to(c, s->j3d_raw, d->joints3d, sizeof(double) * 3 * J);
-    stage_to(c, s->v2d, d->valid2d, J + 4);
-    stage_to(c, s->v3d, d->valid3d, J);
-}
 
+// Queues the next frame of one stream (at most two queued frames per
+// stream: the one the next step solves and the one after it, whose upload
+// and preprocessing then overlap that solve).
 extern "C" int lc_tracker_set_frame(lc_tracker *t, int32_t stream, const double *image, const uint8_t *mask,
                                     const lc_detections *det, int32_t on_device) {
     API_BEGIN
     require(t && det, "null argument");
     require(stream >= 0 && stream < t->S, "stream index out of range");
+    require(image && mask, "null image or mask");
     Slot *s = t->slots[stream];
     lc_ctx *c = t->ctx;
+    FrameIn &f = s->in[s->in_tail];
+    require(f.state == 0, "two frames are already queued for this stream: call lc_tracker_step first");
     const size_t HW = (size_t)s->H * s->W;
     if (on_device) {
-        s->image_src = image;
-        s->mask_src = mask;
+        f.image_src = image;
+        f.mask_src = mask;
     } else {
-        CK(cudaMemcpyAsync(s->image, image, HW * 3 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(s->mask, mask, HW, cudaMemcpyHostToDevice, c->stream));
-        s->image_src = s->image;
-        s->mask_src = s->mask;
+        // the host copies go on the auxiliary stream, after the solve that last read the buffer
+        if (f.used) CK(cudaStreamWaitEvent(c->aux, f.freed, 0));
+        CK(cudaMemcpyAsync(f.image, image, HW * 3 * sizeof(double), cudaMemcpyHostToDevice, c->aux));
+        CK(cudaMemcpyAsync(f.mask, mask, HW, cudaMemcpyHostToDevice, c->aux));
+        f.image_src = f.image;
+        f.mask_src = f.mask;
     }
-    upload_dets(c, s, det, t->actor->skel.J);
+    const int J = t->actor->skel.J;
+    stage_to(c, f.j2d, det->joints2d, sizeof(double) * 2 * (J + 4));
+    stage_to(c, f.j3d_raw, det->joints3d, sizeof(double) * 3 * J);
+    stage_to(c, f.v2d, det->valid2d, J + 4);
+    stage_to(c, f.v3d, det->valid3d, J);
+    f.state = 1;
+    s->in_tail ^= 1;
     return LC_OK;
     API_END
 }
@@ -1208,9 +1287,33 @@ extern "C" int lc_tracker_set_frame(lc_tracker *t, int32_t stream, const double 
 extern "C" int lc_tracker_step(lc_tracker *t) {
     API_BEGIN
     require(t != nullptr, "null tracker");
-    CK(cudaSetDevice(t->ctx->device));
-    FrameBatch fb{t->ctx, t->actor, t->cam, &t->cfg, &t->conf, t->slots};
+    lc_ctx *c = t->ctx;
+    CK(cudaSetDevice(c->device));
+    std::vector<FrameIn *> cur, todo, next;
+    bool all_next = true;
+    for (Slot *s : t->slots) {
+        FrameIn &f = s->in[s->in_head];
+        require(f.state >= 1, "no frame queued for a stream: call lc_tracker_set_frame first");
+        cur.push_back(&f);
+        if (f.state == 1) todo.push_back(&f);
+        FrameIn &n = s->in[s->in_head ^ 1];
+        if (n.state == 1) next.push_back(&n);
+        else all_next = false;
+    }
+    const int H = t->cam.height, W = t->cam.width;
+    launch_preprocess(c, t->conf, t->cfg, todo, H, W);
+    // every stream already has its next frame: preprocess it during this solve
+    if (all_next) launch_preprocess(c, t->conf, t->cfg, next, H, W);
+    for (size_t i = 0; i < t->slots.size(); ++i) t->slots[i]->view(*cur[i]);
+    FrameBatch fb{c, t->actor, t->cam, &t->cfg, &t->conf, t->slots, cur};
     run_frame(fb);
+    for (size_t i = 0; i < t->slots.size(); ++i) {
+        FrameIn &f = *cur[i];
+        CK(cudaEventRecord(f.freed, c->stream));
+        f.used = true;
+        f.state = 0;
+        t->slots[i]->in_head ^= 1;
+    }
     t->frame_counter++;
     return last_launch_status();
     API_END

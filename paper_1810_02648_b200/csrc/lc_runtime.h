@@ -72,6 +72,27 @@ struct GridBufs {
     int qP, qL;
 };
 
+// One queued frame of a tracker stream: inputs plus their preprocessing
+// products (pipeline.py:156-162).  A stream has two, so the next frame can be
+// uploaded and preprocessed while the current one is solved (the
+// reference's pipelined driver, pipeline.py:432-499).
+struct FrameIn {
+    double *image = nullptr;           // own copy (host inputs)
+    uint8_t *mask = nullptr;
+    const double *image_src = nullptr;  // own copy or the caller's device pointer
+    const uint8_t *mask_src = nullptr;
+    double *pyr = nullptr;
+    double *tmp = nullptr;             // blur scratch (the slot's, shared by its queue)
+    GridBufs obs{};
+    double *j2d = nullptr, *j3d_raw = nullptr;
+    uint8_t *v2d = nullptr, *v3d = nullptr;
+    cudaEvent_t ready_obs = nullptr;   // observed-silhouette grid built (aux stream)
+    cudaEvent_t ready = nullptr;       // all preprocessing done (aux stream)
+    cudaEvent_t freed = nullptr;       // last solve that read this buffer done (main stream)
+    bool used = false;                 // `freed` has been recorded at least once
+    int state = 0;                     // 0 empty, 1 staged, 2 preprocessing launched
+};
+
 // per-stream device state + scratch
 struct Slot {
     DevArena mem;
@@ -109,7 +130,13 @@ struct Slot {
     lc_nonrigid_report *nr_rep;
     long long *counters;   // LC_NCOUNTERS cumulative work counters (device)
     long long *phase_pose, *phase_surf;   // LC_NPHASE timestamps of the last solves
+    // tracker input queue (in[0] aliases the buffers above)
+    FrameIn in[2];
+    int in_head = 0, in_tail = 0;
     void allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J);
+    void allocate_queue();
+    void view(const FrameIn &f);
+    ~Slot();
 };
 
 struct lc_field {

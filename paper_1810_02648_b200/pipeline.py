@@ -108,13 +108,31 @@ class SequenceResult:
 
 
 def run_sequence(inputs, config=None, pipelined=False) -> SequenceResult:
-    """Sequential driver (pipeline.py:378-397): state stays on the device."""
+    """Sequence drivers (pipeline.py:378-515); the track state stays on the device.
+
+    pipelined=False is run_sequence_sequential: frame f is uploaded,
+    preprocessed and solved before frame f+1 is touched.  pipelined=True is
+    run_sequence_pipelined's 2-slot schedule: frame f+1 is queued before
+    frame f is solved, so its upload and preprocessing (pyramid, observed
+    contour grid) overlap frame f's solve.  The solves themselves are the
+    same, so both drivers return identical results (pipelined == sequential).
+    """
     config = SequenceConfig.from_reference(config) if config is not None else SequenceConfig()
     tr = Tracker(inputs.actor, inputs.camera, config, 1)
     frames = []
-    t0 = time.perf_counter()
-    for f in range(inputs.n_frames):
+    n = inputs.n_frames
+
+    def queue(f):
         tr.set_frame(0, inputs.images[f], inputs.masks[f], inputs.detections[f])
+
+    t0 = time.perf_counter()
+    if pipelined and n:
+        queue(0)
+    for f in range(n):
+        if not pipelined:
+            queue(f)
+        elif f + 1 < n:
+            queue(f + 1)
         tr.step()
         x, v, vs, rep = tr.result(0)
         frames.append(FrameResult(f, PoseParams.from_vector(x), v, vs, pose_report_from_c(rep.pose),

@@ -76,3 +76,38 @@ def test_tracker_batched_streams_identical():
 @pytest.mark.slow
 def test_tracker_x5k_frame0():
     _run("x5k", 1024, 2, directional=False)
+
+
+def test_pipelined_equals_sequential():
+    """run_sequence_pipelined's 2-slot schedule (pipeline.py:432-499): frame
+    f+1 is queued (uploaded + preprocessed on the auxiliary stream) before
+    frame f is solved.  The solves are the same, so results are bit-identical."""
+    from paper_1810_02648_b200.config import SequenceConfig
+    from paper_1810_02648_b200.pipeline import SequenceInputs, run_sequence
+    actor, cam, frames = scene("standard", 256, 4)
+    inputs = SequenceInputs(actor, cam, [f.image for f in frames], [f.mask for f in frames],
+                            [f.detections for f in frames])
+    cfg = SequenceConfig(directional=False)
+    a = run_sequence(inputs, cfg, pipelined=False)
+    b = run_sequence(inputs, cfg, pipelined=True)
+    assert b.pipelined and not a.pipelined
+    assert np.array_equal(a.poses, b.poses)
+    assert np.array_equal(a.vertices, b.vertices)
+
+
+def test_queue_depth_is_two():
+    from paper_1810_02648_b200.config import SequenceConfig
+    from paper_1810_02648_b200.device import Tracker
+    actor, cam, frames = scene("small", 128, 3)
+    tr = Tracker(actor, cam, SequenceConfig(directional=False), 1)
+    with pytest.raises(Exception):
+        tr.step()                       # nothing queued
+    tr.set_frame(0, frames[0].image, frames[0].mask, frames[0].detections)
+    tr.set_frame(0, frames[1].image, frames[1].mask, frames[1].detections)
+    with pytest.raises(ValueError):
+        tr.set_frame(0, frames[2].image, frames[2].mask, frames[2].detections)
+    tr.step()
+    tr.set_frame(0, frames[2].image, frames[2].mask, frames[2].detections)
+    tr.step()
+    tr.step()
+    tr.close()
