@@ -205,7 +205,8 @@ def run_ours(args):
     actor = S.build_actor(args.preset, with_skirt=True)
     cam = suggest_camera(args.res, args.res)
     Sn, K, W = args.streams, args.steps, args.warmup
-    F = W + K + 1     # one frame beyond the timed steps is queued, never solved
+    AHEAD = 2         # frames queued ahead of the one being solved (the library holds 3)
+    F = W + K + AHEAD  # frames beyond the timed steps are queued, never solved
     t_gen = time.perf_counter()
     frames = [make_stream_frames(actor, cam, F, seed, device_renderer(ctx), device_posing(ctx))
               for seed in shard_seeds(rank, Sn)]
@@ -252,9 +253,10 @@ def run_ours(args):
             tr.set_frame(s, img_d[s, f].data_ptr(), msk_d[s, f].data_ptr(), dets[s][f], on_device=True)
 
     clocks = ClockSampler(local)     # sampling spans warm-up + the timed region
-    queue_dev(0)
+    for f in range(AHEAD):
+        queue_dev(f)
     for f in range(W):
-        queue_dev(f + 1)
+        queue_dev(f + AHEAD)
         tr.step()
     ctx.synchronize()
     c0 = [tr.counters(s) for s in range(Sn)]
@@ -265,7 +267,7 @@ def run_ours(args):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for f in range(W, W + K):
-        queue_dev(f + 1)
+        queue_dev(f + AHEAD)
         tr.step()
     ctx.synchronize()            # joins the auxiliary (preprocessing) stream too
     ev1.record(stream)
@@ -290,32 +292,45 @@ def run_ours(args):
     pcg_iters = sum(int((c1[s] - c0[s])[2]) for s in range(Sn))
     tr.close()
 
-    # ---- e2e: public API from pinned host buffers, results read back each
-    # step; frames are queued one ahead as above (uploads overlap the solve)
+    # ---- e2e: public API from pinned host buffers.  Frames are queued one
+    # ahead as above (uploads overlap the solve) and every step's poses +
+    # surfaces are read back into pinned host buffers with the streaming
+    # readout; the host consumes frame f's results (event wait) while frame
+    # f+1 is being solved (the pipelined driver's 2-slot latency).
     tr2 = Tracker(actor, cam, cfg, Sn, ctx=ctx)
-    x_out = np.empty(36)
-    v_out = np.empty((N, 3))
+    x_h = torch.empty((2, Sn, 36), dtype=torch.float64, pin_memory=True)
+    v_h = torch.empty((2, Sn, N, 3), dtype=torch.float64, pin_memory=True)
+    done = [torch.cuda.Event(), torch.cuda.Event()]
+    checksum = [0.0]
 
     def queue_host(f):
         for s in range(Sn):
             tr2.set_frame(s, img_h[s, f].numpy(), msk_h[s, f].numpy(), dets[s][f])
 
-    def step_host():
+    def step_host(f, first):
         tr2.step()
+        b = f & 1
         for s in range(Sn):
-            _lib.check(ctx.lib.lc_tracker_get_result(tr2.handle, s, _lib.ptr(x_out), _lib.ptr(v_out), None, None))
+            tr2.result_async(s, x_h[b, s], v_h[b, s])
+        done[b].record(stream)
+        if not first:                     # frame f-1's results are complete on the host
+            done[b ^ 1].synchronize()
+            checksum[0] += float(x_h[b ^ 1, :, 3].sum())
 
-    queue_host(0)
+    for f in range(AHEAD):
+        queue_host(f)
     for f in range(W):
-        queue_host(f + 1)
-        step_host()
+        queue_host(f + AHEAD)
+        step_host(f, f == 0)
+    ctx.synchronize()
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for f in range(W, W + K):
-        queue_host(f + 1)
-        step_host()
+        queue_host(f + AHEAD)
+        step_host(f, False)
+    done[(W + K - 1) & 1].synchronize()   # the last frame's results
     ctx.synchronize()
     e1.record(stream)
     e1.synchronize()

@@ -242,14 +242,25 @@ int lc_nonrigid_solve(lc_ctx *ctx, const lc_actor *actor, const lc_camera *cam,
 int lc_tracker_create(lc_ctx *ctx, const lc_actor *actor, const lc_camera *cam,
                       const lc_config *cfg, int32_t n_streams, lc_tracker **out);
 int lc_tracker_destroy(lc_tracker *tr);
-/* stage frame inputs of one stream: image H*W*3 f64, mask H*W u8.
- * on_device != 0: pointers are device pointers (already resident in HBM). */
+/* queue the next frame of one stream: image H*W*3 f64, mask H*W u8.
+ * on_device != 0: pointers are device pointers (already resident in HBM).
+ * Up to 3 frames may be queued per stream; host inputs are uploaded
+ * asynchronously (pinned memory must stay valid until the frame is solved),
+ * and a queued frame is preprocessed while the one before it is solved
+ * (the reference's pipelined driver, pipeline.py:432-499). */
 int lc_tracker_set_frame(lc_tracker *tr, int32_t stream, const double *image,
                          const uint8_t *mask, const lc_detections *det, int32_t on_device);
-/* preprocess + condition + solve_frame for every stream (asynchronous) */
+/* condition + solve_frame for the oldest queued frame of every stream
+ * (asynchronous); launches the preprocessing of the next queued frames */
 int lc_tracker_step(lc_tracker *tr);
 int lc_tracker_get_result(lc_tracker *tr, int32_t stream, double *pose_out, double *verts_out,
                           double *skinned_out, lc_frame_report *report);
+/* streaming readout (the pipelined driver's emit, pipeline.py:449-499):
+ * enqueue D2H copies of the last stepped frame's pose (36) and surface
+ * (N*3) on the context's stream and return immediately; the host buffers
+ * (pinned for full asynchrony) hold the data once the stream passes this
+ * point, so frame f can be read while frame f+1 is solved. */
+int lc_tracker_get_result_async(lc_tracker *tr, int32_t stream, double *pose_out, double *verts_out);
 /* TrackState injection / readout (pipeline.py:135-142); NULL pointers = None */
 int lc_tracker_set_state(lc_tracker *tr, int32_t stream, const double *x_prev,
                          const double *x_prev2, const double *joints_prev,

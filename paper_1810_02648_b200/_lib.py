@@ -135,6 +135,7 @@ _SIGS = {
     "lc_tracker_create": (C.c_int, [P, P, P, P, i32, P]),
     "lc_tracker_destroy": (C.c_int, [P]),
     "lc_tracker_set_frame": (C.c_int, [P, i32, P, P, P, i32]),
+    "lc_tracker_get_result_async": (C.c_int, [P, i32, P, P]),
     "lc_tracker_step": (C.c_int, [P]),
     "lc_tracker_get_result": (C.c_int, [P, i32, P, P, P, P]),
     "lc_tracker_set_state": (C.c_int, [P, i32, P, P, P, P, P, P]),

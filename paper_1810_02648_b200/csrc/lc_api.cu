@@ -133,27 +133,62 @@ extern "C" int lc_version(void) { return 1; }
 // ---------------------------------------------------------------------------
 // job staging: small per-launch descriptor arrays copied H2D in stream order
 
-// Pinned host ring + device ring: descriptors are memcpy'd into pinned
-// memory and copied with a truly asynchronous cudaMemcpyAsync (a pageable
-// source would synchronize the stream on every launch).  Before the ring
-// wraps, the stream is drained so no in-flight copy still reads a slot.
+// Job descriptors reach the device as kernel parameters: a one-CTA
+// k_stage launch carries the bytes by value and writes them into a device
+// ring slot (or a given buffer) in stream order.  No copy engine is
+// involved, so descriptor staging never queues behind a large host upload
+// of a queued frame (which would stall the solve for the whole transfer),
+// and the host never blocks.  Before the ring wraps, the streams are
+// drained so no pending kernel still reads a slot.
+template <int CAP>
+struct StageBlob { uint4 w[CAP / 16]; };
+
+template <int CAP>
+__global__ void k_stage(unsigned char *dst, int bytes, StageBlob<CAP> blob) {
+    const unsigned char *src = reinterpret_cast<const unsigned char *>(blob.w);
+    const bool vec = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+    const int nv = vec ? bytes / 16 : 0;
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) reinterpret_cast<uint4 *>(dst)[i] = blob.w[i];
+    for (int i = 16 * nv + threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+}
+
+template <int CAP>
+static void stage_launch(cudaStream_t st, void *dst, const void *src, size_t bytes) {
+    StageBlob<CAP> b;
+    std::memcpy(b.w, src, bytes);
+    k_stage<CAP><<<1, 128, 0, st>>>(static_cast<unsigned char *>(dst), (int)bytes, b);
+}
+
+static void stage_bytes(cudaStream_t st, void *dst, const void *src, size_t bytes) {
+    if (bytes <= 512) stage_launch<512>(st, dst, src, bytes);
+    else if (bytes <= 4096) stage_launch<4096>(st, dst, src, bytes);
+    else if (bytes <= 16384) stage_launch<16384>(st, dst, src, bytes);
+    else {
+        for (size_t o = 0; o < bytes; o += 16384)
+            stage_launch<16384>(st, static_cast<char *>(dst) + o, static_cast<const char *>(src) + o,
+                                std::min<size_t>(16384, bytes - o));
+    }
+}
+
 struct JobRing {
     char *dev = nullptr;
-    char *host = nullptr;
     size_t cap = 0, off = 0;
-    cudaStream_t aux = nullptr;
+    cudaStream_t main = nullptr, aux = nullptr;
     void *put(cudaStream_t st, const void *src, size_t bytes, void *dst = nullptr) {
-        const size_t padded = (bytes + 255) & ~size_t(255);
-        if (padded > cap) throw ApiError("job descriptor larger than the staging ring");
-        if (off + padded > cap) {
-            cudaStreamSynchronize(st);
-            if (aux) cudaStreamSynchronize(aux);
-            off = 0;
+        void *d = dst;
+        if (!d) {
+            const size_t padded = (bytes + 255) & ~size_t(255);
+            if (padded > cap) throw ApiError("job descriptor larger than the staging ring");
+            if (off + padded > cap) {
+                cudaStreamSynchronize(st);
+                cudaStreamSynchronize(main);
+                if (aux) cudaStreamSynchronize(aux);
+                off = 0;
+            }
+            d = dev + off;
+            off += padded;
         }
-        std::memcpy(host + off, src, bytes);
-        void *d = dst ? dst : dev + off;
-        cudaMemcpyAsync(d, host + off, bytes, cudaMemcpyHostToDevice, st);
-        off += padded;
+        stage_bytes(st, d, src, bytes);
         return d;
     }
 };
@@ -163,9 +198,9 @@ static JobRing &ring_of(lc_ctx *c) {
         if (r.first == c) return r.second;
     JobRing jr;
     jr.cap = 16 << 20;
+    jr.main = c->stream;
     jr.aux = c->aux;
     if (cudaMalloc(&jr.dev, jr.cap) != cudaSuccess) throw std::bad_alloc();
-    if (cudaMallocHost(&jr.host, jr.cap) != cudaSuccess) throw std::bad_alloc();
     rings.push_back({c, jr});
     return rings.back().second;
 }
@@ -173,7 +208,7 @@ template <typename T>
 static const T *stage(lc_ctx *c, const std::vector<T> &v) {
     return static_cast<const T *>(ring_of(c).put(c->stream, v.data(), v.size() * sizeof(T)));
 }
-// small host array -> existing device buffer, asynchronously via the pinned ring
+// small host array -> existing device buffer, in stream order
 static void stage_to(lc_ctx *c, void *dst, const void *src, size_t bytes) {
     if (bytes) ring_of(c).put(c->stream, src, bytes, dst);
 }
@@ -202,6 +237,7 @@ extern "C" int lc_ctx_create(int32_t device, uint64_t cuda_stream, lc_ctx **out)
         c->own_stream = true;
     }
     CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio_lo));
+    CK(cudaStreamCreateWithPriority(&c->copy, cudaStreamNonBlocking, prio_lo));
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_obs, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_pyr, cudaEventDisableTiming));
@@ -227,7 +263,9 @@ extern "C" int lc_ctx_destroy(lc_ctx *c) {
     cudaStreamSynchronize(c->stream);
     delete c->call_slot;
     cudaStreamSynchronize(c->aux);
+    cudaStreamSynchronize(c->copy);
     cudaStreamDestroy(c->aux);
+    cudaStreamDestroy(c->copy);
     cudaEventDestroy(c->ev_fork);
     cudaEventDestroy(c->ev_obs);
     cudaEventDestroy(c->ev_pyr);
@@ -240,6 +278,7 @@ extern "C" int lc_ctx_synchronize(lc_ctx *c) {
     require(c != nullptr, "null ctx");
     CK(cudaStreamSynchronize(c->stream));
     CK(cudaStreamSynchronize(c->aux));
+    CK(cudaStreamSynchronize(c->copy));
     return last_launch_status();
 }
 
@@ -565,27 +604,31 @@ void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) 
     cudaMemset(counters, 0, sizeof(long long) * LC_NCOUNTERS);
 }
 
-// second input buffer + events of a tracker stream; in[0] is the slot's own
+// the other input buffers + events of a tracker stream; in[0] is the slot's own
 void Slot::allocate_queue() {
     const size_t HW = (size_t)H * W;
     FrameIn &a = in[0];
     a.image = image; a.mask = mask; a.image_src = image; a.mask_src = mask;
     a.pyr = pyr; a.obs = obs; a.j2d = j2d; a.j3d_raw = j3d_raw; a.v2d = v2d; a.v3d = v3d;
-    FrameIn &b = in[1];
-    b.image = mem.alloc<double>(HW * 3);
-    b.mask = mem.alloc<uint8_t>(HW);
-    b.image_src = b.image; b.mask_src = b.mask;
-    b.pyr = mem.alloc<double>(HW * 3 * std::max(levels, 1));
-    alloc_grid(mem, b.obs, H, W);
-    b.j2d = mem.alloc<double>(2 * (LC_MAXJ + 4));
-    b.j3d_raw = mem.alloc<double>(3 * LC_MAXJ);
-    b.v2d = mem.alloc<uint8_t>(LC_MAXJ + 4);
-    b.v3d = mem.alloc<uint8_t>(LC_MAXJ);
-    a.tmp = b.tmp = blur_tmp;
+    a.tmp = blur_tmp;
+    for (int q = 1; q < LC_QUEUE; ++q) {
+        FrameIn &b = in[q];
+        b.image = mem.alloc<double>(HW * 3);
+        b.mask = mem.alloc<uint8_t>(HW);
+        b.image_src = b.image; b.mask_src = b.mask;
+        b.pyr = mem.alloc<double>(HW * 3 * std::max(levels, 1));
+        alloc_grid(mem, b.obs, H, W);
+        b.j2d = mem.alloc<double>(2 * (LC_MAXJ + 4));
+        b.j3d_raw = mem.alloc<double>(3 * LC_MAXJ);
+        b.v2d = mem.alloc<uint8_t>(LC_MAXJ + 4);
+        b.v3d = mem.alloc<uint8_t>(LC_MAXJ);
+        b.tmp = blur_tmp;
+    }
     for (FrameIn &f : in) {
         cudaEventCreateWithFlags(&f.ready_obs, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&f.ready, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&f.freed, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&f.uploaded, cudaEventDisableTiming);
     }
 }
 
@@ -600,6 +643,7 @@ Slot::~Slot() {
         if (f.ready_obs) cudaEventDestroy(f.ready_obs);
         if (f.ready) cudaEventDestroy(f.ready);
         if (f.freed) cudaEventDestroy(f.freed);
+        if (f.uploaded) cudaEventDestroy(f.uploaded);
     }
 }
 
@@ -963,8 +1007,11 @@ static void launch_preprocess(lc_ctx *c, const ConfigDev &cf, const lc_config &c
     if (fs.empty()) return;
     cudaEventRecord(c->ev_fork, c->stream);
     cudaStreamWaitEvent(c->aux, c->ev_fork, 0);
-    for (FrameIn *f : fs)
+    for (FrameIn *f : fs) {
         if (f->used) cudaStreamWaitEvent(c->aux, f->freed, 0);
+        if (f->pending_upload) cudaStreamWaitEvent(c->aux, f->uploaded, 0);
+        f->pending_upload = false;
+    }
     OnStream on(c, c->aux);
     std::vector<std::pair<const GridBufs *, const uint8_t *>> gs;
     for (FrameIn *f : fs) gs.push_back({&f->obs, f->mask_src});
@@ -1242,14 +1289,15 @@ extern "C" int lc_tracker_destroy(lc_tracker *t) {
     if (!t) return LC_OK;
     cudaStreamSynchronize(t->ctx->stream);
     cudaStreamSynchronize(t->ctx->aux);   // queued frames may still be preprocessing
+    cudaStreamSynchronize(t->ctx->copy);
     for (Slot *s : t->slots) delete s;
     delete t;
     return LC_OK;
 }
 
 
-// Queues the next frame of one stream (at most two queued frames per
-// stream: the one the next step solves and the one after it, whose upload
+// Queues the next frame of one stream (at most LC_QUEUE queued frames per
+// stream: the one the next step solves and the ones after it, whose upload
 // and preprocessing then overlap that solve).
 extern "C" int lc_tracker_set_frame(lc_tracker *t, int32_t stream, const double *image, const uint8_t *mask,
                                     const lc_detections *det, int32_t on_device) {
@@ -1260,16 +1308,19 @@ extern "C" int lc_tracker_set_frame(lc_tracker *t, int32_t stream, const double 
     Slot *s = t->slots[stream];
     lc_ctx *c = t->ctx;
     FrameIn &f = s->in[s->in_tail];
-    require(f.state == 0, "two frames are already queued for this stream: call lc_tracker_step first");
+    require(f.state == 0, "the stream's frame queue is full: call lc_tracker_step first");
     const size_t HW = (size_t)s->H * s->W;
     if (on_device) {
         f.image_src = image;
         f.mask_src = mask;
     } else {
-        // the host copies go on the auxiliary stream, after the solve that last read the buffer
-        if (f.used) CK(cudaStreamWaitEvent(c->aux, f.freed, 0));
-        CK(cudaMemcpyAsync(f.image, image, HW * 3 * sizeof(double), cudaMemcpyHostToDevice, c->aux));
-        CK(cudaMemcpyAsync(f.mask, mask, HW, cudaMemcpyHostToDevice, c->aux));
+        // the host copies go on the copy stream, after the solve that last
+        // read the buffer; the buffer's preprocessing waits for them
+        if (f.used) CK(cudaStreamWaitEvent(c->copy, f.freed, 0));
+        CK(cudaMemcpyAsync(f.image, image, HW * 3 * sizeof(double), cudaMemcpyHostToDevice, c->copy));
+        CK(cudaMemcpyAsync(f.mask, mask, HW, cudaMemcpyHostToDevice, c->copy));
+        CK(cudaEventRecord(f.uploaded, c->copy));
+        f.pending_upload = true;
         f.image_src = f.image;
         f.mask_src = f.mask;
     }
@@ -1279,7 +1330,7 @@ extern "C" int lc_tracker_set_frame(lc_tracker *t, int32_t stream, const double 
     stage_to(c, f.v2d, det->valid2d, J + 4);
     stage_to(c, f.v3d, det->valid3d, J);
     f.state = 1;
-    s->in_tail ^= 1;
+    s->in_tail = (s->in_tail + 1) % LC_QUEUE;
     return LC_OK;
     API_END
 }
@@ -1296,7 +1347,7 @@ extern "C" int lc_tracker_step(lc_tracker *t) {
         require(f.state >= 1, "no frame queued for a stream: call lc_tracker_set_frame first");
         cur.push_back(&f);
         if (f.state == 1) todo.push_back(&f);
-        FrameIn &n = s->in[s->in_head ^ 1];
+        FrameIn &n = s->in[(s->in_head + 1) % LC_QUEUE];
         if (n.state == 1) next.push_back(&n);
         else all_next = false;
     }
@@ -1312,7 +1363,7 @@ extern "C" int lc_tracker_step(lc_tracker *t) {
         CK(cudaEventRecord(f.freed, c->stream));
         f.used = true;
         f.state = 0;
-        t->slots[i]->in_head ^= 1;
+        t->slots[i]->in_head = (t->slots[i]->in_head + 1) % LC_QUEUE;
     }
     t->frame_counter++;
     return last_launch_status();
@@ -1337,6 +1388,24 @@ extern "C" int lc_tracker_get_result(lc_tracker *t, int32_t stream, double *pose
     }
     CK(cudaStreamSynchronize(c->stream));
     return last_launch_status();
+    API_END
+}
+
+// Streaming readout: enqueue the D2H copies of the last stepped frame's pose
+// and surface on the solve stream and return at once (pinned destinations
+// make it fully asynchronous).  The data is on the host once the stream has
+// passed this point (an event recorded after it, or lc_ctx_synchronize), so
+// a caller can read frame f while frame f+1 is being solved.
+extern "C" int lc_tracker_get_result_async(lc_tracker *t, int32_t stream, double *pose_out, double *verts_out) {
+    API_BEGIN
+    require(t != nullptr, "null tracker");
+    require(stream >= 0 && stream < t->S, "stream index out of range");
+    Slot *s = t->slots[stream];
+    lc_ctx *c = t->ctx;
+    if (pose_out) CK(cudaMemcpyAsync(pose_out, s->x_prev, sizeof(double) * LC_NP, cudaMemcpyDeviceToHost, c->stream));
+    if (verts_out)
+        CK(cudaMemcpyAsync(verts_out, s->v_prev, sizeof(double) * 3 * s->N, cudaMemcpyDeviceToHost, c->stream));
+    return LC_OK;
     API_END
 }
 

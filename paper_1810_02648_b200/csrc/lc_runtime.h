@@ -14,6 +14,8 @@ struct lc_ctx {
     // auxiliary stream for work independent of Stage I (pyramid, observed grid)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_obs = nullptr, ev_pyr = nullptr;
+    // host->device uploads of queued frames (copy engine, overlaps both)
+    cudaStream_t copy = nullptr;
     long long launches = 0;
     // optional per-kernel timing: CUDA events around every launch of `prof_name`
     std::string prof_name;
@@ -72,10 +74,13 @@ struct GridBufs {
     int qP, qL;
 };
 
+#define LC_QUEUE 3   // queued frames per tracker stream (solve, preprocess, upload)
+
 // One queued frame of a tracker stream: inputs plus their preprocessing
 // products (pipeline.py:156-162).  A stream has two, so the next frame can be
 // uploaded and preprocessed while the current one is solved (the
-// reference's pipelined driver, pipeline.py:432-499).
+// reference's pipelined driver, pipeline.py:432-499); a third lets the
+// upload of frame f+2 overlap frame f+1's preprocessing and frame f's solve.
 struct FrameIn {
     double *image = nullptr;           // own copy (host inputs)
     uint8_t *mask = nullptr;
@@ -89,6 +94,8 @@ struct FrameIn {
     cudaEvent_t ready_obs = nullptr;   // observed-silhouette grid built (aux stream)
     cudaEvent_t ready = nullptr;       // all preprocessing done (aux stream)
     cudaEvent_t freed = nullptr;       // last solve that read this buffer done (main stream)
+    cudaEvent_t uploaded = nullptr;    // host inputs copied (copy stream)
+    bool pending_upload = false;
     bool used = false;                 // `freed` has been recorded at least once
     int state = 0;                     // 0 empty, 1 staged, 2 preprocessing launched
 };
@@ -130,8 +137,8 @@ struct Slot {
     lc_nonrigid_report *nr_rep;
     long long *counters;   // LC_NCOUNTERS cumulative work counters (device)
     long long *phase_pose, *phase_surf;   // LC_NPHASE timestamps of the last solves
-    // tracker input queue (in[0] aliases the buffers above)
-    FrameIn in[2];
+    // tracker input queue, a ring of LC_QUEUE frames (in[0] aliases the buffers above)
+    FrameIn in[LC_QUEUE];
     int in_head = 0, in_tail = 0;
     void allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J);
     void allocate_queue();

@@ -282,6 +282,17 @@ class Tracker:
                                                    C.byref(rep) if rep is not None else None))
         return x, v, vs, rep
 
+    def result_async(self, stream: int, pose_out, verts_out):
+        """Enqueue the D2H readout of the last stepped frame into caller
+        buffers (pinned: fully asynchronous); valid once the context's stream
+        passes this point.  Arguments are objects with a data pointer
+        (numpy arrays, or torch tensors via .data_ptr())."""
+        def p(a):
+            if a is None:
+                return None
+            return C.c_void_p(a.data_ptr()) if hasattr(a, "data_ptr") else L.ptr(a)
+        L.check(self.ctx.lib.lc_tracker_get_result_async(self.handle, stream, p(pose_out), p(verts_out)))
+
     def set_state(self, stream: int, state):
         """Inject a TrackState (teacher forcing / resume)."""
         def arr(a, shape):

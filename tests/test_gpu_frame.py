@@ -95,19 +95,21 @@ def test_pipelined_equals_sequential():
     assert np.array_equal(a.vertices, b.vertices)
 
 
-def test_queue_depth_is_two():
+def test_queue_depth_is_three():
     from paper_1810_02648_b200.config import SequenceConfig
     from paper_1810_02648_b200.device import Tracker
-    actor, cam, frames = scene("small", 128, 3)
+    actor, cam, frames = scene("small", 128, 4)
     tr = Tracker(actor, cam, SequenceConfig(directional=False), 1)
     with pytest.raises(Exception):
         tr.step()                       # nothing queued
-    tr.set_frame(0, frames[0].image, frames[0].mask, frames[0].detections)
-    tr.set_frame(0, frames[1].image, frames[1].mask, frames[1].detections)
+    for f in range(3):
+        tr.set_frame(0, frames[f].image, frames[f].mask, frames[f].detections)
     with pytest.raises(ValueError):
-        tr.set_frame(0, frames[2].image, frames[2].mask, frames[2].detections)
+        tr.set_frame(0, frames[3].image, frames[3].mask, frames[3].detections)
     tr.step()
-    tr.set_frame(0, frames[2].image, frames[2].mask, frames[2].detections)
-    tr.step()
-    tr.step()
+    tr.set_frame(0, frames[3].image, frames[3].mask, frames[3].detections)
+    for _ in range(3):
+        tr.step()
+    with pytest.raises(Exception):
+        tr.step()
     tr.close()
