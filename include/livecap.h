@@ -255,6 +255,9 @@ int lc_tracker_set_frame(lc_tracker *tr, int32_t stream, const double *image,
 int lc_tracker_step(lc_tracker *tr);
 int lc_tracker_get_result(lc_tracker *tr, int32_t stream, double *pose_out, double *verts_out,
                           double *skinned_out, lc_frame_report *report);
+/* developer timeline (LIVECAP_TRACE=1 at context creation): text lines
+ * "lane name t_ms" for the marks recorded since the last dump */
+int lc_trace_dump(lc_ctx *ctx, char *buf, int64_t cap);
 /* streaming readout (the pipelined driver's emit, pipeline.py:449-499):
  * enqueue D2H copies of the last stepped frame's pose (36) and surface
  * (N*3) on the context's stream and return immediately; the host buffers

@@ -136,6 +136,7 @@ _SIGS = {
     "lc_tracker_destroy": (C.c_int, [P]),
     "lc_tracker_set_frame": (C.c_int, [P, i32, P, P, P, i32]),
     "lc_tracker_get_result_async": (C.c_int, [P, i32, P, P]),
+    "lc_trace_dump": (C.c_int, [P, C.c_char_p, C.c_int64]),
     "lc_tracker_step": (C.c_int, [P]),
     "lc_tracker_get_result": (C.c_int, [P, i32, P, P, P, P]),
     "lc_tracker_set_state": (C.c_int, [P, i32, P, P, P, P, P, P]),

@@ -67,6 +67,17 @@ static void launch_named(const char *name, lc_ctx *c, K kernel, dim3 g, dim3 b, 
 }
 #define launch(c, kernel, ...) launch_named(#kernel, c, kernel, __VA_ARGS__)
 
+// timeline marks (LIVECAP_TRACE=1): an event with timing on the context's
+// current stream; lane 0 = solve stream, 1 = auxiliary, 2 = copy
+static void mark(lc_ctx *c, const char *name) {
+    if (!c->tracing) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, c->stream);
+    const int lane = c->stream == c->aux ? 1 : (c->stream == c->copy ? 2 : 0);
+    c->marks.push_back({name, lane, e});
+}
+
 // temporarily route a context's launches to another stream
 struct OnStream {
     lc_ctx *c;
@@ -238,6 +249,7 @@ extern "C" int lc_ctx_create(int32_t device, uint64_t cuda_stream, lc_ctx **out)
     }
     CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio_lo));
     CK(cudaStreamCreateWithPriority(&c->copy, cudaStreamNonBlocking, prio_lo));
+    c->tracing = getenv("LIVECAP_TRACE") != nullptr;
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_obs, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_pyr, cudaEventDisableTiming));
@@ -271,6 +283,28 @@ extern "C" int lc_ctx_destroy(lc_ctx *c) {
     cudaEventDestroy(c->ev_pyr);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
+    return LC_OK;
+}
+
+// timeline dump: one line per mark "lane name t_ms" (t relative to the first mark), marks cleared
+extern "C" int lc_trace_dump(lc_ctx *c, char *buf, int64_t cap) {
+    require(c && buf && cap > 0, "null argument");
+    cudaDeviceSynchronize();
+    std::string out;
+    if (!c->marks.empty()) {
+        for (auto &m : c->marks) {
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, c->marks[0].ev, m.ev);
+            char line[160];
+            snprintf(line, sizeof line, "%d %s %.4f\n", m.lane, m.name, ms);
+            out += line;
+        }
+        for (auto &m : c->marks) cudaEventDestroy(m.ev);
+        c->marks.clear();
+    }
+    const size_t n = std::min<size_t>(out.size(), (size_t)cap - 1);
+    std::memcpy(buf, out.data(), n);
+    buf[n] = 0;
     return LC_OK;
 }
 
@@ -567,8 +601,19 @@ void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) 
     fk = mem.alloc<FkState>(1);
     zbuf = mem.alloc<unsigned long long>(HW);
     tri_id = mem.alloc<int>(HW);
-    big = mem.alloc<int>(std::max(T, 1));
-    n_big = mem.alloc<int>(1);
+    {
+        const int ntx = (W + LC_RT_TILE - 1) / LC_RT_TILE, nty = (H + LC_RT_TILE - 1) / LC_RT_TILE;
+        rt_rec = mem.alloc<TriRec>(std::max(T, 1));
+        rt_diff = mem.alloc<int>((size_t)ntx * nty);
+        rt_off = mem.alloc<int>((size_t)ntx * nty + 1);
+        rt_fill = mem.alloc<int>((size_t)ntx * nty);
+        rt_cap = std::max(1 << 20, 64 * T);
+        rt_list = mem.alloc<int>(rt_cap);
+        rt_ioff = mem.alloc<int>((size_t)ntx * nty + 1);
+        const size_t items = 2 * (size_t)ntx * nty + rt_cap / LC_RT_CHUNK + 1;
+        rt_pz = mem.alloc<unsigned long long>(items * 256);
+        rt_pid = mem.alloc<int>(items * 256);
+    }
     tri_front = mem.alloc<uint8_t>(T);
     vflag = mem.alloc<uint8_t>(N);
     enabled = mem.alloc<uint8_t>(N);
@@ -722,22 +767,36 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
     launch(c, k_cand_fill, dim3((ncx * ncy + 3) / 4, S), dim3(128), 0, dj, H, W);
 }
 
-static void raster(lc_ctx *c, const lc_actor *a, const lc_camera &cam, std::vector<RasterJob> jobs,
-                   bool winner, bool mask) {
+// depth buffer + winning triangle ids (+ mask) of a batch of meshes with
+// the same triangles (rasterizer.py:18-68): tile-binned single pass
+static void raster_tris(lc_ctx *c, const CamDev &cd, const int *tris, int T, const std::vector<RasterJob> &jobs) {
     if (jobs.empty()) return;
     const RasterJob *dj = stage(c, jobs);
-    const int S = (int)jobs.size();
-    const int HW = cam.width * cam.height;
-    const CamDev cd = cam_dev(cam);
-    const int T = a->dev.T;
-    launch(c, k_raster_clear, dim3(592, S), dim3(256), 0, dj, HW);
-    launch(c, k_raster_depth, dim3((T + 127) / 128, S), dim3(128), 0, dj, cd, a->dev.tris, T);
-    launch(c, k_raster_depth_big, dim3(64, S), dim3(256), 0, dj, cd, a->dev.tris);
-    if (winner) {
-        launch(c, k_raster_winner, dim3((T + 127) / 128, S), dim3(128), 0, dj, cd, a->dev.tris, T);
-        launch(c, k_raster_winner_big, dim3(64, S), dim3(256), 0, dj, cd, a->dev.tris);
-    }
-    if (mask) launch(c, k_raster_mask, dim3(592, S), dim3(256), 0, dj, HW);
+    const unsigned S = (unsigned)jobs.size();
+    const int ntx = (cd.W + LC_RT_TILE - 1) / LC_RT_TILE, nty = (cd.H + LC_RT_TILE - 1) / LC_RT_TILE;
+    const int nt = ntx * nty;
+    launch(c, k_rt_clear, dim3((nt + 255) / 256, S), dim3(256), 0, dj, nt);
+    launch(c, k_rt_setup, dim3((T + 127) / 128, S), dim3(128), 0, dj, cd, tris, T);
+    launch(c, k_rt_bin<0>, dim3((T + 3) / 4, S), dim3(128), 0, dj, T, ntx);
+    launch(c, k_rt_scan, dim3(S), dim3(1024), 0, dj, nt, T);
+    launch(c, k_rt_bin<1>, dim3((T + 3) / 4, S), dim3(128), 0, dj, T, ntx);
+    mark(c, "raster:bin");
+    launch(c, k_rt_tiles, dim3(std::max(1, 1184 / (int)S), S), dim3(256), 0, dj, cd, T, ntx, nt);
+    launch(c, k_rt_merge, dim3(std::max(1, 1184 / (int)S), S), dim3(256), 0, dj, cd, ntx, nt);
+    mark(c, "raster:tiles");
+}
+
+static RasterJob raster_job(Slot *s, const double *verts, uint8_t *mask) {
+    RasterJob j{};
+    j.verts = verts; j.zbuf = s->zbuf; j.tri_id = s->tri_id; j.mask = mask;
+    j.rec = s->rt_rec; j.tcount = s->rt_diff; j.toff = s->rt_off; j.tfill = s->rt_fill; j.tlist = s->rt_list;
+    j.tcap = s->rt_cap;
+    j.ioff = s->rt_ioff; j.pz = s->rt_pz; j.pid = s->rt_pid;
+    return j;
+}
+
+static void raster(lc_ctx *c, const lc_actor *a, const lc_camera &cam, const std::vector<RasterJob> &jobs) {
+    raster_tris(c, cam_dev(cam), a->dev.tris, a->dev.T, jobs);
 }
 
 // ---------------------------------------------------------------------------
@@ -1013,15 +1072,18 @@ static void launch_preprocess(lc_ctx *c, const ConfigDev &cf, const lc_config &c
         f->pending_upload = false;
     }
     OnStream on(c, c->aux);
+    mark(c, "pre:start");
     std::vector<std::pair<const GridBufs *, const uint8_t *>> gs;
     for (FrameIn *f : fs) gs.push_back({&f->obs, f->mask_src});
     build_grids(c, gs, H, W, obs_list_radius());
+    mark(c, "pre:grid");
     for (FrameIn *f : fs) cudaEventRecord(f->ready_obs, c->aux);
     if (cfg.mode == 0) {
         std::vector<PyrTarget> ts;
         for (FrameIn *f : fs) ts.push_back(PyrTarget{f->image_src, f->pyr, f->tmp});
         pyramid(c, cf, ts, H, W, cfg.nonrigid.n_levels);
     }
+    mark(c, "pre:pyramid");
     for (FrameIn *f : fs) {
         cudaEventRecord(f->ready, c->aux);
         f->state = 2;
@@ -1056,8 +1118,8 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
     const lc_actor *a = fb.a;
     const int H = fb.cam.height, W = fb.cam.width;
     std::vector<RasterJob> rj;
-    for (Slot *s : ss) rj.push_back(RasterJob{s->*verts, s->zbuf, s->tri_id, s->own_mask, s->big, s->n_big});
-    raster(c, a, fb.cam, rj, !stage1 && fb.cfg->enable_part_mask, true);
+    for (Slot *s : ss) rj.push_back(raster_job(s, s->*verts, s->own_mask));
+    raster(c, a, fb.cam, rj);
     std::vector<std::pair<const GridBufs *, const uint8_t *>> gs;
     for (Slot *s : ss) gs.push_back({&s->own, s->own_mask});
     build_grids(c, gs, H, W, 0.0, false);   // rim queries stay near the own contour: quadtree only
@@ -1138,6 +1200,7 @@ static void run_frame(FrameBatch &fb) {
             p.N = a->dev.N;
             pj.push_back(p);
         }
+        mark(c, "frame:start");
         launch(c, k_prep, dim3(16, S), dim3(256), 0, stage(c, pj), (const SkelDev *)a->skel_dev);
         for (Slot *s : ss) {
             cudaMemsetAsync(s->pose_rep, 0, sizeof(lc_pose_report), c->stream);
@@ -1158,7 +1221,9 @@ static void run_frame(FrameBatch &fb) {
         for (unsigned i = 0; i < S; ++i)
             if (r < rounds[i]) act.push_back(ss[i]);
         fk_skin(fb, act, true, true, &Slot::model, nullptr);
+        mark(c, "s1:skin");
         contour_and_rim(fb, act, &Slot::model, true);
+        mark(c, "s1:contour+rim");
         std::vector<PoseJob> pj;
         int k = 0;
         for (unsigned i = 0; i < S; ++i) {
@@ -1194,7 +1259,9 @@ static void run_frame(FrameBatch &fb) {
         }
         if (r == 0)
             for (FrameIn *f : fb.in) cudaStreamWaitEvent(c->stream, f->ready_obs, 0);
+        mark(c, "s1:waited-grid");
         pose_launch(c, a, fb.cam, pj);
+        mark(c, "s1:pose");
     }
     // ---- Stage II (pipeline.py:227-260) or the pose-only surface
     if (cfg.mode == 0) {
@@ -1204,7 +1271,9 @@ static void run_frame(FrameBatch &fb) {
         fk_skin(fb, ss, true, false, &Slot::vs, &Slot::rot);
     }
     if (cfg.mode == 0) {
+        mark(c, "s2:skin");
         contour_and_rim(fb, ss, &Slot::vinit, false);
+        mark(c, "s2:contour+rim");
         std::vector<SurfJob> sj;
         for (Slot *s : ss) {
             SurfJob j{};
@@ -1229,7 +1298,9 @@ static void run_frame(FrameBatch &fb) {
             sj.push_back(j);
         }
         for (FrameIn *f : fb.in) cudaStreamWaitEvent(c->stream, f->ready, 0);
+        mark(c, "s2:waited-pyr");
         surface_launch(c, a, fb.cam, *fb.cf, sj);
+        mark(c, "s2:surface");
     }
     for (FrameIn *f : fb.in) cudaStreamWaitEvent(c->stream, f->ready, 0);   // join the aux stream in every mode
     // ---- state update (pipeline.py:281-299)
@@ -1245,6 +1316,7 @@ static void run_frame(FrameBatch &fb) {
         fj.push_back(f);
     }
     launch(c, k_finish, dim3(16, S), dim3(256), 0, stage(c, fj));
+    mark(c, "frame:end");
     for (Slot *s : ss) {
         s->has_prev2 = s->has_prev;
         s->has_prev = true;
@@ -1763,7 +1835,7 @@ extern "C" int lc_contour_vertices(lc_ctx *c, const lc_actor *a, const lc_camera
     Slot *s = call_slot(c, a, H, W, 1);
     cudaStream_t st = c->stream;
     CK(cudaMemcpyAsync(s->model, verts, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
-    raster(c, a, *cam, {RasterJob{s->model, s->zbuf, s->tri_id, nullptr, s->big, s->n_big}}, false, false);
+    raster(c, a, *cam, {raster_job(s, s->model, nullptr)});
     ContourJob j{};
     j.verts = s->model; j.zbuf = s->zbuf; j.tri_front = s->tri_front; j.tri_n = s->tri_n; j.vflag = s->vflag;
     j.idx = s->cidx; j.n2d = s->n2d; j.B = s->B; j.vis = nullptr; j.P = nullptr; j.active = 1;
@@ -1826,16 +1898,24 @@ extern "C" int lc_render(lc_ctx *c, const lc_camera *cam, int32_t n, const doubl
         di = m.upload(ii.data(), ii.size(), st);
         io = m.alloc<long long>(HW);
     }
-    int *big = m.alloc<int>(std::max(t, 1)), *nbig = m.alloc<int>(1);
-    const RasterJob *dj = stage(c, std::vector<RasterJob>{RasterJob{dv, zb, tid, nullptr, big, nbig}});
     const CamDev cd = cam_dev(*cam);
-    launch(c, k_raster_clear, dim3(592), dim3(256), 0, dj, (int)HW);
-    launch(c, k_raster_depth, dim3((t + 127) / 128), dim3(128), 0, dj, cd, (const int *)dt, t);
-    launch(c, k_raster_depth_big, dim3(64), dim3(256), 0, dj, cd, (const int *)dt);
-    if (mode) {
-        launch(c, k_raster_winner, dim3((t + 127) / 128), dim3(128), 0, dj, cd, (const int *)dt, t);
-        launch(c, k_raster_winner_big, dim3(64), dim3(256), 0, dj, cd, (const int *)dt);
+    RasterJob rj{};
+    {
+        const int ntx = (cam->width + LC_RT_TILE - 1) / LC_RT_TILE, nty = (cam->height + LC_RT_TILE - 1) / LC_RT_TILE;
+        rj.verts = dv; rj.zbuf = zb; rj.tri_id = tid; rj.mask = nullptr;
+        rj.rec = m.alloc<TriRec>(std::max(t, 1));
+        rj.tcount = m.alloc<int>((size_t)ntx * nty);
+        rj.toff = m.alloc<int>((size_t)ntx * nty + 1);
+        rj.tfill = m.alloc<int>((size_t)ntx * nty);
+        rj.tcap = std::max(1 << 20, 64 * t);
+        rj.tlist = m.alloc<int>(rj.tcap);
+        rj.ioff = m.alloc<int>((size_t)ntx * nty + 1);
+        const size_t items = 2 * (size_t)ntx * nty + rj.tcap / LC_RT_CHUNK + 1;
+        rj.pz = m.alloc<unsigned long long>(items * 256);
+        rj.pid = m.alloc<int>(items * 256);
     }
+    raster_tris(c, cd, dt, t, {rj});
+    const RasterJob *dj = stage(c, std::vector<RasterJob>{rj});
     launch(c, k_raster_resolve, dim3(592), dim3(256), 0, dj, cd, (const int *)dt, mode, (const double *)da,
            n_attr, (const int *)di, bg_attr, (long long)bg_id, za, ao, io);
     CK(cudaMemcpyAsync(zbuf_out, za, HW * sizeof(double), cudaMemcpyDeviceToHost, st));

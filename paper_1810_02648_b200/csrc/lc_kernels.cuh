@@ -56,20 +56,40 @@ __global__ void k_cand_scan(const GridJob *jobs, int ncells);
 __global__ void k_cand_fill(const GridJob *jobs, int H, int W);
 
 // ----- rasterizer (rasterizer.py:18-120) -----------------------------------
+// Tile-binned rasterizer scratch.  Triangles are set up once (projection,
+// inverse area, clipped bbox) into TriRec, binned into 16x16-pixel tiles,
+// and every tile resolves its pixels in one pass.
+#define LC_RT_TILE 16
+#define LC_RT_SHIFT 4
+struct TriRec {
+    double P[6];   // projected vertices (x0 y0 x1 y1 x2 y2)
+    double D[3];   // depths
+    double inv;    // 1 / signed area
+    int bb[4];     // clipped pixel bbox x0 x1 y0 y1; bb[0] > bb[1] marks a culled triangle
+};
 struct RasterJob {
     const double *verts;        // N*3
     unsigned long long *zbuf;   // H*W, fp64 bit patterns (+inf = empty)
     int *tri_id;                // H*W, INT_MAX = empty
     uint8_t *mask;              // H*W out (isfinite(zbuf)), may be null
-    int *big;                   // T capacity: triangles whose clipped bbox is large
-    int *n_big;                 // count (reset by k_raster_clear)
+    TriRec *rec;                // T
+    int *tcount;                // ntiles triangles per tile
+    int *toff;                  // ntiles+1 list offsets
+    int *tfill;                 // ntiles append counters
+    int *tlist;                 // tcap triangle ids, grouped by tile
+    int tcap;
+    int *ioff;                  // ntiles+1 work-item offsets (chunks of LC_RT_CHUNK triangles)
+    unsigned long long *pz;     // items x 256 per-chunk partial depths (multi-chunk tiles);
+    int *pid;                   // items <= 2 ntiles + tcap / LC_RT_CHUNK
 };
-#define LC_RASTER_SMALL 256     // bbox pixels handled by one thread; larger -> one CTA
-__global__ void k_raster_clear(const RasterJob *jobs, int HW);
-__global__ void k_raster_depth(const RasterJob *jobs, CamDev cam, const int *tris, int T);
-__global__ void k_raster_winner(const RasterJob *jobs, CamDev cam, const int *tris, int T);
-__global__ void k_raster_depth_big(const RasterJob *jobs, CamDev cam, const int *tris);
-__global__ void k_raster_winner_big(const RasterJob *jobs, CamDev cam, const int *tris);
+#define LC_RT_CHUNK 256
+__global__ void k_rt_clear(const RasterJob *jobs, int n);
+__global__ void k_rt_setup(const RasterJob *jobs, CamDev cam, const int *tris, int T);
+template <int FILL>
+__global__ void k_rt_bin(const RasterJob *jobs, int T, int ntx);
+__global__ void k_rt_scan(const RasterJob *jobs, int n, int T);
+__global__ void k_rt_tiles(const RasterJob *jobs, CamDev cam, int T, int ntx, int nt);
+__global__ void k_rt_merge(const RasterJob *jobs, CamDev cam, int ntx, int nt);
 __global__ void k_raster_mask(const RasterJob *jobs, int HW);
 __global__ void k_raster_resolve(const RasterJob *jobs, CamDev cam, const int *tris, int mode,
                                  const double *attrs, int n_attr, const int *ids,

@@ -16,6 +16,10 @@ struct lc_ctx {
     cudaEvent_t ev_fork = nullptr, ev_obs = nullptr, ev_pyr = nullptr;
     // host->device uploads of queued frames (copy engine, overlaps both)
     cudaStream_t copy = nullptr;
+    // optional timeline (LIVECAP_TRACE=1): timing events at phase boundaries
+    bool tracing = false;
+    struct Mark { const char *name; int lane; cudaEvent_t ev; };
+    std::vector<Mark> marks;
     long long launches = 0;
     // optional per-kernel timing: CUDA events around every launch of `prof_name`
     std::string prof_name;
@@ -124,7 +128,11 @@ struct Slot {
     FkState *fk;
     unsigned long long *zbuf;
     int *tri_id;
-    int *big, *n_big;
+    // tile-binned raster scratch (RasterJob)
+    TriRec *rt_rec;
+    int *rt_diff, *rt_off, *rt_fill, *rt_list, *rt_ioff, *rt_pid;
+    unsigned long long *rt_pz;
+    int rt_cap = 0;
     uint8_t *tri_front, *vflag, *enabled;
     double *tri_n, *n2d, *crest;
     int *cidx, *B, *vis, *P;

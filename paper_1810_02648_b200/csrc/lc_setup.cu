@@ -591,95 +591,241 @@ __device__ __forceinline__ bool bary(const double P[3][2], double inv, int ix, i
     return !(l0 < 0.0 || l1 < 0.0 || l2 < 0.0);
 }
 
-__global__ void k_raster_clear(const RasterJob *jobs, int HW) {
+// Tile-binned single pass.  The sequential rule "first triangle with a
+// strictly smaller depth wins" (rasterizer.py:46-58) leaves every pixel with
+// the lexicographic minimum of (depth, triangle index) over the triangles
+// covering it, so the order in which a tile meets its triangles does not
+// matter.  Setup: one thread per triangle writes its TriRec (the reference's
+// arithmetic: projection, signed area, clipped bbox).  Binning: one warp per
+// triangle counts, then (after a per-stream scan) appends, the triangle in
+// every tile of its bbox it can touch.  Resolve: one CTA per 16x16 tile
+// stages the tile's triangles in shared memory and every thread resolves
+// its pixel (depth, id and mask) in registers: no per-pixel atomics, no
+// second pass, coalesced stores.  A tile whose list overflowed the buffer
+// tests every triangle (still exact).
+
+__global__ void k_rt_clear(const RasterJob *jobs, int n) {
     const RasterJob J = jobs[blockIdx.y];
-    if (blockIdx.x == 0 && threadIdx.x == 0) *J.n_big = 0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += gridDim.x * blockDim.x) {
-        J.zbuf[i] = 0x7ff0000000000000ULL;
-        J.tri_id[i] = INT_MAX;
-    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) J.tcount[i] = 0;
 }
 
-__device__ __forceinline__ void depth_pixel(const RasterJob &J, CamDev cam, const double P[3][2],
-                                            const double D[3], double inv, int x, int y) {
-    double l0, l1, l2;
-    if (!bary(P, inv, x, y, l0, l1, l2)) return;
-    const double z = l0 * D[0] + l1 * D[1] + l2 * D[2];
-    // result unused -> compiled to a fire-and-forget RED.MIN (no load latency on the path)
-    atomicMin(J.zbuf + (size_t)y * cam.W + x, (unsigned long long)__double_as_longlong(z));
-}
-
-__device__ __forceinline__ void winner_pixel(const RasterJob &J, CamDev cam, const double P[3][2],
-                                             const double D[3], double inv, int x, int y, int t) {
-    double l0, l1, l2;
-    if (!bary(P, inv, x, y, l0, l1, l2)) return;
-    const double z = l0 * D[0] + l1 * D[1] + l2 * D[2];
-    const size_t pi = (size_t)y * cam.W + x;
-    if ((unsigned long long)__double_as_longlong(z) == J.zbuf[pi] && t < J.tri_id[pi])
-        atomicMin(J.tri_id + pi, t);
-}
-
-__device__ __forceinline__ long long bbox_pixels(const int bb[4]) {
-    return (long long)(bb[1] - bb[0] + 1) * (long long)(bb[3] - bb[2] + 1);
-}
-
-// one thread per small triangle; large (clipped) triangles are deferred to
-// the one-CTA-per-triangle pass so no thread walks a megapixel bbox (the
-// reference's own trackers produce such triangles once they lose track)
-__global__ void k_raster_depth(const RasterJob *jobs, CamDev cam, const int *tris, int T) {
+__global__ void k_rt_setup(const RasterJob *jobs, CamDev cam, const int *tris, int T) {
     const RasterJob J = jobs[blockIdx.y];
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= T) return;
-    double P[3][2], D[3], inv;
+    double P[3][2], D[3], inv = 0.0;
     int bb[4];
-    if (!tri_setup(cam, J.verts, tris, t, P, D, inv, bb)) return;
-    if (bbox_pixels(bb) > LC_RASTER_SMALL) {
-        J.big[atomicAdd(J.n_big, 1)] = t;
-        return;
+    const bool ok = tri_setup(cam, J.verts, tris, t, P, D, inv, bb);
+    TriRec r;
+    for (int k = 0; k < 3; ++k) {
+        r.P[2 * k] = P[k][0];
+        r.P[2 * k + 1] = P[k][1];
+        r.D[k] = D[k];
     }
-    for (int y = bb[2]; y <= bb[3]; ++y)
-        for (int x = bb[0]; x <= bb[1]; ++x) depth_pixel(J, cam, P, D, inv, x, y);
+    r.inv = inv;
+    if (ok) {
+        for (int k = 0; k < 4; ++k) r.bb[k] = bb[k];
+    } else {
+        r.bb[0] = 1; r.bb[1] = 0; r.bb[2] = 1; r.bb[3] = 0;
+    }
+    J.rec[t] = r;
 }
 
-__global__ void k_raster_winner(const RasterJob *jobs, CamDev cam, const int *tris, int T) {
+// Can triangle r cover a pixel of tile (tx, ty)?  No only when one
+// barycentric coordinate is below -eps at all four corners of the tile's
+// pixel box: the coordinate is affine, so every pixel of the tile then has
+// it below -eps + 2 delta < 0 in the exact per-pixel test (delta bounds the
+// rounding of bary's arithmetic; eps is set well above it).  This keeps
+// slivers with huge bboxes (the reference's trackers produce them once they
+// lose track) out of most tiles.
+struct RtCull { double eps; bool on; };
+__device__ __forceinline__ RtCull rt_cull(const TriRec &r, int ntiles) {
+    double big = 2048.0;
+    for (int k = 0; k < 6; ++k) big = fmax(big, fabs(r.P[k]));
+    RtCull c;
+    c.eps = 1e-3 + 64.0 * 2.220446049250313e-16 * (4.0 * big * big) * fabs(r.inv);
+    c.on = ntiles > 1 && c.eps < 0.25;
+    return c;
+}
+__device__ __forceinline__ bool rt_tile_hit(const TriRec &r, const int4 bb, RtCull c, int tx, int ty) {
+    if (!c.on) return true;
+    const double(*P)[2] = reinterpret_cast<const double(*)[2]>(r.P);
+    const int x0 = max(tx << LC_RT_SHIFT, bb.x), x1 = min((tx << LC_RT_SHIFT) + LC_RT_TILE - 1, bb.y);
+    const int y0 = max(ty << LC_RT_SHIFT, bb.z), y1 = min((ty << LC_RT_SHIFT) + LC_RT_TILE - 1, bb.w);
+    bool out0 = true, out1 = true, out2 = true;
+    const int cx[4] = {x0, x1, x0, x1}, cy[4] = {y0, y0, y1, y1};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        double l0, l1, l2;
+        bary(P, r.inv, cx[q], cy[q], l0, l1, l2);
+        out0 = out0 && l0 < -c.eps;
+        out1 = out1 && l1 < -c.eps;
+        out2 = out2 && l2 < -c.eps;
+    }
+    return !(out0 || out1 || out2);
+}
+
+// one warp per triangle over the tiles of its bbox: count (fill = 0) or append (fill = 1)
+template <int FILL>
+__global__ void k_rt_bin(const RasterJob *jobs, int T, int ntx) {
     const RasterJob J = jobs[blockIdx.y];
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (t >= T) return;
-    double P[3][2], D[3], inv;
-    int bb[4];
-    if (!tri_setup(cam, J.verts, tris, t, P, D, inv, bb)) return;
-    if (bbox_pixels(bb) > LC_RASTER_SMALL) return;
-    for (int y = bb[2]; y <= bb[3]; ++y)
-        for (int x = bb[0]; x <= bb[1]; ++x) winner_pixel(J, cam, P, D, inv, x, y, t);
+    const TriRec &r = J.rec[t];
+    const int4 bb = *reinterpret_cast<const int4 *>(r.bb);
+    if (bb.x > bb.y) return;
+    const int tx0 = bb.x >> LC_RT_SHIFT, tx1 = bb.y >> LC_RT_SHIFT;
+    const int ty0 = bb.z >> LC_RT_SHIFT, ty1 = bb.w >> LC_RT_SHIFT;
+    const int nx = tx1 - tx0 + 1, nt = nx * (ty1 - ty0 + 1);
+    const RtCull c = rt_cull(r, nt);
+    for (int k = lane; k < nt; k += 32) {
+        const int ty = ty0 + k / nx, tx = tx0 + k % nx;
+        if (!rt_tile_hit(r, bb, c, tx, ty)) continue;
+        const int tile = ty * ntx + tx;
+        if (FILL) {
+            const int off = J.toff[tile] + atomicAdd(&J.tfill[tile], 1);
+            if (off < J.tcap) J.tlist[off] = t;
+        } else {
+            atomicAdd(&J.tcount[tile], 1);
+        }
+    }
+}
+template __global__ void k_rt_bin<0>(const RasterJob *, int, int);
+template __global__ void k_rt_bin<1>(const RasterJob *, int, int);
+
+// block-wide exclusive scan of v(i), i < n, into out[i] (out[n] = total)
+template <typename V>
+__device__ void rt_block_scan(int n, V &&v, int *out, int *zero = nullptr) {
+    __shared__ int wt[32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int base = 0; base < n; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const int x = i < n ? v(i) : 0;
+        int sc = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, sc, o);
+            if (lane >= o) sc += u;
+        }
+        if (lane == 31) wt[w] = sc;
+        __syncthreads();
+        if (w == 0) {
+            int u = lane < (int)(blockDim.x >> 5) ? wt[lane] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int q = __shfl_up_sync(0xffffffffu, u, o);
+                if (lane >= o) u += q;
+            }
+            if (lane < (int)(blockDim.x >> 5)) wt[lane] = u;
+        }
+        __syncthreads();
+        const int before = (w > 0 ? wt[w - 1] : 0) + carry;
+        if (i < n) {
+            out[i] = before + sc - x;
+            if (zero) zero[i] = 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = before + sc;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[n] = carry;
+    __syncthreads();
 }
 
-__global__ void k_raster_depth_big(const RasterJob *jobs, CamDev cam, const int *tris) {
-    const RasterJob J = jobs[blockIdx.y];
-    const int nb = *J.n_big;
-    for (int k = blockIdx.x; k < nb; k += gridDim.x) {
-        const int t = J.big[k];
-        double P[3][2], D[3], inv;
-        int bb[4];
-        tri_setup(cam, J.verts, tris, t, P, D, inv, bb);
-        const int w = bb[1] - bb[0] + 1;
-        const long long n = bbox_pixels(bb);
-        for (long long i = threadIdx.x; i < n; i += blockDim.x)
-            depth_pixel(J, cam, P, D, inv, bb[0] + (int)(i % w), bb[2] + (int)(i / w));
+// Per stream (one CTA): list offsets from the per-tile counts, then work
+// items: a tile's list is resolved in chunks of LC_RT_CHUNK triangles by
+// separate CTAs (merged by k_rt_merge) so a tile that collects thousands of
+// triangles (a collapsed, far-away surface) is still resolved in parallel.
+// A tile whose list overflowed the buffer resolves every triangle in one CTA.
+__global__ void k_rt_scan(const RasterJob *jobs, int n, int T) {
+    const RasterJob J = jobs[blockIdx.x];
+    rt_block_scan(n, [&](int i) { return J.tcount[i]; }, J.toff, J.tfill);
+    rt_block_scan(n, [&](int i) {
+        if (J.toff[i + 1] > J.tcap) return 1;   // overflowed: one CTA over every triangle
+        return max(1, (J.tcount[i] + LC_RT_CHUNK - 1) / LC_RT_CHUNK);
+    }, J.ioff);
+}
+
+__device__ __forceinline__ void rt_pixel(const TriRec &r, int id, int x, int y, unsigned long long &zb, int &tb) {
+    if (x < r.bb[0] || x > r.bb[1] || y < r.bb[2] || y > r.bb[3]) return;
+    const double(*P)[2] = reinterpret_cast<const double(*)[2]>(r.P);
+    double l0, l1, l2;
+    if (!bary(P, r.inv, x, y, l0, l1, l2)) return;
+    const double z = l0 * r.D[0] + l1 * r.D[1] + l2 * r.D[2];
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(z);   // z > 0
+    if (bits < zb || (bits == zb && id < tb)) { zb = bits; tb = id; }
+}
+
+__device__ __forceinline__ void rt_write(const RasterJob &J, CamDev cam, int x, int y, unsigned long long zb, int tb) {
+    if (x < cam.W && y < cam.H) {
+        const size_t pi = (size_t)y * cam.W + x;
+        J.zbuf[pi] = zb;
+        J.tri_id[pi] = tb;
+        if (J.mask) J.mask[pi] = zb != 0x7ff0000000000000ULL;
     }
 }
 
-__global__ void k_raster_winner_big(const RasterJob *jobs, CamDev cam, const int *tris) {
+// work items (tile, chunk), grid-strided; thread = pixel of the tile
+__global__ void __launch_bounds__(256) k_rt_tiles(const RasterJob *jobs, CamDev cam, int T, int ntx, int nt) {
     const RasterJob J = jobs[blockIdx.y];
-    const int nb = *J.n_big;
-    for (int k = blockIdx.x; k < nb; k += gridDim.x) {
-        const int t = J.big[k];
-        double P[3][2], D[3], inv;
-        int bb[4];
-        tri_setup(cam, J.verts, tris, t, P, D, inv, bb);
-        const int w = bb[1] - bb[0] + 1;
-        const long long n = bbox_pixels(bb);
-        for (long long i = threadIdx.x; i < n; i += blockDim.x)
-            winner_pixel(J, cam, P, D, inv, bb[0] + (int)(i % w), bb[2] + (int)(i / w), t);
+    constexpr int CH = 64;
+    __shared__ TriRec sr[CH];
+    __shared__ int sid[CH];
+    const int total = J.ioff[nt];
+    for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        // the tile owning this item: last tile with ioff[tile] <= item
+        int lo = 0, hi = nt - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (J.ioff[mid] <= item) lo = mid;
+            else hi = mid - 1;
+        }
+        const int tile = lo, chunk = item - J.ioff[tile], nchunks = J.ioff[tile + 1] - J.ioff[tile];
+        const int x = (tile % ntx) * LC_RT_TILE + (threadIdx.x & (LC_RT_TILE - 1));
+        const int y = (tile / ntx) * LC_RT_TILE + (threadIdx.x >> LC_RT_SHIFT);
+        const bool all = J.toff[tile + 1] > J.tcap;   // overflowed list: every triangle (bbox-rejected cheaply)
+        const int b0 = all ? 0 : J.toff[tile] + chunk * LC_RT_CHUNK;
+        const int b1 = all ? T : min(J.toff[tile + 1], b0 + LC_RT_CHUNK);
+        unsigned long long zb = 0x7ff0000000000000ULL;
+        int tb = INT_MAX;
+        for (int base = b0; base < b1; base += CH) {
+            const int n = min(CH, b1 - base);
+            __syncthreads();
+            if ((int)threadIdx.x < n) {
+                const int id = all ? base + threadIdx.x : J.tlist[base + threadIdx.x];
+                sid[threadIdx.x] = id;
+                sr[threadIdx.x] = J.rec[id];
+            }
+            __syncthreads();
+            for (int k = 0; k < n; ++k) rt_pixel(sr[k], sid[k], x, y, zb, tb);
+        }
+        if (nchunks == 1) {
+            rt_write(J, cam, x, y, zb, tb);
+        } else {
+            J.pz[(size_t)item * 256 + threadIdx.x] = zb;
+            J.pid[(size_t)item * 256 + threadIdx.x] = tb;
+        }
+    }
+}
+
+// lexicographic (depth, id) minimum over the chunks of multi-chunk tiles
+__global__ void __launch_bounds__(256) k_rt_merge(const RasterJob *jobs, CamDev cam, int ntx, int nt) {
+    const RasterJob J = jobs[blockIdx.y];
+    for (int tile = blockIdx.x; tile < nt; tile += gridDim.x) {
+        const int i0 = J.ioff[tile], i1 = J.ioff[tile + 1];
+        if (i1 - i0 <= 1) continue;
+        unsigned long long zb = 0x7ff0000000000000ULL;
+        int tb = INT_MAX;
+        for (int i = i0; i < i1; ++i) {
+            const unsigned long long z = J.pz[(size_t)i * 256 + threadIdx.x];
+            const int id = J.pid[(size_t)i * 256 + threadIdx.x];
+            if (z < zb || (z == zb && id < tb)) { zb = z; tb = id; }
+        }
+        const int x = (tile % ntx) * LC_RT_TILE + (threadIdx.x & (LC_RT_TILE - 1));
+        const int y = (tile / ntx) * LC_RT_TILE + (threadIdx.x >> LC_RT_SHIFT);
+        rt_write(J, cam, x, y, zb, tb);
     }
 }
 
