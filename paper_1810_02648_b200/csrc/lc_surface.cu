@@ -30,10 +30,12 @@ struct SurfCtx {
     double *red;
 };
 
-__device__ __forceinline__ V3 trial_pos(const double *v, const double *step, int i) {
+// v_i + sc * step_i; sc is a power of two (exact), so this has the bits of
+// the reference's in-place halvings of the step
+__device__ __forceinline__ V3 trial_pos(const double *v, const double *step, int i, double sc = 1.0) {
     const V3 a = ld3(v + 3 * (size_t)i);
     if (!step) return a;
-    return a + ld3(step + 3 * (size_t)i);
+    return a + sc * ld3(step + 3 * (size_t)i);
 }
 
 // photometric row of visible vertex i at position p (nonrigid_stage.py:196-213)
@@ -91,9 +93,9 @@ __device__ __forceinline__ void sil_row(const SurfCtx &c, int b, V3 p, bool with
 struct EdgeQ { V3 u, d; double len_err; bool degenerate; double e_smooth, e_edge; };
 
 __device__ __forceinline__ void edge_q(const SurfCtx &c, int e, const double *v, const double *step,
-                                       EdgeQ &q) {
+                                       EdgeQ &q, double sc = 1.0) {
     const int a = c.A.edges[2 * e], b = c.A.edges[2 * e + 1];
-    const V3 ev = trial_pos(v, step, a) - trial_pos(v, step, b);
+    const V3 ev = trial_pos(v, step, a, sc) - trial_pos(v, step, b, sc);
     const V3 sd = ld3(c.J->vs + 3 * (size_t)a) - ld3(c.J->vs + 3 * (size_t)b);
     q.u = ev - sd;
     const double len = norm3(ev);
@@ -151,6 +153,73 @@ __device__ void surf_energy(const SurfCtx &c, int level, const double *v, const 
     }
     T::template sums<8>(acc, c.red);
     for (int k = 0; k < 6; ++k) en[k] = acc[k];
+}
+
+// energies of nt <= 4 line-search trials v + step * 0.5^h at once (h < nt):
+// each element's trials are evaluated back to back (their gathers and
+// nearest-contour queries overlap), one team reduction for all 24 sums
+constexpr int kSurfTrials = 4;
+template <typename T>
+__device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v, const double *step, int nt,
+                                   double en[kSurfTrials][6]) {
+    const SurfJob &J = *c.J;
+    double acc[kSurfTrials * 6];
+    for (int k = 0; k < kSurfTrials * 6; ++k) acc[k] = 0.0;
+    const double *img = J.pyr + (size_t)level * c.H * c.W * 3;
+    if (J.enable_photo)
+        for (int k = T::tid(); k < c.P; k += T::size) {
+            const int i = J.vis[k];
+            double sc = 1.0;
+#pragma unroll
+            for (int h = 0; h < kSurfTrials; ++h, sc *= 0.5) {
+                if (h >= nt) break;
+                PhotoRow o;
+                photo_row(c, img, i, trial_pos(v, step, i, sc), false, o);
+                acc[6 * h] += o.r[0] * o.r[0] + o.r[1] * o.r[1] + o.r[2] * o.r[2];
+            }
+        }
+    if (c.sil_on)
+        for (int b = T::tid(); b < c.B; b += T::size) {
+            double sc = 1.0;
+#pragma unroll
+            for (int h = 0; h < kSurfTrials; ++h, sc *= 0.5) {
+                if (h >= nt) break;
+                SilRow o;
+                sil_row(c, b, trial_pos(v, step, J.bidx[b], sc), false, o);
+                acc[6 * h + 1] += o.r * o.r;
+            }
+        }
+    for (int e = T::tid(); e < c.E; e += T::size) {
+        double sc = 1.0;
+#pragma unroll
+        for (int h = 0; h < kSurfTrials; ++h, sc *= 0.5) {
+            if (h >= nt) break;
+            EdgeQ q;
+            edge_q(c, e, v, step, q, sc);
+            acc[6 * h + 2] += q.e_smooth;
+            acc[6 * h + 3] += q.e_edge;
+        }
+    }
+    if (c.has_prev) {
+        const double cv = sqrt(c.hp.w_vel), ca = sqrt(c.hp.w_acc);
+        for (int i = T::tid(); i < c.N; i += T::size) {
+            const V3 q1 = ld3(J.prev + 3 * (size_t)i);
+            const V3 q2 = J.prev2 ? ld3(J.prev2 + 3 * (size_t)i) : q1;
+            double sc = 1.0;
+#pragma unroll
+            for (int h = 0; h < kSurfTrials; ++h, sc *= 0.5) {
+                if (h >= nt) break;
+                const V3 p = trial_pos(v, step, i, sc);
+                const V3 vr = (p - q1) * cv;
+                const V3 ar = ((p - 2.0 * q1) + q2) * ca;
+                acc[6 * h + 4] += vr.x * vr.x + vr.y * vr.y + vr.z * vr.z;
+                acc[6 * h + 5] += ar.x * ar.x + ar.y * ar.y + ar.z * ar.z;
+            }
+        }
+    }
+    T::template sums<kSurfTrials * 6>(acc, c.red);
+    for (int h = 0; h < kSurfTrials; ++h)
+        for (int k = 0; k < 6; ++k) en[h][k] = acc[6 * h + k];
 }
 
 __device__ __forceinline__ double total_energy(const double en[6], bool has_prev) {
@@ -552,22 +621,38 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve_t(const SurfJob *jobs, 
             const bool breakdown = surf_pcg<T>(c, hp.pcg);
             stamp<T>(J, ph);
             const double e0 = total_energy(en, c.has_prev);
+            // halving line search (nonrigid_stage.py:386-399): the first
+            // trial v + best * 0.5^h (h <= max_halvings) with e1 <= e0 is
+            // taken, else the step is rejected.  Trials are evaluated up to
+            // four at a time (exact halvings: the sequential search's bits).
             int halv = 0;
             bool rejected = false;
-            double e1;
-            for (;;) {
-                double et[6];
-                surf_energy<T>(c, level, v, J.best, et);
-                e1 = total_energy(et, c.has_prev);
-                if (e1 <= e0) {
-                    for (int i = T::tid(); i < c.N * 3; i += T::size) v[i] = v[i] + J.best[i];
+            double e1 = e0;
+            double base_sc = 1.0;
+            // (the full step is accepted about two times in three, so it is
+            // tried alone first; the remaining halvings are batched)
+            for (int base = 0, nt = 1;; base += nt, nt = kSurfTrials) {
+                nt = min(nt, hp.max_halvings + 1 - base);
+                double et[kSurfTrials][6];
+                surf_energy_trials<T>(c, level, v, J.best, nt, et);
+                int hit = -1;
+                double sc = base_sc, hit_sc = 0.0;
+                for (int h = 0; h < nt; ++h, sc *= 0.5) {
+                    const double eh = total_energy(et[h], c.has_prev);
+                    if (eh <= e0) { hit = h; e1 = eh; hit_sc = sc; break; }
+                }
+                if (hit >= 0) {
+                    for (int i = T::tid(); i < c.N * 3; i += T::size) v[i] = v[i] + hit_sc * J.best[i];
                     T::sync();
+                    halv = base + hit;
                     break;
                 }
-                if (halv >= hp.max_halvings) { rejected = true; e1 = e0; break; }
-                for (int i = T::tid(); i < c.N * 3; i += T::size) J.best[i] = 0.5 * J.best[i];
+                if (base + nt > hp.max_halvings) { halv = hp.max_halvings; rejected = true; e1 = e0; break; }
+                for (int h = 0; h < nt; ++h) base_sc *= 0.5;
+                // later batches scale the step in place (keeps trial_pos's sc <= 1 exact)
+                for (int i = T::tid(); i < c.N * 3; i += T::size) J.best[i] = base_sc * J.best[i];
                 T::sync();
-                ++halv;
+                base_sc = 1.0;
             }
             stamp<T>(J, ph);
             if (T::tid() == 0 && J.counters) {
