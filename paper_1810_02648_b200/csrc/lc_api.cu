@@ -514,6 +514,24 @@ extern "C" int lc_actor_upload(lc_ctx *c, const lc_actor_desc *d, lc_actor **out
     A.adj_edge = a->mem.upload(adj_edge.data(), adj_edge.size(), st);
     A.adj_nbr = a->mem.upload(adj_nbr.data(), adj_nbr.size(), st);
     A.degrees = a->mem.upload(deg.data(), deg.size(), st);
+    {
+        std::vector<int> ell_nbr((size_t)LC_ELL * N, 0), ell_edge((size_t)LC_ELL * N, -1), ell_cnt(N),
+            epos(2 * (size_t)E, -1);
+        for (int i = 0; i < N; ++i) {
+            const int cnt = adj_ptr[i + 1] - adj_ptr[i];
+            ell_cnt[i] = cnt;
+            for (int k = 0; k < std::min(cnt, LC_ELL); ++k) {
+                const int idx = adj_ptr[i] + k, e = adj_edge[idx], pos = k * N + i;
+                ell_nbr[pos] = adj_nbr[idx];
+                ell_edge[pos] = e;
+                epos[2 * (size_t)e + (edges[2 * e] == i ? 0 : 1)] = pos;
+            }
+        }
+        A.ell_nbr = a->mem.upload(ell_nbr.data(), ell_nbr.size(), st);
+        A.ell_cnt = a->mem.upload(ell_cnt.data(), ell_cnt.size(), st);
+        A.epos = a->mem.upload(epos.data(), epos.size(), st);
+        a->host_ell_edge = ell_edge;
+    }
     A.w_dir = a->mem.upload(d->directed_weights, 2 * (size_t)E, st);
     A.skin_idx = a->mem.upload(sidx.data(), sidx.size(), st);
     A.skin_w = a->mem.upload(d->skin_weights, 4 * (size_t)N, st);
@@ -636,6 +654,8 @@ void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) 
     sbest = mem.alloc<double>(3 * (size_t)N);
     edir = mem.alloc<double>(3 * (size_t)E);
     eg = mem.alloc<double>(3 * (size_t)E);
+    ell_d = mem.alloc<double>(3 * (size_t)LC_ELL * N);
+    ell_g = mem.alloc<double>(3 * (size_t)LC_ELL * N);
     off0 = mem.alloc<double>(3 * (size_t)N);
     off1 = mem.alloc<double>(3 * (size_t)N);
     hold = mem.alloc<uint8_t>(N);
@@ -902,6 +922,14 @@ static void build_config(lc_ctx *c, const lc_actor *a, const lc_nonrigid_hyper *
         cf.ec.ce_r = cf.mem.upload(cer.data(), E, st);
         cf.ec.alpha = cf.mem.upload(al.data(), E, st);
         cf.ec.beta = cf.mem.upload(be.data(), E, st);
+        const int N = a->dev.N;
+        std::vector<double> ea((size_t)LC_ELL * N, 0.0), eb((size_t)LC_ELL * N, 0.0);
+        for (size_t q = 0; q < ea.size(); ++q) {
+            const int e = a->host_ell_edge[q];
+            if (e >= 0) { ea[q] = al[e]; eb[q] = be[e]; }
+        }
+        cf.ec.ell_a = cf.mem.upload(ea.data(), ea.size(), st);
+        cf.ec.ell_b = cf.mem.upload(eb.data(), eb.size(), st);
         fill_surf_hyper(cf.shp, *nh);
         std::vector<double> taps(4 * 32, 0.0);
         for (int l = 0; l < nh->n_levels && l < 4; ++l) {
@@ -1290,6 +1318,7 @@ static void run_frame(FrameBatch &fb) {
             j.directional = cfg.directional; j.enable_photo = 1; j.enable_sil = 1;
             j.diag = s->diag; j.minv = s->minv; j.rhs = s->rhs; j.x = s->sx; j.r = s->sr; j.z = s->sz;
             j.p = s->sp; j.ap = s->sap; j.best = s->sbest; j.edir = s->edir; j.eg = s->eg;
+            j.ell_d = s->ell_d; j.ell_g = s->ell_g;
             j.off0 = s->off0; j.off1 = s->off1; j.hold = s->hold;
             j.report = s->nr_rep;
             j.nn_hint = s->nn_hint;
@@ -1743,6 +1772,7 @@ extern "C" int lc_nonrigid_solve(lc_ctx *c, const lc_actor *a, const lc_camera *
     j.directional = pb->directional; j.enable_photo = pb->enable_photo; j.enable_sil = pb->enable_sil;
     j.diag = s->diag; j.minv = s->minv; j.rhs = s->rhs; j.x = s->sx; j.r = s->sr; j.z = s->sz;
     j.p = s->sp; j.ap = s->sap; j.best = s->sbest; j.edir = s->edir; j.eg = s->eg;
+    j.ell_d = s->ell_d; j.ell_g = s->ell_g;
     j.off0 = s->off0; j.off1 = s->off1; j.hold = s->hold;
     j.report = s->nr_rep;
     j.nn_hint = s->nn_hint;

@@ -12,6 +12,7 @@
 #define LC_NDOF 27
 #define LC_NROT 30       // 3 root Euler + 27 joint angles
 #define LC_NP 36
+#define LC_ELL 8  // ELL adjacency slots per vertex
 #define LC_GRID_CELL 16  // NN grid cell edge in pixels
 #define LC_GRID_SHIFT 4
 #define LC_NCOUNTERS 8
@@ -48,6 +49,12 @@ struct ActorDev {
     const int *adj_edge;       //       reference's directed order (as src: forward
     const int *adj_nbr;        //       edges asc., then reversed edges asc.)
     const int *degrees;        // N
+    // ELL copy of the first LC_ELL incident edges of each vertex (slot k of
+    // vertex i at k*N + i, the CSR order above): coalesced and independent
+    // loads in the assembly / matvec; degrees beyond LC_ELL use the CSR tail
+    const int *ell_nbr;        // LC_ELL*N neighbour vertex
+    const int *ell_cnt;        // N incident edge count (= CSR degree)
+    const int *epos;           // 2E ELL position of edge e at its src (2e) / dst (2e+1), -1 = CSR tail
     const double *w_dir;       // 2E directed material weights
     const int *skin_idx;       // N*4 (-1 padding)
     const double *skin_w;      // N*4
@@ -99,6 +106,7 @@ struct EdgeConstDev {
     const double *ce_f, *ce_r;  // E : sqrt(w_edge s / deg(src))
     const double *alpha;        // E : cs_f^2 + cs_r^2
     const double *beta;         // E : ce_f^2 + ce_r^2
+    const double *ell_a, *ell_b; // LC_ELL*N alpha / beta gathered into the ELL slots
 };
 
 struct PoseHyperDev {

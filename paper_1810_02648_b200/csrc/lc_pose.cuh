@@ -49,6 +49,7 @@ struct SurfJob {
     double *diag, *minv;      // N*6 (sym: xx xy xz yy yz zz)
     double *rhs, *x, *r, *z, *p, *ap, *best;   // N*3
     double *edir, *eg;        // E*3
+    double *ell_d, *ell_g;    // 3*LC_ELL*N edge direction / signed gradient per ELL slot (SoA)
     double *off0, *off1;      // N*3 snap offsets
     uint8_t *hold;            // N
     lc_nonrigid_report *report;

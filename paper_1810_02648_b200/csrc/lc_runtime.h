@@ -62,6 +62,7 @@ struct lc_actor {
     std::vector<int> host_edges;      // E*2
     std::vector<int> host_degrees;    // N
     std::vector<double> host_wdir;    // 2E
+    std::vector<int> host_ell_edge;   // LC_ELL*N edge id per ELL slot (-1 = empty)
 };
 
 // NN grid buffers for one mask
@@ -139,6 +140,7 @@ struct Slot {
     int *nn_hint;
     // surface scratch
     double *diag, *minv, *rhs, *sx, *sr, *sz, *sp, *sap, *sbest, *edir, *eg, *off0, *off1;
+    double *ell_d, *ell_g;   // 3*LC_ELL*N current edge directions / signed gradients in ELL slots (SoA)
     uint8_t *hold;
     // reports (device)
     lc_pose_report *pose_rep;

@@ -253,7 +253,19 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
         degen += q.degenerate ? 2.0 : 0.0;
         st3(J.edir + 3 * (size_t)e, q.d);
         const double al = c.ec.alpha[e], be = c.ec.beta[e];
-        st3(J.eg + 3 * (size_t)e, al * q.u + be * (q.len_err * q.d));
+        const V3 g = al * q.u + be * (q.len_err * q.d);
+        st3(J.eg + 3 * (size_t)e, g);
+        // the edge's ELL slots at its two endpoints (the src side subtracts g)
+        const size_t LN = (size_t)LC_ELL * c.N;
+        const int ps = c.A.epos[2 * e], pd = c.A.epos[2 * e + 1];
+        if (ps >= 0) {
+            J.ell_d[ps] = q.d.x; J.ell_d[LN + ps] = q.d.y; J.ell_d[2 * LN + ps] = q.d.z;
+            J.ell_g[ps] = -g.x; J.ell_g[LN + ps] = -g.y; J.ell_g[2 * LN + ps] = -g.z;
+        }
+        if (pd >= 0) {
+            J.ell_d[pd] = q.d.x; J.ell_d[LN + pd] = q.d.y; J.ell_d[2 * LN + pd] = q.d.z;
+            J.ell_g[pd] = g.x; J.ell_g[LN + pd] = g.y; J.ell_g[2 * LN + pd] = g.z;
+        }
     }
     T::sync();
     fst(0);
@@ -300,15 +312,30 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
         double dg[6];
         for (int k = 0; k < 6; ++k) dg[k] = J.diag[6 * (size_t)i + k];
         V3 rh = ld3(J.rhs + 3 * (size_t)i);
-        for (int k = c.A.adj_ptr[i]; k < c.A.adj_ptr[i + 1]; ++k) {
-            const int e = c.A.adj_edge[k];
-            const V3 d = ld3(J.edir + 3 * (size_t)e);
-            const double al = c.ec.alpha[e], be = c.ec.beta[e];
+        // incident edges in the reference's order: ELL slots (coalesced,
+        // independent loads), then the CSR tail of high-degree vertices
+        const int cnt = c.A.ell_cnt[i];
+        const size_t LN = (size_t)LC_ELL * c.N;
+#pragma unroll
+        for (int k = 0; k < LC_ELL; ++k) {
+            if (k >= cnt) continue;
+            const size_t pos = (size_t)k * c.N + i;
+            const V3 d = v3(J.ell_d[pos], J.ell_d[LN + pos], J.ell_d[2 * LN + pos]);
+            const double al = c.ec.ell_a[pos], be = c.ec.ell_b[pos];
             dg[0] += al + be * (d.x * d.x); dg[1] += be * (d.x * d.y); dg[2] += be * (d.x * d.z);
             dg[3] += al + be * (d.y * d.y); dg[4] += be * (d.y * d.z); dg[5] += al + be * (d.z * d.z);
-            const V3 g = ld3(J.eg + 3 * (size_t)e);
-            rh = (c.A.edges[2 * e] == i) ? rh - g : rh + g;
+            rh = rh + v3(J.ell_g[pos], J.ell_g[LN + pos], J.ell_g[2 * LN + pos]);
         }
+        if (cnt > LC_ELL)
+            for (int k = c.A.adj_ptr[i] + LC_ELL; k < c.A.adj_ptr[i + 1]; ++k) {
+                const int e = c.A.adj_edge[k];
+                const V3 d = ld3(J.edir + 3 * (size_t)e);
+                const double al = c.ec.alpha[e], be = c.ec.beta[e];
+                dg[0] += al + be * (d.x * d.x); dg[1] += be * (d.x * d.y); dg[2] += be * (d.x * d.z);
+                dg[3] += al + be * (d.y * d.y); dg[4] += be * (d.y * d.z); dg[5] += al + be * (d.z * d.z);
+                const V3 g = ld3(J.eg + 3 * (size_t)e);
+                rh = (c.A.edges[2 * e] == i) ? rh - g : rh + g;
+            }
         if (c.has_prev) {
             const double cc = cv * cv + ca * ca;
             dg[0] += cc; dg[3] += cc; dg[5] += cc;
@@ -341,8 +368,12 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
 
 // block-Jacobi PCG from zero, best-residual iterate (solvers.py:104-145)
 template <typename T>
-__device__ bool surf_pcg(const SurfCtx &c, int iters) {
+__device__ bool surf_pcg(const SurfCtx &c, int iters, int fine = -1) {
     const SurfJob &J = *c.J;
+    auto fst = [&](int k) {
+        if (fine >= 0 && J.phase && T::tid() == 0) J.phase[fine + k] = gtimer();
+    };
+    fst(0);
     double part[2] = {0, 0};
     for (int i = T::tid(); i < c.N; i += T::size) {
         const V3 r = ld3(J.rhs + 3 * (size_t)i);
@@ -356,6 +387,7 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters) {
         part[1] += r.x * r.x + r.y * r.y + r.z * r.z;
     }
     T::template sums<2>(part, c.red);
+    fst(1);
     double rz = part[0];
     double best_norm = sqrt(part[1]);
     bool breakdown = false;
@@ -364,17 +396,33 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters) {
         for (int i = T::tid(); i < c.N; i += T::size) {
             const V3 pi = ld3(J.p + 3 * (size_t)i);
             V3 y = sym3_mul(J.diag + 6 * (size_t)i, pi);
-            for (int k = c.A.adj_ptr[i]; k < c.A.adj_ptr[i + 1]; ++k) {
-                const int e = c.A.adj_edge[k];
-                const V3 pj = ld3(J.p + 3 * (size_t)c.A.adj_nbr[k]);
-                const V3 d = ld3(J.edir + 3 * (size_t)e);
-                y = y - (c.ec.alpha[e] * pj + (c.ec.beta[e] * dot3(d, pj)) * d);
+            // matrix-free off-diagonal blocks -(a I + b d d^T) p_j: ELL slots
+            // (one round of independent coalesced loads + the p_j gathers),
+            // then the CSR tail of high-degree vertices
+            const int cnt = c.A.ell_cnt[i];
+            const size_t LN = (size_t)LC_ELL * c.N;
+#pragma unroll
+            for (int k = 0; k < LC_ELL; ++k) {
+                if (k >= cnt) continue;
+                const size_t pos = (size_t)k * c.N + i;
+                const V3 pj = ld3(J.p + 3 * (size_t)c.A.ell_nbr[pos]);
+                const V3 d = v3(J.ell_d[pos], J.ell_d[LN + pos], J.ell_d[2 * LN + pos]);
+                y = y - (c.ec.ell_a[pos] * pj + (c.ec.ell_b[pos] * dot3(d, pj)) * d);
             }
+            if (cnt > LC_ELL)
+                for (int k = c.A.adj_ptr[i] + LC_ELL; k < c.A.adj_ptr[i + 1]; ++k) {
+                    const int e = c.A.adj_edge[k];
+                    const V3 pj = ld3(J.p + 3 * (size_t)c.A.adj_nbr[k]);
+                    const V3 d = ld3(J.edir + 3 * (size_t)e);
+                    y = y - (c.ec.alpha[e] * pj + (c.ec.beta[e] * dot3(d, pj)) * d);
+                }
             st3(J.ap + 3 * (size_t)i, y);
             s1[0] += pi.x * y.x + pi.y * y.y + pi.z * y.z;
             s1[1] += pi.x * pi.x + pi.y * pi.y + pi.z * pi.z;
         }
+        if (it == 0) fst(2);
         T::template sums<2>(s1, c.red);
+        if (it == 0) fst(3);
         const double pap = s1[0];
         if (pap <= 1e-14 * fmax(s1[1], 1e-300)) { breakdown = true; break; }
         const double alpha = rz / pap;
@@ -389,7 +437,9 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters) {
             s2[0] += r.x * z.x + r.y * z.y + r.z * z.z;
             s2[1] += r.x * r.x + r.y * r.y + r.z * r.z;
         }
+        if (it == 0) fst(4);
         T::template sums<2>(s2, c.red);
+        if (it == 0) fst(5);
         const double nrm = sqrt(s2[1]);
         const bool better = nrm < best_norm;
         if (better) best_norm = nrm;
@@ -401,6 +451,7 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters) {
                 st3(J.p + 3 * (size_t)i, ld3(J.z + 3 * (size_t)i) + beta * ld3(J.p + 3 * (size_t)i));
         }
         T::sync();
+        if (it == 0) fst(6);
         if (stop) { breakdown = true; break; }
         rz = s2[0];
     }
@@ -538,8 +589,15 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
         for (int i = T::tid(); i < c.N; i += T::size) {
             if (J.hold[i]) { st3(dst + 3 * (size_t)i, ld3(src + 3 * (size_t)i)); continue; }
             V3 a = v3(0, 0, 0);
-            for (int k = c.A.adj_ptr[i]; k < c.A.adj_ptr[i + 1]; ++k)
-                a = a + ld3(src + 3 * (size_t)c.A.adj_nbr[k]);
+            const int cnt = c.A.ell_cnt[i];
+#pragma unroll
+            for (int k = 0; k < LC_ELL; ++k) {
+                if (k >= cnt) continue;
+                a = a + ld3(src + 3 * (size_t)c.A.ell_nbr[(size_t)k * c.N + i]);
+            }
+            if (cnt > LC_ELL)
+                for (int k = c.A.adj_ptr[i] + LC_ELL; k < c.A.adj_ptr[i + 1]; ++k)
+                    a = a + ld3(src + 3 * (size_t)c.A.adj_nbr[k]);
             const double dg = (double)c.A.degrees[i];
             st3(dst + 3 * (size_t)i, v3(a.x / dg, a.y / dg, a.z / dg));
         }
@@ -618,7 +676,7 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve_t(const SurfJob *jobs, 
             surf_assemble<T>(c, level, v, en, counts, it == 1 ? 16 : -1);
             stamp<T>(J, ph);
             for (int k = 0; k < 3; ++k) tot[k] += counts[k];
-            const bool breakdown = surf_pcg<T>(c, hp.pcg);
+            const bool breakdown = surf_pcg<T>(c, hp.pcg, it == 1 ? 40 : -1);
             stamp<T>(J, ph);
             const double e0 = total_energy(en, c.has_prev);
             // halving line search (nonrigid_stage.py:386-399): the first

@@ -79,7 +79,8 @@ def main():
             pp, ss = np.zeros(64, dtype=np.int64), np.zeros(64, dtype=np.int64)
             _lib.check(ctx.lib.lc_tracker_phase_times(tr.handle, 0, _lib.ptr(pp), _lib.ptr(ss)))
             for name, arr, a0, n in (("pose evalJ", pp, 32, 6), ("pose trial", pp, 40, 6),
-                                     ("surf asm", ss, 16, 5), ("surf snap", ss, 24, 5)):
+                                     ("surf asm", ss, 16, 5), ("surf snap", ss, 24, 5),
+                                     ("surf pcg init|mv|red1|upd|red2|p", ss, 40, 7)):
                 d = np.diff(arr[a0:a0 + n]) / 1e3
                 print(f"   stream0 {name} (us): " + " ".join(f"{x:.1f}" for x in d))
 
