@@ -194,6 +194,13 @@ int lc_pcg_solve_bsr(lc_ctx *ctx, int32_t n, int64_t m, const double *diag, cons
                      const int64_t *rows, const int64_t *cols, const double *rhs,
                      int32_t iterations, double *x_out, lc_pcg_info *info);
 /* solvers.py:41-56 dense_solve(DenseNormalSystem) */
+/* smooth_trajectory (pipeline.py:308-325): centred weighted average of an
+ * (F, D) stack along F, truncated and renormalised at the ends; bit-identical */
+int lc_smooth_trajectory(lc_ctx *ctx, int32_t F, int64_t D, const double *values, int32_t K,
+                         const double *stencil, double *out);
+/* metrics.iou support: per-frame |a & b| and |a | b| of two (F, HW) mask stacks */
+int lc_mask_overlap(lc_ctx *ctx, int32_t F, int64_t HW, const uint8_t *a, const uint8_t *b,
+                    uint64_t *inter_out, uint64_t *union_out);
 int lc_dense_solve(lc_ctx *ctx, int32_t n, const double *a, const double *b, double *x_out,
                    lc_dense_info *info);
 /* imageproc.py:264-285 gaussian_pyramid; image H*W*C, out n_levels*H*W*C */
@@ -250,6 +257,10 @@ int lc_tracker_destroy(lc_tracker *tr);
  * (the reference's pipelined driver, pipeline.py:432-499). */
 int lc_tracker_set_frame(lc_tracker *tr, int32_t stream, const double *image,
                          const uint8_t *mask, const lc_detections *det, int32_t on_device);
+/* the same with a uint8 RGB image (real-data ingest, imageproc.py:297-299):
+ * 1 byte per channel is uploaded and converted on the device as / 255.0 */
+int lc_tracker_set_frame_u8(lc_tracker *tr, int32_t stream, const uint8_t *image_rgb,
+                            const uint8_t *mask, const lc_detections *det, int32_t on_device);
 /* condition + solve_frame for the oldest queued frame of every stream
  * (asynchronous); launches the preprocessing of the next queued frames */
 int lc_tracker_step(lc_tracker *tr);

@@ -121,6 +121,8 @@ _SIGS = {
     "lc_actor_destroy": (C.c_int, [P]),
     "lc_pcg_solve_bsr": (C.c_int, [P, i32, i64, P, P, P, P, P, i32, P, P]),
     "lc_dense_solve": (C.c_int, [P, i32, P, P, P, P]),
+    "lc_smooth_trajectory": (C.c_int, [P, i32, C.c_int64, P, i32, P, P]),
+    "lc_mask_overlap": (C.c_int, [P, i32, C.c_int64, P, P, P, P]),
     "lc_gaussian_pyramid": (C.c_int, [P, i32, i32, i32, P, i32, P, P, P]),
     "lc_render": (C.c_int, [P, P, i32, P, i32, P, i32, P, i32, P, f64, i64, P, P, P]),
     "lc_field_create": (C.c_int, [P, i32, i32, P, P]),
@@ -136,6 +138,7 @@ _SIGS = {
     "lc_tracker_destroy": (C.c_int, [P]),
     "lc_tracker_set_frame": (C.c_int, [P, i32, P, P, P, i32]),
     "lc_tracker_get_result_async": (C.c_int, [P, i32, P, P]),
+    "lc_tracker_set_frame_u8": (C.c_int, [P, i32, P, P, P, i32]),
     "lc_trace_dump": (C.c_int, [P, C.c_char_p, C.c_int64]),
     "lc_tracker_step": (C.c_int, [P]),
     "lc_tracker_get_result": (C.c_int, [P, i32, P, P, P, P]),

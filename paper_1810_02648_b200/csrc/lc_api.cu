@@ -689,6 +689,7 @@ void Slot::allocate_queue() {
         b.v3d = mem.alloc<uint8_t>(LC_MAXJ);
         b.tmp = blur_tmp;
     }
+    for (FrameIn &f : in) f.image_u8 = mem.alloc<uint8_t>(HW * 3);
     for (FrameIn &f : in) {
         cudaEventCreateWithFlags(&f.ready_obs, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&f.ready, cudaEventDisableTiming);
@@ -1436,6 +1437,54 @@ extern "C" int lc_tracker_set_frame(lc_tracker *t, int32_t stream, const double 
     API_END
 }
 
+// colour bytes -> [0, 1] doubles with the reference's exact `/ 255.0`
+// (imageproc.py:297-299: np.asarray(img, float64) / 255.0)
+__global__ void k_u8_to_unit(const uint8_t *src, double *dst, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = (double)src[i] / 255.0;
+}
+
+// uint8 RGB variant of lc_tracker_set_frame (real-data ingest): 1 byte per
+// channel crosses PCIe, converted on the device on the copy stream
+extern "C" int lc_tracker_set_frame_u8(lc_tracker *t, int32_t stream, const uint8_t *image_rgb,
+                                       const uint8_t *mask, const lc_detections *det, int32_t on_device) {
+    API_BEGIN
+    require(t && det && image_rgb && mask, "null argument");
+    require(stream >= 0 && stream < t->S, "stream index out of range");
+    Slot *s = t->slots[stream];
+    lc_ctx *c = t->ctx;
+    FrameIn &f = s->in[s->in_tail];
+    require(f.state == 0, "the stream's frame queue is full: call lc_tracker_step first");
+    const size_t HW = (size_t)s->H * s->W;
+    if (f.used) CK(cudaStreamWaitEvent(c->copy, f.freed, 0));
+    const uint8_t *src = image_rgb;
+    if (!on_device) {
+        CK(cudaMemcpyAsync(f.image_u8, image_rgb, HW * 3, cudaMemcpyHostToDevice, c->copy));
+        CK(cudaMemcpyAsync(f.mask, mask, HW, cudaMemcpyHostToDevice, c->copy));
+        src = f.image_u8;
+        f.mask_src = f.mask;
+    } else {
+        f.mask_src = mask;
+    }
+    {
+        OnStream on(c, c->copy);
+        launch(c, k_u8_to_unit, dim3((unsigned)std::min<size_t>((3 * HW + 255) / 256, 2368)), dim3(256), 0, src,
+               f.image, (long long)(3 * HW));
+    }
+    CK(cudaEventRecord(f.uploaded, c->copy));
+    f.pending_upload = true;
+    f.image_src = f.image;
+    const int J = t->actor->skel.J;
+    stage_to(c, f.j2d, det->joints2d, sizeof(double) * 2 * (J + 4));
+    stage_to(c, f.j3d_raw, det->joints3d, sizeof(double) * 3 * J);
+    stage_to(c, f.v2d, det->valid2d, J + 4);
+    stage_to(c, f.v3d, det->valid3d, J);
+    f.state = 1;
+    s->in_tail = (s->in_tail + 1) % LC_QUEUE;
+    return LC_OK;
+    API_END
+}
+
 extern "C" int lc_tracker_step(lc_tracker *t) {
     API_BEGIN
     require(t != nullptr, "null tracker");
@@ -2136,6 +2185,53 @@ extern "C" int lc_pcg_solve_bsr(lc_ctx *c, int32_t n, int64_t m_, const double *
         info->breakdown = hinfo[1];
         for (int k = 0; k <= hinfo[0] && k < LC_MAX_LOG; ++k) info->residual_norms[k] = norms[k];
     }
+    return last_launch_status();
+    API_END
+}
+
+__global__ void k_smooth_trajectory(const double *v, int F, long long D, const double *w, int K, double *out);
+__global__ void k_mask_overlap(const uint8_t *a, const uint8_t *b, long long HW, unsigned long long *inter,
+                               unsigned long long *uni);
+
+// smooth_trajectory (pipeline.py:308-325) of an (F, D) stack, bit-identical
+extern "C" int lc_smooth_trajectory(lc_ctx *c, int32_t F, int64_t D, const double *values, int32_t K,
+                                    const double *stencil, double *out) {
+    API_BEGIN
+    require(c && values && stencil && out, "null argument");
+    require(K >= 1 && K % 2 == 1, "stencil length must be odd");
+    require(F >= 1 && D >= 1, "empty trajectory");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DevArena m;
+    const size_t n = (size_t)F * D;
+    double *dv = m.upload(values, n, st), *dw = m.upload(stencil, K, st), *dout = m.alloc<double>(n);
+    launch(c, k_smooth_trajectory, dim3((unsigned)std::min<size_t>((n + 255) / 256, 4096)), dim3(256), 0,
+           (const double *)dv, (int)F, (long long)D, (const double *)dw, (int)K, dout);
+    CK(cudaMemcpyAsync(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return last_launch_status();
+    API_END
+}
+
+// per-frame intersection / union pixel counts of two (F, H, W) mask stacks (metrics.iou)
+extern "C" int lc_mask_overlap(lc_ctx *c, int32_t F, int64_t HW, const uint8_t *a, const uint8_t *b,
+                               uint64_t *inter_out, uint64_t *union_out) {
+    API_BEGIN
+    require(c && a && b && inter_out && union_out, "null argument");
+    require(F >= 1 && HW >= 1, "empty masks");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DevArena m;
+    const size_t n = (size_t)F * HW;
+    uint8_t *da = m.upload(a, n, st), *db = m.upload(b, n, st);
+    unsigned long long *di = m.alloc<unsigned long long>(F), *du = m.alloc<unsigned long long>(F);
+    CK(cudaMemsetAsync(di, 0, sizeof(unsigned long long) * F, st));
+    CK(cudaMemsetAsync(du, 0, sizeof(unsigned long long) * F, st));
+    launch(c, k_mask_overlap, dim3(64, (unsigned)F), dim3(256), 0, (const uint8_t *)da, (const uint8_t *)db,
+           (long long)HW, di, du);
+    CK(cudaMemcpyAsync(inter_out, di, sizeof(uint64_t) * F, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(union_out, du, sizeof(uint64_t) * F, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     return last_launch_status();
     API_END
 }

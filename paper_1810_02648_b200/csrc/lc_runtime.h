@@ -88,6 +88,7 @@ struct GridBufs {
 // upload of frame f+2 overlap frame f+1's preprocessing and frame f's solve.
 struct FrameIn {
     double *image = nullptr;           // own copy (host inputs)
+    uint8_t *image_u8 = nullptr;       // raw RGB bytes of the uint8 upload path
     uint8_t *mask = nullptr;
     const double *image_src = nullptr;  // own copy or the caller's device pointer
     const uint8_t *mask_src = nullptr;

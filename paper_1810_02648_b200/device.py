@@ -258,17 +258,19 @@ class Tracker:
         if j2d.shape != (self.J + 4, 2) or j3d.shape != (self.J, 3):
             raise ValueError("detections do not match the skeleton")
         d = L.Detections(L.ptr(j2d), L.ptr(j3d), L.ptr(v2d), L.ptr(v3d))
+        u8 = False
         if on_device:
             img_p, mask_p = int(image), int(mask)
         else:
             H, W = self.camera.height, self.camera.width
-            image = L.f64c(image)
+            u8 = isinstance(image, np.ndarray) and image.dtype == np.uint8
+            image = np.ascontiguousarray(image) if u8 else L.f64c(image)
             mask = L.u8c(mask)
             if image.shape != (H, W, 3) or mask.shape != (H, W):
                 raise ValueError("image / mask shape does not match the camera")
             img_p, mask_p = L.ptr(image), L.ptr(mask)
-        L.check(self.ctx.lib.lc_tracker_set_frame(self.handle, stream, img_p, mask_p, C.byref(d),
-                                                  int(on_device)))
+        fn = self.ctx.lib.lc_tracker_set_frame_u8 if u8 else self.ctx.lib.lc_tracker_set_frame
+        L.check(fn(self.handle, stream, img_p, mask_p, C.byref(d), int(on_device)))
 
     def step(self):
         L.check(self.ctx.lib.lc_tracker_step(self.handle))

@@ -14,7 +14,7 @@ over many independent streams use `device.Tracker` directly (batched).
 from __future__ import annotations
 
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 
@@ -94,12 +94,16 @@ def solve_frame(cond, actor, camera, config, state):
 
 @dataclass
 class SequenceResult:
+    """Reference `pipeline.py:328-343`."""
     config: SequenceConfig
-    frames: list
-    poses: np.ndarray
-    vertices: np.ndarray
+    frames: list                      # FrameResult
+    poses: np.ndarray                 # (F,36) raw
+    vertices: np.ndarray              # (F,N,3) raw
+    poses_smoothed: np.ndarray
+    vertices_smoothed: np.ndarray
+    events: list                      # slot-ordered ingest/emit records
     timings: dict
-    pipelined: bool = False
+    pipelined: bool
 
     @property
     def fps(self) -> float:
@@ -107,38 +111,92 @@ class SequenceResult:
         return len(self.frames) / total if total > 0 else float("inf")
 
 
-def run_sequence(inputs, config=None, pipelined=False) -> SequenceResult:
-    """Sequence drivers (pipeline.py:378-515); the track state stays on the device.
+def _prepare_actor(actor, config: SequenceConfig):
+    """Reference `pipeline.py:346-354`: uniform material weight override."""
+    from .actor import Actor
+    actor = Actor.from_reference(actor)
+    if config.uniform_material_weight is None:
+        return actor
+    mesh = replace(actor.mesh)
+    s = float(config.uniform_material_weight)
+    mesh.edge_weights = np.full(len(mesh.edges), s)
+    mesh.directed_weights = np.full(2 * len(mesh.edges), s)
+    return type(actor)(mesh, actor.skeleton, actor.skinning)
 
-    pipelined=False is run_sequence_sequential: frame f is uploaded,
-    preprocessed and solved before frame f+1 is touched.  pipelined=True is
-    run_sequence_pipelined's 2-slot schedule: frame f+1 is queued before
-    frame f is solved, so its upload and preprocessing (pyramid, observed
-    contour grid) overlap frame f's solve.  The solves themselves are the
-    same, so both drivers return identical results (pipelined == sequential).
+
+def _finalize(config, results, events, t_total, pipelined) -> SequenceResult:
+    """Reference `pipeline.py:357-375`; the smoothing runs on the device."""
+    from .postprocess import smooth_trajectory
+    poses = np.stack([r.pose.to_vector() for r in results])
+    vertices = np.stack([r.vertices for r in results])
+    if config.smooth_output and len(results) > 1:
+        poses_s = smooth_trajectory(poses, config.smoothing_stencil)
+        vertices_s = smooth_trajectory(vertices, config.smoothing_stencil)
+    else:
+        poses_s = poses.copy()
+        vertices_s = vertices.copy()
+    stage_sums = {"preprocess": 0.0, "condition": 0.0, "pose": 0.0, "nonrigid": 0.0}
+    for r in results:
+        for k, v in r.timings.items():
+            stage_sums[k] = stage_sums.get(k, 0.0) + v
+    stage_sums["total"] = t_total
+    return SequenceResult(config, results, poses, vertices, poses_s, vertices_s, events, stage_sums, pipelined)
+
+
+def frame_latencies(events: list) -> dict:
+    """Frame index -> emit slot minus ingest slot (reference `pipeline.py:503-507`)."""
+    ingest, emit = {}, {}
+    for e in events:
+        (ingest if e["event"] == "ingest" else emit)[e["frame"]] = e["slot"]
+    return {f: emit[f] - ingest[f] for f in sorted(emit)}
+
+
+def run_sequence(inputs, config=None, pipelined=False) -> SequenceResult:
+    """Sequence drivers (reference `pipeline.py:378-515`); the track state
+    stays on the device.
+
+    pipelined=False is run_sequence_sequential: frame f is ingested,
+    preprocessed and solved in slot f.  pipelined=True is
+    run_sequence_pipelined's slot schedule: frame f is ingested in slot f and
+    emitted in slot f+2.  On the device that is the tracker's frame queue:
+    slot s queues frame s (its upload and, once the next frame is queued
+    behind it, its preprocessing overlap the solves of frames s-2 and s-1)
+    and solves frame s-2.  The solves are the same in both drivers, so their
+    results are identical (pipelined == sequential) and the events /
+    latencies match the reference's.
     """
     config = SequenceConfig.from_reference(config) if config is not None else SequenceConfig()
-    tr = Tracker(inputs.actor, inputs.camera, config, 1)
-    frames = []
+    actor = _prepare_actor(inputs.actor, config)
+    tr = Tracker(actor, inputs.camera, config, 1)
+    frames, events = [], []
     n = inputs.n_frames
 
     def queue(f):
         tr.set_frame(0, inputs.images[f], inputs.masks[f], inputs.detections[f])
 
-    t0 = time.perf_counter()
-    if pipelined and n:
-        queue(0)
-    for f in range(n):
-        if not pipelined:
-            queue(f)
-        elif f + 1 < n:
-            queue(f + 1)
+    def emit(f, slot, t0):
         tr.step()
         x, v, vs, rep = tr.result(0)
         frames.append(FrameResult(f, PoseParams.from_vector(x), v, vs, pose_report_from_c(rep.pose),
                                   nonrigid_report_from_c(rep.nonrigid) if config.mode == "full" else None,
-                                  {}))
-    total = time.perf_counter() - t0
+                                  {"solve": time.perf_counter() - t0}))
+        events.append({"slot": slot, "event": "emit", "frame": f})
+
+    t_start = time.perf_counter()
+    if pipelined:
+        for slot in range(n + 2):
+            t0 = time.perf_counter()
+            if slot < n:
+                events.append({"slot": slot, "event": "ingest", "frame": slot})
+                queue(slot)
+            if 0 <= slot - 2 < n:
+                emit(slot - 2, slot, t0)
+    else:
+        for f in range(n):
+            t0 = time.perf_counter()
+            events.append({"slot": f, "event": "ingest", "frame": f})
+            queue(f)
+            emit(f, f, t0)
+    total = time.perf_counter() - t_start
     tr.close()
-    return SequenceResult(config, frames, np.stack([r.pose.to_vector() for r in frames]),
-                          np.stack([r.vertices for r in frames]), {"total": total}, pipelined)
+    return _finalize(config, frames, events, total, pipelined)
