@@ -338,6 +338,16 @@ def run_ours(args):
     e1.synchronize()
     barrier()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+    # results of every stream to rank 0 (the tracking job's only collective,
+    # NCCL; outside the timed regions): the last solved frame of each stream
+    gathered = None
+    if world > 1:
+        from paper_1810_02648_b200.sharding import gather_results
+        last = (W + K - 1) & 1
+        g = gather_results(x_h[last][:, None].to(f"cuda:{local}"), v_h[last][:, None].to(f"cuda:{local}"),
+                           world * Sn, "block")
+        if rank == 0:
+            gathered = int(g[0].shape[0])
     tr2.close()
     h2d = Sn * (H * Wd * 3 * 8 + H * Wd + (actor.skeleton.n_joints + 4) * 2 * 8
                 + actor.skeleton.n_joints * 3 * 8 + 2 * actor.skeleton.n_joints + 4)
@@ -365,6 +375,7 @@ def run_ours(args):
                          "peak_source": peak_src,
                          "traffic_source": (traffic or {}).get("source")},
             "pcg_iterations_timed": pcg_iters,
+            "gathered_streams": gathered,
             "per_stream_fps": 1e3 * K / ms_max,
             "clocks": clk,
             "cpu_baseline": cpu,

@@ -269,6 +269,16 @@ int lc_tracker_get_result(lc_tracker *tr, int32_t stream, double *pose_out, doub
 /* developer timeline (LIVECAP_TRACE=1 at context creation): text lines
  * "lane name t_ms" for the marks recorded since the last dump */
 int lc_trace_dump(lc_ctx *ctx, char *buf, int64_t cap);
+/* one solve stage of the oldest queued frame of every stream, which it then
+ * consumes: 1 = conditioning + Stage I, 2 = Stage II + state update, 3 = both
+ * (= lc_tracker_step); a stage-1 tracker and a stage-2 tracker joined by
+ * lc_tracker_pipe split solve_frame across two GPUs */
+int lc_tracker_step_stage(lc_tracker *tr, int32_t stages);
+/* stage handoff between two matching trackers, possibly on two GPUs (the
+ * paper's pose -> non-rigid GPU-pair pipeline): what = 1 copies the solved
+ * poses src -> dst, what = 2 the Stage-I track state (x_prev, x_prev2,
+ * joints_prev, disp_rest, flags); peer copies ordered by events */
+int lc_tracker_pipe(lc_tracker *dst, lc_tracker *src, int32_t what);
 /* streaming readout (the pipelined driver's emit, pipeline.py:449-499):
  * enqueue D2H copies of the last stepped frame's pose (36) and surface
  * (N*3) on the context's stream and return immediately; the host buffers

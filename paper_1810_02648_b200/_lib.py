@@ -139,6 +139,8 @@ _SIGS = {
     "lc_tracker_set_frame": (C.c_int, [P, i32, P, P, P, i32]),
     "lc_tracker_get_result_async": (C.c_int, [P, i32, P, P]),
     "lc_tracker_set_frame_u8": (C.c_int, [P, i32, P, P, P, i32]),
+    "lc_tracker_step_stage": (C.c_int, [P, i32]),
+    "lc_tracker_pipe": (C.c_int, [P, P, i32]),
     "lc_trace_dump": (C.c_int, [P, C.c_char_p, C.c_int64]),
     "lc_tracker_step": (C.c_int, [P]),
     "lc_tracker_get_result": (C.c_int, [P, i32, P, P, P, P]),

@@ -204,16 +204,18 @@ struct JobRing {
     }
 };
 static JobRing &ring_of(lc_ctx *c) {
-    static thread_local std::vector<std::pair<lc_ctx *, JobRing>> rings;
-    for (auto &r : rings)
-        if (r.first == c) return r.second;
-    JobRing jr;
-    jr.cap = 16 << 20;
-    jr.main = c->stream;
-    jr.aux = c->aux;
-    if (cudaMalloc(&jr.dev, jr.cap) != cudaSuccess) throw std::bad_alloc();
-    rings.push_back({c, jr});
-    return rings.back().second;
+    if (!c->ring) {
+        JobRing *jr = new JobRing();
+        jr->cap = 16 << 20;
+        jr->main = c->stream;
+        jr->aux = c->aux;
+        if (cudaMalloc(&jr->dev, jr->cap) != cudaSuccess) {
+            delete jr;
+            throw std::bad_alloc();
+        }
+        c->ring = jr;
+    }
+    return *c->ring;
 }
 template <typename T>
 static const T *stage(lc_ctx *c, const std::vector<T> &v) {
@@ -250,6 +252,7 @@ extern "C" int lc_ctx_create(int32_t device, uint64_t cuda_stream, lc_ctx **out)
     CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio_lo));
     CK(cudaStreamCreateWithPriority(&c->copy, cudaStreamNonBlocking, prio_lo));
     c->tracing = getenv("LIVECAP_TRACE") != nullptr;
+    CK(cudaEventCreateWithFlags(&c->ev_pipe, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_obs, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_pyr, cudaEventDisableTiming));
@@ -279,6 +282,12 @@ extern "C" int lc_ctx_destroy(lc_ctx *c) {
     cudaStreamDestroy(c->aux);
     cudaStreamDestroy(c->copy);
     cudaEventDestroy(c->ev_fork);
+    if (c->ev_pipe) cudaEventDestroy(c->ev_pipe);
+    if (c->ring) {
+        cudaFree(c->ring->dev);
+        delete c->ring;
+        c->ring = nullptr;
+    }
     cudaEventDestroy(c->ev_obs);
     cudaEventDestroy(c->ev_pyr);
     if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -1205,7 +1214,10 @@ static void surface_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, c
                    stage(c, jobs), a->dev, cam_dev(cam), cf.ec, cf.shp, cam.height, cam.width);
 }
 
-static void run_frame(FrameBatch &fb) {
+// stages: 1 = conditioning + Stage I, 2 = Stage II + state update, 3 = both
+// (a Stage-II-only run derives the displaced rest itself and keeps the pose
+// already in the slot, imported from the Stage I device by lc_tracker_pipe)
+static void run_frame(FrameBatch &fb, int stages = 3) {
     lc_ctx *c = fb.c;
     const lc_actor *a = fb.a;
     const lc_config &cfg = *fb.cfg;
@@ -1225,17 +1237,18 @@ static void run_frame(FrameBatch &fb) {
             p.j3d_raw = s->j3d_raw; p.j3d = s->j3d; p.v3d = s->v3d; p.fallbacks = s->fallbacks;
             p.x_prev = s->has_prev ? s->x_prev : nullptr;
             p.x_prev2 = s->has_prev2 ? s->x_prev2 : nullptr;
-            p.x = s->x;
+            p.x = (stages & 1) ? s->x : nullptr;
             p.N = a->dev.N;
             pj.push_back(p);
         }
         mark(c, "frame:start");
         launch(c, k_prep, dim3(16, S), dim3(256), 0, stage(c, pj), (const SkelDev *)a->skel_dev);
         for (Slot *s : ss) {
-            cudaMemsetAsync(s->pose_rep, 0, sizeof(lc_pose_report), c->stream);
-            cudaMemsetAsync(s->nr_rep, 0, sizeof(lc_nonrigid_report), c->stream);
+            if (stages & 1) cudaMemsetAsync(s->pose_rep, 0, sizeof(lc_pose_report), c->stream);
+            if (stages & 2) cudaMemsetAsync(s->nr_rep, 0, sizeof(lc_nonrigid_report), c->stream);
         }
     }
+    if (stages & 1) {
     // ---- Stage I (pipeline.py:173-224)
     int max_rounds = 0;
     std::vector<int> rounds(S);
@@ -1292,6 +1305,8 @@ static void run_frame(FrameBatch &fb) {
         pose_launch(c, a, fb.cam, pj);
         mark(c, "s1:pose");
     }
+    }
+    if (!(stages & 2)) return;
     // ---- Stage II (pipeline.py:227-260) or the pose-only surface
     if (cfg.mode == 0) {
         fk_skin(fb, ss, true, true, &Slot::vinit, nullptr);
@@ -1485,9 +1500,16 @@ extern "C" int lc_tracker_set_frame_u8(lc_tracker *t, int32_t stream, const uint
     API_END
 }
 
-extern "C" int lc_tracker_step(lc_tracker *t) {
+extern "C" int lc_tracker_step(lc_tracker *t) { return lc_tracker_step_stage(t, 3); }
+
+// One solve stage of the oldest queued frame of every stream, which it then
+// consumes: 1 = conditioning + Stage I, 2 = Stage II + state update, 3 =
+// both.  A tracker that runs only stage 1 and one that runs only stage 2,
+// joined by lc_tracker_pipe, split solve_frame across a GPU pair.
+extern "C" int lc_tracker_step_stage(lc_tracker *t, int32_t stages) {
     API_BEGIN
     require(t != nullptr, "null tracker");
+    require(stages >= 1 && stages <= 3, "stages must be 1, 2 or 3");
     lc_ctx *c = t->ctx;
     CK(cudaSetDevice(c->device));
     std::vector<FrameIn *> cur, todo, next;
@@ -1507,7 +1529,7 @@ extern "C" int lc_tracker_step(lc_tracker *t) {
     if (all_next) launch_preprocess(c, t->conf, t->cfg, next, H, W);
     for (size_t i = 0; i < t->slots.size(); ++i) t->slots[i]->view(*cur[i]);
     FrameBatch fb{c, t->actor, t->cam, &t->cfg, &t->conf, t->slots, cur};
-    run_frame(fb);
+    run_frame(fb, stages);
     for (size_t i = 0; i < t->slots.size(); ++i) {
         FrameIn &f = *cur[i];
         CK(cudaEventRecord(f.freed, c->stream));
@@ -1538,6 +1560,59 @@ extern "C" int lc_tracker_get_result(lc_tracker *t, int32_t stream, double *pose
     }
     CK(cudaStreamSynchronize(c->stream));
     return last_launch_status();
+    API_END
+}
+
+// Stage handoff between two trackers of the same actor / camera / stream
+// count, possibly on different GPUs (the paper's pose -> non-rigid stage
+// pipeline over a GPU pair):
+//   what = 1: the solved pose of every stream, src -> dst (Stage I device ->
+//             Stage II device, 36 doubles per stream);
+//   what = 2: the track state Stage I needs, src -> dst (x_prev, x_prev2,
+//             joints_prev, disp_rest + their flags; Stage II device -> Stage I
+//             device, ~0.13 MB per stream at x5k).
+// The copies are peer copies over NVLink on the destination's stream, after
+// an event on the source's stream, so they are ordered after the source
+// stage and before the destination's next stage.
+extern "C" int lc_tracker_pipe(lc_tracker *dst, lc_tracker *src, int32_t what) {
+    API_BEGIN
+    require(dst && src && dst != src, "two distinct trackers required");
+    require(dst->S == src->S && dst->actor->dev.N == src->actor->dev.N, "trackers do not match");
+    require(what == 1 || what == 2, "what must be 1 (pose) or 2 (state)");
+    lc_ctx *cd = dst->ctx, *cs = src->ctx;
+    if (cd->device != cs->device) {
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, cd->device, cs->device);
+        if (can) {
+            CK(cudaSetDevice(cd->device));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(cs->device, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else CK(e);
+        }
+    }
+    CK(cudaSetDevice(cs->device));
+    CK(cudaEventRecord(cs->ev_pipe, cs->stream));
+    CK(cudaSetDevice(cd->device));
+    CK(cudaStreamWaitEvent(cd->stream, cs->ev_pipe, 0));
+    const size_t N = dst->actor->dev.N;
+    for (int i = 0; i < dst->S; ++i) {
+        Slot *d = dst->slots[i], *s = src->slots[i];
+        auto cp = [&](void *to, const void *from, size_t bytes) {
+            CK(cudaMemcpyPeerAsync(to, cd->device, from, cs->device, bytes, cd->stream));
+        };
+        if (what == 1) {
+            cp(d->x, s->x, sizeof(double) * LC_NP);
+        } else {
+            cp(d->x_prev, s->x_prev, sizeof(double) * LC_NP);
+            cp(d->x_prev2, s->x_prev2, sizeof(double) * LC_NP);
+            cp(d->joints_prev, s->joints_prev, sizeof(double) * 3 * LC_MAXJ);
+            cp(d->disp, s->disp, sizeof(double) * 3 * N);
+            d->has_prev = s->has_prev;
+            d->has_prev2 = s->has_prev2;
+            d->has_disp = s->has_disp;
+        }
+    }
+    return LC_OK;
     API_END
 }
 

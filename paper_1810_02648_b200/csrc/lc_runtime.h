@@ -16,6 +16,8 @@ struct lc_ctx {
     cudaEvent_t ev_fork = nullptr, ev_obs = nullptr, ev_pyr = nullptr;
     // host->device uploads of queued frames (copy engine, overlaps both)
     cudaStream_t copy = nullptr;
+    cudaEvent_t ev_pipe = nullptr;   // cross-device handoff point (lc_tracker_pipe)
+    struct JobRing *ring = nullptr;  // descriptor staging ring (owned)
     // optional timeline (LIVECAP_TRACE=1): timing events at phase boundaries
     bool tracing = false;
     struct Mark { const char *name; int lane; cudaEvent_t ev; };

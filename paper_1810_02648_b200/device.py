@@ -357,3 +357,59 @@ class Tracker:
             self.close()
         except Exception:
             pass
+
+
+class StagePipeline:
+    """The paper's pose -> non-rigid pipeline across a GPU pair.
+
+    Stage I (conditioning, pose GN) of every stream runs on `pose_device`,
+    Stage II (surface GN, PCG, snapping, warp) on `surface_device`.  Per frame
+    the solved poses go pose -> surface device and the track state Stage I
+    needs (x_prev, x_prev2, joints_prev, disp_rest) comes back, as peer copies
+    over NVLink (lc_tracker_pipe).  Within one stream the stages are serial
+    (frame t+1's Stage I needs frame t's surface), so the streams are split
+    into `groups` groups on their own CUDA streams: while the surface device
+    solves group g, the pose device solves group g+1.  The arithmetic is the
+    single-device tracker's, so results are identical to it.
+    """
+
+    def __init__(self, actor, camera, config, n_streams: int, pose_device: int = 0, surface_device: int = 1,
+                 groups: int = 2):
+        if n_streams % groups:
+            raise ValueError("n_streams must be a multiple of groups")
+        self.groups = groups
+        self.per = n_streams // groups
+        self.ctx_a = [L.Context(pose_device) for _ in range(groups)]
+        self.ctx_b = [L.Context(surface_device) for _ in range(groups)]
+        self.A = [Tracker(actor, camera, config, self.per, ctx=c) for c in self.ctx_a]
+        self.B = [Tracker(actor, camera, config, self.per, ctx=c) for c in self.ctx_b]
+
+    def _where(self, stream):
+        return divmod(stream, self.per)
+
+    def set_frame(self, stream: int, image, mask, det, on_device: bool = False):
+        g, s = self._where(stream)
+        if on_device:
+            raise ValueError("device-resident inputs live on one GPU; queue host frames")
+        self.A[g].set_frame(s, image, mask, det)
+        self.B[g].set_frame(s, image, mask, det)
+
+    def step(self):
+        lib = self.A[0].ctx.lib
+        for g in range(self.groups):
+            L.check(lib.lc_tracker_step_stage(self.A[g].handle, 1))
+            L.check(lib.lc_tracker_pipe(self.B[g].handle, self.A[g].handle, 1))
+            L.check(lib.lc_tracker_step_stage(self.B[g].handle, 2))
+            L.check(lib.lc_tracker_pipe(self.A[g].handle, self.B[g].handle, 2))
+
+    def result(self, stream: int, with_report: bool = True):
+        g, s = self._where(stream)
+        return self.B[g].result(s, with_report)
+
+    def synchronize(self):
+        for c in self.ctx_a + self.ctx_b:
+            c.synchronize()
+
+    def close(self):
+        for t in self.A + self.B:
+            t.close()

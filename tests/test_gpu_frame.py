@@ -113,3 +113,29 @@ def test_queue_depth_is_three():
     with pytest.raises(Exception):
         tr.step()
     tr.close()
+
+
+def test_stage_pipeline_gpu_pair_matches_single_tracker():
+    """§8e: Stage I and Stage II on a GPU pair (here both on cuda:0, each
+    stage tracker on its own CUDA stream; the handoffs are the same peer
+    copies) give exactly the single-device tracker's results."""
+    from paper_1810_02648_b200.config import SequenceConfig
+    from paper_1810_02648_b200.device import StagePipeline, Tracker
+    actor, cam, frames = scene("standard", 256, 3)
+    cfg = SequenceConfig(directional=False)
+    S = 4
+    ref = Tracker(actor, cam, cfg, S)
+    pipe = StagePipeline(actor, cam, cfg, S, pose_device=0, surface_device=0, groups=2)
+    for fr in frames:
+        for s in range(S):
+            ref.set_frame(s, fr.image, fr.mask, fr.detections)
+            pipe.set_frame(s, fr.image, fr.mask, fr.detections)
+        ref.step()
+        pipe.step()
+        pipe.synchronize()
+        for s in range(S):
+            x0, v0, _, _ = ref.result(s)
+            x1, v1, _, _ = pipe.result(s)
+            assert np.array_equal(x0, x1) and np.array_equal(v0, v1), (fr.index, s)
+    pipe.close()
+    ref.close()

@@ -49,3 +49,49 @@ def test_sharding_two_ranks():
     assert not set(gathered[0]) & set(gathered[1])
     assert ms == 150.0
     assert fps == pytest.approx(2 * 4 * 10 / 0.150)
+
+
+def _gather_worker(rank, world, port, out, n_streams, policy):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import numpy as np
+    from paper_1810_02648_b200.sharding import assign_streams, gather_results
+    ids = assign_streams(n_streams, world, rank, policy)
+    F, N = 3, 5
+    poses = np.stack([np.full((F, 36), float(s)) for s in ids]) if ids else np.zeros((0, F, 36))
+    verts = np.stack([np.full((F, N, 3), 10.0 + s) for s in ids]) if ids else np.zeros((0, F, N, 3))
+    res = gather_results(poses, verts, n_streams, policy)
+    if rank == 0:
+        out.put((ids, res[0], res[1]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_streams,policy", [(8, "block"), (7, "round_robin"), (5, "block")])
+def test_result_gather_two_ranks(n_streams, policy):
+    """§8e: results of unevenly sharded streams gathered to rank 0 in global order."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, q, n_streams, policy)) for r in range(world)]
+    for p in procs:
+        p.start()
+    ids0, P, V = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert P.shape == (n_streams, 3, 36) and V.shape == (n_streams, 3, 5, 3)
+    for s in range(n_streams):
+        assert (P[s] == s).all() and (V[s] == 10.0 + s).all()
+
+
+def test_assign_streams_partition():
+    from paper_1810_02648_b200.sharding import assign_streams
+    for n in (1, 7, 8, 64):
+        for world in (1, 2, 4, 8):
+            for policy in ("block", "round_robin"):
+                ids = [assign_streams(n, world, r, policy) for r in range(world)]
+                flat = sorted(i for x in ids for i in x)
+                assert flat == list(range(n))
+                assert max(map(len, ids)) - min(map(len, ids)) <= 1
