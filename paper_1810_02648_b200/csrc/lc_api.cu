@@ -605,6 +605,11 @@ void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) 
     alloc_grid(mem, obs, H, W);
     alloc_grid(mem, own, H, W);
     own_mask = mem.alloc<uint8_t>(HW);
+    {
+        const size_t nc = (size_t)((W + LC_GRID_CELL - 1) / LC_GRID_CELL) * ((H + LC_GRID_CELL - 1) / LC_GRID_CELL);
+        own_cnt = mem.alloc<int>(nc);
+        own_keys = mem.alloc<int>(nc * 256);
+    }
     j2d = mem.alloc<double>(2 * (LC_MAXJ + 4));
     j3d_raw = mem.alloc<double>(3 * LC_MAXJ);
     j3d = mem.alloc<double>(3 * LC_MAXJ);
@@ -1158,9 +1163,13 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
     std::vector<RasterJob> rj;
     for (Slot *s : ss) rj.push_back(raster_job(s, s->*verts, s->own_mask));
     raster(c, a, fb.cam, rj);
-    std::vector<std::pair<const GridBufs *, const uint8_t *>> gs;
-    for (Slot *s : ss) gs.push_back({&s->own, s->own_mask});
-    build_grids(c, gs, H, W, 0.0, false);   // rim queries stay near the own contour: quadtree only
+    // own-silhouette contour buckets: the rim's bounded queries need nothing else
+    {
+        std::vector<OwnCellsJob> oj;
+        for (Slot *s : ss) oj.push_back(OwnCellsJob{s->own_mask, s->own_cnt, s->own_keys});
+        const int ncx = (W + LC_GRID_CELL - 1) / LC_GRID_CELL, ncy = (H + LC_GRID_CELL - 1) / LC_GRID_CELL;
+        launch(c, k_own_cells, dim3(ncx * ncy, (unsigned)ss.size()), dim3(256), 0, stage(c, oj), H, W, ncx);
+    }
     std::vector<ContourJob> cj;
     for (Slot *s : ss) {
         ContourJob j{};
@@ -1181,9 +1190,8 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
         RimJob r{};
         r.verts = s->*verts; r.idx = s->cidx; r.B = s->B;
         r.own = grid_dev(s->own, s->own_mask, H, W);
-        r.own.cand_range = nullptr;                       // no per-cell lists for own-mask grids
-        r.own.cand_blk = nullptr;
-        r.ownK = s->own.K;
+        r.own_cnt = s->own_cnt;
+        r.own_keys = s->own_keys;
         r.keep = s->enabled;
         r.stage1 = stage1;
         r.active = 1;

@@ -134,12 +134,22 @@ __global__ void k_tri_front(const ContourJob *jobs, ActorDev A);
 __global__ void k_sil_edges(const ContourJob *jobs, ActorDev A);
 __global__ void k_contour_compact(const ContourJob *jobs, ActorDev A, CamDev cam);
 
+// own-silhouette contour pixels bucketed by 16x16 cell (fixed 256 slots per
+// cell, row-major within a cell): all the rim's bounded queries need
+struct OwnCellsJob {
+    const uint8_t *mask;       // H*W own mask
+    int *cnt;                  // ncells
+    int *keys;                 // ncells*256 site keys y << 16 | x
+};
+__global__ void k_own_cells(const OwnCellsJob *jobs, int H, int W, int ncx);
+
 struct RimJob {
     const double *verts;       // N*3
     const int *idx;            // B
     const int *B;
-    NnGridDev own;             // own-mask field
-    const int *ownK;
+    NnGridDev own;             // own-mask field (mask, grid dims)
+    const int *own_cnt;        // per-cell contour counts (k_own_cells)
+    const int *own_keys;       // per-cell contour keys
     uint8_t *keep;             // B out
     int stage1;                // 1: thickness probes + rigidity gate
     int active;

@@ -187,7 +187,8 @@ __device__ double pose_row(const PoseCtx &c, const PoseView &pv, int r, double *
 // per-term energies in terms[5], behind-camera count.  Rows are split over
 // the team's CTAs; every CTA ends with the same totals.
 template <typename T>
-__device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &behind_out, int fine = -1) {
+__device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &behind_out, int fine = -1,
+                            bool fk_valid = false) {
     PoseSmem &s = *c.s;
     auto fst = [&](int k) {
         if (fine >= 0 && c.J->phase && T::tid() == 0) c.J->phase[fine + k] = gtimer();
@@ -196,7 +197,9 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
     const SkelDev &sk = s.sk;
     const int nj = sk.J;
     const PoseView pv{&s.f, s.xt, s.pix, s.okz};
-    if (threadIdx.x < 32) fk_warp(sk, s.xt, s.f);
+    // s.f already holds the FK of this point when it is the previous line
+    // search's accepted trial (or the unchanged point of a rejected step)
+    if (!fk_valid && threadIdx.x < 32) fk_warp(sk, s.xt, s.f);
     __syncthreads();
     fst(1);
     // projections of joints + markers
@@ -436,12 +439,13 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(const PoseJob *jobs, con
     };
     stamp();
     int behind_total = 0, gimbal = 0;
+    bool fk_valid = false;   // s.f holds FK(s.x) (block-uniform)
     for (int it = 0; it < J.hp.gn; ++it) {
         for (int i = threadIdx.x; i < LC_NP; i += NT) s.xt[i] = s.x[i];
         __syncthreads();
         double terms[5];
         int behind;
-        const double e0 = pose_eval<T>(c, true, terms, behind, it == 1 ? 32 : -1);
+        const double e0 = pose_eval<T>(c, true, terms, behind, it == 1 ? 32 : -1, fk_valid);
         stamp();
         behind_total += behind;
         gimbal |= s.f.gimbal;
@@ -481,10 +485,16 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(const PoseJob *jobs, con
                 s.step[i] = st;
                 if (hit >= 0) s.x[i] = ts.xt[hit][i];
             }
+            if (hit >= 0) {   // the accepted trial's FK is FK(new x): keep it for the next evaluation
+                const unsigned long long *src = reinterpret_cast<const unsigned long long *>(&ts.f[hit]);
+                unsigned long long *dst = reinterpret_cast<unsigned long long *>(&s.f);
+                for (int i = threadIdx.x; i < (int)(sizeof(FkState) / 8); i += NT) dst[i] = src[i];
+            }
             __syncthreads();
             if (hit >= 0) { halv = base + hit; e1 = et[hit]; break; }
             if (last) { halv = J.hp.max_halvings; rejected = true; e1 = e0; break; }
         }
+        fk_valid = true;   // accepted: copied from the trial; rejected: s.f is still FK(s.x)
         stamp();
         if (T::tid() == 0 && rep) {
             const int k = log0 + it;

@@ -120,6 +120,7 @@ struct Slot {
     double *pyr = nullptr, *blur_tmp = nullptr;
     GridBufs obs{}, own{};
     uint8_t *own_mask = nullptr;
+    int *own_cnt = nullptr, *own_keys = nullptr;   // own-silhouette contour buckets (rim)
     // detections
     double *j2d, *j3d_raw, *j3d;
     uint8_t *v2d, *v3d;

@@ -1043,14 +1043,64 @@ __device__ __forceinline__ int part_at(const ActorDev &A, CamDev cam, const doub
     return A.vpart[A.tris[3 * t + w]];
 }
 
+// One CTA per 16x16 cell: the cell's contour pixels of the own mask
+// (foreground with a background 4-neighbour, the image border counting as
+// background; imageproc.py:34-49), compacted in row-major order.
+__global__ void __launch_bounds__(256) k_own_cells(const OwnCellsJob *jobs, int H, int W, int ncx) {
+    const OwnCellsJob J = jobs[blockIdx.y];
+    const int c = blockIdx.x;
+    const int x = (c % ncx) * LC_GRID_CELL + (threadIdx.x & (LC_GRID_CELL - 1));
+    const int y = (c / ncx) * LC_GRID_CELL + (threadIdx.x >> LC_GRID_SHIFT);
+    bool on = false;
+    if (x < W && y < H && J.mask[(size_t)y * W + x]) {
+        const bool l = x > 0 && J.mask[(size_t)y * W + x - 1], r = x + 1 < W && J.mask[(size_t)y * W + x + 1];
+        const bool u = y > 0 && J.mask[(size_t)(y - 1) * W + x], d = y + 1 < H && J.mask[(size_t)(y + 1) * W + x];
+        on = !(l && r && u && d);
+    }
+    __shared__ int wcount[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned bal = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) wcount[w] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int k = 0; k < 8; ++k) {
+        before += k < w ? wcount[k] : 0;
+        total += wcount[k];
+    }
+    if (on) J.keys[(size_t)c * 256 + before + __popc(bal & ((1u << lane) - 1u))] = (y << 16) | x;
+    if (threadIdx.x == 0) J.cnt[c] = total;
+}
+
+// nn_within2 over the own-silhouette cell buckets
+__device__ inline double own_within2(const NnGridDev &g, const int *cnt, const int *keys, double qx, double qy,
+                                     double R) {
+    double best = LC_INF;
+    if (!(isfinite(qx) && isfinite(qy))) return best;
+    const int cx0 = max(0, (int)floor((qx - R) / LC_GRID_CELL));
+    const int cx1 = min(g.ncx - 1, (int)floor((qx + R) / LC_GRID_CELL));
+    const int cy0 = max(0, (int)floor((qy - R) / LC_GRID_CELL));
+    const int cy1 = min(g.ncy - 1, (int)floor((qy + R) / LC_GRID_CELL));
+    for (int cy = cy0; cy <= cy1; ++cy)
+        for (int cx = cx0; cx <= cx1; ++cx) {
+            const int c = cy * g.ncx + cx;
+            const int n = cnt[c];
+            const int *kk = keys + (size_t)c * 256;
+            for (int k = 0; k < n; ++k) {
+                const int key = kk[k];
+                const double dx = qx - (double)(key & 0xffff), dy = qy - (double)(key >> 16);
+                best = fmin(best, dx * dx + dy * dy);
+            }
+        }
+    return best <= R * R ? best : LC_INF;
+}
+
 __global__ void k_rim(const RimJob *jobs, ActorDev A, CamDev cam, const double *probe_offs) {
     const RimJob J = jobs[blockIdx.y];
     if (!J.active) return;
     const int B = *J.B;
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
-    NnGridDev own = J.own;
-    own.K = *J.ownK;
+    const NnGridDev own = J.own;
     for (int b = blockIdx.x * wpb + (threadIdx.x >> 5); b < B; b += gridDim.x * wpb) {
         const int v = J.idx[b];
         const V3 p = ld3(J.verts + 3 * (size_t)v);
@@ -1061,8 +1111,8 @@ __global__ void k_rim(const RimJob *jobs, ActorDev A, CamDev cam, const double *
         // least 6 px (2 * depth >= 12) from it.  Both are threshold tests, so
         // bounded exact searches decide them (nn_within2).
         bool keep = false;
-        if (own.K > 0 && ok) {
-            const double d2 = nn_within2(own, px, py, 2.0);
+        if (ok) {
+            const double d2 = own_within2(own, J.own_cnt, J.own_keys, px, py, 2.0);
             keep = d2 != LC_INF && sqrt(d2) <= 1.5;
         }
         if (J.stage1) {
@@ -1075,7 +1125,7 @@ __global__ void k_rim(const RimJob *jobs, ActorDev A, CamDev cam, const double *
                     const int k = dir * 8 + r;
                     const double qx = px + probe_offs[2 * k], qy = py + probe_offs[2 * k + 1];
                     if (!field_inside(own, qx, qy)) continue;
-                    const double d2 = nn_within2(own, qx, qy, 7.0);
+                    const double d2 = own_within2(own, J.own_cnt, J.own_keys, qx, qy, 7.0);
                     deep = fmax(deep, d2 == LC_INF ? 7.0 : sqrt(d2));   // > 7 px: any value >= 6 decides
                 }
                 for (int o = 16; o > 0; o >>= 1) deep = fmax(deep, __shfl_xor_sync(0xffffffffu, deep, o));
