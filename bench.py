@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--streams", type=int, default=8, help="capture streams per GPU")
+    ap.add_argument("--groups", type=int, default=4,
+                    help="stream groups stepped concurrently on their own CUDA streams (BatchTracker)")
     ap.add_argument("--preset", default="x5k")
     ap.add_argument("--res", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -75,6 +77,7 @@ def workload(args, world):
     return {"workload": f"cfg3-shaped full two-stage solve_frame, {args.preset} template @ "
                         f"{args.res}x{args.res}, {args.streams} synthetic streams per GPU (cfg5 sharding)",
             "preset": args.preset, "resolution": args.res, "streams_per_gpu": args.streams,
+            "stream_groups": args.groups,
             "total_streams": args.streams * world, "parallelism": f"stream-sharded x{world}",
             "l2": "per-step inputs (images + pyramids) exceed the 126 MB L2; no flush needed"}
 
@@ -198,7 +201,7 @@ def run_ours(args):
     from paper_1810_02648_b200 import synthetic as S
     from paper_1810_02648_b200.camera import suggest_camera
     from paper_1810_02648_b200.config import SequenceConfig
-    from paper_1810_02648_b200.device import Tracker
+    from paper_1810_02648_b200.device import BatchTracker
 
     stream = torch.cuda.Stream(device=local, priority=-1)   # above the library's preprocessing stream
     ctx = _lib.Context(local, stream.cuda_stream)
@@ -241,12 +244,15 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- value: inputs resident in HBM.  Frames are queued one ahead (the
-    # reference's pipelined driver): step() solves frame f while frame f+1's
-    # preprocessing runs on the library's auxiliary stream.  Every timed step
-    # queues one frame and solves one, so the timed region holds exactly K
-    # solves and K preprocessings.
-    tr = Tracker(actor, cam, cfg, Sn, ctx=ctx)
+    # ---- value: inputs resident in HBM.  Frames are queued ahead (the
+    # reference's pipelined driver): step() solves frame f while the next
+    # frame's preprocessing runs on the library's auxiliary stream.  Every
+    # timed step queues one frame and solves one, so the timed region holds
+    # exactly K solves and K preprocessings.  The S streams are split into
+    # `groups` trackers stepped concurrently on their own CUDA streams; the
+    # timed region is bracketed by device-wide synchronisations, so the
+    # events measure the whole device.
+    tr = BatchTracker(actor, cam, cfg, Sn, groups=args.groups, device=local)
 
     def queue_dev(f):
         for s in range(Sn):
@@ -259,27 +265,27 @@ def run_ours(args):
     for f in range(W):
         queue_dev(f + AHEAD)
         tr.step()
-    ctx.synchronize()
+    tr.synchronize()
     c0 = [tr.counters(s) for s in range(Sn)]
     barrier()
     torch.cuda.synchronize()
     if not os.environ.get("BENCH_NO_PROFILE"):
-        ctx.profile_kernel(DOMINANT)
-    l0 = ctx.launches()
+        tr.profile_kernel(DOMINANT)
+    l0 = tr.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for f in range(W, W + K):
         queue_dev(f + AHEAD)
         tr.step()
-    ctx.synchronize()            # joins the auxiliary (preprocessing) stream too
+    tr.synchronize()             # every group's solve, preprocessing and copy streams
     ev1.record(stream)
     ev1.synchronize()
     barrier()
     clk = clocks.stop() if clocks else None
-    launches = ctx.launches() - l0
+    launches = tr.launches() - l0
     ms_dev = ev0.elapsed_time(ev1)
-    k_ms, k_n = ctx.profile_read()
-    ctx.profile_kernel(None)
+    k_ms, k_n = tr.profile_read()
+    tr.profile_kernel(None)
     c1 = [tr.counters(s) for s in range(Sn)]
     ms_max = max_over_ranks(ms_dev)
     value = aggregate_fps([ms_max], world, Sn, K)
@@ -299,10 +305,10 @@ def run_ours(args):
     # surfaces are read back into pinned host buffers with the streaming
     # readout; the host consumes frame f's results (event wait) while frame
     # f+1 is being solved (the pipelined driver's 2-slot latency).
-    tr2 = Tracker(actor, cam, cfg, Sn, ctx=ctx)
+    tr2 = BatchTracker(actor, cam, cfg, Sn, groups=args.groups, device=local)
     x_h = torch.empty((2, Sn, 36), dtype=torch.float64, pin_memory=True)
     v_h = torch.empty((2, Sn, N, 3), dtype=torch.float64, pin_memory=True)
-    done = [torch.cuda.Event(), torch.cuda.Event()]
+    done = [[torch.cuda.Event() for _ in tr2.ctxs] for _ in range(2)]
     checksum = [0.0]
 
     def queue_host(f):
@@ -314,9 +320,11 @@ def run_ours(args):
         b = f & 1
         for s in range(Sn):
             tr2.result_async(s, x_h[b, s], v_h[b, s])
-        done[b].record(stream)
+        for ev, ts in zip(done[b], tr2.torch_streams):
+            ev.record(ts)
         if not first:                     # frame f-1's results are complete on the host
-            done[b ^ 1].synchronize()
+            for ev in done[b ^ 1]:
+                ev.synchronize()
             checksum[0] += float(x_h[b ^ 1, :, 3].sum())
 
     for f in range(AHEAD):
@@ -324,7 +332,7 @@ def run_ours(args):
     for f in range(W):
         queue_host(f + AHEAD)
         step_host(f, f == 0)
-    ctx.synchronize()
+    tr2.synchronize()
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -332,8 +340,9 @@ def run_ours(args):
     for f in range(W, W + K):
         queue_host(f + AHEAD)
         step_host(f, False)
-    done[(W + K - 1) & 1].synchronize()   # the last frame's results
-    ctx.synchronize()
+    for ev in done[(W + K - 1) & 1]:       # the last frame's results
+        ev.synchronize()
+    tr2.synchronize()
     e1.record(stream)
     e1.synchronize()
     barrier()

@@ -413,3 +413,92 @@ class StagePipeline:
     def close(self):
         for t in self.A + self.B:
             t.close()
+
+
+class BatchTracker:
+    """`n_streams` streams split into `groups` trackers, each on its own
+    library context (CUDA solve / preprocessing / copy streams), stepped
+    together.  Each group's kernel chain runs independently, so one group's
+    raster / contour phases overlap another's solver phases and a slow stream
+    only holds back its own group.  Same API as `Tracker` (global stream
+    indices); results are identical to a single tracker's.
+    """
+
+    def __init__(self, actor, camera, config: SequenceConfig | None = None, n_streams: int = 1,
+                 groups: int = 1, device: int = 0, priority_streams: bool = True):
+        groups = max(1, min(groups, n_streams))
+        base, extra = divmod(n_streams, groups)
+        self.sizes = [base + (1 if g < extra else 0) for g in range(groups)]
+        self.starts = np.cumsum([0] + self.sizes[:-1]).tolist()
+        self.torch_streams = []
+        self.ctxs = []
+        for _ in range(groups):
+            st = 0
+            if priority_streams:
+                try:
+                    import torch
+                    ts = torch.cuda.Stream(device=device, priority=-1)
+                    self.torch_streams.append(ts)
+                    st = ts.cuda_stream
+                except Exception:   # noqa: BLE001 - torch only provides the high-priority stream
+                    st = 0
+            self.ctxs.append(L.Context(device, st))
+        self.trackers = [Tracker(actor, camera, config, n, ctx=c) for n, c in zip(self.sizes, self.ctxs)]
+        self.S = n_streams
+
+    def _where(self, stream):
+        for g, (a, n) in enumerate(zip(self.starts, self.sizes)):
+            if a <= stream < a + n:
+                return g, stream - a
+        raise IndexError("stream index out of range")
+
+    def set_frame(self, stream, image, mask, det, on_device=False):
+        g, s = self._where(stream)
+        self.trackers[g].set_frame(s, image, mask, det, on_device)
+
+    def step(self):
+        for t in self.trackers:
+            t.step()
+
+    def result(self, stream, with_report=True):
+        g, s = self._where(stream)
+        return self.trackers[g].result(s, with_report)
+
+    def result_async(self, stream, pose_out, verts_out):
+        g, s = self._where(stream)
+        self.trackers[g].result_async(s, pose_out, verts_out)
+
+    def set_state(self, stream, state):
+        g, s = self._where(stream)
+        self.trackers[g].set_state(s, state)
+
+    def get_state(self, stream):
+        g, s = self._where(stream)
+        return self.trackers[g].get_state(s)
+
+    def counters(self, stream):
+        g, s = self._where(stream)
+        return self.trackers[g].counters(s)
+
+    def synchronize(self):
+        for c in self.ctxs:
+            c.synchronize()
+
+    def launches(self) -> int:
+        return sum(c.launches() for c in self.ctxs)
+
+    def profile_kernel(self, name):
+        for c in self.ctxs:
+            c.profile_kernel(name)
+
+    def profile_read(self):
+        ms, n = 0.0, 0
+        for c in self.ctxs:
+            a, b = c.profile_read()
+            ms += a
+            n += b
+        return ms, n
+
+    def close(self):
+        for t in self.trackers:
+            t.close()

@@ -139,3 +139,27 @@ def test_stage_pipeline_gpu_pair_matches_single_tracker():
             assert np.array_equal(x0, x1) and np.array_equal(v0, v1), (fr.index, s)
     pipe.close()
     ref.close()
+
+
+def test_batch_tracker_groups_identical():
+    """Streams split over concurrently stepped groups (own contexts / CUDA
+    streams) give exactly the single tracker's results."""
+    from paper_1810_02648_b200.config import SequenceConfig
+    from paper_1810_02648_b200.device import BatchTracker, Tracker
+    actor, cam, frames = scene("small", 128, 3)
+    cfg = SequenceConfig(directional=False)
+    ref = Tracker(actor, cam, cfg, 5)
+    bt = BatchTracker(actor, cam, cfg, 5, groups=3)
+    assert bt.sizes == [2, 2, 1]
+    for fr in frames:
+        for s in range(5):
+            ref.set_frame(s, fr.image, fr.mask, fr.detections)
+            bt.set_frame(s, fr.image, fr.mask, fr.detections)
+        ref.step()
+        bt.step()
+        for s in range(5):
+            x0, v0, _, _ = ref.result(s)
+            x1, v1, _, _ = bt.result(s)
+            assert np.array_equal(x0, x1) and np.array_equal(v0, v1)
+    bt.close()
+    ref.close()
