@@ -285,6 +285,7 @@ def run_ours(args):
     launches = tr.launches() - l0
     ms_dev = ev0.elapsed_time(ev1)
     k_ms, k_n = tr.profile_read()
+    k_busy_ms = tr.profile_busy_ms()
     tr.profile_kernel(None)
     c1 = [tr.counters(s) for s in range(Sn)]
     ms_max = max_over_ranks(ms_dev)
@@ -296,6 +297,9 @@ def run_ours(args):
     k_avg_s = (k_ms / max(k_n, 1)) / 1e3
     peak, peak_src = read_peaks()
     achieved = per_launch / k_avg_s / 1e9 if k_avg_s > 0 else 0.0
+    # the groups' launches run concurrently: all of the kernel's algorithmic
+    # bytes over the union of its launch intervals
+    achieved_agg = alg / (k_busy_ms / 1e3) / 1e9 if k_busy_ms > 0 else 0.0
     traffic = read_traffic()
     pcg_iters = sum(int((c1[s] - c0[s])[2]) for s in range(Sn))
     tr.close()
@@ -377,10 +381,18 @@ def run_ours(args):
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "kernel": DOMINANT, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak if peak else None,
-                         "traffic": ((traffic or {}).get("dram_bytes_per_launch")
-                                     if (traffic or {}).get("streams") == Sn else None),
+                         # ncu DRAM bytes of one launch, scaled from the captured
+                         # launch's stream count to this run's streams per launch
+                         "traffic": (traffic["dram_bytes_per_launch"] * (Sn / max(args.groups, 1))
+                                     / traffic["streams"] if traffic and traffic.get("streams") else None),
                          "algorithmic_bytes_per_launch": per_launch,
                          "kernel_ms_per_launch": k_avg_s * 1e3, "launches": k_n,
+                         "achieved_concurrent": achieved_agg,
+                         "frac_concurrent": achieved_agg / peak if peak else None,
+                         "kernel_busy_ms": k_busy_ms,
+                         "note": ("achieved/frac: per launch (one launch = one group of "
+                                  f"{args.streams // max(args.groups, 1)} streams); *_concurrent: every launch's "
+                                  "algorithmic bytes over the union of the launch intervals of all groups"),
                          "peak_source": peak_src,
                          "traffic_source": (traffic or {}).get("source")},
             "pcg_iterations_timed": pcg_iters,

@@ -301,6 +301,8 @@ int lc_tracker_counters(lc_tracker *tr, int32_t stream, int64_t *out);
  * context's stream (NULL disables); read returns total ms and launch count */
 int lc_profile_kernel(lc_ctx *ctx, const char *kernel_name);
 int lc_profile_read(lc_ctx *ctx, double *total_ms, int64_t *count);
+/* (start, end) ms of every profiled launch after the profiling origin */
+int lc_profile_intervals(lc_ctx *ctx, double *out, int64_t cap, int64_t *count);
 /* introspection of a stream's last Stage II setup (tests / debugging):
  * what 0: boundary vertex ids (int64), 1: boundary enabled (as int64 0/1),
  * 2: visible vertex ids (int64), 3: normals2d (B*2 f64), 4: v_init (N*3 f64),

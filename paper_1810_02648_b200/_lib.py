@@ -142,6 +142,7 @@ _SIGS = {
     "lc_tracker_step_stage": (C.c_int, [P, i32]),
     "lc_tracker_pipe": (C.c_int, [P, P, i32]),
     "lc_trace_dump": (C.c_int, [P, C.c_char_p, C.c_int64]),
+    "lc_profile_intervals": (C.c_int, [P, P, C.c_int64, P]),
     "lc_tracker_step": (C.c_int, [P]),
     "lc_tracker_get_result": (C.c_int, [P, i32, P, P, P, P]),
     "lc_tracker_set_state": (C.c_int, [P, i32, P, P, P, P, P, P]),
@@ -242,6 +243,12 @@ class Context:
         ms, n = C.c_double(), C.c_int64()
         check(self.lib.lc_profile_read(self.handle, C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+    def profile_intervals(self):
+        out = np.zeros(2 * 65536)
+        n = C.c_int64()
+        check(self.lib.lc_profile_intervals(self.handle, out.ctypes.data, 65536, C.byref(n)))
+        return out[:2 * n.value].reshape(-1, 2)
 
     def synchronize(self):
         check(self.lib.lc_ctx_synchronize(self.handle))

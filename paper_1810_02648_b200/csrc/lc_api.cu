@@ -334,6 +334,29 @@ extern "C" int lc_profile_kernel(lc_ctx *c, const char *name) {
     }
     c->prof_events.clear();
     c->prof_name = name ? name : "";
+    if (!c->prof_ref) cudaEventCreate(&c->prof_ref);
+    cudaEventRecord(c->prof_ref, c->stream);
+    return LC_OK;
+}
+
+// (start, end) of every profiled launch in ms after the profiling origin
+// (the event recorded by lc_profile_kernel on this context's stream): with
+// several contexts profiled right after a device-wide synchronisation the
+// origins coincide, so the intervals of concurrent launches can be unioned
+extern "C" int lc_profile_intervals(lc_ctx *c, double *out, int64_t cap, int64_t *count) {
+    if (!c || !out || !count) return fail(LC_EINVAL, "null argument");
+    CK(cudaStreamSynchronize(c->stream));
+    int64_t n = 0;
+    for (auto &p : c->prof_events) {
+        if (n >= cap) break;
+        float a = 0.f, b = 0.f;
+        CK(cudaEventElapsedTime(&a, c->prof_ref, p.first));
+        CK(cudaEventElapsedTime(&b, c->prof_ref, p.second));
+        out[2 * n] = a;
+        out[2 * n + 1] = b;
+        ++n;
+    }
+    *count = n;
     return LC_OK;
 }
 
@@ -582,7 +605,7 @@ static void alloc_grid(DevArena &m, GridBufs &g, int H, int W) {
     g.K = m.alloc<int>(1);
     g.cand_cnt = m.alloc<int>(ncx * ncy);
     g.cand_range = m.alloc<int2>(ncx * ncy);
-    g.cand_pts = m.alloc<int>((size_t)ncx * ncy * LC_CAND_PER_CELL);
+    g.cand_pts = m.alloc<int>((size_t)ncx * ncy * LC_CAND_MAX);   // fixed-capacity per-cell lists
     g.cand_blk = m.alloc<int>((size_t)ncx * ncy * 32);
     g.cand_total = m.alloc<int>(1);
     g.cand_u2 = m.alloc<double>(ncx * ncy);
@@ -797,9 +820,7 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
     launch(c, k_contour_fill, dim3(64, S), dim3(256), 0, dj, ncx);
     if (!lists) return;
     launch(c, k_cell_jfa, dim3(S), dim3(1024), sizeof(int) * 2 * ncx * ncy, dj, ncx, ncy);
-    launch(c, k_cand_count, dim3((ncx * ncy + 7) / 8, S), dim3(256), 0, dj, H, W);
-    launch(c, k_cand_scan, dim3(S), dim3(1024), 0, dj, ncx * ncy);
-    launch(c, k_cand_fill, dim3((ncx * ncy + 3) / 4, S), dim3(128), 0, dj, H, W);
+    launch(c, k_cand_build, dim3((ncx * ncy + 3) / 4, S), dim3(128), 0, dj, H, W);
 }
 
 // depth buffer + winning triangle ids (+ mask) of a batch of meshes with

@@ -34,7 +34,7 @@ struct GridJob {
     int *K;                // out: contour pixel count
     int *cand_cnt;         // ncells
     int2 *cand_range;      // ncells
-    int *cand_pts;         // capacity ncells * LC_CAND_PER_CELL: site keys y << 16 | x, lists 16 B aligned
+    int *cand_pts;         // ncells * LC_CAND_MAX: fixed-capacity per-cell lists of site keys y << 16 | x
     int *cand_blk;         // ncells * 32: {start, count, LC_CAND_HEAD keys}
     int *cand_total;       // 1
     double *cand_u2;       // ncells: per-cell bound U^2 (count -> fill)
@@ -49,11 +49,9 @@ __global__ void k_contour_scan_rows(const GridJob *jobs, int H, int ncells);
 __global__ void k_contour_emit(const GridJob *jobs, int H, int W, int ncx);
 __global__ void k_contour_scan_cells(const GridJob *jobs, int ncells);
 __global__ void k_contour_fill(const GridJob *jobs, int ncx);
-__global__ void k_cand_count(const GridJob *jobs, int H, int W);
+__global__ void k_cand_build(const GridJob *jobs, int H, int W);
 __global__ void k_cell_jfa(const GridJob *jobs, int ncx, int ncy);
 __global__ void k_quad_build(const GridJob *jobs, int ncx, int ncy);
-__global__ void k_cand_scan(const GridJob *jobs, int ncells);
-__global__ void k_cand_fill(const GridJob *jobs, int H, int W);
 
 // ----- rasterizer (rasterizer.py:18-120) -----------------------------------
 // Tile-binned rasterizer scratch.  Triangles are set up once (projection,

@@ -26,6 +26,7 @@ struct lc_ctx {
     // optional per-kernel timing: CUDA events around every launch of `prof_name`
     std::string prof_name;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+    cudaEvent_t prof_ref = nullptr;   // recorded when profiling starts (interval origin)
     struct Slot *call_slot = nullptr;          // scratch slot for single-call entry points
     const lc_actor *call_actor = nullptr;
     int call_w = 0, call_h = 0;

@@ -410,141 +410,83 @@ __global__ void k_cell_jfa(const GridJob *jobs, int ncx, int ncy) {
 }
 
 // warp per cell: bound U^2 (warp min), then the candidate count (warp sum)
-__global__ void k_cand_count(const GridJob *jobs, int H, int W) {
-    const GridJob J = jobs[blockIdx.y];
-    const NnGridDev g = grid_of(J, H, W);
-    const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-    for (int c = blockIdx.x * wpb + (threadIdx.x >> 5); c < g.ncx * g.ncy; c += gridDim.x * wpb) {
-        const int cx = c % g.ncx, cy = c / g.ncx;
-        int cnt = 0;
-        double u2 = -1.0;
-        if (g.K > 0) {
-            const CellBox cb = cell_box(cx, cy);
-            const int seed = J.cell_seed[c];
-            // upper bound of the cell's farthest-point nearest distance
-            u2 = seed >= 0 ? cell_far2(cx, cy, g.pts[seed]) : LC_INF;
-            if (u2 > J.max_u2) u2 = -1.0;      // far cell: queries use the quadtree
-            else {
-                quad_walk_warp(g, cb, [&](double n2) { return n2 <= u2; },
-                               [&](int k0, int k1) {
-                                   for (int k = k0 + lane; k < k1; k += 32)
-                                       cnt += cell_near2(cx, cy, g.pts[g.cell_pts[k]]) <= u2;
-                               },
-                               [&]() {});
-                for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-            }
-        }
-        if (lane == 0) {
-            J.cand_cnt[c] = (u2 < 0.0 || cnt > LC_CAND_MAX) ? -1 : cnt;
-            J.cand_u2[c] = u2;
-        }
-    }
-}
-
-__global__ void k_cand_scan(const GridJob *jobs, int ncells) {
-    const GridJob J = jobs[blockIdx.x];
-    // exclusive scan of max(count, 0) into cand_range[].x (count kept in .y)
-    __shared__ int wt[32];
-    __shared__ int carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < ncells; base += blockDim.x) {
-        const int i = base + threadIdx.x;
-        const int raw = i < ncells ? J.cand_cnt[i] : 0;
-        const int v = raw > 0 ? (raw + 3) & ~3 : 0;   // lists start 16 B aligned
-        int s = v;
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, s, o);
-            if (lane >= o) s += t;
-        }
-        if (lane == 31) wt[w] = s;
-        __syncthreads();
-        if (w == 0) {
-            int t = lane < (int)(blockDim.x >> 5) ? wt[lane] : 0;
-            for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_up_sync(0xffffffffu, t, o);
-                if (lane >= o) t += u;
-            }
-            if (lane < (int)(blockDim.x >> 5)) wt[lane] = t;
-        }
-        __syncthreads();
-        const int before = (w > 0 ? wt[w - 1] : 0) + carry;
-        if (i < ncells) {
-            const int start = before + s - v;
-            // lists past the buffer capacity fall back to the ring search
-            const bool fits = start + v <= ncells * LC_CAND_PER_CELL;
-            const int cnt = (raw >= 0 && fits) ? raw : -1;
-            J.cand_range[i] = make_int2(start, cnt);
-            J.cand_blk[32 * (size_t)i] = start;
-            J.cand_blk[32 * (size_t)i + 1] = cnt;
-            J.cell_fill[i] = 0;   // reused as the per-cell append counter by k_cand_fill
-        }
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = before + s;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *J.cand_total = carry;
-}
-
-// Candidate lists are emitted by the quadtree walk, then sorted per cell by
-// (squared distance from the cell's square, site key): a query scans its
-// cell's list in that order and stops at the first entry whose cell
-// distance exceeds its best distance so far (nn_query), so only the head of
-// the list is read.  Sort: warp-local bitonic network in shared memory over
-// 64-bit keys (near2 << 32 | id); lists are capped at LC_CAND_MAX.
-__global__ void __launch_bounds__(128) k_cand_fill(const GridJob *jobs, int H, int W) {
+// Exact per-cell candidate sets from the site-count quadtree, one warp per
+// cell, in a single pass.  U2 bounds the cell's farthest-point nearest
+// distance (via the jump-flooded seed); the candidates are the sites whose
+// squared distance to the cell is <= U2, so any query inside the cell has
+// its nearest site (and every site tied with it) among them.  The warp
+// collects the keys (near2 << 32 | id) in shared memory while walking the
+// quadtree, sorts them (bitonic network) by (distance to the cell, key) and
+// writes the cell's fixed-capacity list (LC_CAND_MAX slots) and its 128 B
+// block {start, count, first LC_CAND_HEAD keys}.  A query scans the list in
+// that order and stops at the first entry farther from the cell than its
+// best distance (nn_query), so only the head is read.  Cells with more than
+// LC_CAND_MAX candidates (or beyond max_u2) keep the quadtree search.
+__global__ void __launch_bounds__(128) k_cand_build(const GridJob *jobs, int H, int W) {
     const GridJob J = jobs[blockIdx.y];
     const NnGridDev g = grid_of(J, H, W);
     const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     __shared__ unsigned long long keys_all[4][LC_CAND_MAX];
     unsigned long long *key = keys_all[threadIdx.x >> 5];
     for (int c = blockIdx.x * wpb + (threadIdx.x >> 5); c < g.ncx * g.ncy; c += gridDim.x * wpb) {
-        const int2 rg = J.cand_range[c];
-        if (rg.y <= 0 || g.K == 0) continue;
         const int cx = c % g.ncx, cy = c / g.ncx;
-        const double u2 = J.cand_u2[c];
+        const int start = c * LC_CAND_MAX;
         int n = 0;
-        quad_walk_warp(g, cell_box(cx, cy), [&](double n2) { return n2 <= u2; },
-                       [&](int k0, int k1) {
-                           for (int k = k0; k < k1; k += 32) {
-                               const int kk = k + lane;
-                               bool take = false;
-                               int pid = 0;
-                               int2 p = make_int2(0, 0);
-                               if (kk < k1) {
-                                   pid = g.cell_pts[kk];
-                                   p = g.pts[pid];
-                                   take = cell_near2(cx, cy, p) <= u2;
+        bool ok = g.K > 0;
+        double u2 = LC_INF;
+        if (ok) {
+            const int seed = J.cell_seed[c];
+            u2 = seed >= 0 ? cell_far2(cx, cy, g.pts[seed]) : LC_INF;
+            ok = u2 <= J.max_u2;
+        }
+        if (ok) {
+            quad_walk_warp(g, cell_box(cx, cy), [&](double n2) { return n2 <= u2; },
+                           [&](int k0, int k1) {
+                               for (int k = k0; k < k1; k += 32) {
+                                   const int kk = k + lane;
+                                   bool take = false;
+                                   int pid = 0;
+                                   int2 p = make_int2(0, 0);
+                                   if (kk < k1) {
+                                       pid = g.cell_pts[kk];
+                                       p = g.pts[pid];
+                                       take = cell_near2(cx, cy, p) <= u2;
+                                   }
+                                   const unsigned bal = __ballot_sync(0xffffffffu, take);
+                                   const int at = n + __popc(bal & ((1u << lane) - 1u));
+                                   if (take && at < LC_CAND_MAX)
+                                       key[at] = ((unsigned long long)cell_near2_int(cx, cy, p) << 32) | (unsigned)pid;
+                                   n += __popc(bal);
                                }
-                               const unsigned bal = __ballot_sync(0xffffffffu, take);
-                               if (take)
-                                   key[n + __popc(bal & ((1u << lane) - 1u))] =
-                                       ((unsigned long long)cell_near2_int(cx, cy, p) << 32) | (unsigned)pid;
-                               n += __popc(bal);
-                           }
-                       },
-                       [&]() {});
-        int P = 1;
-        while (P < n) P <<= 1;
-        for (int i = n + lane; i < P; i += 32) key[i] = ~0ull;
-        __syncwarp();
-        for (int k = 2; k <= P; k <<= 1)
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = lane; i < P; i += 32) {
-                    const int ixj = i ^ j;
-                    if (ixj > i) {
-                        const unsigned long long a = key[i], b = key[ixj];
-                        if ((a > b) == ((i & k) == 0)) { key[i] = b; key[ixj] = a; }
+                           },
+                           [&]() {});
+            ok = n <= LC_CAND_MAX;
+        }
+        if (ok) {
+            int P = 1;
+            while (P < n) P <<= 1;
+            for (int i = n + lane; i < P; i += 32) key[i] = ~0ull;
+            __syncwarp();
+            for (int k = 2; k <= P; k <<= 1)
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    for (int i = lane; i < P; i += 32) {
+                        const int ixj = i ^ j;
+                        if (ixj > i) {
+                            const unsigned long long a = key[i], b = key[ixj];
+                            if ((a > b) == ((i & k) == 0)) { key[i] = b; key[ixj] = a; }
+                        }
                     }
+                    __syncwarp();
                 }
-                __syncwarp();
+            for (int i = lane; i < n; i += 32) {
+                const int k = site_key(g.pts[(int)(unsigned)(key[i] & 0xffffffffu)]);
+                J.cand_pts[start + i] = k;
+                if (i < LC_CAND_HEAD) J.cand_blk[32 * (size_t)c + 2 + i] = k;
             }
-        for (int i = lane; i < n; i += 32) {
-            const int pid = (int)(unsigned)(key[i] & 0xffffffffu);
-            const int k = site_key(g.pts[pid]);
-            J.cand_pts[rg.x + i] = k;
-            if (i < LC_CAND_HEAD) J.cand_blk[32 * (size_t)c + 2 + i] = k;
+        }
+        if (lane == 0) {
+            J.cand_blk[32 * (size_t)c] = start;
+            J.cand_blk[32 * (size_t)c + 1] = ok ? n : -1;
         }
         __syncwarp();
     }

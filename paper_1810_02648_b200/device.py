@@ -491,6 +491,23 @@ class BatchTracker:
         for c in self.ctxs:
             c.profile_kernel(name)
 
+    def profile_busy_ms(self) -> float:
+        """Length of the union of the profiled kernel's launch intervals over
+        all groups (the time the device spent in that kernel, concurrency
+        counted once)."""
+        iv = np.concatenate([c.profile_intervals() for c in self.ctxs]) if self.ctxs else np.zeros((0, 2))
+        if len(iv) == 0:
+            return 0.0
+        iv = iv[np.argsort(iv[:, 0])]
+        busy, cur_s, cur_e = 0.0, iv[0, 0], iv[0, 1]
+        for a, b in iv[1:]:
+            if a > cur_e:
+                busy += cur_e - cur_s
+                cur_s, cur_e = a, b
+            else:
+                cur_e = max(cur_e, b)
+        return float(busy + (cur_e - cur_s))
+
     def profile_read(self):
         ms, n = 0.0, 0
         for c in self.ctxs:
