@@ -218,8 +218,16 @@ static JobRing &ring_of(lc_ctx *c) {
     return *c->ring;
 }
 template <typename T>
-static const T *stage(lc_ctx *c, const std::vector<T> &v) {
-    return static_cast<const T *>(ring_of(c).put(c->stream, v.data(), v.size() * sizeof(T)));
+static JobArg<T> stage(lc_ctx *c, const std::vector<T> &v) {
+    JobArg<T> a{};
+    a.n = (int)v.size();
+    if (v.size() <= LC_JOB_INLINE) {
+        a.ptr = nullptr;
+        for (size_t i = 0; i < v.size(); ++i) a.inl[i] = v[i];
+    } else {
+        a.ptr = static_cast<const T *>(ring_of(c).put(c->stream, v.data(), v.size() * sizeof(T)));
+    }
+    return a;
 }
 // small host array -> existing device buffer, in stream order
 static void stage_to(lc_ctx *c, void *dst, const void *src, size_t bytes) {
@@ -808,7 +816,7 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
         j.cell_seed = p.first->cell_seed;
         jobs.push_back(j);
     }
-    const GridJob *dj = stage(c, jobs);
+    const auto dj = stage(c, jobs);
     const int S = (int)jobs.size();
     const int ncx = (W + LC_GRID_CELL - 1) / LC_GRID_CELL, ncy = (H + LC_GRID_CELL - 1) / LC_GRID_CELL;
     const int rows_grid = std::min(H, 1024);
@@ -827,7 +835,7 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
 // the same triangles (rasterizer.py:18-68): tile-binned single pass
 static void raster_tris(lc_ctx *c, const CamDev &cd, const int *tris, int T, const std::vector<RasterJob> &jobs) {
     if (jobs.empty()) return;
-    const RasterJob *dj = stage(c, jobs);
+    const auto dj = stage(c, jobs);
     const unsigned S = (unsigned)jobs.size();
     const int ntx = (cd.W + LC_RT_TILE - 1) / LC_RT_TILE, nty = (cd.H + LC_RT_TILE - 1) / LC_RT_TILE;
     const int nt = ntx * nty;
@@ -1022,7 +1030,7 @@ static void pyramid(lc_ctx *c, const ConfigDev &cf, const std::vector<PyrTarget>
     for (int l = 0; l < levels; ++l) {
         std::vector<PyrJob> jobs;
         for (const PyrTarget &t : ts) jobs.push_back(PyrJob{t.src, t.tmp, t.dst + (size_t)l * n});
-        const PyrJob *dj = stage(c, jobs);
+        const auto dj = stage(c, jobs);
         launch(c, k_blur_axis, dim3(grid, (unsigned)ts.size()), dim3(256), 0, dj, H, W, 3,
                (const double *)(cf.taps + 32 * l), cf.half[l], 0);
         launch(c, k_blur_axis, dim3(grid, (unsigned)ts.size()), dim3(256), 0, dj, H, W, 3,
@@ -1053,7 +1061,7 @@ struct PrepJob {
     int N;
 };
 
-__global__ void k_prep(const PrepJob *jobs, const SkelDev *skg) {
+__global__ void k_prep(JobArg<PrepJob> jobs, const SkelDev *skg) {
     const PrepJob J = jobs[blockIdx.y];
     const SkelDev &sk = *skg;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 3 * J.N; i += gridDim.x * blockDim.x)
@@ -1097,7 +1105,7 @@ struct FinishJob {
     int N, J;
 };
 
-__global__ void k_finish(const FinishJob *jobs) {
+__global__ void k_finish(JobArg<FinishJob> jobs) {
     const FinishJob F = jobs[blockIdx.y];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < F.N; i += gridDim.x * blockDim.x) {
         const V3 v = ld3(F.v + 3 * (size_t)i);
@@ -1215,7 +1223,7 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
         j.active = 1;
         cj.push_back(j);
     }
-    const ContourJob *dcj = stage(c, cj);
+    const auto dcj = stage(c, cj);
     const unsigned S = (unsigned)ss.size();
     launch(c, k_tri_front, dim3(64, S), dim3(256), 0, dcj, a->dev);
     launch(c, k_sil_edges, dim3(64, S), dim3(256), 0, dcj, a->dev);
@@ -2044,7 +2052,7 @@ extern "C" int lc_contour_vertices(lc_ctx *c, const lc_actor *a, const lc_camera
     ContourJob j{};
     j.verts = s->model; j.zbuf = s->zbuf; j.tri_front = s->tri_front; j.tri_n = s->tri_n; j.vflag = s->vflag;
     j.idx = s->cidx; j.n2d = s->n2d; j.B = s->B; j.vis = nullptr; j.P = nullptr; j.active = 1;
-    const ContourJob *dj = stage(c, std::vector<ContourJob>{j});
+    const auto dj = stage(c, std::vector<ContourJob>{j});
     launch(c, k_tri_front, dim3(64), dim3(256), 0, dj, a->dev);
     launch(c, k_sil_edges, dim3(64), dim3(256), 0, dj, a->dev);
     launch(c, k_contour_compact, dim3(1), dim3(1024), 0, dj, a->dev, cam_dev(*cam));
@@ -2120,7 +2128,7 @@ extern "C" int lc_render(lc_ctx *c, const lc_camera *cam, int32_t n, const doubl
         rj.pid = m.alloc<int>(items * 256);
     }
     raster_tris(c, cd, dt, t, {rj});
-    const RasterJob *dj = stage(c, std::vector<RasterJob>{rj});
+    const auto dj = stage(c, std::vector<RasterJob>{rj});
     launch(c, k_raster_resolve, dim3(592), dim3(256), 0, dj, cd, (const int *)dt, mode, (const double *)da,
            n_attr, (const int *)di, bg_attr, (long long)bg_id, za, ao, io);
     CK(cudaMemcpyAsync(zbuf_out, za, HW * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -2157,7 +2165,7 @@ extern "C" int lc_gaussian_pyramid(lc_ctx *c, int32_t h, int32_t w, int32_t ch, 
             hs[l] = kernel_sizes[l] / 2;
         }
         const int tiles = ((w + LC_PYR_TILE - 1) / LC_PYR_TILE) * ((h + LC_PYR_TILE - 1) / LC_PYR_TILE);
-        const PyrAllJob *dj = stage(c, std::vector<PyrAllJob>{PyrAllJob{src, dst}});
+        const auto dj = stage(c, std::vector<PyrAllJob>{PyrAllJob{src, dst}});
         launch(c, k_pyramid_fused, dim3(tiles), dim3(256), pyramid_fused_smem(), dj, h, w, n_levels,
                (const double *)dt, hs[0], hs[1], hs[2], hs[3]);
         CK(cudaMemcpyAsync(out, dst, n * n_levels * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -2170,7 +2178,7 @@ extern "C" int lc_gaussian_pyramid(lc_ctx *c, int32_t h, int32_t w, int32_t ch, 
         require(k <= 31 || !given_taps, "kernel sizes above 31 need library taps");
         auto taps = given_taps ? std::vector<double>(given_taps + 32 * l, given_taps + 32 * l + k) : gaussian_taps(k);
         double *dt = m.upload(taps.data(), taps.size(), st);
-        const PyrJob *dj = stage(c, std::vector<PyrJob>{PyrJob{src, tmp, dst + n * l}});
+        const auto dj = stage(c, std::vector<PyrJob>{PyrJob{src, tmp, dst + n * l}});
         launch(c, k_blur_axis, dim3(grid), dim3(256), 0, dj, h, w, ch, (const double *)dt, k / 2, 0);
         launch(c, k_blur_axis, dim3(grid), dim3(256), 0, dj, h, w, ch, (const double *)dt, k / 2, 1);
     }

@@ -121,3 +121,16 @@ struct SurfHyperDev {
     double snap_step, snap_band;
     int snap_max_steps;
 };
+
+// Job descriptors of a batched launch, passed by value as a kernel parameter
+// (up to LC_JOB_INLINE streams; larger batches use a device array staged by
+// k_stage).  Parameters live in the constant bank, so no copy engine and no
+// extra launch is needed to get them to the device.
+#define LC_JOB_INLINE 8
+template <typename T>
+struct JobArg {
+    const T *ptr;              // device array (n > LC_JOB_INLINE), else null
+    int n;
+    T inl[LC_JOB_INLINE];
+    __host__ __device__ __forceinline__ const T &operator[](int i) const { return ptr ? ptr[i] : inl[i]; }
+};

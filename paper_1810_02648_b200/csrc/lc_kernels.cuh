@@ -8,7 +8,7 @@ struct PyrJob {
     double *tmp;         // H*W*C
     double *dst;         // H*W*C
 };
-__global__ void k_blur_axis(const PyrJob *jobs, int H, int W, int C, const double *taps, int half,
+__global__ void k_blur_axis(JobArg<PyrJob> jobs, int H, int W, int C, const double *taps, int half,
                             int axis);
 // all levels of an (H,W,3) image from one haloed tile per CTA (levels*H*W*3 out)
 #define LC_PYR_TILE 32
@@ -17,7 +17,7 @@ struct PyrAllJob {
     const double *src;   // H*W*3
     double *dst;         // levels*H*W*3
 };
-__global__ void k_pyramid_fused(const PyrAllJob *jobs, int H, int W, int levels, const double *taps,
+__global__ void k_pyramid_fused(JobArg<PyrAllJob> jobs, int H, int W, int levels, const double *taps,
                                 int h0, int h1, int h2, int h3);
 size_t pyramid_fused_smem();
 
@@ -44,14 +44,14 @@ struct GridJob {
     double max_u2;         // cells whose bound U^2 exceeds this keep the quadtree search
     int *cell_seed;        // ncells: a nearby site per cell (jump flooding), -1 = none
 };
-__global__ void k_contour_rows(const GridJob *jobs, int H, int W);
-__global__ void k_contour_scan_rows(const GridJob *jobs, int H, int ncells);
-__global__ void k_contour_emit(const GridJob *jobs, int H, int W, int ncx);
-__global__ void k_contour_scan_cells(const GridJob *jobs, int ncells);
-__global__ void k_contour_fill(const GridJob *jobs, int ncx);
-__global__ void k_cand_build(const GridJob *jobs, int H, int W);
-__global__ void k_cell_jfa(const GridJob *jobs, int ncx, int ncy);
-__global__ void k_quad_build(const GridJob *jobs, int ncx, int ncy);
+__global__ void k_contour_rows(JobArg<GridJob> jobs, int H, int W);
+__global__ void k_contour_scan_rows(JobArg<GridJob> jobs, int H, int ncells);
+__global__ void k_contour_emit(JobArg<GridJob> jobs, int H, int W, int ncx);
+__global__ void k_contour_scan_cells(JobArg<GridJob> jobs, int ncells);
+__global__ void k_contour_fill(JobArg<GridJob> jobs, int ncx);
+__global__ void k_cand_build(JobArg<GridJob> jobs, int H, int W);
+__global__ void k_cell_jfa(JobArg<GridJob> jobs, int ncx, int ncy);
+__global__ void k_quad_build(JobArg<GridJob> jobs, int ncx, int ncy);
 
 // ----- rasterizer (rasterizer.py:18-120) -----------------------------------
 // Tile-binned rasterizer scratch.  Triangles are set up once (projection,
@@ -81,15 +81,15 @@ struct RasterJob {
     int *pid;                   // items <= 2 ntiles + tcap / LC_RT_CHUNK
 };
 #define LC_RT_CHUNK 256
-__global__ void k_rt_clear(const RasterJob *jobs, int n);
-__global__ void k_rt_setup(const RasterJob *jobs, CamDev cam, const int *tris, int T);
+__global__ void k_rt_clear(JobArg<RasterJob> jobs, int n);
+__global__ void k_rt_setup(JobArg<RasterJob> jobs, CamDev cam, const int *tris, int T);
 template <int FILL>
-__global__ void k_rt_bin(const RasterJob *jobs, int T, int ntx);
-__global__ void k_rt_scan(const RasterJob *jobs, int n, int T);
-__global__ void k_rt_tiles(const RasterJob *jobs, CamDev cam, int T, int ntx, int nt);
-__global__ void k_rt_merge(const RasterJob *jobs, CamDev cam, int ntx, int nt);
-__global__ void k_raster_mask(const RasterJob *jobs, int HW);
-__global__ void k_raster_resolve(const RasterJob *jobs, CamDev cam, const int *tris, int mode,
+__global__ void k_rt_bin(JobArg<RasterJob> jobs, int T, int ntx);
+__global__ void k_rt_scan(JobArg<RasterJob> jobs, int n, int T);
+__global__ void k_rt_tiles(JobArg<RasterJob> jobs, CamDev cam, int T, int ntx, int nt);
+__global__ void k_rt_merge(JobArg<RasterJob> jobs, CamDev cam, int ntx, int nt);
+__global__ void k_raster_mask(JobArg<RasterJob> jobs, int HW);
+__global__ void k_raster_resolve(JobArg<RasterJob> jobs, CamDev cam, const int *tris, int mode,
                                  const double *attrs, int n_attr, const int *ids,
                                  double bg_attr, long long bg_id, double *zout, double *aout,
                                  long long *iout);
@@ -100,7 +100,7 @@ struct FkJob {
     FkState *fk;         // out
     int active;
 };
-__global__ void k_fk(const FkJob *jobs, const SkelDev *sk);
+__global__ void k_fk(JobArg<FkJob> jobs, const SkelDev *sk);
 struct SkinJob {
     const FkState *fk;
     const double *rest;      // M*3 rest points (already gathered for subsets)
@@ -112,7 +112,7 @@ struct SkinJob {
     int M;
     int active;
 };
-__global__ void k_skin(const SkinJob *jobs, ActorDev A);
+__global__ void k_skin(JobArg<SkinJob> jobs, ActorDev A);
 
 // ----- occluding contour + rim filter + part gating -------------------------
 struct ContourJob {
@@ -128,9 +128,9 @@ struct ContourJob {
     int *P;                         // out count
     int active;
 };
-__global__ void k_tri_front(const ContourJob *jobs, ActorDev A);
-__global__ void k_sil_edges(const ContourJob *jobs, ActorDev A);
-__global__ void k_contour_compact(const ContourJob *jobs, ActorDev A, CamDev cam);
+__global__ void k_tri_front(JobArg<ContourJob> jobs, ActorDev A);
+__global__ void k_sil_edges(JobArg<ContourJob> jobs, ActorDev A);
+__global__ void k_contour_compact(JobArg<ContourJob> jobs, ActorDev A, CamDev cam);
 
 // own-silhouette contour pixels bucketed by 16x16 cell (fixed 256 slots per
 // cell, row-major within a cell): all the rim's bounded queries need
@@ -139,7 +139,7 @@ struct OwnCellsJob {
     int *cnt;                  // ncells
     int *keys;                 // ncells*256 site keys y << 16 | x
 };
-__global__ void k_own_cells(const OwnCellsJob *jobs, int H, int W, int ncx);
+__global__ void k_own_cells(JobArg<OwnCellsJob> jobs, int H, int W, int ncx);
 
 struct RimJob {
     const double *verts;       // N*3
@@ -156,7 +156,7 @@ struct RimJob {
     int part_gate;
     int dilation;
 };
-__global__ void k_rim(const RimJob *jobs, ActorDev A, CamDev cam, const double *probe_offs);
+__global__ void k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double *probe_offs);
 
 // ----- surface solve (nonrigid_stage.py:189-500) ---------------------------
 struct SurfJob;

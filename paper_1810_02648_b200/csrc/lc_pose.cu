@@ -394,10 +394,13 @@ __device__ void pose_trials(PoseCtx &c, TrialSmem &ts, int nt, double e[kTrials]
 }  // namespace
 
 template <int CS>
-__global__ void __launch_bounds__(NT, 1) k_pose_solve_t(const PoseJob *jobs, const SkelDev *skg,
+__global__ void __launch_bounds__(NT, 1) k_pose_solve_t(JobArg<PoseJob> jobs, const SkelDev *skg,
                                                         ActorDev A, CamDev cam) {
     using T = Team<CS, NT>;
-    const PoseJob &J = jobs[T::stream()];
+    __shared__ PoseJob sJ;   // this stream's descriptor, parameter bank -> shared memory
+    if (threadIdx.x == 0) sJ = jobs[T::stream()];
+    __syncthreads();
+    const PoseJob &J = sJ;
     if (!J.active) return;
     extern __shared__ __align__(16) unsigned char dsm[];
     PoseSmem &s = *reinterpret_cast<PoseSmem *>(dsm);
@@ -523,10 +526,10 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(const PoseJob *jobs, con
     }
 }
 
-template __global__ void k_pose_solve_t<1>(const PoseJob *, const SkelDev *, ActorDev, CamDev);
-template __global__ void k_pose_solve_t<4>(const PoseJob *, const SkelDev *, ActorDev, CamDev);
-template __global__ void k_pose_solve_t<8>(const PoseJob *, const SkelDev *, ActorDev, CamDev);
-template __global__ void k_pose_solve_t<16>(const PoseJob *, const SkelDev *, ActorDev, CamDev);
+template __global__ void k_pose_solve_t<1>(JobArg<PoseJob>, const SkelDev *, ActorDev, CamDev);
+template __global__ void k_pose_solve_t<4>(JobArg<PoseJob>, const SkelDev *, ActorDev, CamDev);
+template __global__ void k_pose_solve_t<8>(JobArg<PoseJob>, const SkelDev *, ActorDev, CamDev);
+template __global__ void k_pose_solve_t<16>(JobArg<PoseJob>, const SkelDev *, ActorDev, CamDev);
 
 size_t pose_smem_bytes(int n_joints) {
     const size_t head = (sizeof(PoseSmem) + 15) & ~size_t(15);

@@ -62,11 +62,11 @@ struct SurfJob {
 };
 
 template <int CS>
-__global__ void k_pose_solve_t(const PoseJob *jobs, const SkelDev *skg, ActorDev A, CamDev cam);
+__global__ void k_pose_solve_t(JobArg<PoseJob> jobs, const SkelDev *skg, ActorDev A, CamDev cam);
 size_t pose_smem_bytes(int n_joints);
 int pose_block_threads();
 
 template <int CS>
-__global__ void k_surface_solve_t(const SurfJob *jobs, ActorDev A, CamDev cam, EdgeConstDev ec,
+__global__ void k_surface_solve_t(JobArg<SurfJob> jobs, ActorDev A, CamDev cam, EdgeConstDev ec,
                                   SurfHyperDev hp, int H, int W);
 int surface_block_threads();

@@ -10,7 +10,7 @@
 // tap first, then symmetric pairs from the outermost inward -- verified
 // bit-exact against scipy 1.18.1).  imageproc.py:276-285
 
-__global__ void k_blur_axis(const PyrJob *jobs, int H, int W, int C, const double *taps, int half,
+__global__ void k_blur_axis(JobArg<PyrJob> jobs, int H, int W, int C, const double *taps, int half,
                             int axis) {
     const PyrJob J = jobs[blockIdx.y];
     const double *in = axis == 0 ? J.src : J.tmp;
@@ -97,7 +97,7 @@ __device__ __forceinline__ void pyr_level(const double *__restrict__ in, double 
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_pyramid_fused(const PyrAllJob *jobs, int H, int W, int levels,
+__global__ void __launch_bounds__(256) k_pyramid_fused(JobArg<PyrAllJob> jobs, int H, int W, int levels,
                                                        const double *taps, int h0, int h1, int h2, int h3) {
     const PyrAllJob J = jobs[blockIdx.y];
     constexpr int T = LC_PYR_TILE, R = LC_PYR_HALO, E = T + 2 * R;
@@ -153,7 +153,7 @@ __device__ __forceinline__ bool is_contour(const uint8_t *m, int H, int W, int x
 }
 
 // one block per row: row_count[y]
-__global__ void k_contour_rows(const GridJob *jobs, int H, int W) {
+__global__ void k_contour_rows(JobArg<GridJob> jobs, int H, int W) {
     const GridJob J = jobs[blockIdx.y];
     __shared__ int cnt;
     for (int y = blockIdx.x; y < H; y += gridDim.x) {
@@ -205,7 +205,7 @@ __device__ int block_exclusive_scan(const int *in, int *out, int n) {
     return carry;
 }
 
-__global__ void k_contour_scan_rows(const GridJob *jobs, int H, int ncells) {
+__global__ void k_contour_scan_rows(JobArg<GridJob> jobs, int H, int ncells) {
     const GridJob J = jobs[blockIdx.x];
     const int total = block_exclusive_scan<1024>(J.row_count, J.row_start, H);
     if (threadIdx.x == 0) {
@@ -219,7 +219,7 @@ __global__ void k_contour_scan_rows(const GridJob *jobs, int H, int ncells) {
 }
 
 // one block per row: ordered emission of (x, y) + per-cell counts
-__global__ void k_contour_emit(const GridJob *jobs, int H, int W, int ncx) {
+__global__ void k_contour_emit(JobArg<GridJob> jobs, int H, int W, int ncx) {
     const GridJob J = jobs[blockIdx.y];
     __shared__ int wsum[32];
     __shared__ int carry;
@@ -251,13 +251,13 @@ __global__ void k_contour_emit(const GridJob *jobs, int H, int W, int ncx) {
     }
 }
 
-__global__ void k_contour_scan_cells(const GridJob *jobs, int ncells) {
+__global__ void k_contour_scan_cells(JobArg<GridJob> jobs, int ncells) {
     const GridJob J = jobs[blockIdx.x];
     const int total = block_exclusive_scan<1024>(J.cell_count, J.cell_start, ncells);
     if (threadIdx.x == 0) J.cell_start[ncells] = total;
 }
 
-__global__ void k_contour_fill(const GridJob *jobs, int ncx) {
+__global__ void k_contour_fill(JobArg<GridJob> jobs, int ncx) {
     const GridJob J = jobs[blockIdx.y];
     const int K = *J.K;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
@@ -269,7 +269,7 @@ __global__ void k_contour_fill(const GridJob *jobs, int ncx) {
 }
 
 // ---- site-count quadtree over the cells (one CTA per stream) -------------
-__global__ void k_quad_build(const GridJob *jobs, int ncx, int ncy) {
+__global__ void k_quad_build(JobArg<GridJob> jobs, int ncx, int ncy) {
     const GridJob J = jobs[blockIdx.x];
     const int P = J.qP;
     for (int i = threadIdx.x; i < P * P; i += blockDim.x) {
@@ -366,7 +366,7 @@ __device__ __forceinline__ CellBox cell_box(int cx, int cy) {
 // site near its centre.  Only used as an upper bound for the candidate band
 // (any real site bounds the nearest distance), so JFA's rare misses cost
 // list length, never exactness.
-__global__ void k_cell_jfa(const GridJob *jobs, int ncx, int ncy) {
+__global__ void k_cell_jfa(JobArg<GridJob> jobs, int ncx, int ncy) {
     const GridJob J = jobs[blockIdx.x];
     extern __shared__ int seeds[];   // 2 * ncells ping-pong
     const int nc = ncx * ncy;
@@ -422,7 +422,7 @@ __global__ void k_cell_jfa(const GridJob *jobs, int ncx, int ncy) {
 // that order and stops at the first entry farther from the cell than its
 // best distance (nn_query), so only the head is read.  Cells with more than
 // LC_CAND_MAX candidates (or beyond max_u2) keep the quadtree search.
-__global__ void __launch_bounds__(128) k_cand_build(const GridJob *jobs, int H, int W) {
+__global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H, int W) {
     const GridJob J = jobs[blockIdx.y];
     const NnGridDev g = grid_of(J, H, W);
     const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
@@ -546,12 +546,12 @@ __device__ __forceinline__ bool bary(const double P[3][2], double inv, int ix, i
 // second pass, coalesced stores.  A tile whose list overflowed the buffer
 // tests every triangle (still exact).
 
-__global__ void k_rt_clear(const RasterJob *jobs, int n) {
+__global__ void k_rt_clear(JobArg<RasterJob> jobs, int n) {
     const RasterJob J = jobs[blockIdx.y];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) J.tcount[i] = 0;
 }
 
-__global__ void k_rt_setup(const RasterJob *jobs, CamDev cam, const int *tris, int T) {
+__global__ void k_rt_setup(JobArg<RasterJob> jobs, CamDev cam, const int *tris, int T) {
     const RasterJob J = jobs[blockIdx.y];
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= T) return;
@@ -609,7 +609,7 @@ __device__ __forceinline__ bool rt_tile_hit(const TriRec &r, const int4 bb, RtCu
 
 // one warp per triangle over the tiles of its bbox: count (fill = 0) or append (fill = 1)
 template <int FILL>
-__global__ void k_rt_bin(const RasterJob *jobs, int T, int ntx) {
+__global__ void k_rt_bin(JobArg<RasterJob> jobs, int T, int ntx) {
     const RasterJob J = jobs[blockIdx.y];
     const int lane = threadIdx.x & 31;
     const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -633,8 +633,8 @@ __global__ void k_rt_bin(const RasterJob *jobs, int T, int ntx) {
         }
     }
 }
-template __global__ void k_rt_bin<0>(const RasterJob *, int, int);
-template __global__ void k_rt_bin<1>(const RasterJob *, int, int);
+template __global__ void k_rt_bin<0>(JobArg<RasterJob>, int, int);
+template __global__ void k_rt_bin<1>(JobArg<RasterJob>, int, int);
 
 // block-wide exclusive scan of v(i), i < n, into out[i] (out[n] = total)
 template <typename V>
@@ -681,7 +681,7 @@ __device__ void rt_block_scan(int n, V &&v, int *out, int *zero = nullptr) {
 // separate CTAs (merged by k_rt_merge) so a tile that collects thousands of
 // triangles (a collapsed, far-away surface) is still resolved in parallel.
 // A tile whose list overflowed the buffer resolves every triangle in one CTA.
-__global__ void k_rt_scan(const RasterJob *jobs, int n, int T) {
+__global__ void k_rt_scan(JobArg<RasterJob> jobs, int n, int T) {
     const RasterJob J = jobs[blockIdx.x];
     rt_block_scan(n, [&](int i) { return J.tcount[i]; }, J.toff, J.tfill);
     rt_block_scan(n, [&](int i) {
@@ -710,7 +710,7 @@ __device__ __forceinline__ void rt_write(const RasterJob &J, CamDev cam, int x, 
 }
 
 // work items (tile, chunk), grid-strided; thread = pixel of the tile
-__global__ void __launch_bounds__(256) k_rt_tiles(const RasterJob *jobs, CamDev cam, int T, int ntx, int nt) {
+__global__ void __launch_bounds__(256) k_rt_tiles(JobArg<RasterJob> jobs, CamDev cam, int T, int ntx, int nt) {
     const RasterJob J = jobs[blockIdx.y];
     constexpr int CH = 64;
     __shared__ TriRec sr[CH];
@@ -753,7 +753,7 @@ __global__ void __launch_bounds__(256) k_rt_tiles(const RasterJob *jobs, CamDev 
 }
 
 // lexicographic (depth, id) minimum over the chunks of multi-chunk tiles
-__global__ void __launch_bounds__(256) k_rt_merge(const RasterJob *jobs, CamDev cam, int ntx, int nt) {
+__global__ void __launch_bounds__(256) k_rt_merge(JobArg<RasterJob> jobs, CamDev cam, int ntx, int nt) {
     const RasterJob J = jobs[blockIdx.y];
     for (int tile = blockIdx.x; tile < nt; tile += gridDim.x) {
         const int i0 = J.ioff[tile], i1 = J.ioff[tile + 1];
@@ -771,7 +771,7 @@ __global__ void __launch_bounds__(256) k_rt_merge(const RasterJob *jobs, CamDev 
     }
 }
 
-__global__ void k_raster_mask(const RasterJob *jobs, int HW) {
+__global__ void k_raster_mask(JobArg<RasterJob> jobs, int HW) {
     const RasterJob J = jobs[blockIdx.y];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += gridDim.x * blockDim.x)
         J.mask[i] = J.zbuf[i] != 0x7ff0000000000000ULL;
@@ -784,7 +784,7 @@ __device__ __forceinline__ int id_pick(double l0, double l1, double l2) {
     return 2;
 }
 
-__global__ void k_raster_resolve(const RasterJob *jobs, CamDev cam, const int *tris, int mode,
+__global__ void k_raster_resolve(JobArg<RasterJob> jobs, CamDev cam, const int *tris, int mode,
                                  const double *attrs, int n_attr, const int *ids, double bg_attr,
                                  long long bg_id, double *zout, double *aout, long long *iout) {
     const RasterJob J = jobs[blockIdx.y];
@@ -821,7 +821,7 @@ __global__ void k_raster_resolve(const RasterJob *jobs, CamDev cam, const int *t
 // ===========================================================================
 // kinematics / skinning
 
-__global__ void k_fk(const FkJob *jobs, const SkelDev *sk) {
+__global__ void k_fk(JobArg<FkJob> jobs, const SkelDev *sk) {
     const FkJob J = jobs[blockIdx.x];
     if (!J.active) return;
     __shared__ FkState f;
@@ -838,7 +838,7 @@ struct GlobalDq {
     __device__ __forceinline__ double operator()(int j, int k) const { return f->dq[j][k]; }
 };
 
-__global__ void k_skin(const SkinJob *jobs, ActorDev A) {
+__global__ void k_skin(JobArg<SkinJob> jobs, ActorDev A) {
     const SkinJob J = jobs[blockIdx.y];
     if (!J.active) return;
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
@@ -860,7 +860,7 @@ __global__ void k_skin(const SkinJob *jobs, ActorDev A) {
 // ===========================================================================
 // occluding contour vertices (extract_contour_vertices, pose_stage.py:151-191)
 
-__global__ void k_tri_front(const ContourJob *jobs, ActorDev A) {
+__global__ void k_tri_front(JobArg<ContourJob> jobs, ActorDev A) {
     const ContourJob J = jobs[blockIdx.y];
     if (!J.active) return;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < A.T; t += gridDim.x * blockDim.x) {
@@ -877,7 +877,7 @@ __global__ void k_tri_front(const ContourJob *jobs, ActorDev A) {
         J.vflag[v] = 0;
 }
 
-__global__ void k_sil_edges(const ContourJob *jobs, ActorDev A) {
+__global__ void k_sil_edges(JobArg<ContourJob> jobs, ActorDev A) {
     const ContourJob J = jobs[blockIdx.y];
     if (!J.active) return;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < A.E; e += gridDim.x * blockDim.x) {
@@ -905,7 +905,7 @@ __device__ __forceinline__ bool depth_visible(CamDev cam, const unsigned long lo
 // one CTA per stream: ordered compaction of contour candidates (np.unique
 // order = ascending vertex id) and, optionally, of visible vertices; then the
 // image-plane normals of the contour vertices.
-__global__ void __launch_bounds__(1024) k_contour_compact(const ContourJob *jobs, ActorDev A,
+__global__ void __launch_bounds__(1024) k_contour_compact(JobArg<ContourJob> jobs, ActorDev A,
                                                           CamDev cam) {
     const ContourJob J = jobs[blockIdx.x];
     if (!J.active) return;
@@ -988,7 +988,7 @@ __device__ __forceinline__ int part_at(const ActorDev &A, CamDev cam, const doub
 // One CTA per 16x16 cell: the cell's contour pixels of the own mask
 // (foreground with a background 4-neighbour, the image border counting as
 // background; imageproc.py:34-49), compacted in row-major order.
-__global__ void __launch_bounds__(256) k_own_cells(const OwnCellsJob *jobs, int H, int W, int ncx) {
+__global__ void __launch_bounds__(256) k_own_cells(JobArg<OwnCellsJob> jobs, int H, int W, int ncx) {
     const OwnCellsJob J = jobs[blockIdx.y];
     const int c = blockIdx.x;
     const int x = (c % ncx) * LC_GRID_CELL + (threadIdx.x & (LC_GRID_CELL - 1));
@@ -1036,7 +1036,7 @@ __device__ inline double own_within2(const NnGridDev &g, const int *cnt, const i
     return best <= R * R ? best : LC_INF;
 }
 
-__global__ void k_rim(const RimJob *jobs, ActorDev A, CamDev cam, const double *probe_offs) {
+__global__ void k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double *probe_offs) {
     const RimJob J = jobs[blockIdx.y];
     if (!J.active) return;
     const int B = *J.B;

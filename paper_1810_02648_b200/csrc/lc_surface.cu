@@ -730,11 +730,15 @@ __device__ __forceinline__ void stamp(const SurfJob &J, int &k) {
 }  // namespace
 
 template <int CS>
-__global__ void __launch_bounds__(NT, 1) k_surface_solve_t(const SurfJob *jobs, ActorDev A, CamDev cam,
+__global__ void __launch_bounds__(NT, 1) k_surface_solve_t(JobArg<SurfJob> jobs, ActorDev A, CamDev cam,
                                                            EdgeConstDev ec, SurfHyperDev hp, int H,
                                                            int W) {
     using T = Team<CS, NT>;
-    const SurfJob &J = jobs[T::stream()];
+    // this stream's descriptor, from the parameter bank into shared memory
+    __shared__ SurfJob sJ;
+    if (threadIdx.x == 0) sJ = jobs[T::stream()];
+    __syncthreads();
+    const SurfJob &J = sJ;
     if (!J.active) return;
     __shared__ double red[T::red_doubles];
     T::init_red(red);
@@ -847,10 +851,10 @@ __global__ void __launch_bounds__(NT, 1) k_surface_solve_t(const SurfJob *jobs, 
     stamp<T>(J, ph);
 }
 
-template __global__ void k_surface_solve_t<1>(const SurfJob *, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
-template __global__ void k_surface_solve_t<4>(const SurfJob *, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
-template __global__ void k_surface_solve_t<8>(const SurfJob *, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
-template __global__ void k_surface_solve_t<16>(const SurfJob *, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
+template __global__ void k_surface_solve_t<1>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
+template __global__ void k_surface_solve_t<4>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
+template __global__ void k_surface_solve_t<8>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
+template __global__ void k_surface_solve_t<16>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
 
 int surface_block_threads() { return NT; }
 
