@@ -123,6 +123,14 @@ static void launch_cluster(const char *name, lc_ctx *c, void (*kernel)(KArgs...)
     }
 }
 
+// per-solver override (LIVECAP_POSE_CLUSTER / LIVECAP_SURFACE_CLUSTER), else LIVECAP_CLUSTER
+static int cluster_size_for(const char *var) {
+    const char *v = getenv(var);
+    if (!v) return -1;
+    const int x = atoi(v);
+    return (x == 1 || x == 4 || x == 8 || x == 16) ? x : -1;
+}
+
 static int cluster_size() {
     static int cs = [] {
         const char *v = getenv("LIVECAP_CLUSTER");
@@ -1249,7 +1257,8 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
 
 static void pose_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, const std::vector<PoseJob> &jobs) {
     const size_t smem = pose_smem_bytes(a->skel.J);
-    const int cs = cluster_size();
+    static const int cs_env = cluster_size_for("LIVECAP_POSE_CLUSTER");
+    const int cs = cs_env > 0 ? cs_env : cluster_size();
     auto k = cs == 1 ? k_pose_solve_t<1> : cs == 4 ? k_pose_solve_t<4> : cs == 8 ? k_pose_solve_t<8>
                                                                            : k_pose_solve_t<16>;
     launch_cluster("k_pose_solve", c, k, (int)jobs.size(), cs, dim3(pose_block_threads()), smem,
@@ -1258,7 +1267,11 @@ static void pose_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, cons
 
 static void surface_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, const ConfigDev &cf,
                            const std::vector<SurfJob> &jobs) {
-    const int cs = cluster_size();
+    // the surface solver's phases (edges, vertices, rows) spread over 16 CTAs
+    // (non-portable cluster) run measurably faster than over 8 on B200
+    static const int cs_env = cluster_size_for("LIVECAP_SURFACE_CLUSTER");
+    static const int cs_def = getenv("LIVECAP_CLUSTER") ? cluster_size() : 16;
+    const int cs = cs_env > 0 ? cs_env : cs_def;
     auto k = cs == 1 ? k_surface_solve_t<1> : cs == 4 ? k_surface_solve_t<4>
              : cs == 8 ? k_surface_solve_t<8> : k_surface_solve_t<16>;
     launch_cluster("k_surface_solve", c, k, (int)jobs.size(), cs, dim3(surface_block_threads()), 0,
