@@ -192,11 +192,20 @@ def run_ours(args):
     import torch
 
     rank, world, local = dist_env()
+    # one process per GPU over NCCL.  BENCH_DIST_BACKEND=gloo exercises the
+    # multi-rank path on fewer GPUs (ranks share devices round-robin)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(torch.cuda.device_count(), 1)
     os.environ["LIVECAP_DEVICE"] = str(local)
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    coll_dev = f"cuda:{local}" if backend == "nccl" else "cpu"
     from paper_1810_02648_b200 import _lib
     from paper_1810_02648_b200 import synthetic as S
     from paper_1810_02648_b200.camera import suggest_camera
@@ -240,7 +249,7 @@ def run_ours(args):
         if world == 1:
             return x
         import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -357,7 +366,7 @@ def run_ours(args):
     if world > 1:
         from paper_1810_02648_b200.sharding import gather_results
         last = (W + K - 1) & 1
-        g = gather_results(x_h[last][:, None].to(f"cuda:{local}"), v_h[last][:, None].to(f"cuda:{local}"),
+        g = gather_results(x_h[last][:, None].to(coll_dev), v_h[last][:, None].to(coll_dev),
                            world * Sn, "block")
         if rank == 0:
             gathered = int(g[0].shape[0])
