@@ -311,6 +311,17 @@ def run_ours(args):
     achieved_agg = alg / (k_busy_ms / 1e3) / 1e9 if k_busy_ms > 0 else 0.0
     traffic = read_traffic()
     pcg_iters = sum(int((c1[s] - c0[s])[2]) for s in range(Sn))
+    # µs per PCG iteration (the metric's second quantity): the PCG phases of
+    # the last timed frame of every stream, from the solver's device
+    # timestamps (%globaltimer; the groups run concurrently)
+    pcg_us = []
+    for s_ in range(Sn):
+        _, sp = tr.phase_times(s_)
+        for it in range(cfg.nonrigid.gn_iterations):
+            a, b = sp[1 + 3 * it], sp[2 + 3 * it]
+            if b > a > 0:
+                pcg_us.append((b - a) / 1e3 / cfg.nonrigid.pcg_iterations)
+    pcg_iter_us = float(np.median(pcg_us)) if pcg_us else None
     tr.close()
 
     # ---- e2e: public API from pinned host buffers.  Frames are queued one
@@ -405,6 +416,9 @@ def run_ours(args):
                          "peak_source": peak_src,
                          "traffic_source": (traffic or {}).get("source")},
             "pcg_iterations_timed": pcg_iters,
+            "pcg_iter_us": pcg_iter_us,
+            "pcg_iter_us_note": "median over the last timed frame's GN steps of every stream of "
+                                "(PCG phase incl. setup) / iterations, device timestamps",
             "gathered_streams": gathered,
             "per_stream_fps": 1e3 * K / ms_max,
             "clocks": clk,

@@ -619,12 +619,8 @@ static void alloc_grid(DevArena &m, GridBufs &g, int H, int W) {
     g.pts = m.alloc<int2>((size_t)H * W);
     g.cell_pts = m.alloc<int>((size_t)H * W);
     g.K = m.alloc<int>(1);
-    g.cand_cnt = m.alloc<int>(ncx * ncy);
-    g.cand_range = m.alloc<int2>(ncx * ncy);
     g.cand_pts = m.alloc<int>((size_t)ncx * ncy * LC_CAND_MAX);   // fixed-capacity per-cell lists
     g.cand_blk = m.alloc<int>((size_t)ncx * ncy * 32);
-    g.cand_total = m.alloc<int>(1);
-    g.cand_u2 = m.alloc<double>(ncx * ncy);
     g.cell_seed = m.alloc<int>(ncx * ncy);
     g.qP = 1;
     g.qL = 0;
@@ -641,8 +637,7 @@ void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) 
     mask_src = mask;
     pyr = mem.alloc<double>(HW * 3 * std::max(levels, 1));
     blur_tmp = mem.alloc<double>(HW * 3);
-    alloc_grid(mem, obs, H, W);
-    alloc_grid(mem, own, H, W);
+    alloc_grid(mem, obs, H, W);   // (the own silhouette uses cell buckets, own_cnt / own_keys)
     own_mask = mem.alloc<uint8_t>(HW);
     {
         const size_t nc = (size_t)((W + LC_GRID_CELL - 1) / LC_GRID_CELL) * ((H + LC_GRID_CELL - 1) / LC_GRID_CELL);
@@ -782,7 +777,6 @@ static NnGridDev grid_dev(const GridBufs &g, const uint8_t *mask, int H, int W) 
     d.cell_start = g.cell_start;
     d.cell_pts = g.cell_pts;
     d.mask = mask;
-    d.cand_range = g.cand_range;
     d.cand_pts = g.cand_pts;
     d.cand_blk = g.cand_blk;
     d.quad = g.quad;
@@ -791,13 +785,10 @@ static NnGridDev grid_dev(const GridBufs &g, const uint8_t *mask, int H, int W) 
     return d;
 }
 
-// contour pixels + grid for a batch of masks
-// candidate lists only for cells within `max_ring` cell rings of a contour
-// pixel; farther queries take the exact quadtree search
 // Candidate lists are built for cells whose bound U (the farthest point of
-// the cell to a nearby site) is at most this many pixels; queries in farther
-// cells take the exact quadtree search.  Far cells have long lists and are
-// rarely queried, so listing them costs more build time than it saves.
+// the cell to a nearby site) is at most this many pixels (default: all);
+// queries in farther cells take the exact quadtree search, which on B200 is
+// slower than scanning even long lists, so every cell is listed.
 static double obs_list_radius() {
     static double r = [] {
         const char *v = getenv("LIVECAP_LIST_RADIUS");
@@ -806,6 +797,7 @@ static double obs_list_radius() {
     return r;
 }
 
+// contour pixels + NN grid (+ candidate lists) for a batch of masks
 static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *, const uint8_t *>> &gs,
                         int H, int W, double max_u = 1e30, bool lists = true) {
     if (gs.empty()) return;
@@ -816,10 +808,9 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
         j.row_count = p.first->row_count; j.row_start = p.first->row_start;
         j.pts = p.first->pts; j.cell_count = p.first->cell_count; j.cell_start = p.first->cell_start;
         j.cell_fill = p.first->cell_fill; j.cell_pts = p.first->cell_pts; j.K = p.first->K;
-        j.cand_cnt = p.first->cand_cnt; j.cand_range = p.first->cand_range;
-        j.cand_pts = p.first->cand_pts; j.cand_total = p.first->cand_total;
+        j.cand_pts = p.first->cand_pts;
         j.cand_blk = p.first->cand_blk;
-        j.cand_u2 = p.first->cand_u2; j.max_ring = 0; j.max_u2 = max_u * max_u;
+        j.max_u2 = max_u * max_u;
         j.quad = p.first->quad; j.qP = p.first->qP; j.qL = p.first->qL;
         j.cell_seed = p.first->cell_seed;
         jobs.push_back(j);

@@ -79,9 +79,7 @@ struct NnGridDev {
     const int *cell_start; // ncx*ncy+1
     const int *cell_pts;   // point ids grouped by cell
     const uint8_t *mask;   // H*W, for inside()
-    // exact per-cell candidate lists (null -> ring search): cand_range[c] =
-    // (start, count); count < 0 marks an overflowed cell (ring search there)
-    const int2 *cand_range; // ncx*ncy
+    // exact per-cell candidate lists (fixed capacity LC_CAND_MAX per cell)
     const int *cand_pts;    // per-cell lists of site keys y << 16 | x (16 B aligned)
     // per-cell 128 B blocks: {list start, list count, first LC_CAND_HEAD keys}
     // so a query gets its cell's range and the head of its list in one line
@@ -96,7 +94,6 @@ __host__ __device__ __forceinline__ int quad_off(int P, int l) {
     for (int k = 0; k < l; ++k) o += (P >> k) * (P >> k);
     return o;
 }
-#define LC_CAND_PER_CELL 384   // average candidate capacity per cell
 #define LC_CAND_MAX 1024       // per-cell cap before falling back to the ring search
 #define LC_CAND_HEAD 30        // keys stored inline in each cell's 128 B block
 

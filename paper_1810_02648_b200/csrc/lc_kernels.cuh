@@ -32,15 +32,10 @@ struct GridJob {
     int *cell_fill;        // ncx*ncy
     int *cell_pts;         // capacity H*W
     int *K;                // out: contour pixel count
-    int *cand_cnt;         // ncells
-    int2 *cand_range;      // ncells
     int *cand_pts;         // ncells * LC_CAND_MAX: fixed-capacity per-cell lists of site keys y << 16 | x
     int *cand_blk;         // ncells * 32: {start, count, LC_CAND_HEAD keys}
-    int *cand_total;       // 1
-    double *cand_u2;       // ncells: per-cell bound U^2 (count -> fill)
     int *quad;             // site-count quadtree (see NnGridDev)
     int qP, qL;
-    int max_ring;          // unused (ring-search builder)
     double max_u2;         // cells whose bound U^2 exceeds this keep the quadtree search
     int *cell_seed;        // ncells: a nearby site per cell (jump flooding), -1 = none
 };
@@ -88,7 +83,6 @@ __global__ void k_rt_bin(JobArg<RasterJob> jobs, int T, int ntx);
 __global__ void k_rt_scan(JobArg<RasterJob> jobs, int n, int T);
 __global__ void k_rt_tiles(JobArg<RasterJob> jobs, CamDev cam, int T, int ntx, int nt);
 __global__ void k_rt_merge(JobArg<RasterJob> jobs, CamDev cam, int ntx, int nt);
-__global__ void k_raster_mask(JobArg<RasterJob> jobs, int HW);
 __global__ void k_raster_resolve(JobArg<RasterJob> jobs, CamDev cam, const int *tris, int mode,
                                  const double *attrs, int n_attr, const int *ids,
                                  double bg_attr, long long bg_id, double *zout, double *aout,

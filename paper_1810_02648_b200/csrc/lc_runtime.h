@@ -72,11 +72,8 @@ struct lc_actor {
 struct GridBufs {
     int *row_count, *row_start, *cell_count, *cell_start, *cell_fill, *cell_pts, *K;
     int2 *pts;
-    int *cand_cnt, *cand_total;
     int *cand_pts;
     int *cand_blk;
-    int2 *cand_range;
-    double *cand_u2;
     int *cell_seed;
     int *quad;
     int qP, qL;

@@ -771,11 +771,6 @@ __global__ void __launch_bounds__(256) k_rt_merge(JobArg<RasterJob> jobs, CamDev
     }
 }
 
-__global__ void k_raster_mask(JobArg<RasterJob> jobs, int HW) {
-    const RasterJob J = jobs[blockIdx.y];
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += gridDim.x * blockDim.x)
-        J.mask[i] = J.zbuf[i] != 0x7ff0000000000000ULL;
-}
 
 // attributes / ids of the winning triangle (mode 1 / 2, rasterizer.py:58-68)
 __device__ __forceinline__ int id_pick(double l0, double l1, double l2) {

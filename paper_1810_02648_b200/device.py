@@ -342,6 +342,15 @@ class Tracker:
             out[key] = buf
         return out
 
+    def phase_times(self, stream: int):
+        """Device timestamps (ns, %globaltimer) of the last frame's solver
+        phases: pose [start, per GN: eval, solve, line search], surface
+        [start, per GN: assembly, PCG, line search, ..., snap]."""
+        p = np.zeros(64, dtype=np.int64)
+        q = np.zeros(64, dtype=np.int64)
+        L.check(self.ctx.lib.lc_tracker_phase_times(self.handle, stream, L.ptr(p), L.ptr(q)))
+        return p, q
+
     def counters(self, stream: int) -> np.ndarray:
         out = np.zeros(8, dtype=np.int64)
         L.check(self.ctx.lib.lc_tracker_counters(self.handle, stream, L.ptr(out)))
@@ -479,6 +488,10 @@ class BatchTracker:
     def counters(self, stream):
         g, s = self._where(stream)
         return self.trackers[g].counters(s)
+
+    def phase_times(self, stream):
+        g, s = self._where(stream)
+        return self.trackers[g].phase_times(s)
 
     def synchronize(self):
         for c in self.ctxs:
