@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--groups", type=int, default=4,
                     help="stream groups stepped concurrently on their own CUDA streams (BatchTracker)")
     ap.add_argument("--preset", default="x5k")
+    ap.add_argument("--gn", type=int, default=None, help="non-rigid GN iterations (cfg4: 4)")
+    ap.add_argument("--pcg", type=int, default=None, help="PCG iterations per GN step (cfg4: 8)")
     ap.add_argument("--res", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-frames", type=int, default=3, help="timed steady frames of the CPU baseline")
@@ -78,6 +80,7 @@ def workload(args, world):
                         f"{args.res}x{args.res}, {args.streams} synthetic streams per GPU (cfg5 sharding)",
             "preset": args.preset, "resolution": args.res, "streams_per_gpu": args.streams,
             "stream_groups": args.groups,
+            "nonrigid_gn_pcg": [args.gn or 3, args.pcg or 4],
             "total_streams": args.streams * world, "parallelism": f"stream-sharded x{world}",
             "l2": "per-step inputs (images + pyramids) exceed the 126 MB L2; no flush needed"}
 
@@ -239,6 +242,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     dets = [[frames[s][f].detections for f in range(F)] for s in range(Sn)]
     cfg = SequenceConfig()
+    if args.gn is not None:
+        cfg.nonrigid.gn_iterations = args.gn
+    if args.pcg is not None:
+        cfg.nonrigid.pcg_iterations = args.pcg
 
     def barrier():
         if world > 1:
@@ -390,7 +397,7 @@ def run_ours(args):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(actor, cam, frames[0], args.cpu_frames)
+            cpu = cpu_baseline(actor, cam, frames[0], args.cpu_frames, cfg)
         out = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
@@ -436,12 +443,10 @@ def run_ours(args):
 # CPU baseline: the oracle (a restatement of the reference, bit-identical to
 # it) timed on one host core on a bounded sample of the same workload
 
-def cpu_baseline(actor, cam, frames, n_timed):
+def cpu_baseline(actor, cam, frames, n_timed, cfg):
     from threadpoolctl import threadpool_limits
 
     from oracle import frame as OF
-    from paper_1810_02648_b200.config import SequenceConfig
-    cfg = SequenceConfig()
     with threadpool_limits(1):
         st = OF.State()
         # untimed cold start (frame 0), then n_timed steady frames end to end
@@ -464,7 +469,7 @@ def cpu_baseline(actor, cam, frames, n_timed):
 # cores, one process per stream
 
 def _ref_worker(a):
-    preset, res, n_frames, seed, warm = a
+    preset, res, n_frames, seed, warm, gn, pcg = a
     os.environ["OMP_NUM_THREADS"] = "1"
     from threadpoolctl import threadpool_limits
 
@@ -483,6 +488,10 @@ def _ref_worker(a):
     cam = suggest_camera(res, res)
     frames = make_stream_frames(actor, cam, n_frames, seed, OI.render_attributes, posing)
     cfg = SequenceConfig()
+    if gn is not None:
+        cfg.nonrigid.gn_iterations = gn
+    if pcg is not None:
+        cfg.nonrigid.pcg_iterations = pcg
     st = OF.State()
     stamps = []
     with threadpool_limits(1):
@@ -502,7 +511,7 @@ def run_reference(args):
     procs = max(1, min(args.streams, cores))
     W = max(1, args.warmup)
     K = max(1, args.steps)
-    jobs = [(args.preset, args.res, W + K, s, W) for s in range(procs)]
+    jobs = [(args.preset, args.res, W + K, s, W, args.gn, args.pcg) for s in range(procs)]
     with mp.get_context("fork").Pool(procs) as pool:
         res = pool.map(_ref_worker, jobs)
     spans = [b - a for a, b, _ in res]
