@@ -29,7 +29,7 @@ def summarize(rep):
     hdr = rows[0]
     units = dict(zip(hdr, rows[1]))
     scale = {"byte": 1.0, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0,
-             "msecond": 1e3, "second": 1e6}
+             "msecond": 1e3, "second": 1e6, "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}
     res = []
     for r in rows[2:]:
         d = dict(zip(hdr, r))
