@@ -28,6 +28,10 @@ struct PoseSmem {
     double red[Team<1, NT>::red_doubles];
     double pix[LC_MAXJ + 4][2];
     int okz[LC_MAXJ + 4];
+    // nonzero DQ Jacobian columns per joint: 0..5 (root) + 6+k for the DOFs k
+    // that move the joint's frame (skinning.py:269-300)
+    unsigned char jcol[LC_MAXJ][LC_NP];
+    int jcnt[LC_MAXJ];
 };
 
 // one evaluation point: FK state, parameters and joint/marker projections
@@ -135,9 +139,14 @@ __device__ double pose_row(const PoseCtx &c, const PoseView &pv, int r, double *
             const double sign = J.directional ? side_sign(c.obs, nn, px, py, J.n2d[2 * b], J.n2d[2 * b + 1]) : 1.0;
             const double sc = ws * sign;
             for (int q = 0; q < LC_NP; ++q) jr[q] = 0.0;
+            // only the parameters that move the joint's frame have nonzero DQ
+            // Jacobian columns (root rotation / translation and the DOFs of
+            // its ancestors and itself, s.jcol): the other columns stay 0
             if (Bl.degenerate) {
                 const double *t = c.dqj + (size_t)Bl.dom * 8 * LC_NP;
-                for (int q = 0; q < LC_NP; ++q) {
+                const unsigned char *cols = s.jcol[Bl.dom];
+                for (int m = 0; m < s.jcnt[Bl.dom]; ++m) {
+                    const int q = cols[m];
                     double a = 0.0;
                     for (int k = 0; k < 8; ++k) a += h[k] * t[k * LC_NP + q];
                     jr[q] = a;
@@ -147,7 +156,9 @@ __device__ double pose_row(const PoseCtx &c, const PoseView &pv, int r, double *
                     const double cf = Bl.coef[sl];
                     if (cf == 0.0) continue;
                     const double *t = c.dqj + (size_t)Bl.js[sl] * 8 * LC_NP;
-                    for (int q = 0; q < LC_NP; ++q) {
+                    const unsigned char *cols = s.jcol[Bl.js[sl]];
+                    for (int m = 0; m < s.jcnt[Bl.js[sl]]; ++m) {
+                        const int q = cols[m];
                         double a = 0.0;
                         for (int k = 0; k < 8; ++k) a += h[k] * t[k * LC_NP + q];
                         jr[q] += cf * a;
@@ -410,6 +421,14 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(JobArg<PoseJob> jobs, co
         const int *src = reinterpret_cast<const int *>(skg);
         int *dst = reinterpret_cast<int *>(&s.sk);
         for (int i = threadIdx.x; i < (int)(sizeof(SkelDev) / sizeof(int)); i += NT) dst[i] = src[i];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < s.sk.J; j += NT) {
+        int n = 0;
+        for (int q = 0; q < 6; ++q) s.jcol[j][n++] = (unsigned char)q;
+        for (int k = 0; k < LC_NDOF; ++k)
+            if ((s.sk.moves_frame[k] >> j) & 1u) s.jcol[j][n++] = (unsigned char)(6 + k);
+        s.jcnt[j] = n;
     }
     __syncthreads();
     PoseCtx c;

@@ -15,7 +15,10 @@
 
 namespace {
 
-constexpr int NT = 512;
+#ifndef LC_SURF_NT
+#define LC_SURF_NT 512
+#endif
+constexpr int NT = LC_SURF_NT;
 
 struct SurfCtx {
     const SurfJob *J;
