@@ -994,20 +994,6 @@ static void build_config(lc_ctx *c, const lc_actor *a, const lc_nonrigid_hyper *
     cf.probe = cf.mem.upload(pr.data(), pr.size(), st);
 }
 
-// Stage II can sample the blur pyramid on demand from the raw image (the
-// blurred 2x2 patch under each sample, bit-identical; LIVECAP_PYRAMID_ON_DEMAND=1)
-// instead of reading the stored full-resolution levels.  Measured slower on
-// B200 (about 2x the surface-kernel time: ~1.6k fp64 MACs per sample on the
-// solver's critical path versus 0.5 ms of off-path HBM traffic), so the
-// stored pyramid stays the default.
-static bool pyramid_on_demand(const ConfigDev &cf, int levels) {
-    static const bool wanted = getenv("LIVECAP_PYRAMID_ON_DEMAND") != nullptr;
-    if (!wanted || levels > 4) return false;
-    for (int l = 0; l < levels; ++l)
-        if (cf.half[l] > LC_PYR_HALO) return false;
-    return true;
-}
-
 // gaussian_pyramid (imageproc.py:276-285) of a batch of images
 struct PyrTarget { const double *src; double *dst; double *tmp; };
 
@@ -1163,7 +1149,7 @@ static void launch_preprocess(lc_ctx *c, const ConfigDev &cf, const lc_config &c
     build_grids(c, gs, H, W, obs_list_radius());
     mark(c, "pre:grid");
     for (FrameIn *f : fs) cudaEventRecord(f->ready_obs, c->aux);
-    if (cfg.mode == 0 && !pyramid_on_demand(cf, cfg.nonrigid.n_levels)) {
+    if (cfg.mode == 0) {
         std::vector<PyrTarget> ts;
         for (FrameIn *f : fs) ts.push_back(PyrTarget{f->image_src, f->pyr, f->tmp});
         pyramid(c, cf, ts, H, W, cfg.nonrigid.n_levels);
@@ -1380,14 +1366,7 @@ static void run_frame(FrameBatch &fb, int stages = 3) {
             j.do_solve = 1;
             j.do_snap = cfg.enable_snapping;
             j.v0 = s->vinit; j.v = s->v; j.vs = s->vs;
-            if (pyramid_on_demand(*fb.cf, cfg.nonrigid.n_levels)) {
-                j.pyr = nullptr;
-                j.image = s->image_src;
-                j.taps = fb.cf->taps;
-                for (int l = 0; l < 4; ++l) j.half[l] = fb.cf->half[l];
-            } else {
-                j.pyr = s->pyr;
-            }
+            j.pyr = s->pyr;
             j.obs = grid_dev(s->obs, s->mask_src, H, W);
             j.obs_K = s->obs.K;
             j.has_field = 1;

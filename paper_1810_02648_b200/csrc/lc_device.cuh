@@ -237,7 +237,7 @@ __device__ __forceinline__ void nn_batch16(const int *e, int n, int x0, int y0, 
 // Returns the key of the nearest site (INT_MAX if there is none).  `hint`
 // (a site key of this grid, or -1) only seeds the search bound: the result
 // is the exact nearest site with the lowest-key tie break whatever the hint.
-__device__ inline int nn_query(const NnGridDev &g, double qx, double qy, double &d2out, int hint = -1) {
+static __device__ __noinline__ int nn_query(const NnGridDev &g, double qx, double qy, double &d2out, int hint = -1) {
     double best = LC_INF;
     int bk = 0x7fffffff;
     if (hint >= 0) nn_consider_key(hint, qx, qy, best, bk);

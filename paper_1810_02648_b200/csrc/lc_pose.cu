@@ -285,6 +285,7 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
         }
         if (with_jac) {
             __syncthreads();
+            if (r0 == T::rank() * NT) fst(6);   // first chunk's rows done (fine timer)
             const int nr = min(NT, c.R - r0);
             if (task < 27) {
                 for (int rr = grp; rr < nr; rr += G) {

@@ -33,10 +33,7 @@ struct SurfJob {
     const double *v0;         // N*3 start
     double *v;                // N*3 result
     const double *vs;         // N*3 skinned V^S
-    const double *pyr;        // levels*H*W*3, or null: blur `image` on demand
-    const double *image;      // H*W*3 raw image (when pyr is null)
-    const double *taps;       // levels*32 Gaussian taps (centre at index half[l])
-    int half[4];
+    const double *pyr;        // levels*H*W*3
     NnGridDev obs;
     const int *obs_K;
     int has_field;

@@ -41,103 +41,18 @@ __device__ __forceinline__ V3 trial_pos(const double *v, const double *step, int
     return a + sc * ld3(step + 3 * (size_t)i);
 }
 
-// Blurred values of the 2x2 pixel patch (x0..x0+1, y0..y0+1) of one pyramid
-// level, computed on demand from the raw image (gaussian_pyramid,
-// imageproc.py:276-285: a vertical then a horizontal convolve1d, mode
-// "nearest").  Every value is the expression of k_pyramid_fused / scipy in
-// the same order -- centre tap, then symmetric pairs outermost first, the
-// vertical pass over clamped rows, the horizontal one over clamped columns
-// -- so it is bit-identical to sampling the stored level, while the level
-// itself (3 x 25 MB per frame and stream at 1024^2) is never written.
-template <int HH>
-__device__ __forceinline__ void blur_patch_h(const double *img, int W, int H, const double *t, int x0, int y0,
-                                             double out[2][2][3]) {
-    double tt[HH + 1];
-#pragma unroll
-    for (int j = 0; j <= HH; ++j) tt[j] = t[j];
-    int xs[2 * HH + 2];
-#pragma unroll
-    for (int k = 0; k < 2 * HH + 2; ++k) xs[k] = min(max(x0 - HH + k, 0), W - 1);
-#pragma unroll
-    for (int dy = 0; dy < 2; ++dy) {
-        const int y = y0 + dy;
-        int ya[HH + 1], yb[HH + 1];
-#pragma unroll
-        for (int j = 1; j <= HH; ++j) { ya[j] = max(y - j, 0); yb[j] = min(y + j, H - 1); }
-        for (int ch = 0; ch < 3; ++ch) {
-            double mid[2 * HH + 2];
-#pragma unroll
-            for (int k = 0; k < 2 * HH + 2; ++k) {
-                double acc = img[((size_t)y * W + xs[k]) * 3 + ch] * tt[0];
-#pragma unroll
-                for (int j = HH; j >= 1; --j)
-                    acc = acc + (img[((size_t)ya[j] * W + xs[k]) * 3 + ch] + img[((size_t)yb[j] * W + xs[k]) * 3 + ch]) * tt[j];
-                mid[k] = acc;
-            }
-#pragma unroll
-            for (int dx = 0; dx < 2; ++dx) {
-                double acc = mid[HH + dx] * tt[0];
-#pragma unroll
-                for (int j = HH; j >= 1; --j) acc = acc + (mid[HH + dx - j] + mid[HH + dx + j]) * tt[j];
-                out[dy][dx][ch] = acc;
-            }
-        }
-    }
-}
-
-__device__ __noinline__ void blur_patch(const double *img, int W, int H, const double *t, int h, int x0, int y0,
-                                        double out[2][2][3]) {
-    switch (h) {
-        case 0: blur_patch_h<0>(img, W, H, t, x0, y0, out); break;
-        case 1: blur_patch_h<1>(img, W, H, t, x0, y0, out); break;
-        case 2: blur_patch_h<2>(img, W, H, t, x0, y0, out); break;
-        case 3: blur_patch_h<3>(img, W, H, t, x0, y0, out); break;
-        case 4: blur_patch_h<4>(img, W, H, t, x0, y0, out); break;
-        case 5: blur_patch_h<5>(img, W, H, t, x0, y0, out); break;
-        case 6: blur_patch_h<6>(img, W, H, t, x0, y0, out); break;
-        default: blur_patch_h<7>(img, W, H, t, x0, y0, out); break;
-    }
-}
-
-// one pyramid level as bilinear3 sees it: stored, or blurred on demand
+// one pyramid level as bilinear3 samples it
 struct LevelSrc {
-    const double *lvl;   // stored level, or null
-    const double *img;   // raw image
-    const double *t;     // taps from the centre
-    int h;
+    const double *lvl;
 };
 
 __device__ __forceinline__ LevelSrc level_src(const SurfCtx &c, int level) {
-    const SurfJob &J = *c.J;
-    LevelSrc L;
-    L.lvl = J.pyr ? J.pyr + (size_t)level * c.H * c.W * 3 : nullptr;
-    L.img = J.image;
-    L.h = J.half[level];
-    L.t = J.taps ? J.taps + 32 * level + L.h : nullptr;
-    return L;
+    return LevelSrc{c.J->pyr + (size_t)level * c.H * c.W * 3};
 }
 
-// sample_bilinear (imageproc.py:127-174) of a level
 __device__ __forceinline__ bool bilinear3_src(const LevelSrc &L, int W, int H, double x, double y, double val[3],
                                               double gx[3], double gy[3]) {
-    if (L.lvl) return bilinear3(L.lvl, W, H, x, y, val, gx, gy);
-    const bool clamped = (x < 0) || (x > W - 1) || (y < 0) || (y > H - 1);
-    const double xc = fmin(fmax(x, 0.0), (double)(W - 1));
-    const double yc = fmin(fmax(y, 0.0), (double)(H - 1));
-    const int x0 = min((int)floor(xc), W - 2), y0 = min((int)floor(yc), H - 2);
-    const double fx = xc - x0, fy = yc - y0;
-    double q[2][2][3];
-    blur_patch(L.img, W, H, L.t, L.h, x0, y0, q);
-    const bool inx = (x >= 0) && (x <= W - 1), iny = (y >= 0) && (y <= H - 1);
-    for (int ch = 0; ch < 3; ++ch) {
-        const double c00 = q[0][0][ch], c01 = q[0][1][ch], c10 = q[1][0][ch], c11 = q[1][1][ch];
-        const double top = c00 * (1 - fx) + c01 * fx;
-        const double bot = c10 * (1 - fx) + c11 * fx;
-        val[ch] = top * (1 - fy) + bot * fy;
-        gx[ch] = inx ? (c01 - c00) * (1 - fy) + (c11 - c10) * fy : 0.0;
-        gy[ch] = iny ? bot - top : 0.0;
-    }
-    return clamped;
+    return bilinear3(L.lvl, W, H, x, y, val, gx, gy);
 }
 
 // photometric row of visible vertex i at position p (nonrigid_stage.py:196-213)

@@ -78,7 +78,7 @@ def main():
             # surface assembly [16..21], snap [24..29]
             pp, ss = np.zeros(64, dtype=np.int64), np.zeros(64, dtype=np.int64)
             _lib.check(ctx.lib.lc_tracker_phase_times(tr.handle, 0, _lib.ptr(pp), _lib.ptr(ss)))
-            for name, arr, a0, n in (("pose evalJ", pp, 32, 6), ("pose trial", pp, 40, 6),
+            for name, arr, a0, n in (("pose evalJ", pp, 32, 6), ("pose rows|jtj", pp[[34, 38, 35]], 0, 3), ("pose trial", pp, 40, 6),
                                      ("surf asm", ss, 16, 5), ("surf snap", ss, 24, 5),
                                      ("surf pcg init|mv|red1|upd|red2|p", ss, 40, 7)):
                 d = np.diff(arr[a0:a0 + n]) / 1e3
