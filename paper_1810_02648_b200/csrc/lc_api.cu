@@ -43,6 +43,12 @@ static int fail(int code, const std::string &msg) {
     catch (const std::exception &ex) { return fail(LC_EINVAL, ex.what()); }
 
 
+// programmatic dependent launch for every kernel (LIVECAP_NO_PDL=1 disables)
+static bool lc_pdl_enabled() {
+    static const bool on = getenv("LIVECAP_NO_PDL") == nullptr;
+    return on;
+}
+
 template <typename K, typename... Args>
 static void launch_named(const char *name, lc_ctx *c, K kernel, dim3 g, dim3 b, size_t smem, Args... args) {
     if (g.x == 0 || g.y == 0 || g.z == 0) return;   // empty batch / empty mesh
@@ -53,7 +59,19 @@ static void launch_named(const char *name, lc_ctx *c, K kernel, dim3 g, dim3 b, 
         cudaEventCreate(&e1);
         cudaEventRecord(e0, c->stream);
     }
-    kernel<<<g, b, smem, c->stream>>>(args...);
+    {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = g;
+        cfg.blockDim = b;
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = c->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = lc_pdl_enabled() ? 1 : 0;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kernel, args...);
+    }
     if (prof) {
         cudaEventRecord(e1, c->stream);
         c->prof_events.push_back({e0, e1});
@@ -96,13 +114,15 @@ static void launch_cluster(const char *name, lc_ctx *c, void (*kernel)(KArgs...)
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c->stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = cs;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = lc_pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     const bool prof = !c->prof_name.empty() && c->prof_name == name;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (prof) {
@@ -164,6 +184,7 @@ struct StageBlob { uint4 w[CAP / 16]; };
 
 template <int CAP>
 __global__ void k_stage(unsigned char *dst, int bytes, StageBlob<CAP> blob) {
+    lc_pdl_wait();
     const unsigned char *src = reinterpret_cast<const unsigned char *>(blob.w);
     const bool vec = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
     const int nv = vec ? bytes / 16 : 0;
@@ -1047,6 +1068,7 @@ struct PrepJob {
 };
 
 __global__ void k_prep(JobArg<PrepJob> jobs, const SkelDev *skg) {
+    lc_pdl_wait();
     const PrepJob J = jobs[blockIdx.y];
     const SkelDev &sk = *skg;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 3 * J.N; i += gridDim.x * blockDim.x)
@@ -1091,6 +1113,7 @@ struct FinishJob {
 };
 
 __global__ void k_finish(JobArg<FinishJob> jobs) {
+    lc_pdl_wait();
     const FinishJob F = jobs[blockIdx.y];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < F.N; i += gridDim.x * blockDim.x) {
         const V3 v = ld3(F.v + 3 * (size_t)i);
@@ -1497,6 +1520,7 @@ extern "C" int lc_tracker_set_frame(lc_tracker *t, int32_t stream, const double 
 // colour bytes -> [0, 1] doubles with the reference's exact `/ 255.0`
 // (imageproc.py:297-299: np.asarray(img, float64) / 255.0)
 __global__ void k_u8_to_unit(const uint8_t *src, double *dst, long long n) {
+    lc_pdl_wait();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         dst[i] = (double)src[i] / 255.0;
 }
@@ -2206,6 +2230,7 @@ extern "C" int lc_field_n_contour(lc_field *f, int32_t *k) {
 }
 
 __global__ void k_field_query(NnGridDev g, long long n, const double *pos, int kind, double *out) {
+    lc_pdl_wait();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const double x = pos[2 * i], y = pos[2 * i + 1];
         double *o = out + 4 * i;

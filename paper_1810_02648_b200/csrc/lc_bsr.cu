@@ -30,6 +30,7 @@ __device__ __forceinline__ V3 m3v(const double *m, V3 v) { return mat_vec(m, v);
 }  // namespace
 
 __global__ void k_bsr_keys(int m, const long long *rows, int *keys, int *vals, int *count) {
+    lc_pdl_wait();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
         keys[i] = (int)rows[i];
         vals[i] = i;
@@ -73,11 +74,13 @@ __device__ int scan_block(const int *in, int *out, int n) {
 }
 
 __global__ void k_bsr_rowptr(int n, const int *count, int *rowptr) {
+    lc_pdl_wait();
     const int tot = scan_block<1024>(count, rowptr, n);
     if (threadIdx.x == 0) rowptr[n] = tot;
 }
 
 __global__ void __launch_bounds__(NT, 1) k_pcg_bsr(BsrJob J) {
+    lc_pdl_wait();
     __shared__ double red[8 * 32 + 16];
     const int n = J.n;
     // M^-1 = inv(diag) (pinv fallback when a block is exactly singular)
@@ -161,6 +164,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_bsr(BsrJob J) {
 
 __global__ void __launch_bounds__(256, 1) k_dense_solve(int n, const double *A, const double *b,
                                                        double *x, double *info) {
+    lc_pdl_wait();
     __shared__ QrSmem s;
     double damping;
     const bool damped = dense_solve_block<256>(s, A, b, n, damping);

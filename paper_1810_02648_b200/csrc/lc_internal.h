@@ -131,3 +131,15 @@ struct JobArg {
     T inl[LC_JOB_INLINE];
     __host__ __device__ __forceinline__ const T &operator[](int i) const { return ptr ? ptr[i] : inl[i]; }
 };
+
+// Programmatic dependent launch: kernels are launched with
+// programmaticStreamSerialization, so a kernel's CTAs may be scheduled
+// before the previous kernel on the stream has finished; every kernel waits
+// here for that grid's completion (and memory flush) before touching its
+// inputs.  This hides the launch latency between the many short kernels of
+// a frame.
+__device__ __forceinline__ void lc_pdl_wait() {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}

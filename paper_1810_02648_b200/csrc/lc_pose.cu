@@ -408,6 +408,7 @@ __device__ void pose_trials(PoseCtx &c, TrialSmem &ts, int nt, double e[kTrials]
 template <int CS>
 __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(JobArg<PoseJob> jobs, const SkelDev *skg,
                                                         ActorDev A, CamDev cam) {
+    lc_pdl_wait();
     using T = Team<CS, NT>;
     __shared__ PoseJob sJ;   // this stream's descriptor, parameter bank -> shared memory
     if (threadIdx.x == 0) sJ = jobs[T::stream()];

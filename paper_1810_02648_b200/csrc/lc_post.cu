@@ -8,8 +8,10 @@
 // order (unfused, --fmad=false), so the result is bit-identical.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include "lc_internal.h"
 
 __global__ void k_smooth_trajectory(const double *v, int F, long long D, const double *w, int K, double *out) {
+    lc_pdl_wait();
     const int half = K / 2;
     const long long n = (long long)F * D;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -30,6 +32,7 @@ __global__ void k_smooth_trajectory(const double *v, int F, long long D, const d
 // per-frame |a & b| and |a | b| of two mask stacks (iou), one CTA per frame
 __global__ void k_mask_overlap(const uint8_t *a, const uint8_t *b, long long HW, unsigned long long *inter,
                                unsigned long long *uni) {
+    lc_pdl_wait();
     const int f = blockIdx.y;
     const uint8_t *pa = a + (long long)f * HW, *pb = b + (long long)f * HW;
     unsigned long long i0 = 0, u0 = 0;

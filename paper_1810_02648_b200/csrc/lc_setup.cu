@@ -12,6 +12,7 @@
 
 __global__ void k_blur_axis(JobArg<PyrJob> jobs, int H, int W, int C, const double *taps, int half,
                             int axis) {
+    lc_pdl_wait();
     const PyrJob J = jobs[blockIdx.y];
     const double *in = axis == 0 ? J.src : J.tmp;
     double *out = axis == 0 ? J.tmp : J.dst;
@@ -99,6 +100,7 @@ __device__ __forceinline__ void pyr_level(const double *__restrict__ in, double 
 
 __global__ void __launch_bounds__(256) k_pyramid_fused(JobArg<PyrAllJob> jobs, int H, int W, int levels,
                                                        const double *taps, int h0, int h1, int h2, int h3) {
+    lc_pdl_wait();
     const PyrAllJob J = jobs[blockIdx.y];
     constexpr int T = LC_PYR_TILE, R = LC_PYR_HALO, E = T + 2 * R;
     extern __shared__ double sm[];
@@ -154,6 +156,7 @@ __device__ __forceinline__ bool is_contour(const uint8_t *m, int H, int W, int x
 
 // one block per row: row_count[y]
 __global__ void k_contour_rows(JobArg<GridJob> jobs, int H, int W) {
+    lc_pdl_wait();
     const GridJob J = jobs[blockIdx.y];
     __shared__ int cnt;
     for (int y = blockIdx.x; y < H; y += gridDim.x) {
@@ -206,6 +209,7 @@ __device__ int block_exclusive_scan(const int *in, int *out, int n) {
 }
 
 __global__ void k_contour_scan_rows(JobArg<GridJob> jobs, int H, int ncells) {
+    lc_pdl_wait();
     const GridJob J = jobs[blockIdx.x];
     const int total = block_exclusive_scan<1024>(J.row_count, J.row_start, H);
     if (threadIdx.x == 0) {
@@ -220,6 +224,7 @@ __global__ void k_contour_scan_rows(JobArg<GridJob> jobs, int H, int ncells) {
 
 // one block per row: ordered emission of (x, y) + per-cell counts
 __global__ void k_contour_emit(JobArg<GridJob> jobs, int H, int W, int ncx) {
+    lc_pdl_wait();
     const GridJob J = jobs[blockIdx.y];
     __shared__ int wsum[32];
     __shared__ int carry;
@@ -252,12 +257,14 @@ __global__ void k_contour_emit(JobArg<GridJob> jobs, int H, int W, int ncx) {
 }
 
 __global__ void k_contour_scan_cells(JobArg<GridJob> jobs, int ncells) {
+    lc_pdl_wait();
     const GridJob J = jobs[blockIdx.x];
     const int total = block_exclusive_scan<1024>(J.cell_count, J.cell_start, ncells);
     if (threadIdx.x == 0) J.cell_start[ncells] = total;
 }
 
 __global__ void k_contour_fill(JobArg<GridJob> jobs, int ncx) {
+    lc_pdl_wait();
     const GridJob J = jobs[blockIdx.y];
     const int K = *J.K;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
@@ -270,6 +277,7 @@ __global__ void k_contour_fill(JobArg<GridJob> jobs, int ncx) {
 
 // ---- site-count quadtree over the cells (one CTA per stream) -------------
 __global__ void k_quad_build(JobArg<GridJob> jobs, int ncx, int ncy) {
+    lc_pdl_wait();
     const GridJob J = jobs[blockIdx.x];
     const int P = J.qP;
     for (int i = threadIdx.x; i < P * P; i += blockDim.x) {
@@ -367,6 +375,7 @@ __device__ __forceinline__ CellBox cell_box(int cx, int cy) {
 // (any real site bounds the nearest distance), so JFA's rare misses cost
 // list length, never exactness.
 __global__ void k_cell_jfa(JobArg<GridJob> jobs, int ncx, int ncy) {
+    lc_pdl_wait();
     const GridJob J = jobs[blockIdx.x];
     extern __shared__ int seeds[];   // 2 * ncells ping-pong
     const int nc = ncx * ncy;
@@ -423,6 +432,7 @@ __global__ void k_cell_jfa(JobArg<GridJob> jobs, int ncx, int ncy) {
 // best distance (nn_query), so only the head is read.  Cells with more than
 // LC_CAND_MAX candidates (or beyond max_u2) keep the quadtree search.
 __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H, int W) {
+    lc_pdl_wait();
     const GridJob J = jobs[blockIdx.y];
     const NnGridDev g = grid_of(J, H, W);
     const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
@@ -547,11 +557,13 @@ __device__ __forceinline__ bool bary(const double P[3][2], double inv, int ix, i
 // tests every triangle (still exact).
 
 __global__ void k_rt_clear(JobArg<RasterJob> jobs, int n) {
+    lc_pdl_wait();
     const RasterJob J = jobs[blockIdx.y];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) J.tcount[i] = 0;
 }
 
 __global__ void k_rt_setup(JobArg<RasterJob> jobs, CamDev cam, const int *tris, int T) {
+    lc_pdl_wait();
     const RasterJob J = jobs[blockIdx.y];
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= T) return;
@@ -610,6 +622,7 @@ __device__ __forceinline__ bool rt_tile_hit(const TriRec &r, const int4 bb, RtCu
 // one warp per triangle over the tiles of its bbox: count (fill = 0) or append (fill = 1)
 template <int FILL>
 __global__ void k_rt_bin(JobArg<RasterJob> jobs, int T, int ntx) {
+    lc_pdl_wait();
     const RasterJob J = jobs[blockIdx.y];
     const int lane = threadIdx.x & 31;
     const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -682,6 +695,7 @@ __device__ void rt_block_scan(int n, V &&v, int *out, int *zero = nullptr) {
 // triangles (a collapsed, far-away surface) is still resolved in parallel.
 // A tile whose list overflowed the buffer resolves every triangle in one CTA.
 __global__ void k_rt_scan(JobArg<RasterJob> jobs, int n, int T) {
+    lc_pdl_wait();
     const RasterJob J = jobs[blockIdx.x];
     rt_block_scan(n, [&](int i) { return J.tcount[i]; }, J.toff, J.tfill);
     rt_block_scan(n, [&](int i) {
@@ -711,6 +725,7 @@ __device__ __forceinline__ void rt_write(const RasterJob &J, CamDev cam, int x, 
 
 // work items (tile, chunk), grid-strided; thread = pixel of the tile
 __global__ void __launch_bounds__(256) k_rt_tiles(JobArg<RasterJob> jobs, CamDev cam, int T, int ntx, int nt) {
+    lc_pdl_wait();
     const RasterJob J = jobs[blockIdx.y];
     constexpr int CH = 64;
     __shared__ TriRec sr[CH];
@@ -754,6 +769,7 @@ __global__ void __launch_bounds__(256) k_rt_tiles(JobArg<RasterJob> jobs, CamDev
 
 // lexicographic (depth, id) minimum over the chunks of multi-chunk tiles
 __global__ void __launch_bounds__(256) k_rt_merge(JobArg<RasterJob> jobs, CamDev cam, int ntx, int nt) {
+    lc_pdl_wait();
     const RasterJob J = jobs[blockIdx.y];
     for (int tile = blockIdx.x; tile < nt; tile += gridDim.x) {
         const int i0 = J.ioff[tile], i1 = J.ioff[tile + 1];
@@ -782,6 +798,7 @@ __device__ __forceinline__ int id_pick(double l0, double l1, double l2) {
 __global__ void k_raster_resolve(JobArg<RasterJob> jobs, CamDev cam, const int *tris, int mode,
                                  const double *attrs, int n_attr, const int *ids, double bg_attr,
                                  long long bg_id, double *zout, double *aout, long long *iout) {
+    lc_pdl_wait();
     const RasterJob J = jobs[blockIdx.y];
     const int HW = cam.W * cam.H;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += gridDim.x * blockDim.x) {
@@ -817,6 +834,7 @@ __global__ void k_raster_resolve(JobArg<RasterJob> jobs, CamDev cam, const int *
 // kinematics / skinning
 
 __global__ void k_fk(JobArg<FkJob> jobs, const SkelDev *sk) {
+    lc_pdl_wait();
     const FkJob J = jobs[blockIdx.x];
     if (!J.active) return;
     __shared__ FkState f;
@@ -834,6 +852,7 @@ struct GlobalDq {
 };
 
 __global__ void k_skin(JobArg<SkinJob> jobs, ActorDev A) {
+    lc_pdl_wait();
     const SkinJob J = jobs[blockIdx.y];
     if (!J.active) return;
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
@@ -856,6 +875,7 @@ __global__ void k_skin(JobArg<SkinJob> jobs, ActorDev A) {
 // occluding contour vertices (extract_contour_vertices, pose_stage.py:151-191)
 
 __global__ void k_tri_front(JobArg<ContourJob> jobs, ActorDev A) {
+    lc_pdl_wait();
     const ContourJob J = jobs[blockIdx.y];
     if (!J.active) return;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < A.T; t += gridDim.x * blockDim.x) {
@@ -873,6 +893,7 @@ __global__ void k_tri_front(JobArg<ContourJob> jobs, ActorDev A) {
 }
 
 __global__ void k_sil_edges(JobArg<ContourJob> jobs, ActorDev A) {
+    lc_pdl_wait();
     const ContourJob J = jobs[blockIdx.y];
     if (!J.active) return;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < A.E; e += gridDim.x * blockDim.x) {
@@ -902,6 +923,7 @@ __device__ __forceinline__ bool depth_visible(CamDev cam, const unsigned long lo
 // image-plane normals of the contour vertices.
 __global__ void __launch_bounds__(1024) k_contour_compact(JobArg<ContourJob> jobs, ActorDev A,
                                                           CamDev cam) {
+    lc_pdl_wait();
     const ContourJob J = jobs[blockIdx.x];
     if (!J.active) return;
     __shared__ int wsum[32];
@@ -984,6 +1006,7 @@ __device__ __forceinline__ int part_at(const ActorDev &A, CamDev cam, const doub
 // (foreground with a background 4-neighbour, the image border counting as
 // background; imageproc.py:34-49), compacted in row-major order.
 __global__ void __launch_bounds__(256) k_own_cells(JobArg<OwnCellsJob> jobs, int H, int W, int ncx) {
+    lc_pdl_wait();
     const OwnCellsJob J = jobs[blockIdx.y];
     const int c = blockIdx.x;
     const int x = (c % ncx) * LC_GRID_CELL + (threadIdx.x & (LC_GRID_CELL - 1));
@@ -1032,6 +1055,7 @@ __device__ inline double own_within2(const NnGridDev &g, const int *cnt, const i
 }
 
 __global__ void k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double *probe_offs) {
+    lc_pdl_wait();
     const RimJob J = jobs[blockIdx.y];
     if (!J.active) return;
     const int B = *J.B;
@@ -1109,6 +1133,7 @@ __global__ void k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double 
 // recomputed from the FK state on the fly.
 __global__ void k_skin_jac(const FkState *fk, const SkelDev *skg, ActorDev A, int M, const double *rest,
                            const int *subset, double *jac) {
+    lc_pdl_wait();
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= M) return;
     const SkelDev &sk = *skg;

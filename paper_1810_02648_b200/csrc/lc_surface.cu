@@ -651,6 +651,7 @@ template <int CS>
 __global__ void __launch_bounds__(NT, 1) k_surface_solve_t(JobArg<SurfJob> jobs, ActorDev A, CamDev cam,
                                                            EdgeConstDev ec, SurfHyperDev hp, int H,
                                                            int W) {
+    lc_pdl_wait();
     using T = Team<CS, NT>;
     // this stream's descriptor, from the parameter bank into shared memory
     __shared__ SurfJob sJ;
