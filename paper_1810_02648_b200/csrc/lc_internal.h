@@ -141,5 +141,8 @@ struct JobArg {
 __device__ __forceinline__ void lc_pdl_wait() {
 #if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
     asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef LC_PDL_EARLY_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 #endif
 }
