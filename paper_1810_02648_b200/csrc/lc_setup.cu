@@ -488,11 +488,53 @@ __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H,
                     }
                     __syncwarp();
                 }
-            for (int i = lane; i < n; i += 32) {
-                const int k = site_key(g.pts[(int)(unsigned)(key[i] & 0xffffffffu)]);
-                J.cand_pts[start + i] = k;
-                if (i < LC_CAND_HEAD) J.cand_blk[32 * (size_t)c + 2 + i] = k;
+            // Dominance pruning.  A candidate s is dropped when one of the
+            // cell's 8 closest candidates t satisfies |q-s|^2 - |q-t|^2 >= 1
+            // at the 4 corners of the (closed) cell: that difference is affine
+            // in q, so it is >= 1 on the whole cell, far beyond the rounding of
+            // the fp64 squared distances (< 1e-7 px^2 here), so s is never the
+            // nearest site -- nor tied with it -- for any query in the cell.
+            // Exact; it removes most of a far cell's list (the contour sites
+            // far along the contour from the cell's nearest ones).
+            const int nd = min(n, 8);
+            int tx[8], ty[8];
+#pragma unroll
+            for (int d = 0; d < 8; ++d) {
+                const int2 p = d < nd ? g.pts[(int)(unsigned)(key[d] & 0xffffffffu)] : make_int2(0, 0);
+                tx[d] = p.x;
+                ty[d] = p.y;
             }
+            const int X0 = cx * LC_GRID_CELL, Y0 = cy * LC_GRID_CELL;
+            const int X1 = X0 + LC_GRID_CELL, Y1 = Y0 + LC_GRID_CELL;
+            int m = 0;
+            for (int base = 0; base < n; base += 32) {
+                const int i = base + lane;
+                bool keep = false;
+                int k = 0;
+                if (i < n) {
+                    const int2 p = g.pts[(int)(unsigned)(key[i] & 0xffffffffu)];
+                    k = site_key(p);
+                    keep = true;
+                    const long long s2 = (long long)p.x * p.x + (long long)p.y * p.y;
+#pragma unroll
+                    for (int d = 0; d < 8; ++d) {
+                        if (d >= nd || (tx[d] == p.x && ty[d] == p.y)) continue;
+                        const long long a = 2LL * (tx[d] - p.x), b = 2LL * (ty[d] - p.y);
+                        const long long c0 = s2 - ((long long)tx[d] * tx[d] + (long long)ty[d] * ty[d]);
+                        const long long f00 = a * X0 + b * Y0 + c0, f10 = a * X1 + b * Y0 + c0;
+                        const long long f01 = a * X0 + b * Y1 + c0, f11 = a * X1 + b * Y1 + c0;
+                        if (f00 >= 1 && f10 >= 1 && f01 >= 1 && f11 >= 1) { keep = false; break; }
+                    }
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    const int pos = m + __popc(bal & ((1u << lane) - 1u));
+                    J.cand_pts[start + pos] = k;
+                    if (pos < LC_CAND_HEAD) J.cand_blk[32 * (size_t)c + 2 + pos] = k;
+                }
+                m += __popc(bal);
+            }
+            n = m;
         }
         if (lane == 0) {
             J.cand_blk[32 * (size_t)c] = start;
