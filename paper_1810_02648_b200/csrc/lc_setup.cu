@@ -431,6 +431,9 @@ __global__ void k_cell_jfa(JobArg<GridJob> jobs, int ncx, int ncy) {
 // that order and stops at the first entry farther from the cell than its
 // best distance (nn_query), so only the head is read.  Cells with more than
 // LC_CAND_MAX candidates (or beyond max_u2) keep the quadtree search.
+#ifndef LC_DOMINATORS
+#define LC_DOMINATORS 16
+#endif
 __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H, int W) {
     lc_pdl_wait();
     const GridJob J = jobs[blockIdx.y];
@@ -489,17 +492,17 @@ __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H,
                     __syncwarp();
                 }
             // Dominance pruning.  A candidate s is dropped when one of the
-            // cell's 8 closest candidates t satisfies |q-s|^2 - |q-t|^2 >= 1
+            // cell's LC_DOMINATORS closest candidates t satisfies |q-s|^2 - |q-t|^2 >= 1
             // at the 4 corners of the (closed) cell: that difference is affine
             // in q, so it is >= 1 on the whole cell, far beyond the rounding of
             // the fp64 squared distances (< 1e-7 px^2 here), so s is never the
             // nearest site -- nor tied with it -- for any query in the cell.
             // Exact; it removes most of a far cell's list (the contour sites
             // far along the contour from the cell's nearest ones).
-            const int nd = min(n, 8);
-            int tx[8], ty[8];
+            const int nd = min(n, LC_DOMINATORS);
+            int tx[LC_DOMINATORS], ty[LC_DOMINATORS];
 #pragma unroll
-            for (int d = 0; d < 8; ++d) {
+            for (int d = 0; d < LC_DOMINATORS; ++d) {
                 const int2 p = d < nd ? g.pts[(int)(unsigned)(key[d] & 0xffffffffu)] : make_int2(0, 0);
                 tx[d] = p.x;
                 ty[d] = p.y;
@@ -517,7 +520,7 @@ __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H,
                     keep = true;
                     const long long s2 = (long long)p.x * p.x + (long long)p.y * p.y;
 #pragma unroll
-                    for (int d = 0; d < 8; ++d) {
+                    for (int d = 0; d < LC_DOMINATORS; ++d) {
                         if (d >= nd || (tx[d] == p.x && ty[d] == p.y)) continue;
                         const long long a = 2LL * (tx[d] - p.x), b = 2LL * (ty[d] - p.y);
                         const long long c0 = s2 - ((long long)tx[d] * tx[d] + (long long)ty[d] * ty[d]);
