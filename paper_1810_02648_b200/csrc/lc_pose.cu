@@ -260,6 +260,7 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
     // J^T J tiles: task = tid / G (27 tasks), group = tid % G
     const int task = threadIdx.x / G, grp = threadIdx.x % G;
     double tile[36];
+#pragma unroll
     for (int k = 0; k < 36; ++k) tile[k] = 0.0;
     int ta = 0, tb = 0;
     bool is_rhs = false;
@@ -292,11 +293,15 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
                     const double *row = c.rows + (size_t)rr * 37;
                     if (is_rhs) {
                         const double F = row[36];
+#pragma unroll
                         for (int i = 0; i < 6; ++i) tile[i] += row[6 * ta + i] * F;
                     } else {
                         double a[6], b[6];
+#pragma unroll
                         for (int i = 0; i < 6; ++i) { a[i] = row[6 * ta + i]; b[i] = row[6 * tb + i]; }
+#pragma unroll
                         for (int i = 0; i < 6; ++i)
+#pragma unroll
                             for (int j = 0; j < 6; ++j) tile[6 * i + j] += a[i] * b[j];
                     }
                 }
@@ -321,7 +326,9 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
         if (task < 27) {
             double *dst = part + (size_t)grp * per_group + (is_rhs ? 21 * 36 + 6 * ta : 36 * task);
             const int cnt = is_rhs ? 6 : 36;
-            for (int k = 0; k < cnt; ++k) dst[k] = tile[k];
+#pragma unroll
+            for (int k = 0; k < 36; ++k)
+                if (k < cnt) dst[k] = tile[k];
         }
         __syncthreads();
         // groups -> this CTA's partial, then the team total in rank order
