@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--streams", type=int, default=8, help="capture streams per GPU")
     ap.add_argument("--groups", type=int, default=4,
                     help="stream groups stepped concurrently on their own CUDA streams (BatchTracker)")
+    ap.add_argument("--host-threads", type=int, default=1,
+                    help="1: one host thread per group enqueues its step (BatchTracker host_threads)")
     ap.add_argument("--preset", default="x5k")
     ap.add_argument("--gn", type=int, default=None, help="non-rigid GN iterations (cfg4: 4)")
     ap.add_argument("--pcg", type=int, default=None, help="PCG iterations per GN step (cfg4: 8)")
@@ -80,6 +82,7 @@ def workload(args, world):
                         f"{args.res}x{args.res}, {args.streams} synthetic streams per GPU (cfg5 sharding)",
             "preset": args.preset, "resolution": args.res, "streams_per_gpu": args.streams,
             "stream_groups": args.groups,
+            "host_threads": bool(args.host_threads),
             "nonrigid_gn_pcg": [args.gn or 3, args.pcg or 4],
             "total_streams": args.streams * world, "parallelism": f"stream-sharded x{world}",
             "l2": "per-step inputs (images + pyramids) exceed the 126 MB L2; no flush needed"}
@@ -122,10 +125,16 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.p = None
+            return
+        # nvidia-smi needs ~0.5 s to start; the timed region of a default run
+        # is ~0.1 s, so wait until the sampler is live before it begins
+        t0 = time.time()
+        while time.time() - t0 < 10.0 and os.path.getsize(self.f.name) == 0 and self.p.poll() is None:
+            time.sleep(0.02)
 
     def stop(self):
         if self.p is None:
@@ -268,7 +277,8 @@ def run_ours(args):
     # `groups` trackers stepped concurrently on their own CUDA streams; the
     # timed region is bracketed by device-wide synchronisations, so the
     # events measure the whole device.
-    tr = BatchTracker(actor, cam, cfg, Sn, groups=args.groups, device=local)
+    tr = BatchTracker(actor, cam, cfg, Sn, groups=args.groups, device=local,
+                      host_threads=bool(args.host_threads))
 
     def queue_dev(f):
         for s in range(Sn):
@@ -336,7 +346,8 @@ def run_ours(args):
     # surfaces are read back into pinned host buffers with the streaming
     # readout; the host consumes frame f's results (event wait) while frame
     # f+1 is being solved (the pipelined driver's 2-slot latency).
-    tr2 = BatchTracker(actor, cam, cfg, Sn, groups=args.groups, device=local)
+    tr2 = BatchTracker(actor, cam, cfg, Sn, groups=args.groups, device=local,
+                       host_threads=bool(args.host_threads))
     x_h = torch.empty((2, Sn, 36), dtype=torch.float64, pin_memory=True)
     v_h = torch.empty((2, Sn, N, 3), dtype=torch.float64, pin_memory=True)
     done = [[torch.cuda.Event() for _ in tr2.ctxs] for _ in range(2)]

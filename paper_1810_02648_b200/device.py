@@ -434,7 +434,8 @@ class BatchTracker:
     """
 
     def __init__(self, actor, camera, config: SequenceConfig | None = None, n_streams: int = 1,
-                 groups: int = 1, device: int = 0, priority_streams: bool = True):
+                 groups: int = 1, device: int = 0, priority_streams: bool = True,
+                 host_threads: bool = True):
         groups = max(1, min(groups, n_streams))
         base, extra = divmod(n_streams, groups)
         self.sizes = [base + (1 if g < extra else 0) for g in range(groups)]
@@ -454,6 +455,14 @@ class BatchTracker:
             self.ctxs.append(L.Context(device, st))
         self.trackers = [Tracker(actor, camera, config, n, ctx=c) for n, c in zip(self.sizes, self.ctxs)]
         self.S = n_streams
+        # one host thread per group enqueues that group's step: the library
+        # calls release the GIL (ctypes) and contexts share no mutable state,
+        # so the groups' host-side launch work (~0.3 ms per group step) runs
+        # in parallel instead of serialising in front of the device
+        self._pool = None
+        if host_threads and groups > 1:
+            from concurrent.futures import ThreadPoolExecutor
+            self._pool = ThreadPoolExecutor(max_workers=groups, thread_name_prefix="lc-group")
 
     def _where(self, stream):
         for g, (a, n) in enumerate(zip(self.starts, self.sizes)):
@@ -466,8 +475,12 @@ class BatchTracker:
         self.trackers[g].set_frame(s, image, mask, det, on_device)
 
     def step(self):
-        for t in self.trackers:
-            t.step()
+        if self._pool is None:
+            for t in self.trackers:
+                t.step()
+            return
+        for f in [self._pool.submit(t.step) for t in self.trackers]:
+            f.result()
 
     def result(self, stream, with_report=True):
         g, s = self._where(stream)
@@ -530,5 +543,8 @@ class BatchTracker:
         return ms, n
 
     def close(self):
+        if self._pool is not None:
+            self._pool.shutdown()
+            self._pool = None
         for t in self.trackers:
             t.close()
