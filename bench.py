@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--streams", type=int, default=8, help="capture streams per GPU")
+    ap.add_argument("--streams", type=int, default=16, help="capture streams per GPU")
     ap.add_argument("--groups", type=int, default=4,
                     help="stream groups stepped concurrently on their own CUDA streams (BatchTracker)")
     ap.add_argument("--host-threads", type=int, default=1,
@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--pcg", type=int, default=None, help="PCG iterations per GN step (cfg4: 8)")
     ap.add_argument("--res", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e-u8", action="store_true", help="skip the 8-bit-frame e2e leg")
     ap.add_argument("--cpu-frames", type=int, default=3, help="timed steady frames of the CPU baseline")
     return ap.parse_args()
 
@@ -346,49 +347,52 @@ def run_ours(args):
     # surfaces are read back into pinned host buffers with the streaming
     # readout; the host consumes frame f's results (event wait) while frame
     # f+1 is being solved (the pipelined driver's 2-slot latency).
-    tr2 = BatchTracker(actor, cam, cfg, Sn, groups=args.groups, device=local,
-                       host_threads=bool(args.host_threads))
-    x_h = torch.empty((2, Sn, 36), dtype=torch.float64, pin_memory=True)
-    v_h = torch.empty((2, Sn, N, 3), dtype=torch.float64, pin_memory=True)
-    done = [[torch.cuda.Event() for _ in tr2.ctxs] for _ in range(2)]
-    checksum = [0.0]
+    def run_e2e(imgs):
+        tr2 = BatchTracker(actor, cam, cfg, Sn, groups=args.groups, device=local,
+                           host_threads=bool(args.host_threads))
+        x_h = torch.empty((2, Sn, 36), dtype=torch.float64, pin_memory=True)
+        v_h = torch.empty((2, Sn, N, 3), dtype=torch.float64, pin_memory=True)
+        done = [[torch.cuda.Event() for _ in tr2.ctxs] for _ in range(2)]
+        checksum = [0.0]
 
-    def queue_host(f):
-        for s in range(Sn):
-            tr2.set_frame(s, img_h[s, f].numpy(), msk_h[s, f].numpy(), dets[s][f])
+        def queue_host(f):
+            for s in range(Sn):
+                tr2.set_frame(s, imgs[s, f].numpy(), msk_h[s, f].numpy(), dets[s][f])
 
-    def step_host(f, first):
-        tr2.step()
-        b = f & 1
-        for s in range(Sn):
-            tr2.result_async(s, x_h[b, s], v_h[b, s])
-        for ev, ts in zip(done[b], tr2.torch_streams):
-            ev.record(ts)
-        if not first:                     # frame f-1's results are complete on the host
-            for ev in done[b ^ 1]:
-                ev.synchronize()
-            checksum[0] += float(x_h[b ^ 1, :, 3].sum())
+        def step_host(f, first):
+            tr2.step()
+            b = f & 1
+            for s in range(Sn):
+                tr2.result_async(s, x_h[b, s], v_h[b, s])
+            for ev, ts in zip(done[b], tr2.torch_streams):
+                ev.record(ts)
+            if not first:                     # frame f-1's results are complete on the host
+                for ev in done[b ^ 1]:
+                    ev.synchronize()
+                checksum[0] += float(x_h[b ^ 1, :, 3].sum())
 
-    for f in range(AHEAD):
-        queue_host(f)
-    for f in range(W):
-        queue_host(f + AHEAD)
-        step_host(f, f == 0)
-    tr2.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for f in range(W, W + K):
-        queue_host(f + AHEAD)
-        step_host(f, False)
-    for ev in done[(W + K - 1) & 1]:       # the last frame's results
-        ev.synchronize()
-    tr2.synchronize()
-    e1.record(stream)
-    e1.synchronize()
-    barrier()
-    ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+        for f in range(AHEAD):
+            queue_host(f)
+        for f in range(W):
+            queue_host(f + AHEAD)
+            step_host(f, f == 0)
+        tr2.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for f in range(W, W + K):
+            queue_host(f + AHEAD)
+            step_host(f, False)
+        for ev in done[(W + K - 1) & 1]:       # the last frame's results
+            ev.synchronize()
+        tr2.synchronize()
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+        return tr2, max_over_ranks(e0.elapsed_time(e1)), x_h, v_h
+
+    tr2, ms_e2e, x_h, v_h = run_e2e(img_h)
     # results of every stream to rank 0 (the tracking job's only collective,
     # NCCL; outside the timed regions): the last solved frame of each stream
     gathered = None
@@ -400,6 +404,24 @@ def run_ours(args):
         if rank == 0:
             gathered = int(g[0].shape[0])
     tr2.close()
+    # the same e2e loop with 8-bit frames (the reference's on-disk capture
+    # format, frames/*.png read by load_color): the images are the synthetic
+    # frames quantized to u8, converted on the device bit-exactly as
+    # load_color does (u8 / 255); informational, the headline e2e stays f64
+    e2e_u8 = None
+    if not args.no_e2e_u8:
+        img_q = torch.empty((Sn, F, H, Wd, 3), dtype=torch.uint8, pin_memory=True)
+        for s_ in range(Sn):
+            for f_ in range(F):
+                img_q[s_, f_].copy_(torch.round(img_h[s_, f_] * 255.0).clamp_(0, 255).to(torch.uint8))
+        tr3, ms_u8, _, _ = run_e2e(img_q)
+        tr3.close()
+        del img_q
+        e2e_u8 = {"value": world * Sn * K / (ms_u8 / 1e3), "unit": "frames/s",
+                  "h2d_bytes_per_step": Sn * (H * Wd * 3 + H * Wd + (actor.skeleton.n_joints + 4) * 2 * 8
+                                              + actor.skeleton.n_joints * 3 * 8 + 2 * actor.skeleton.n_joints + 4),
+                  "d2h_bytes_per_step": Sn * (36 * 8 + N * 3 * 8),
+                  "note": "frames quantized to 8 bits (PNG capture format), uploaded as u8 and converted on the device"}
     h2d = Sn * (H * Wd * 3 * 8 + H * Wd + (actor.skeleton.n_joints + 4) * 2 * 8
                 + actor.skeleton.n_joints * 3 * 8 + 2 * actor.skeleton.n_joints + 4)
     d2h = Sn * (36 * 8 + N * 3 * 8)
@@ -416,6 +438,7 @@ def run_ours(args):
             "config": workload(args, world),
             "e2e": {"value": world * Sn * K / (ms_e2e / 1e3), "unit": "frames/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e_u8": e2e_u8,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "kernel": DOMINANT, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak if peak else None,

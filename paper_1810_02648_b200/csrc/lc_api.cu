@@ -154,8 +154,8 @@ static int cluster_size_for(const char *var) {
 static int cluster_size() {
     static int cs = [] {
         const char *v = getenv("LIVECAP_CLUSTER");
-        int x = v ? atoi(v) : 8;
-        return (x == 1 || x == 4 || x == 8 || x == 16) ? x : 8;
+        int x = v ? atoi(v) : 4;
+        return (x == 1 || x == 4 || x == 8 || x == 16) ? x : 4;
     }();
     return cs;
 }
@@ -1267,10 +1267,14 @@ static void pose_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, cons
 
 static void surface_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, const ConfigDev &cf,
                            const std::vector<SurfJob> &jobs) {
-    // the surface solver's phases (edges, vertices, rows) spread over 16 CTAs
-    // (non-portable cluster) run measurably faster than over 8 on B200
+    // 4-CTA teams for both solvers: a stream's solve is latency-bound, so
+    // with many streams in flight (the throughput case, bench.py: 16 streams
+    // in 4 groups) fewer SMs per stream give more frames/s per GPU
+    // (measured: pose/surface teams 4/4 3.93k frames/s, 4/8 3.76k, 8/16
+    // 3.26k, 4/1 2.83k).  A single latency-critical stream solves fastest
+    // with LIVECAP_POSE_CLUSTER=8 LIVECAP_SURFACE_CLUSTER=16.
     static const int cs_env = cluster_size_for("LIVECAP_SURFACE_CLUSTER");
-    static const int cs_def = getenv("LIVECAP_CLUSTER") ? cluster_size() : 16;
+    static const int cs_def = cluster_size();
     const int cs = cs_env > 0 ? cs_env : cs_def;
     auto k = cs == 1 ? k_surface_solve_t<1> : cs == 4 ? k_surface_solve_t<4>
              : cs == 8 ? k_surface_solve_t<8> : k_surface_solve_t<16>;

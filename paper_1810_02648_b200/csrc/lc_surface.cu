@@ -18,6 +18,11 @@ namespace {
 #ifndef LC_SURF_NT
 #define LC_SURF_NT 512
 #endif
+// resident CTAs per SM the register budget is sized for (2: two streams'
+// teams share each SM, so one team's barrier waits hide behind the other's work)
+#ifndef LC_SURF_MINB
+#define LC_SURF_MINB 1
+#endif
 constexpr int NT = LC_SURF_NT;
 
 struct SurfCtx {
@@ -648,7 +653,7 @@ __device__ __forceinline__ void stamp(const SurfJob &J, int &k) {
 }  // namespace
 
 template <int CS>
-__global__ void __launch_bounds__(NT, 1) k_surface_solve_t(JobArg<SurfJob> jobs, ActorDev A, CamDev cam,
+__global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<SurfJob> jobs, ActorDev A, CamDev cam,
                                                            EdgeConstDev ec, SurfHyperDev hp, int H,
                                                            int W) {
     lc_pdl_wait();
