@@ -301,9 +301,14 @@ def run_ours(args):
     l0 = tr.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
+    host_q = host_s = 0.0
     for f in range(W, W + K):
+        h0 = time.perf_counter()
         queue_dev(f + AHEAD)
+        h1 = time.perf_counter()
         tr.step()
+        host_s += time.perf_counter() - h1
+        host_q += h1 - h0
     tr.synchronize()             # every group's solve, preprocessing and copy streams
     ev1.record(stream)
     ev1.synchronize()
@@ -462,6 +467,9 @@ def run_ours(args):
                                 "(PCG phase incl. setup) / iterations, device timestamps",
             "gathered_streams": gathered,
             "per_stream_fps": 1e3 * K / ms_max,
+            # host wall time per step spent queueing frames / enqueueing the
+            # groups' steps (close to ms_per_step = host-bound enqueue)
+            "host_ms_per_step": {"queue": 1e3 * host_q / K, "step": 1e3 * host_s / K},
             "clocks": clk,
             "cpu_baseline": cpu,
             "input_generation_s": round(t_gen, 2),

@@ -434,6 +434,9 @@ __global__ void k_cell_jfa(JobArg<GridJob> jobs, int ncx, int ncy) {
 #ifndef LC_DOMINATORS
 #define LC_DOMINATORS 16
 #endif
+#ifndef LC_SEED_PRUNE
+#define LC_SEED_PRUNE 1
+#endif
 __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H, int W) {
     lc_pdl_wait();
     const GridJob J = jobs[blockIdx.y];
@@ -452,6 +455,27 @@ __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H,
             u2 = seed >= 0 ? cell_far2(cx, cy, g.pts[seed]) : LC_INF;
             ok = u2 <= J.max_u2;
         }
+        // the jump-flooded seed (a real site near the cell) already dominates
+        // most far candidates: drop them while collecting, so the sort and
+        // the full dominance pass below see short lists (same exactness
+        // argument as the dominance pruning: |q-s|^2 - |q-t|^2 >= 1 over the
+        // whole cell means s is never the nearest, nor tied with it)
+        const int X0 = cx * LC_GRID_CELL, Y0 = cy * LC_GRID_CELL;
+        const int X1 = X0 + LC_GRID_CELL, Y1 = Y0 + LC_GRID_CELL;
+        int2 sd = make_int2(0, 0);
+        bool has_sd = false;
+        if (ok && LC_SEED_PRUNE) {
+            const int seed = J.cell_seed[c];
+            if (seed >= 0) { sd = g.pts[seed]; has_sd = true; }
+        }
+        auto seed_dominates = [&](int2 p) {
+            if (!has_sd || (sd.x == p.x && sd.y == p.y)) return false;
+            const long long s2 = (long long)p.x * p.x + (long long)p.y * p.y;
+            const long long a = 2LL * (sd.x - p.x), b = 2LL * (sd.y - p.y);
+            const long long c0 = s2 - ((long long)sd.x * sd.x + (long long)sd.y * sd.y);
+            return a * X0 + b * Y0 + c0 >= 1 && a * X1 + b * Y0 + c0 >= 1 && a * X0 + b * Y1 + c0 >= 1 &&
+                   a * X1 + b * Y1 + c0 >= 1;
+        };
         if (ok) {
             quad_walk_warp(g, cell_box(cx, cy), [&](double n2) { return n2 <= u2; },
                            [&](int k0, int k1) {
@@ -463,7 +487,7 @@ __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H,
                                    if (kk < k1) {
                                        pid = g.cell_pts[kk];
                                        p = g.pts[pid];
-                                       take = cell_near2(cx, cy, p) <= u2;
+                                       take = cell_near2(cx, cy, p) <= u2 && !seed_dominates(p);
                                    }
                                    const unsigned bal = __ballot_sync(0xffffffffu, take);
                                    const int at = n + __popc(bal & ((1u << lane) - 1u));
@@ -507,8 +531,6 @@ __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H,
                 tx[d] = p.x;
                 ty[d] = p.y;
             }
-            const int X0 = cx * LC_GRID_CELL, Y0 = cy * LC_GRID_CELL;
-            const int X1 = X0 + LC_GRID_CELL, Y1 = Y0 + LC_GRID_CELL;
             int m = 0;
             for (int base = 0; base < n; base += 32) {
                 const int i = base + lane;
