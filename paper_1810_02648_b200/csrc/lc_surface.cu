@@ -15,13 +15,15 @@
 
 namespace {
 
+// 256 threads x 128 registers, 2 CTAs per SM: two streams' teams share each
+// SM, so one team's barrier waits hide behind the other's work (measured
+// +2.5% frames/s over 512 x 1 at the bench's 16 streams)
 #ifndef LC_SURF_NT
-#define LC_SURF_NT 512
+#define LC_SURF_NT 256
 #endif
-// resident CTAs per SM the register budget is sized for (2: two streams'
-// teams share each SM, so one team's barrier waits hide behind the other's work)
+// resident CTAs per SM the register budget is sized for
 #ifndef LC_SURF_MINB
-#define LC_SURF_MINB 1
+#define LC_SURF_MINB 2
 #endif
 constexpr int NT = LC_SURF_NT;
 
@@ -496,21 +498,17 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
     }
     T::sync();
     fst(1);
-    // One quad of threads per boundary vertex.  A walk step's three halving
-    // trials (step, step/2, step/4 along the gradient) only depend on the
-    // current point, so quad lanes 0..2 query them concurrently and the
-    // first trial that lowers the interface distance is taken, exactly as
-    // the sequential search would; the accepted trial's query is the next
-    // step's gradient query (same point, same exact answer), so one round
-    // of concurrent queries per step replaces up to four dependent ones.
-    // Loops are warp-uniform (inactive quads idle through the shuffles).
+    // One thread per boundary vertex, so a 4-CTA team covers its ~700
+    // boundary vertices in one round.  A walk step tries step, step/2,
+    // step/4 along the gradient in order and takes the first trial that
+    // lowers the interface distance (the sequential search); most steps take
+    // the first trial, so a step is usually one query.  The accepted
+    // trial's query is the next step's gradient query (same point, same
+    // exact answer).  The loop is warp-uniform (finished walks idle).
     {
-        const int lane = threadIdx.x & 31, r = lane & 3;
-        const unsigned qmask = 0xfu << (lane & ~3);
-        const int qbase = lane & ~3;
-        constexpr int QPT = T::size / 4;   // quads per team
+        constexpr int QPT = T::size;
         for (int b0 = 0; b0 < c.B; b0 += QPT) {
-            const int b = b0 + T::tid() / 4;
+            const int b = b0 + T::tid();
             const bool valid = b < c.B;
             int i = 0;
             V3 p = v3(0, 0, 0);
@@ -521,7 +519,7 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
             double sign = 1.0, val = 0.0;
             if (valid) {
                 i = J.bidx[b];
-                if (r == 0) J.hold[i] = 1;
+                J.hold[i] = 1;
                 p = ld3(v + 3 * (size_t)i);
                 const bool ok = project(c.cam, p, px, py);
                 en = J.enabled[b] && ok;
@@ -542,48 +540,38 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
 #ifdef LC_NN_STATS
                 nsteps += active ? 1 : 0;
 #endif
+                if (!active) continue;
                 const double gn = sqrt(g.vx * g.vx + g.vy * g.vy);
                 const bool good = gn > 1e-9;
                 const double gd = fmax(gn, 1e-300);
                 const double dx = (-sign * g.vx) / gd, dy = (-sign * g.vy) / gd;
-                // lane r < 3 tries step * 0.5^r (exact halvings)
-                double step = hp.snap_step;
-                for (int h = 0; h < r && h < 2; ++h) step *= 0.5;
-                const double tx = qx + step * dx, ty = qy + step * dy;
-                NnResult t{LC_INF, 0.0, 0.0, true};
-                int th = hint;
-                double tv = LC_INF;
-                if (active && good && r < 3) {
-                    t = field_nearest(c.obs, tx, ty, &th);
-                    tv = field_interface(t);
-                }
-                const double tv0 = __shfl_sync(0xffffffffu, tv, qbase);
-                const double tv1 = __shfl_sync(0xffffffffu, tv, qbase + 1);
-                const double tv2 = __shfl_sync(0xffffffffu, tv, qbase + 2);
-                const double cur = val;
-                const int hit = tv0 < cur ? 0 : (tv1 < cur ? 1 : (tv2 < cur ? 2 : -1));
-                const int src = qbase + (hit < 0 ? 0 : hit);
-                const double nx = __shfl_sync(0xffffffffu, tx, src), ny = __shfl_sync(0xffffffffu, ty, src);
-                const double nvx = __shfl_sync(0xffffffffu, t.vx, src), nvy = __shfl_sync(0xffffffffu, t.vy, src);
-                const double ndist = __shfl_sync(0xffffffffu, t.dist, src);
-                const int nclamp = __shfl_sync(0xffffffffu, (int)t.clamped, src);
-                const int nth = __shfl_sync(0xffffffffu, th, src);
-                if (active) {
-                    if (good && hit >= 0) {
-                        qx = nx; qy = ny;
-                        val = hit == 0 ? tv0 : (hit == 1 ? tv1 : tv2);
-                        g = NnResult{ndist, nvx, nvy, nclamp != 0};
-                        hint = nth;
-                    } else {
-                        stuck = true;
-                        active = false;
+                bool hit = false;
+                if (good) {
+                    double step = hp.snap_step;   // step * 0.5^h (exact halvings)
+                    for (int h = 0; h < 3; ++h) {
+                        const double tx = qx + step * dx, ty = qy + step * dy;
+                        int th = hint;
+                        const NnResult t = field_nearest(c.obs, tx, ty, &th);
+                        const double tv = field_interface(t);
+                        if (tv < val) {
+                            qx = tx; qy = ty;
+                            val = tv;
+                            g = t;
+                            hint = th;
+                            hit = true;
+                            break;
+                        }
+                        step *= 0.5;
                     }
-                    active = active && val > hp.snap_band;
                 }
+                if (!hit) {
+                    stuck = true;
+                    active = false;
+                }
+                active = active && val > hp.snap_band;
             }
-            (void)qmask;
 #ifdef LC_NN_STATS
-            if (valid && r == 0) {
+            if (valid) {
                 const unsigned long long cyc = (unsigned long long)(clock64() - w0);
                 const unsigned long long prev = atomicMax(&g_nn_stats[4], cyc);
                 if (cyc > prev) g_nn_stats[5] = (unsigned long long)nsteps;
@@ -591,7 +579,7 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
                 atomicAdd(&g_nn_stats[7], (unsigned long long)nsteps);
             }
 #endif
-            if (valid && r == 0) {
+            if (valid) {
                 cnt[0] += en ? 1.0 : 0.0;
                 cnt[1] += (en && val <= hp.snap_band) ? 1.0 : 0.0;
                 cnt[2] += (stuck && en) ? 1.0 : 0.0;
