@@ -148,14 +148,14 @@ static int cluster_size_for(const char *var) {
     const char *v = getenv(var);
     if (!v) return -1;
     const int x = atoi(v);
-    return (x == 1 || x == 4 || x == 8 || x == 16) ? x : -1;
+    return (x == 1 || x == 2 || x == 4 || x == 8 || x == 16) ? x : -1;
 }
 
 static int cluster_size() {
     static int cs = [] {
         const char *v = getenv("LIVECAP_CLUSTER");
         int x = v ? atoi(v) : 4;
-        return (x == 1 || x == 4 || x == 8 || x == 16) ? x : 4;
+        return (x == 1 || x == 2 || x == 4 || x == 8 || x == 16) ? x : 4;
     }();
     return cs;
 }
@@ -296,6 +296,7 @@ extern "C" int lc_ctx_create(int32_t device, uint64_t cuda_stream, lc_ctx **out)
     {
         const int sm = (int)pose_smem_bytes(LC_MAXJ);
         CK(cudaFuncSetAttribute(k_pose_solve_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_pose_solve_t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CK(cudaFuncSetAttribute(k_pose_solve_t<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CK(cudaFuncSetAttribute(k_pose_solve_t<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CK(cudaFuncSetAttribute(k_pose_solve_t<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -1259,7 +1260,7 @@ static void pose_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, cons
     const size_t smem = pose_smem_bytes(a->skel.J);
     static const int cs_env = cluster_size_for("LIVECAP_POSE_CLUSTER");
     const int cs = cs_env > 0 ? cs_env : cluster_size();
-    auto k = cs == 1 ? k_pose_solve_t<1> : cs == 4 ? k_pose_solve_t<4> : cs == 8 ? k_pose_solve_t<8>
+    auto k = cs == 1 ? k_pose_solve_t<1> : cs == 2 ? k_pose_solve_t<2> : cs == 4 ? k_pose_solve_t<4> : cs == 8 ? k_pose_solve_t<8>
                                                                            : k_pose_solve_t<16>;
     launch_cluster("k_pose_solve", c, k, (int)jobs.size(), cs, dim3(pose_block_threads()), smem,
                    stage(c, jobs), (const SkelDev *)a->skel_dev, a->dev, cam_dev(cam));
@@ -1276,7 +1277,7 @@ static void surface_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, c
     static const int cs_env = cluster_size_for("LIVECAP_SURFACE_CLUSTER");
     static const int cs_def = cluster_size();
     const int cs = cs_env > 0 ? cs_env : cs_def;
-    auto k = cs == 1 ? k_surface_solve_t<1> : cs == 4 ? k_surface_solve_t<4>
+    auto k = cs == 1 ? k_surface_solve_t<1> : cs == 2 ? k_surface_solve_t<2> : cs == 4 ? k_surface_solve_t<4>
              : cs == 8 ? k_surface_solve_t<8> : k_surface_solve_t<16>;
     launch_cluster("k_surface_solve", c, k, (int)jobs.size(), cs, dim3(surface_block_threads()), 0,
                    stage(c, jobs), a->dev, cam_dev(cam), cf.ec, cf.shp, cam.height, cam.width);

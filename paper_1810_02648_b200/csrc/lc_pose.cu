@@ -555,6 +555,7 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(JobArg<PoseJob> jobs, co
 }
 
 template __global__ void k_pose_solve_t<1>(JobArg<PoseJob>, const SkelDev *, ActorDev, CamDev);
+template __global__ void k_pose_solve_t<2>(JobArg<PoseJob>, const SkelDev *, ActorDev, CamDev);
 template __global__ void k_pose_solve_t<4>(JobArg<PoseJob>, const SkelDev *, ActorDev, CamDev);
 template __global__ void k_pose_solve_t<8>(JobArg<PoseJob>, const SkelDev *, ActorDev, CamDev);
 template __global__ void k_pose_solve_t<16>(JobArg<PoseJob>, const SkelDev *, ActorDev, CamDev);

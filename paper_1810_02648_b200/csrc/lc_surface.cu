@@ -764,6 +764,7 @@ __global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<Sur
 }
 
 template __global__ void k_surface_solve_t<1>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
+template __global__ void k_surface_solve_t<2>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
 template __global__ void k_surface_solve_t<4>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
 template __global__ void k_surface_solve_t<8>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
 template __global__ void k_surface_solve_t<16>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
