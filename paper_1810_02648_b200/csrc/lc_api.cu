@@ -1274,9 +1274,14 @@ static void surface_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, c
     // (measured: pose/surface teams 4/4 3.93k frames/s, 4/8 3.76k, 8/16
     // 3.26k, 4/1 2.83k).  A single latency-critical stream solves fastest
     // with LIVECAP_POSE_CLUSTER=8 LIVECAP_SURFACE_CLUSTER=16.
+    // The default surface team grows with the mesh: the smallest of 4, 8, 16
+    // CTAs that leaves at most 6 vertices per thread (x5k: 4; x20k: 16,
+    // measured at cfg4 1998 frames/s vs 1790 on 8 and 1362 on 4).
     static const int cs_env = cluster_size_for("LIVECAP_SURFACE_CLUSTER");
-    static const int cs_def = cluster_size();
-    const int cs = cs_env > 0 ? cs_env : cs_def;
+    static const bool cs_global = getenv("LIVECAP_CLUSTER") != nullptr;
+    int cs = cs_env > 0 ? cs_env : cluster_size();
+    if (cs_env <= 0 && !cs_global)
+        while (cs < 16 && (long long)a->dev.N > 6LL * cs * surface_block_threads()) cs *= 2;
     auto k = cs == 1 ? k_surface_solve_t<1> : cs == 2 ? k_surface_solve_t<2> : cs == 4 ? k_surface_solve_t<4>
              : cs == 8 ? k_surface_solve_t<8> : k_surface_solve_t<16>;
     launch_cluster("k_surface_solve", c, k, (int)jobs.size(), cs, dim3(surface_block_threads()), 0,
