@@ -56,6 +56,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e-u8", action="store_true", help="skip the 8-bit-frame e2e leg")
     ap.add_argument("--cpu-frames", type=int, default=3, help="timed steady frames of the CPU baseline")
+    ap.add_argument("--directional", action="store_true",
+                    help="SequenceConfig(directional=True): the reference's default, which loses the subject "
+                         "on this workload (VERDICT r01); the default workload tracks (directional=False)")
+    ap.add_argument("--no-quality", action="store_true", help="skip the untimed tracking-quality replay")
     return ap.parse_args()
 
 
@@ -78,13 +82,25 @@ def aggregate_fps(ms_per_rank, world, streams_per_gpu, steps):
     return world * streams_per_gpu * steps / (max(ms_per_rank) / 1e3)
 
 
+def make_config(args):
+    from paper_1810_02648_b200.config import SequenceConfig
+    cfg = SequenceConfig(directional=bool(args.directional))
+    if args.gn is not None:
+        cfg.nonrigid.gn_iterations = args.gn
+    if args.pcg is not None:
+        cfg.nonrigid.pcg_iterations = args.pcg
+    return cfg
+
+
 def workload(args, world):
     return {"workload": f"cfg3-shaped full two-stage solve_frame, {args.preset} template @ "
-                        f"{args.res}x{args.res}, {args.streams} synthetic streams per GPU (cfg5 sharding)",
+                        f"{args.res}x{args.res}, {args.streams} synthetic streams per GPU (cfg5 sharding), "
+                        f"{'directional' if args.directional else 'in-track (directional=False)'} silhouette rows",
             "preset": args.preset, "resolution": args.res, "streams_per_gpu": args.streams,
             "stream_groups": args.groups,
             "host_threads": bool(args.host_threads),
             "nonrigid_gn_pcg": [args.gn or 3, args.pcg or 4],
+            "directional": bool(args.directional),
             "total_streams": args.streams * world, "parallelism": f"stream-sharded x{world}",
             "l2": "per-step inputs (images + pyramids) exceed the 126 MB L2; no flush needed"}
 
@@ -251,11 +267,7 @@ def run_ours(args):
     msk_d.copy_(msk_h)
     torch.cuda.synchronize()
     dets = [[frames[s][f].detections for f in range(F)] for s in range(Sn)]
-    cfg = SequenceConfig()
-    if args.gn is not None:
-        cfg.nonrigid.gn_iterations = args.gn
-    if args.pcg is not None:
-        cfg.nonrigid.pcg_iterations = args.pcg
+    cfg = make_config(args)
 
     def barrier():
         if world > 1:
@@ -427,6 +439,14 @@ def run_ours(args):
                                               + actor.skeleton.n_joints * 3 * 8 + 2 * actor.skeleton.n_joints + 4),
                   "d2h_bytes_per_step": Sn * (36 * 8 + N * 3 * 8),
                   "note": "frames quantized to 8 bits (PNG capture format), uploaded as u8 and converted on the device"}
+    # ---- tracking quality of the timed frames (untimed replay: the tracker
+    # is deterministic, so the replay solves exactly the frames the timed
+    # legs solved; checked against the e2e leg's last poses)
+    quality = None
+    if not args.no_quality:
+        last = (W + K - 1) & 1
+        quality = tracking_quality(actor, cam, cfg, Sn, args.groups, local, img_d, msk_d, dets, frames, W, K,
+                                   x_h[last].numpy().copy())
     h2d = Sn * (H * Wd * 3 * 8 + H * Wd + (actor.skeleton.n_joints + 4) * 2 * 8
                 + actor.skeleton.n_joints * 3 * 8 + 2 * actor.skeleton.n_joints + 4)
     d2h = Sn * (36 * 8 + N * 3 * 8)
@@ -471,6 +491,7 @@ def run_ours(args):
             # groups' steps (close to ms_per_step = host-bound enqueue)
             "host_ms_per_step": {"queue": 1e3 * host_q / K, "step": 1e3 * host_s / K},
             "clocks": clk,
+            "tracking": quality,
             "cpu_baseline": cpu,
             "input_generation_s": round(t_gen, 2),
         }
@@ -479,6 +500,52 @@ def run_ours(args):
         import torch.distributed as dist
         dist.destroy_process_group()
     return out
+
+
+# ---------------------------------------------------------------------------
+# tracking quality of the timed frames (metrics.py / evaluation.py on the device)
+
+def tracking_quality(actor, cam, cfg, Sn, groups, local, img_d, msk_d, dets, frames, W, K, x_last_e2e):
+    import numpy as np
+
+    from paper_1810_02648_b200.device import BatchTracker
+    from paper_1810_02648_b200.imageproc import render_mask
+    from paper_1810_02648_b200.metrics import aligned_joint_error_batch, iou_batch, mean_vertex_error_batch
+    from paper_1810_02648_b200.skinning import forward_kinematics
+
+    tr = BatchTracker(actor, cam, cfg, Sn, groups=groups, device=local, host_threads=False)
+    N = actor.mesh.n_vertices
+    V = np.empty((Sn, K, N, 3))
+    X = np.empty((Sn, K, 36))
+    for f in range(W + K):
+        for s in range(Sn):
+            tr.set_frame(s, img_d[s, f].data_ptr(), msk_d[s, f].data_ptr(), dets[s][f], on_device=True)
+        tr.step()
+        if f >= W:
+            for s in range(Sn):
+                x, v, _, _ = tr.result(s, with_report=False)
+                X[s, f - W], V[s, f - W] = x, v
+    tr.close()
+    ious, verr, jerr = [], [], []
+    for s in range(Sn):
+        fr = frames[s][W:W + K]
+        verr.append(mean_vertex_error_batch(V[s], np.stack([q.gt_vertices for q in fr])))
+        joints = np.stack([forward_kinematics(actor, X[s, k]).positions for k in range(K)])
+        jerr.append(aligned_joint_error_batch(joints, np.stack([q.gt_joints for q in fr])))
+        masks = np.stack([render_mask(cam, V[s, k], actor.mesh.triangles) for k in range(K)])
+        ious.append(iou_batch(masks, np.stack([q.mask for q in fr])))
+    ious, verr, jerr = np.array(ious), np.array(verr), np.array(jerr)
+    per_stream = ious.mean(axis=1)
+    return {"frames": [W, W + K - 1], "streams": Sn,
+            "iou_mean": float(ious.mean()), "iou_min": float(ious.min()),
+            "iou_per_stream": [round(float(v), 4) for v in per_stream],
+            "streams_iou_ge_0_9": int((per_stream >= 0.9).sum()),
+            "vertex_error_mm_mean": 1e3 * float(verr.mean()), "vertex_error_mm_max": 1e3 * float(verr.max()),
+            "aligned_joint_error_mm_mean": 1e3 * float(jerr.mean()),
+            "replay_identical": bool(np.array_equal(X[:, K - 1], x_last_e2e)),
+            "how": "untimed replay of the timed frames through the public API; silhouette IoU of the "
+                   "solved surface vs the observed mask, centred mean vertex error vs ground truth, "
+                   "Procrustes-aligned joint error (metrics.py, on the device)"}
 
 
 # ---------------------------------------------------------------------------
@@ -511,7 +578,7 @@ def cpu_baseline(actor, cam, frames, n_timed, cfg):
 # cores, one process per stream
 
 def _ref_worker(a):
-    preset, res, n_frames, seed, warm, gn, pcg = a
+    preset, res, n_frames, seed, warm, gn, pcg, directional = a
     os.environ["OMP_NUM_THREADS"] = "1"
     from threadpoolctl import threadpool_limits
 
@@ -529,7 +596,7 @@ def _ref_worker(a):
     actor = S.build_actor(preset, with_skirt=True)
     cam = suggest_camera(res, res)
     frames = make_stream_frames(actor, cam, n_frames, seed, OI.render_attributes, posing)
-    cfg = SequenceConfig()
+    cfg = SequenceConfig(directional=directional)
     if gn is not None:
         cfg.nonrigid.gn_iterations = gn
     if pcg is not None:
@@ -553,7 +620,7 @@ def run_reference(args):
     procs = max(1, min(args.streams, cores))
     W = max(1, args.warmup)
     K = max(1, args.steps)
-    jobs = [(args.preset, args.res, W + K, s, W, args.gn, args.pcg) for s in range(procs)]
+    jobs = [(args.preset, args.res, W + K, s, W, args.gn, args.pcg, bool(args.directional)) for s in range(procs)]
     with mp.get_context("fork").Pool(procs) as pool:
         res = pool.map(_ref_worker, jobs)
     spans = [b - a for a, b, _ in res]

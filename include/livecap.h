@@ -182,6 +182,10 @@ int lc_version(void);
 int lc_ctx_create(int32_t device, uint64_t cuda_stream, lc_ctx **out);
 int lc_ctx_destroy(lc_ctx *ctx);
 int lc_ctx_synchronize(lc_ctx *ctx);
+/* team (thread-block cluster) sizes of the pose / surface solvers launched
+ * from this context: 1, 2, 4, 8 or 16 CTAs per stream, 0 = default policy
+ * (overrides LIVECAP_POSE_CLUSTER / LIVECAP_SURFACE_CLUSTER) */
+int lc_ctx_set_team_sizes(lc_ctx *ctx, int32_t pose_ctas, int32_t surface_ctas);
 int lc_kernel_launches(lc_ctx *ctx, int64_t *count);   /* kernels launched on ctx so far */
 
 /* ---- actor (template.py:68-256; uploaded once, immutable) ---- */
@@ -193,7 +197,6 @@ int lc_actor_destroy(lc_actor *actor);
 int lc_pcg_solve_bsr(lc_ctx *ctx, int32_t n, int64_t m, const double *diag, const double *off,
                      const int64_t *rows, const int64_t *cols, const double *rhs,
                      int32_t iterations, double *x_out, lc_pcg_info *info);
-/* solvers.py:41-56 dense_solve(DenseNormalSystem) */
 /* smooth_trajectory (pipeline.py:308-325): centred weighted average of an
  * (F, D) stack along F, truncated and renormalised at the ends; bit-identical */
 int lc_smooth_trajectory(lc_ctx *ctx, int32_t F, int64_t D, const double *values, int32_t K,
@@ -201,6 +204,20 @@ int lc_smooth_trajectory(lc_ctx *ctx, int32_t F, int64_t D, const double *values
 /* metrics.iou support: per-frame |a & b| and |a | b| of two (F, HW) mask stacks */
 int lc_mask_overlap(lc_ctx *ctx, int32_t F, int64_t HW, const uint8_t *a, const uint8_t *b,
                     uint64_t *inter_out, uint64_t *union_out);
+/* metrics.py:26-46 mean_vertex_error, batched over F frames of (N,3) vertex
+ * arrays (pred, gt: F*N*3).  indices (n_idx, ascending or any order; negative
+ * = from the end) selects vertices after centring on the full clouds, NULL =
+ * all.  center 0/1.  on_device: pred, gt, indices are device pointers.
+ * Bit-identical to numpy (sequential axis-0 means, pairwise mean). */
+int lc_mean_vertex_error(lc_ctx *ctx, int32_t F, int64_t N, const double *pred, const double *gt,
+                         const int64_t *indices, int64_t n_idx, int32_t center, int32_t on_device, double *out);
+/* metrics.py:49-84 umeyama_alignment + aligned_joint_error, batched over F
+ * frames of M 3-D points: per frame scale, rot (3x3 row-major), t (3) and the
+ * mean distance after alignment (scale/rot/t outputs may be NULL). */
+int lc_aligned_error(lc_ctx *ctx, int32_t F, int32_t M, const double *pred, const double *gt,
+                     int32_t with_scaling, int32_t on_device, double *scale_out, double *rot_out,
+                     double *t_out, double *err_out);
+/* solvers.py:41-56 dense_solve(DenseNormalSystem) */
 int lc_dense_solve(lc_ctx *ctx, int32_t n, const double *a, const double *b, double *x_out,
                    lc_dense_info *info);
 /* imageproc.py:264-285 gaussian_pyramid; image H*W*C, out n_levels*H*W*C */
@@ -234,6 +251,17 @@ int lc_skin_points(lc_ctx *ctx, const lc_actor *actor, const double *x36, int32_
  * returns indices/normals, n_out = B; capacity = N. */
 int lc_contour_vertices(lc_ctx *ctx, const lc_actor *actor, const lc_camera *cam,
                         const double *verts, int32_t *n_out, int64_t *idx_out, double *n2d_out);
+
+/* The tracker's Stage I / II index and set work on caller vertices (N*3):
+ * contour indices + normals2d (capacity N), the rim keep flags (stage 1:
+ * outer_rim_mask with thickness probes AND rigidity >= 2, pipeline.py:211;
+ * stage 2: outer_rim_mask(min_thickness=0), AND the part gating of
+ * pipeline.py:241-249 when part_gate), visible ids (stage 2; capacity N),
+ * optional full part label image (H*W int32, nonrigid_stage.py:102-128). */
+int lc_surface_sets(lc_ctx *ctx, const lc_actor *actor, const lc_camera *cam, const double *verts,
+                    int32_t stage, int32_t part_gate, int32_t dilation, int32_t *n_contour,
+                    int64_t *idx_out, double *n2d_out, uint8_t *keep_out, int32_t *n_visible,
+                    int64_t *vis_out, int32_t *labels_out);
 
 /* ---- stage solvers ---- */
 /* pose_stage.py:429-459 solve_pose */

@@ -116,6 +116,8 @@ _SIGS = {
     "lc_ctx_create": (C.c_int, [i32, u64, P]),
     "lc_ctx_destroy": (C.c_int, [P]),
     "lc_ctx_synchronize": (C.c_int, [P]),
+    "lc_ctx_set_team_sizes": (C.c_int, [P, i32, i32]),
+    "lc_surface_sets": (C.c_int, [P, P, P, P, i32, i32, i32, P, P, P, P, P, P, P]),
     "lc_kernel_launches": (C.c_int, [P, P]),
     "lc_actor_upload": (C.c_int, [P, P, P]),
     "lc_actor_destroy": (C.c_int, [P]),
@@ -123,6 +125,8 @@ _SIGS = {
     "lc_dense_solve": (C.c_int, [P, i32, P, P, P, P]),
     "lc_smooth_trajectory": (C.c_int, [P, i32, C.c_int64, P, i32, P, P]),
     "lc_mask_overlap": (C.c_int, [P, i32, C.c_int64, P, P, P, P]),
+    "lc_mean_vertex_error": (C.c_int, [P, i32, C.c_int64, P, P, P, C.c_int64, i32, i32, P]),
+    "lc_aligned_error": (C.c_int, [P, i32, i32, P, P, i32, i32, P, P, P, P]),
     "lc_gaussian_pyramid": (C.c_int, [P, i32, i32, i32, P, i32, P, P, P]),
     "lc_render": (C.c_int, [P, P, i32, P, i32, P, i32, P, i32, P, f64, i64, P, P, P]),
     "lc_field_create": (C.c_int, [P, i32, i32, P, P]),
@@ -252,6 +256,10 @@ class Context:
 
     def synchronize(self):
         check(self.lib.lc_ctx_synchronize(self.handle))
+
+    def set_team_sizes(self, pose: int = 0, surface: int = 0):
+        """CTAs per stream of the pose / surface solver teams (0 = default)."""
+        check(self.lib.lc_ctx_set_team_sizes(self.handle, int(pose), int(surface)))
 
     def close(self):
         if self.handle:

@@ -1,6 +1,6 @@
 """Pinhole intrinsics container (reference `camera.py:20-33`).
 
-Projection itself runs on the device (`csrc/common.cuh: project`); this
+Projection itself runs on the device (`csrc/lc_device.cuh: project`); this
 module only validates and carries the six numbers across the C-ABI.
 """
 

@@ -620,8 +620,23 @@ extern "C" int lc_actor_upload(lc_ctx *c, const lc_actor_desc *d, lc_actor **out
     API_END
 }
 
+// per-context team sizes of the pose / surface solvers (1, 2, 4, 8 or 16
+// CTAs per stream; 0 restores the default policy).  Results do not depend on
+// the team size beyond fp64 reduction order.
+extern "C" int lc_ctx_set_team_sizes(lc_ctx *c, int32_t pose_ctas, int32_t surface_ctas) {
+    API_BEGIN
+    require(c != nullptr, "null context");
+    auto ok = [](int x) { return x == 0 || x == 1 || x == 2 || x == 4 || x == 8 || x == 16; };
+    require(ok(pose_ctas) && ok(surface_ctas), "team sizes must be 0 (default), 1, 2, 4, 8 or 16");
+    c->pose_cs = pose_ctas;
+    c->surf_cs = surface_ctas;
+    return LC_OK;
+    API_END
+}
+
 extern "C" int lc_actor_destroy(lc_actor *a) {
     if (!a) return LC_OK;
+    cudaSetDevice(a->ctx->device);
     cudaStreamSynchronize(a->ctx->stream);
     if (a->ctx->call_actor == a) a->ctx->call_actor = nullptr;
     delete a;
@@ -1259,7 +1274,7 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
 static void pose_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, const std::vector<PoseJob> &jobs) {
     const size_t smem = pose_smem_bytes(a->skel.J);
     static const int cs_env = cluster_size_for("LIVECAP_POSE_CLUSTER");
-    const int cs = cs_env > 0 ? cs_env : cluster_size();
+    const int cs = c->pose_cs > 0 ? c->pose_cs : cs_env > 0 ? cs_env : cluster_size();
     auto k = cs == 1 ? k_pose_solve_t<1> : cs == 2 ? k_pose_solve_t<2> : cs == 4 ? k_pose_solve_t<4> : cs == 8 ? k_pose_solve_t<8>
                                                                            : k_pose_solve_t<16>;
     launch_cluster("k_pose_solve", c, k, (int)jobs.size(), cs, dim3(pose_block_threads()), smem,
@@ -1279,8 +1294,8 @@ static void surface_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, c
     // measured at cfg4 1998 frames/s vs 1790 on 8 and 1362 on 4).
     static const int cs_env = cluster_size_for("LIVECAP_SURFACE_CLUSTER");
     static const bool cs_global = getenv("LIVECAP_CLUSTER") != nullptr;
-    int cs = cs_env > 0 ? cs_env : cluster_size();
-    if (cs_env <= 0 && !cs_global)
+    int cs = c->surf_cs > 0 ? c->surf_cs : cs_env > 0 ? cs_env : cluster_size();
+    if (c->surf_cs <= 0 && cs_env <= 0 && !cs_global)
         while (cs < 16 && (long long)a->dev.N > 6LL * cs * surface_block_threads()) cs *= 2;
     auto k = cs == 1 ? k_surface_solve_t<1> : cs == 2 ? k_surface_solve_t<2> : cs == 4 ? k_surface_solve_t<4>
              : cs == 8 ? k_surface_solve_t<8> : k_surface_solve_t<16>;
@@ -1479,6 +1494,7 @@ extern "C" int lc_tracker_create(lc_ctx *c, const lc_actor *a, const lc_camera *
 
 extern "C" int lc_tracker_destroy(lc_tracker *t) {
     if (!t) return LC_OK;
+    cudaSetDevice(t->ctx->device);
     cudaStreamSynchronize(t->ctx->stream);
     cudaStreamSynchronize(t->ctx->aux);   // queued frames may still be preprocessing
     cudaStreamSynchronize(t->ctx->copy);
@@ -1496,6 +1512,7 @@ extern "C" int lc_tracker_set_frame(lc_tracker *t, int32_t stream, const double 
     API_BEGIN
     require(t && det, "null argument");
     require(stream >= 0 && stream < t->S, "stream index out of range");
+    CK(cudaSetDevice(t->ctx->device));   // the tracker's streams belong to its device
     require(image && mask, "null image or mask");
     Slot *s = t->slots[stream];
     lc_ctx *c = t->ctx;
@@ -1542,6 +1559,7 @@ extern "C" int lc_tracker_set_frame_u8(lc_tracker *t, int32_t stream, const uint
     API_BEGIN
     require(t && det && image_rgb && mask, "null argument");
     require(stream >= 0 && stream < t->S, "stream index out of range");
+    CK(cudaSetDevice(t->ctx->device));   // the tracker's streams belong to its device
     Slot *s = t->slots[stream];
     lc_ctx *c = t->ctx;
     FrameIn &f = s->in[s->in_tail];
@@ -1623,6 +1641,7 @@ extern "C" int lc_tracker_get_result(lc_tracker *t, int32_t stream, double *pose
     API_BEGIN
     require(t != nullptr, "null tracker");
     require(stream >= 0 && stream < t->S, "stream index out of range");
+    CK(cudaSetDevice(t->ctx->device));   // the tracker's streams belong to its device
     Slot *s = t->slots[stream];
     lc_ctx *c = t->ctx;
     const size_t N = s->N;
@@ -1701,6 +1720,7 @@ extern "C" int lc_tracker_get_result_async(lc_tracker *t, int32_t stream, double
     API_BEGIN
     require(t != nullptr, "null tracker");
     require(stream >= 0 && stream < t->S, "stream index out of range");
+    CK(cudaSetDevice(t->ctx->device));   // the tracker's streams belong to its device
     Slot *s = t->slots[stream];
     lc_ctx *c = t->ctx;
     if (pose_out) CK(cudaMemcpyAsync(pose_out, s->x_prev, sizeof(double) * LC_NP, cudaMemcpyDeviceToHost, c->stream));
@@ -1716,6 +1736,7 @@ extern "C" int lc_tracker_set_state(lc_tracker *t, int32_t stream, const double 
     API_BEGIN
     require(t != nullptr, "null tracker");
     require(stream >= 0 && stream < t->S, "stream index out of range");
+    CK(cudaSetDevice(t->ctx->device));   // the tracker's streams belong to its device
     Slot *s = t->slots[stream];
     lc_ctx *c = t->ctx;
     const size_t N = s->N;
@@ -1746,6 +1767,7 @@ extern "C" int lc_tracker_get_state(lc_tracker *t, int32_t stream, int32_t *flag
     API_BEGIN
     require(t != nullptr, "null tracker");
     require(stream >= 0 && stream < t->S, "stream index out of range");
+    CK(cudaSetDevice(t->ctx->device));   // the tracker's streams belong to its device
     Slot *s = t->slots[stream];
     lc_ctx *c = t->ctx;
     const size_t N = s->N;
@@ -1772,6 +1794,7 @@ extern "C" int lc_tracker_counters(lc_tracker *t, int32_t stream, int64_t *out) 
     API_BEGIN
     require(t && out, "null argument");
     require(stream >= 0 && stream < t->S, "stream index out of range");
+    CK(cudaSetDevice(t->ctx->device));   // the tracker's streams belong to its device
     CK(cudaMemcpyAsync(out, t->slots[stream]->counters, sizeof(long long) * LC_NCOUNTERS,
                        cudaMemcpyDeviceToHost, t->ctx->stream));
     CK(cudaStreamSynchronize(t->ctx->stream));
@@ -1784,6 +1807,7 @@ extern "C" int lc_tracker_inspect(lc_tracker *t, int32_t stream, int32_t what, v
     API_BEGIN
     require(t && out && n_out, "null argument");
     require(stream >= 0 && stream < t->S, "stream index out of range");
+    CK(cudaSetDevice(t->ctx->device));   // the tracker's streams belong to its device
     Slot *s = t->slots[stream];
     cudaStream_t st = t->ctx->stream;
     int B = 0, P = 0;
@@ -1823,6 +1847,7 @@ extern "C" int lc_tracker_phase_times(lc_tracker *t, int32_t stream, int64_t *po
     API_BEGIN
     require(t != nullptr, "null tracker");
     require(stream >= 0 && stream < t->S, "stream index out of range");
+    CK(cudaSetDevice(t->ctx->device));   // the tracker's streams belong to its device
     Slot *s = t->slots[stream];
     if (pose_ns) CK(cudaMemcpy(pose_ns, s->phase_pose, sizeof(long long) * LC_NPHASE, cudaMemcpyDeviceToHost));
     if (surf_ns) CK(cudaMemcpy(surf_ns, s->phase_surf, sizeof(long long) * LC_NPHASE, cudaMemcpyDeviceToHost));
@@ -2085,6 +2110,65 @@ extern "C" int lc_contour_vertices(lc_ctx *c, const lc_actor *a, const lc_camera
     *n_out = B;
     if (idx_out)
         for (int i = 0; i < B; ++i) idx_out[i] = idx[i];
+    return last_launch_status();
+    API_END
+}
+
+// The tracker's own index / set work on caller vertices (test seam for the
+// bit-exact set parity): raster, contour vertices +
+// normals (extract_contour_vertices, pose_stage.py:139-191), visible ids
+// (visible_vertices, nonrigid_stage.py:87-99, stage 2), the rim filter
+// (outer_rim_mask, pose_stage.py:218-264: stage 1 with the thickness probes
+// and the rigidity >= 2 gate of pipeline.py:211, stage 2 without), the part
+// gating of pipeline.py:241-249 (stage 2, part_gate) and optionally the full
+// part label image (build_body_part_mask, nonrigid_stage.py:102-128).
+extern "C" int lc_surface_sets(lc_ctx *c, const lc_actor *a, const lc_camera *cam, const double *verts,
+                               int32_t stage, int32_t part_gate, int32_t dilation, int32_t *n_contour,
+                               int64_t *idx_out, double *n2d_out, uint8_t *keep_out, int32_t *n_visible,
+                               int64_t *vis_out, int32_t *labels_out) {
+    API_BEGIN
+    require(c && a && cam && verts && n_contour, "null argument");
+    require(stage == 1 || stage == 2, "stage must be 1 or 2");
+    require(dilation >= 0 && dilation <= 64, "dilation out of range");
+    CK(cudaSetDevice(c->device));
+    const int H = cam->height, W = cam->width, N = a->dev.N;
+    Slot *s = call_slot(c, a, H, W, 1);
+    cudaStream_t st = c->stream;
+    CK(cudaMemcpyAsync(s->vinit, verts, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    lc_config cfg{};
+    cfg.enable_part_mask = part_gate;
+    cfg.nonrigid.part_dilation = dilation;
+    ConfigDev cf;
+    auto pr = probe_offsets();
+    cf.probe = cf.mem.upload(pr.data(), pr.size(), st);
+    FrameBatch fb{c, a, *cam, &cfg, &cf, {s}, {}};
+    contour_and_rim(fb, {s}, &Slot::vinit, stage == 1);
+    DevArena m;
+    int *lab = nullptr;
+    if (labels_out) {
+        lab = m.alloc<int>((size_t)H * W);
+        launch(c, k_part_labels, dim3(592), dim3(256), 0, a->dev, cam_dev(*cam), (const double *)s->vinit,
+               (const int *)s->tri_id, (int)dilation, lab);
+    }
+    int B = 0, P = 0;
+    CK(cudaMemcpyAsync(&B, s->B, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (stage == 2) CK(cudaMemcpyAsync(&P, s->P, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int> idx(B), vis(P);
+    if (B) {
+        CK(cudaMemcpyAsync(idx.data(), s->cidx, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+        if (n2d_out) CK(cudaMemcpyAsync(n2d_out, s->n2d, sizeof(double) * 2 * B, cudaMemcpyDeviceToHost, st));
+        if (keep_out) CK(cudaMemcpyAsync(keep_out, s->enabled, B, cudaMemcpyDeviceToHost, st));
+    }
+    if (P) CK(cudaMemcpyAsync(vis.data(), s->vis, sizeof(int) * P, cudaMemcpyDeviceToHost, st));
+    if (labels_out) CK(cudaMemcpyAsync(labels_out, lab, sizeof(int) * H * W, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *n_contour = B;
+    if (n_visible) *n_visible = P;
+    if (idx_out)
+        for (int i = 0; i < B; ++i) idx_out[i] = idx[i];
+    if (vis_out)
+        for (int i = 0; i < P; ++i) vis_out[i] = vis[i];
     return last_launch_status();
     API_END
 }
@@ -2383,6 +2467,73 @@ extern "C" int lc_mask_overlap(lc_ctx *c, int32_t F, int64_t HW, const uint8_t *
            (long long)HW, di, du);
     CK(cudaMemcpyAsync(inter_out, di, sizeof(uint64_t) * F, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(union_out, du, sizeof(uint64_t) * F, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return last_launch_status();
+    API_END
+}
+
+__global__ void k_vertex_error(int F, long long N, const double *pred, const double *gt, const long long *idx,
+                               long long n_sel, int center, double *dist, double *out);
+__global__ void k_umeyama(int F, int M, const double *src_all, const double *dst_all, int with_scaling,
+                          double *scale_out, double *rot_out, double *t_out, double *err_out, double *scratch);
+
+// metrics.mean_vertex_error over F frames (bit-identical to numpy)
+extern "C" int lc_mean_vertex_error(lc_ctx *c, int32_t F, int64_t N, const double *pred, const double *gt,
+                                    const int64_t *indices, int64_t n_idx, int32_t center, int32_t on_device,
+                                    double *out) {
+    API_BEGIN
+    require(c && pred && gt && out, "null argument");
+    require(F >= 1 && N >= 1, "empty vertex arrays");
+    require(!indices || n_idx >= 1, "empty index selection");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DevArena m;
+    const size_t n = (size_t)F * N * 3;
+    const long long n_sel = indices ? n_idx : N;
+    if (indices && !on_device)
+        for (int64_t k = 0; k < n_idx; ++k) require(indices[k] >= -N && indices[k] < N, "index out of range");
+    const double *dp = on_device ? pred : m.upload(pred, n, st);
+    const double *dg = on_device ? gt : m.upload(gt, n, st);
+    const long long *di = nullptr;
+    if (indices) {
+        if (on_device) di = reinterpret_cast<const long long *>(indices);
+        else {
+            std::vector<long long> ix(n_idx);
+            for (int64_t k = 0; k < n_idx; ++k) ix[k] = indices[k] < 0 ? indices[k] + N : indices[k];
+            di = m.upload(ix.data(), ix.size(), st);
+        }
+    }
+    double *dist = m.alloc<double>((size_t)F * n_sel), *dout = m.alloc<double>(F);
+    launch(c, k_vertex_error, dim3((unsigned)F), dim3(256), 0, (int)F, (long long)N, dp, dg, di, n_sel,
+           (int)center, dist, dout);
+    CK(cudaMemcpyAsync(out, dout, sizeof(double) * F, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return last_launch_status();
+    API_END
+}
+
+// metrics.umeyama_alignment + aligned_joint_error over F frames of M 3-D points
+extern "C" int lc_aligned_error(lc_ctx *c, int32_t F, int32_t M, const double *pred, const double *gt,
+                                int32_t with_scaling, int32_t on_device, double *scale_out, double *rot_out,
+                                double *t_out, double *err_out) {
+    API_BEGIN
+    require(c && pred && gt && err_out, "null argument");
+    require(F >= 1, "no frames");
+    require(M >= 3, "need at least 3 points to align");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DevArena m;
+    const size_t n = (size_t)F * M * 3;
+    const double *dp = on_device ? pred : m.upload(pred, n, st);
+    const double *dg = on_device ? gt : m.upload(gt, n, st);
+    double *sc = m.alloc<double>(F), *rot = m.alloc<double>(9 * (size_t)F), *tt = m.alloc<double>(3 * (size_t)F);
+    double *err = m.alloc<double>(F), *scr = m.alloc<double>((size_t)F * M);
+    launch(c, k_umeyama, dim3((unsigned)((F + 63) / 64)), dim3(64), 0, (int)F, (int)M, dp, dg, (int)with_scaling,
+           sc, rot, tt, err, scr);
+    CK(cudaMemcpyAsync(err_out, err, sizeof(double) * F, cudaMemcpyDeviceToHost, st));
+    if (scale_out) CK(cudaMemcpyAsync(scale_out, sc, sizeof(double) * F, cudaMemcpyDeviceToHost, st));
+    if (rot_out) CK(cudaMemcpyAsync(rot_out, rot, sizeof(double) * 9 * F, cudaMemcpyDeviceToHost, st));
+    if (t_out) CK(cudaMemcpyAsync(t_out, tt, sizeof(double) * 3 * F, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return last_launch_status();
     API_END

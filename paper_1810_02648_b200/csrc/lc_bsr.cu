@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_bsr(BsrJob J) {
     lc_pdl_wait();
     __shared__ double red[8 * 32 + 16];
     const int n = J.n;
-    // M^-1 = inv(diag) (pinv fallback when a block is exactly singular)
+    // M^-1 = inv(diag); every block pseudo-inverted when one is exactly singular
     __shared__ int singular;
     if (threadIdx.x == 0) singular = 0;
     __syncthreads();
@@ -95,6 +95,11 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_bsr(BsrJob J) {
         }
         for (int k = 0; k < 9; ++k) J.minv[9 * (size_t)i + k] = o[k];
     }
+    __syncthreads();
+    // np.linalg.inv raised: the reference pseudo-inverts the whole batch
+    if (singular)
+        for (int i = threadIdx.x; i < n; i += NT) pinv3(J.diag + 9 * (size_t)i, J.minv + 9 * (size_t)i);
+    __syncthreads();
     double part[2] = {0, 0};
     for (int i = threadIdx.x; i < n; i += NT) {
         const V3 r = ld3(J.rhs + 3 * (size_t)i);

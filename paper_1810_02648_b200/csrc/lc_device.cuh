@@ -484,6 +484,92 @@ __device__ __forceinline__ bool sym3_inverse(const double s[6], double o[6]) {
     o[5] = (a * d - b * b) * id;
     return true;
 }
+// Eigen-decomposition of a symmetric 3x3 (full storage m[9], row-major) by
+// cyclic Jacobi rotations: m = V diag(lam) V^T, eigenvectors in V's columns.
+__device__ inline void sym3_eig(const double m_in[9], double lam[3], double V[9]) {
+    double a[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            a[i][j] = m_in[3 * i + j];
+            V[3 * i + j] = i == j ? 1.0 : 0.0;
+        }
+    for (int sweep = 0; sweep < 50; ++sweep) {
+        const double off = a[0][1] * a[0][1] + a[0][2] * a[0][2] + a[1][2] * a[1][2];
+        const double dia = a[0][0] * a[0][0] + a[1][1] * a[1][1] + a[2][2] * a[2][2];
+        if (off == 0.0 || off <= 1e-36 * dia) break;
+        for (int p = 0; p < 2; ++p)
+            for (int q = p + 1; q < 3; ++q) {
+                if (a[p][q] == 0.0) continue;
+                const double th = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+                const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+                const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+                for (int k = 0; k < 3; ++k) {   // a <- a G (columns p, q)
+                    const double akp = a[k][p], akq = a[k][q];
+                    a[k][p] = c * akp - s * akq;
+                    a[k][q] = s * akp + c * akq;
+                }
+                for (int k = 0; k < 3; ++k) {   // a <- G^T a (rows p, q)
+                    const double apk = a[p][k], aqk = a[q][k];
+                    a[p][k] = c * apk - s * aqk;
+                    a[q][k] = s * apk + c * aqk;
+                }
+                for (int k = 0; k < 3; ++k) {   // V <- V G
+                    const double vkp = V[3 * k + p], vkq = V[3 * k + q];
+                    V[3 * k + p] = c * vkp - s * vkq;
+                    V[3 * k + q] = s * vkp + c * vkq;
+                }
+            }
+    }
+    for (int i = 0; i < 3; ++i) lam[i] = a[i][i];
+}
+
+// Moore-Penrose pseudo-inverse of a 3x3 block (np.linalg.pinv, rcond 1e-15:
+// singular values <= 1e-15 * max are dropped).  The reference switches every
+// Jacobi block to pinv once np.linalg.inv hits an exactly singular block
+// (solvers.py:110-114).  Symmetric blocks (every normal-system diagonal) use
+// their eigen-decomposition (s = |lam|, pinv = sum v v^T / lam); general ones
+// the eigen-decomposition of A^T A (pinv = sum v (A v)^T / s^2).
+__device__ inline void pinv3(const double a[9], double o[9]) {
+    const bool sym = a[1] == a[3] && a[2] == a[6] && a[5] == a[7];
+    double B[9];
+    if (sym)
+        for (int k = 0; k < 9; ++k) B[k] = a[k];
+    else
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) B[3 * i + j] = a[i] * a[j] + a[3 + i] * a[3 + j] + a[6 + i] * a[6 + j];
+    double lam[3], V[9];
+    sym3_eig(B, lam, V);
+    double sv[3], smax = 0.0;
+    for (int k = 0; k < 3; ++k) {
+        sv[k] = sym ? fabs(lam[k]) : sqrt(fmax(lam[k], 0.0));
+        smax = fmax(smax, sv[k]);
+    }
+    const double cut = 1e-15 * smax;
+    for (int k = 0; k < 9; ++k) o[k] = 0.0;
+    for (int k = 0; k < 3; ++k) {
+        if (!(sv[k] > cut)) continue;
+        const double v0 = V[k], v1 = V[3 + k], v2 = V[6 + k];
+        double u0, u1, u2, sc;
+        if (sym) { u0 = v0; u1 = v1; u2 = v2; sc = 1.0 / lam[k]; }
+        else {
+            u0 = a[0] * v0 + a[1] * v1 + a[2] * v2;
+            u1 = a[3] * v0 + a[4] * v1 + a[5] * v2;
+            u2 = a[6] * v0 + a[7] * v1 + a[8] * v2;
+            sc = 1.0 / lam[k];
+        }
+        o[0] += sc * v0 * u0; o[1] += sc * v0 * u1; o[2] += sc * v0 * u2;
+        o[3] += sc * v1 * u0; o[4] += sc * v1 * u1; o[5] += sc * v1 * u2;
+        o[6] += sc * v2 * u0; o[7] += sc * v2 * u1; o[8] += sc * v2 * u2;
+    }
+}
+__device__ __forceinline__ void sym3_pinv(const double s[6], double o[6]) {
+    const double a[9] = {s[0], s[1], s[2], s[1], s[3], s[4], s[2], s[4], s[5]};
+    double f[9];
+    pinv3(a, f);
+    o[0] = f[0]; o[1] = 0.5 * (f[1] + f[3]); o[2] = 0.5 * (f[2] + f[6]);
+    o[3] = f[4]; o[4] = 0.5 * (f[5] + f[7]); o[5] = f[8];
+}
+
 __device__ __forceinline__ V3 sym3_mul(const double s[6], V3 v) {
     return V3{s[0] * v.x + s[1] * v.y + s[2] * v.z, s[1] * v.x + s[3] * v.y + s[4] * v.z,
               s[2] * v.x + s[4] * v.y + s[5] * v.z};

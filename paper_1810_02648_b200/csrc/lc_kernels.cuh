@@ -151,6 +151,8 @@ struct RimJob {
     int dilation;
 };
 __global__ void k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double *probe_offs);
+__global__ void k_part_labels(ActorDev A, CamDev cam, const double *verts, const int *tri_id, int dilation,
+                              int *labels);
 
 // ----- surface solve (nonrigid_stage.py:189-500) ---------------------------
 struct SurfJob;

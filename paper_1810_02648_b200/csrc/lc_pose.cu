@@ -552,6 +552,9 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(JobArg<PoseJob> jobs, co
         rep->n_contour = c.B;
         rep->has_temporal = J.prev_pos != nullptr;
     }
+    // peers may still be reading this CTA's shared memory (the last team
+    // reduction reads every rank's partials over DSMEM): no CTA may exit first
+    T::sync();
 }
 
 template __global__ void k_pose_solve_t<1>(JobArg<PoseJob>, const SkelDev *, ActorDev, CamDev);

@@ -30,6 +30,8 @@ struct lc_ctx {
     struct Slot *call_slot = nullptr;          // scratch slot for single-call entry points
     const lc_actor *call_actor = nullptr;
     int call_w = 0, call_h = 0;
+    // team (thread-block cluster) sizes of the two solvers; 0 = default policy
+    int pose_cs = 0, surf_cs = 0;
 };
 
 // device allocation list owned by an object

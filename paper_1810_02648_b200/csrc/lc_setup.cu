@@ -1195,6 +1195,41 @@ __global__ void k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double 
     }
 }
 
+// Full body-part label image (build_body_part_mask, nonrigid_stage.py:102-128)
+// for the set-parity seam: the label k_rim reads at one pixel, evaluated at
+// every pixel with the same device logic (own part from the winning
+// triangle's max-barycentric vertex; background pixels take the nearest part
+// within `dilation` px, lowest id on ties, torso override).
+__global__ void k_part_labels(ActorDev A, CamDev cam, const double *verts, const int *tri_id, int dilation,
+                              int *labels) {
+    lc_pdl_wait();
+    const long long HW = (long long)cam.W * cam.H;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < HW; q += (long long)gridDim.x * blockDim.x) {
+        const int xi = (int)(q % cam.W), yi = (int)(q / cam.W);
+        int label = part_at(A, cam, verts, tri_id, xi, yi);
+        if (label == 0) {
+            const int R = dilation;
+            int best[LC_MAX_PARTS];
+            for (int k = 0; k < LC_MAX_PARTS; ++k) best[k] = INT_MAX;
+            for (int dy = -R; dy <= R; ++dy)
+                for (int dx = -R; dx <= R; ++dx) {
+                    const int x = xi + dx, y = yi + dy;
+                    if (x < 0 || y < 0 || x >= cam.W || y >= cam.H) continue;
+                    const int d2 = dx * dx + dy * dy;
+                    if (d2 > R * R) continue;
+                    const int pp = part_at(A, cam, verts, tri_id, x, y);
+                    if (pp > 0 && pp < LC_MAX_PARTS && d2 < best[pp]) best[pp] = d2;
+                }
+            int arg = 0, bd = INT_MAX;
+            for (int k = 1; k < LC_MAX_PARTS; ++k)
+                if (best[k] < bd) { bd = best[k]; arg = k; }
+            label = arg;
+            if (best[1] != INT_MAX) label = 1;
+        }
+        labels[q] = label;
+    }
+}
+
 // (M,3,36) skinning Jacobian for the lc_skin_points seam (skin_points with
 // dq_jacobian, skinning.py:391-397); the per-joint DQ Jacobian columns are
 // recomputed from the FK state on the fly.

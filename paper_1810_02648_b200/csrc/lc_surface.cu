@@ -261,7 +261,7 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
         if (fine >= 0 && J.phase && T::tid() == 0) J.phase[fine + k] = gtimer();
     };
     const double cv = sqrt(c.hp.w_vel), ca = sqrt(c.hp.w_acc);
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // 6 energies, pruned, behind
+    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // 6 energies, pruned, behind, singular blocks
     double degen = 0.0;
     // P0: clear data blocks; per-edge direction + gradient contribution
     for (int i = T::tid(); i < c.N; i += T::size) {
@@ -375,13 +375,26 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
         for (int k = 0; k < 6; ++k) J.diag[6 * (size_t)i + k] = dg[k];
         st3(J.rhs + 3 * (size_t)i, rh);
         double mi[6];
-        if (!sym3_inverse(dg, mi))
-            for (int k = 0; k < 6; ++k) mi[k] = 0.0;  // pinv of an all-zero block
+        if (!sym3_inverse(dg, mi)) {
+            acc[8] += 1.0;
+            for (int k = 0; k < 6; ++k) mi[k] = 0.0;
+        }
         for (int k = 0; k < 6; ++k) J.minv[6 * (size_t)i + k] = mi[k];
     }
     fst(3);
-    T::template sums<8>(acc, c.red);
+    T::template sums<9>(acc, c.red);
     fst(4);
+    // np.linalg.inv raised on an exactly singular block: the reference
+    // pseudo-inverts every block (solvers.py:110-114)
+    if (acc[8] > 0.0) {
+        for (int i = T::tid(); i < c.N; i += T::size) {
+            double dg[6], mi[6];
+            for (int k = 0; k < 6; ++k) dg[k] = J.diag[6 * (size_t)i + k];
+            sym3_pinv(dg, mi);
+            for (int k = 0; k < 6; ++k) J.minv[6 * (size_t)i + k] = mi[k];
+        }
+        T::sync();
+    }
     for (int k = 0; k < 6; ++k) en[k] = acc[k];
     counts[0] = (int)acc[6];
     counts[2] = (int)acc[7];
@@ -761,6 +774,8 @@ __global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<Sur
     }
     if (J.do_snap && has_field && c.B > 0) surf_snap<T>(c, v);
     stamp<T>(J, ph);
+    // no CTA exits while a peer may still read its shared memory (DSMEM)
+    T::sync();
 }
 
 template __global__ void k_surface_solve_t<1>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);

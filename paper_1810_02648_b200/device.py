@@ -83,6 +83,12 @@ def config_c(cfg: SequenceConfig) -> L.Config:
     c.frame0_rounds, c.frame0_iteration_scale = int(cfg.frame0_rounds), int(cfg.frame0_iteration_scale)
     c.pose = pose_hyper_c(cfg.pose)
     c.nonrigid = nonrigid_hyper_c(cfg.nonrigid)
+    # frame 0 logs every cold-start round's GN iterations in one report
+    # (pipeline.py:182-195: 2 override rounds + max(1, rounds - 2) full ones)
+    f0 = int(cfg.pose.gn_iterations) * int(cfg.frame0_iteration_scale) * (2 + max(1, int(cfg.frame0_rounds) - 2))
+    if f0 > L.LC_MAX_LOG:
+        raise ValueError(f"frame 0 would log {f0} pose GN iterations; at most {L.LC_MAX_LOG} are supported "
+                         f"(gn_iterations * frame0_iteration_scale * cold-start rounds)")
     return c
 
 
@@ -153,13 +159,19 @@ class DeviceActor:
         self.n_vertices = m.n_vertices
         self.n_joints = sk.n_joints
 
+    CACHE_SIZE = 4   # uploaded actors kept per process (LRU; evicted ones are freed)
+
     @classmethod
     def _cached(cls, key, owner, build):
-        hit = cls._cache.get(key)
+        hit = cls._cache.pop(key, None)
         if hit is not None and hit[0] is owner:
+            cls._cache[key] = hit          # most recently used last
             return hit[1]
         dev = build()
         cls._cache[key] = (owner, dev)
+        while len(cls._cache) > cls.CACHE_SIZE:
+            # dropped from the cache; freed by __del__ once no Tracker holds it
+            cls._cache.pop(next(iter(cls._cache)))
         return dev
 
     @classmethod
@@ -184,9 +196,15 @@ class DeviceActor:
         return cls._cached(key, mesh, lambda: cls(mesh, default_skeleton(), None, ctx))
 
     def close(self):
-        if self.handle:
+        if getattr(self, "handle", None):
             self.ctx.lib.lc_actor_destroy(self.handle)
             self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ---------------------------------------------------------------------------
@@ -300,7 +318,8 @@ class Tracker:
         def arr(a, shape):
             if a is None:
                 return None
-            a = L.f64c(a.to_vector() if isinstance(a, PoseParams) else a)
+            # this package's PoseParams or the reference's (duck-typed)
+            a = L.f64c(a.to_vector() if hasattr(a, "to_vector") else a)
             if a.shape != shape:
                 raise ValueError(f"state array has shape {a.shape}, expected {shape}")
             return a

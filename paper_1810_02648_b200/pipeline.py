@@ -60,15 +60,21 @@ def condition_detections(pre, det, actor=None) -> ConditionedFrame:
 
 
 _trackers: dict = {}
+TRACKER_CACHE = 2   # single-stream drop-in trackers kept alive (LRU); evicted ones are closed
 
 
 def _tracker_for(actor, camera, config) -> Tracker:
     key = (id(actor), id(getattr(actor, "mesh", None)), camera.fx, camera.fy, camera.cx, camera.cy,
            camera.width, camera.height, repr(config))
-    t = _trackers.get(key)
-    if t is None or t[0] is not actor:
+    t = _trackers.pop(key, None)
+    if t is not None and t[0] is not actor:
+        t[1].close()
+        t = None
+    if t is None:
         t = (actor, Tracker(actor, camera, config, 1))
-        _trackers[key] = t
+    _trackers[key] = t                       # most recently used last
+    while len(_trackers) > TRACKER_CACHE:
+        _trackers.pop(next(iter(_trackers)))[1].close()
     return t[1]
 
 

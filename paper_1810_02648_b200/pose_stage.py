@@ -78,3 +78,33 @@ def extract_contour_vertices(verts, actor, camera, ctx: L.Context | None = None)
     L.check(ctx.lib.lc_contour_vertices(ctx.handle, dev.handle, C.byref(cam), L.ptr(v), C.byref(n),
                                         L.ptr(idx), L.ptr(n2d)))
     return ContourVertexSet(idx[:n.value].copy(), n2d[:n.value].copy())
+
+
+def tracker_sets(verts, actor, camera, stage: int = 2, part_gate: bool = True, dilation: int = 10,
+                 with_labels: bool = False, ctx: L.Context | None = None) -> dict:
+    """The tracker's own index / set work on `verts` (one lc_surface_sets
+    call): contour indices + normals2d (extract_contour_vertices), the rim
+    keep flags (outer_rim_mask; stage 1 with the thickness probes and the
+    rigidity >= 2 gate of pipeline.py:211, stage 2 without, AND the part
+    gating of pipeline.py:241-249 when part_gate), the visible ids (stage 2,
+    visible_vertices) and optionally the part label image
+    (build_body_part_mask)."""
+    ctx = ctx or L.default_context()
+    dev = DeviceActor.get(actor, ctx)
+    v = L.f64c(verts)
+    N = len(v)
+    nb, nv = C.c_int32(), C.c_int32()
+    idx, vis = np.empty(N, dtype=np.int64), np.empty(N, dtype=np.int64)
+    n2d, keep = np.empty((N, 2)), np.empty(N, dtype=np.uint8)
+    labels = np.empty((camera.height, camera.width), dtype=np.int32) if with_labels else None
+    cam = camera_c(camera)
+    L.check(ctx.lib.lc_surface_sets(ctx.handle, dev.handle, C.byref(cam), L.ptr(v), int(stage), int(bool(part_gate)),
+                                    int(dilation), C.byref(nb), L.ptr(idx), L.ptr(n2d), L.ptr(keep), C.byref(nv),
+                                    L.ptr(vis), L.ptr(labels)))
+    out = {"contour": idx[:nb.value].copy(), "normals2d": n2d[:nb.value].copy(),
+           "keep": keep[:nb.value].astype(bool)}
+    if stage == 2:
+        out["visible"] = vis[:nv.value].copy()
+    if with_labels:
+        out["labels"] = labels
+    return out

@@ -1,0 +1,112 @@
+"""Parity on exactly the workloads bench.py times.
+
+* The bench's seed-0 stream (x5k @1024², directional=False, the bench's
+  SequenceConfig), teacher-forced through frames 0-24: every frame starts
+  from the oracle's TrackState; per-iteration energies and surface energy
+  terms within 1e-4, identical decision traces, vertices within 1e-4 of the
+  bbox diagonal.  Four identical streams in one launch (the bench's group
+  shape) must agree bit for bit.
+* cfg4 (x20k @1024², 4 GN x 8 PCG), whose default surface team is the
+  16-CTA cluster, teacher-forced through frames 0-2.
+* Every team-size instantiation of both solvers (1, 2, 4, 8, 16 CTAs per
+  stream) on small @128 and standard @256.
+
+The oracle is pinned to the real reference on these same workloads by
+tests/test_oracle_bench_golden.py (digests of the reference's own runs).
+"""
+
+import numpy as np
+import pytest
+
+from helpers import bbox_diag, check_frame_strict, oracle_state_to_mirror, scene, scene_bench
+from test_oracle_golden import check_digest, load
+
+pytestmark = pytest.mark.gpu
+
+
+def _teacher_forced(actor, cam, frames, cfg, streams=1, ctx=None, check_streams_equal=True):
+    from oracle import frame as OF
+    from paper_1810_02648_b200.device import Tracker
+    tr = Tracker(actor, cam, cfg, streams, ctx=ctx)
+    st = OF.State()
+    diag = bbox_diag(actor)
+    worst = 0.0
+    for fr in frames:
+        prep = OF.prepare(fr.image, fr.mask, fr.detections, actor, cfg)
+        for s in range(streams):
+            tr.set_state(s, oracle_state_to_mirror(st))
+            tr.set_frame(s, fr.image, fr.mask, fr.detections)
+        tr.step()
+        xo, vo, _, st_new, plogs, slogs = OF.solve_frame(prep, actor, cam, cfg, st)
+        out0 = None
+        for s in range(streams):
+            x, v, _, rep = tr.result(s)
+            worst = max(worst, check_frame_strict(rep, plogs, slogs, v, vo, diag, (fr.index, s)))
+            if check_streams_equal:
+                if out0 is None:
+                    out0 = (x, v)
+                else:
+                    assert np.array_equal(out0[0], x) and np.array_equal(out0[1], v), (fr.index, s)
+        st = st_new
+    tr.close()
+    return worst
+
+
+def test_bench_workload_teacher_forced_25_frames():
+    from paper_1810_02648_b200.config import SequenceConfig
+    actor, cam, frames = scene_bench("x5k", 1024, 25, seed=0)
+    check_digest(load("ref_digest_x5k1024_dir0.npz"), frames)     # the reference's own inputs
+    worst = _teacher_forced(actor, cam, frames, SequenceConfig(directional=False), streams=4)
+    print(f"x5k@1024 frames 0-24: worst vertex err / diag {worst:.2e}")
+
+
+def test_cfg4_x20k_teacher_forced():
+    from paper_1810_02648_b200.config import SequenceConfig
+    actor, cam, frames = scene_bench("x20k", 1024, 3, seed=0)
+    check_digest(load("ref_digest_x20k1024_cfg4.npz"), frames)
+    cfg = SequenceConfig(directional=False)
+    cfg.nonrigid.gn_iterations, cfg.nonrigid.pcg_iterations = 4, 8
+    worst = _teacher_forced(actor, cam, frames, cfg, streams=2)
+    print(f"x20k@1024 cfg4 frames 0-2: worst vertex err / diag {worst:.2e}")
+
+
+@pytest.mark.parametrize("cs", [1, 2, 4, 8, 16])
+@pytest.mark.parametrize("preset,res", [("small", 128), ("standard", 256)])
+def test_every_team_size(cs, preset, res):
+    from paper_1810_02648_b200 import _lib
+    from paper_1810_02648_b200.config import SequenceConfig
+    ctx = _lib.Context(0)
+    ctx.set_team_sizes(pose=cs, surface=cs)
+    actor, cam, frames = scene(preset, res, 3)
+    _teacher_forced(actor, cam, frames, SequenceConfig(directional=False), streams=2, ctx=ctx)
+
+
+def test_team_sizes_agree():
+    """Teams of different sizes reduce in different orders (fp64 rounding
+    only): results agree to 1e-9 of the bbox diagonal on a free-running run."""
+    from paper_1810_02648_b200 import _lib
+    from paper_1810_02648_b200.config import SequenceConfig
+    from paper_1810_02648_b200.device import Tracker
+    actor, cam, frames = scene("standard", 256, 3)
+    res = {}
+    for cs in (1, 4, 16):
+        ctx = _lib.Context(0)
+        ctx.set_team_sizes(pose=cs, surface=cs)
+        tr = Tracker(actor, cam, SequenceConfig(directional=False), 1, ctx=ctx)
+        out = []
+        for fr in frames:
+            tr.set_frame(0, fr.image, fr.mask, fr.detections)
+            tr.step()
+            out.append(tr.result(0, with_report=False)[1])
+        res[cs] = np.stack(out)
+        tr.close()
+    diag = bbox_diag(actor)
+    for cs in (4, 16):
+        assert np.abs(res[cs] - res[1]).max() <= 1e-6 * diag
+
+
+def test_team_size_validation():
+    from paper_1810_02648_b200 import _lib
+    ctx = _lib.Context(0)
+    with pytest.raises(ValueError):
+        ctx.set_team_sizes(pose=3)

@@ -1,7 +1,7 @@
 """Generate golden fixtures by running the REAL reference (`montrack`).
 
 Run in the build container only (the reference is not on the GPU box):
-  PYTHONPATH=/root/reference/pkg/src python tools/make_golden.py
+  PYTHONPATH=/root/reference/pkg/src python tools/make_golden.py [--bench]
 Writes tests/golden/*.npz.  The fixtures hold small outputs plus input
 checksums; inputs are regenerated from seeds by the restated generator
 (`paper_1810_02648_b200.synthetic`, pinned by those checksums).
@@ -56,6 +56,58 @@ def frames_fixture(preset, res, n, directional, seed=0):
                                                                    "velocity", "acceleration")]
                                  for it in fr.nonrigid_report.iterations] for fr in r.frames])
     out["meta"] = np.array([preset, str(res), str(n), str(int(directional)), str(seed)])
+    return out
+
+
+# the survey's runtime presets, registered without editing the reference
+RUNTIME_PRESETS = {
+    "x5k": dict(segs=26, limb_rings=11, torso_rings=16, head=(16, 26), skirt=(26, 80)),
+    "x20k": dict(segs=48, limb_rings=22, torso_rings=30, head=(32, 48), skirt=(50, 150)),
+}
+
+
+def _rows_digest(v):
+    """A compact, order-sensitive digest of a (F, N, 3) vertex stack: per-frame
+    sums, sums of squares, and every 97th row."""
+    return dict(sum=v.sum(axis=(1, 2)), sq=(v ** 2).sum(axis=(1, 2)), rows=v[:, ::97].copy())
+
+
+def frames_digest_fixture(preset, res, n, directional, seed=0, gn=None, pcg=None):
+    """Like frames_fixture for the bench-sized scenes, with vertex digests in
+    place of full vertex stacks (x20k @1024: 0.46 MB per frame)."""
+    import dataclasses
+
+    import montrack.actors as A
+    from montrack.pipeline import SequenceConfig, SequenceInputs, run_sequence
+    from montrack.synthetic import NoiseParams, default_script, generate_synthetic_sequence
+    A._PRESETS.update(RUNTIME_PRESETS)
+    actor = A.build_actor(preset, with_skirt=True)
+    cam = A.suggest_camera(res, res)
+    seq = generate_synthetic_sequence(actor, cam, default_script(n, noise=NoiseParams(sigma2d=1.0, sigma3d=0.008,
+                                                                                      seed=seed)))
+    inp = SequenceInputs(actor, cam, [f.image for f in seq.frames], [f.mask for f in seq.frames],
+                         [f.detections for f in seq.frames])
+    cfg = SequenceConfig(directional=directional)
+    if gn is not None or pcg is not None:
+        nr = cfg.nonrigid
+        cfg = dataclasses.replace(cfg, nonrigid=dataclasses.replace(
+            nr, gn_iterations=gn if gn is not None else nr.gn_iterations,
+            pcg_iterations=pcg if pcg is not None else nr.pcg_iterations))
+    r = run_sequence(inp, cfg, pipelined=False)
+    out = _inputs_digest(seq.frames)
+    out["poses"] = np.stack([fr.pose.to_vector() for fr in r.frames])
+    for k, v in _rows_digest(np.stack([fr.vertices for fr in r.frames])).items():
+        out["v_" + k] = v
+    pe = [[it.energy_before for it in fr.pose_report.iterations] for fr in r.frames]
+    pa = [[it.energy_after for it in fr.pose_report.iterations] for fr in r.frames]
+    ph = [[it.halvings for it in fr.pose_report.iterations] for fr in r.frames]
+    width = max(len(x) for x in pe)
+    pad = lambda rows, fill: np.array([x + [fill] * (width - len(x)) for x in rows])  # noqa: E731
+    out["pose_e0"], out["pose_e1"], out["pose_halv"] = pad(pe, np.nan), pad(pa, np.nan), pad(ph, -1)
+    out["nr_e0"] = np.array([[it.energy_before for it in fr.nonrigid_report.iterations] for fr in r.frames])
+    out["nr_e1"] = np.array([[it.energy_after for it in fr.nonrigid_report.iterations] for fr in r.frames])
+    out["nr_halv"] = np.array([[it.halvings for it in fr.nonrigid_report.iterations] for fr in r.frames])
+    out["meta"] = np.array([preset, str(res), str(n), str(int(directional)), str(seed), str(gn), str(pcg)])
     return out
 
 
@@ -145,7 +197,19 @@ def kernels_fixture():
     return out
 
 
+def main_bench():
+    """The bench's own workloads: x5k @1024, seed 0,
+    directional=False, frames 0-24; cfg4 x20k @1024, 4 GN x 8 PCG, frames 0-2."""
+    os.makedirs(OUT, exist_ok=True)
+    np.savez_compressed(os.path.join(OUT, "ref_digest_x5k1024_dir0.npz"),
+                        **frames_digest_fixture("x5k", 1024, 25, False))
+    np.savez_compressed(os.path.join(OUT, "ref_digest_x20k1024_cfg4.npz"),
+                        **frames_digest_fixture("x20k", 1024, 3, False, gn=4, pcg=8))
+
+
 def main():
+    if "--bench" in sys.argv:
+        return main_bench()
     os.makedirs(OUT, exist_ok=True)
     np.savez_compressed(os.path.join(OUT, "ref_frames_small128_dir1.npz"), **frames_fixture("small", 128, 4, True))
     np.savez_compressed(os.path.join(OUT, "ref_frames_small128_dir0.npz"), **frames_fixture("small", 128, 4, False))
