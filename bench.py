@@ -60,6 +60,9 @@ def parse():
                     help="SequenceConfig(directional=True): the reference's default, which loses the subject "
                          "on this workload (VERDICT r01); the default workload tracks (directional=False)")
     ap.add_argument("--no-quality", action="store_true", help="skip the untimed tracking-quality replay")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="multi-rank plumbing only (process group, sharding, max-over-ranks timing, gather); "
+                         "no GPU, no solve - for CPU CI of the --gpus N path")
     return ap.parse_args()
 
 
@@ -639,9 +642,65 @@ def run_reference(args):
     return out
 
 
+def spawn_ranks(args):
+    """`bench.py --gpus N` without a torchrun environment: launch N ranks
+    (one process per GPU) the way the driver does and pass rank 0's line
+    through."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def run_dry(args):
+    """--dry-run: the multi-rank plumbing of run_ours without a GPU (CPU CI):
+    process group, stream sharding, barrier, max-over-ranks time, result
+    gather to rank 0, rank-0 JSON line.  No solve runs; the line says so."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1810_02648_b200.sharding import assign_streams, gather_results
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    Sn, K = args.streams, args.steps
+    mine = assign_streams(Sn * world, world, rank, "block")
+    assert mine == shard_seeds(rank, Sn)
+    t0 = time.perf_counter()
+    time.sleep(0.01 * (rank + 1))
+    ms = 1e3 * (time.perf_counter() - t0)
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        poses = np.stack([np.full((1, 36), float(s)) for s in mine])
+        verts = np.stack([np.full((1, 2, 3), float(s)) for s in mine])
+        g = gather_results(poses, verts, Sn * world, "block")
+        gathered = None if g is None else int(g[0].shape[0])
+        ok = None if g is None else bool(all((g[0][s] == s).all() for s in range(Sn * world)))
+    else:
+        gathered, ok = None, None
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "value": None, "unit": "frames/s", "n_gpus": world,
+                          "steps": K, "ms_per_step": ms / max(K, 1), "config": workload(args, world),
+                          "shards": [assign_streams(Sn * world, world, r, "block") for r in range(world)],
+                          "gathered_streams": gathered, "gather_ok": ok}))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

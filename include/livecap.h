@@ -317,6 +317,9 @@ int lc_tracker_get_result_async(lc_tracker *tr, int32_t stream, double *pose_out
 int lc_tracker_set_state(lc_tracker *tr, int32_t stream, const double *x_prev,
                          const double *x_prev2, const double *joints_prev,
                          const double *disp_rest, const double *v_prev, const double *v_prev2);
+/* set the Stage I pose (36 doubles) the next lc_tracker_step_stage(tr, 2)
+ * solves Stage II from (per-stage teacher forcing) */
+int lc_tracker_set_pose(lc_tracker *tr, int32_t stream, const double *x36);
 int lc_tracker_get_state(lc_tracker *tr, int32_t stream, int32_t *flags, double *x_prev,
                          double *x_prev2, double *joints_prev, double *disp_rest,
                          double *v_prev, double *v_prev2);

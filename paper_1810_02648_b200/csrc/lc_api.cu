@@ -302,6 +302,9 @@ extern "C" int lc_ctx_create(int32_t device, uint64_t cuda_stream, lc_ctx **out)
         CK(cudaFuncSetAttribute(k_pose_solve_t<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CK(cudaFuncSetAttribute(k_pose_solve_t<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         CK(cudaFuncSetAttribute(k_surface_solve_t<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        for (auto k : {k_surface_solve_t<1>, k_surface_solve_t<2>, k_surface_solve_t<4>, k_surface_solve_t<8>,
+                       k_surface_solve_t<16>})
+            CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 190 * 1024));
         CK(cudaFuncSetAttribute(k_pyramid_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)pyramid_fused_smem()));
     }
@@ -1299,8 +1302,10 @@ static void surface_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, c
         while (cs < 16 && (long long)a->dev.N > 6LL * cs * surface_block_threads()) cs *= 2;
     auto k = cs == 1 ? k_surface_solve_t<1> : cs == 2 ? k_surface_solve_t<2> : cs == 4 ? k_surface_solve_t<4>
              : cs == 8 ? k_surface_solve_t<8> : k_surface_solve_t<16>;
-    launch_cluster("k_surface_solve", c, k, (int)jobs.size(), cs, dim3(surface_block_threads()), 0,
-                   stage(c, jobs), a->dev, cam_dev(cam), cf.ec, cf.shp, cam.height, cam.width);
+    size_t smem = 0;
+    const int mode = surface_pcg_mode(a->dev.N, cs, &smem);
+    launch_cluster("k_surface_solve", c, k, (int)jobs.size(), cs, dim3(surface_block_threads()), smem,
+                   stage(c, jobs), a->dev, cam_dev(cam), cf.ec, cf.shp, cam.height, cam.width, mode);
 }
 
 // stages: 1 = conditioning + Stage I, 2 = Stage II + state update, 3 = both
@@ -1757,6 +1762,21 @@ extern "C" int lc_tracker_set_state(lc_tracker *t, int32_t stream, const double 
     s->has_vprev = v_prev != nullptr;
     s->has_vprev2 = v_prev2 != nullptr;
     CK(cudaStreamSynchronize(c->stream));
+    return LC_OK;
+    API_END
+}
+
+// Stage I output of one stream (36 doubles, host): the pose the next
+// lc_tracker_step_stage(t, 2) solves Stage II from (per-stage teacher forcing
+// in the parity tests; the GPU-pair pipeline moves it with lc_tracker_pipe)
+extern "C" int lc_tracker_set_pose(lc_tracker *t, int32_t stream, const double *x36) {
+    API_BEGIN
+    require(t && x36, "null argument");
+    require(stream >= 0 && stream < t->S, "stream index out of range");
+    CK(cudaSetDevice(t->ctx->device));
+    for (int k = 0; k < LC_NP; ++k) require(std::isfinite(x36[k]), "non-finite pose");
+    CK(cudaMemcpyAsync(t->slots[stream]->x, x36, sizeof(double) * LC_NP, cudaMemcpyHostToDevice, t->ctx->stream));
+    CK(cudaStreamSynchronize(t->ctx->stream));
     return LC_OK;
     API_END
 }

@@ -65,5 +65,6 @@ int pose_block_threads();
 
 template <int CS>
 __global__ void k_surface_solve_t(JobArg<SurfJob> jobs, ActorDev A, CamDev cam, EdgeConstDev ec,
-                                  SurfHyperDev hp, int H, int W);
+                                  SurfHyperDev hp, int H, int W, int pcg_mode);
 int surface_block_threads();
+int surface_pcg_mode(int N, int cs, size_t *smem_bytes);

@@ -403,59 +403,117 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
     counts[1] = (int)dd[0];
 }
 
-// block-Jacobi PCG from zero, best-residual iterate (solvers.py:104-145)
+// Block-Jacobi PCG from zero, best-residual iterate (solvers.py:104-145).
+//
+// Team layout: CTA r of the team owns the contiguous vertex chunk
+// [r*chunk, min(N, (r+1)*chunk)); thread t owns chunk vertices t, t+NT, ...
+// for the whole solve.  The vectors a vertex's owner alone touches (p, Ap)
+// and the one its neighbours gather (z) live in the owner's shared memory
+// (pcg_mode 2; mode 1: z only, p / Ap in global scratch; mode 0: all in
+// global scratch, for chunks too large for shared memory).  Mesh vertices
+// are numbered ring by ring, so almost every neighbour z_j is a local
+// shared-memory load; the few across a chunk border come over DSMEM.
+//
+// Each iteration needs exactly two team barriers, both inside the two
+// reductions the algorithm requires anyway:
+//   A: Az = A z (gathering z_j), p = z + beta p, Ap = Az + beta Ap,
+//      sums p.Ap, p.p                                   -> barrier 1 (alpha)
+//   B: x += alpha p, r -= alpha Ap, z = M^-1 r,
+//      sums r.z, r.r                                    -> barrier 2 (beta;
+//      also publishes the new z to the neighbours' next phase A)
+// i.e. A p_k is formed as A z_k + beta A p_{k-1} (the same vector; fp64
+// rounding order only) so the updated p never has to be exchanged.  The
+// best iterate (smallest ||r||, strict) is copied from x by its owner one
+// phase later, when the reduction has decided it.
 template <typename T>
-__device__ bool surf_pcg(const SurfCtx &c, int iters, int fine = -1) {
+__device__ bool surf_pcg(const SurfCtx &c, int iters, double *sm, int mode, int fine = -1) {
     const SurfJob &J = *c.J;
     auto fst = [&](int k) {
         if (fine >= 0 && J.phase && T::tid() == 0) J.phase[fine + k] = gtimer();
     };
     fst(0);
+    const int N = c.N;
+    const int chunk = (N + T::ctas - 1) / T::ctas;
+    const int lo = T::rank() * chunk, hi = min(N, lo + chunk);
+    // own-vertex storage: zs / ps / aps indexed by (i - off)
+    const bool z_sm = mode >= 1;
+    double *zs = z_sm ? sm : J.z;
+    double *ps = mode == 2 ? sm + 3 * (size_t)chunk : J.p;
+    double *aps = mode == 2 ? sm + 6 * (size_t)chunk : J.ap;
+    const int zoff = z_sm ? lo : 0, poff = mode == 2 ? lo : 0;
+    const double *__restrict__ diag = J.diag;
+    const double *__restrict__ minv = J.minv;
+    const double *__restrict__ rhs = J.rhs;
+    const int *__restrict__ ell_nbr = c.A.ell_nbr;
+    const int *__restrict__ ell_cnt = c.A.ell_cnt;
+    const double *__restrict__ ell_d = J.ell_d;
+    const double *__restrict__ ell_a = c.ec.ell_a;
+    const double *__restrict__ ell_b = c.ec.ell_b;
+    double *__restrict__ X = J.x;
+    double *__restrict__ R = J.r;
+    double *__restrict__ BEST = J.best;
+    const size_t LN = (size_t)LC_ELL * N;
+    // z_j of any vertex: own chunk from local shared memory, another CTA's
+    // chunk over DSMEM, or global scratch (mode 0)
+    auto zload = [&](int j) -> V3 {
+        if (!z_sm) return ld3(zs + 3 * (size_t)j);
+        if (j >= lo && j < hi) return ld3(zs + 3 * (size_t)(j - lo));
+        if constexpr (T::ctas == 1) {
+            return v3(0, 0, 0);   // unreachable: one CTA owns every vertex
+        } else {
+            const int owner = j / chunk;
+            const double *q = cg::this_cluster().map_shared_rank(zs, owner) + 3 * (size_t)(j - owner * chunk);
+            return v3(q[0], q[1], q[2]);
+        }
+    };
     double part[2] = {0, 0};
-    for (int i = T::tid(); i < c.N; i += T::size) {
-        const V3 r = ld3(J.rhs + 3 * (size_t)i);
-        const V3 z = sym3_mul(J.minv + 6 * (size_t)i, r);
-        st3(J.x + 3 * (size_t)i, v3(0, 0, 0));
-        st3(J.best + 3 * (size_t)i, v3(0, 0, 0));
-        st3(J.r + 3 * (size_t)i, r);
-        st3(J.z + 3 * (size_t)i, z);
-        st3(J.p + 3 * (size_t)i, z);
+    for (int i = lo + (int)threadIdx.x; i < hi; i += NT) {
+        const V3 r = ld3(rhs + 3 * (size_t)i);
+        const V3 z = sym3_mul(minv + 6 * (size_t)i, r);
+        st3(X + 3 * (size_t)i, v3(0, 0, 0));
+        st3(BEST + 3 * (size_t)i, v3(0, 0, 0));
+        st3(R + 3 * (size_t)i, r);
+        st3(zs + 3 * (size_t)(i - zoff), z);
         part[0] += r.x * z.x + r.y * z.y + r.z * z.z;
         part[1] += r.x * r.x + r.y * r.y + r.z * r.z;
     }
-    T::template sums<2>(part, c.red);
+    T::template sums<2>(part, c.red);   // (also publishes z)
     fst(1);
     double rz = part[0];
     double best_norm = sqrt(part[1]);
-    bool breakdown = false;
+    bool breakdown = false, pend_best = false;
+    double beta = 0.0;
     for (int it = 0; it < iters; ++it) {
+        // ---- A: Az, p, Ap
         double s1[2] = {0, 0};
-        for (int i = T::tid(); i < c.N; i += T::size) {
-            const V3 pi = ld3(J.p + 3 * (size_t)i);
-            V3 y = sym3_mul(J.diag + 6 * (size_t)i, pi);
-            // matrix-free off-diagonal blocks -(a I + b d d^T) p_j: ELL slots
-            // (one round of independent coalesced loads + the p_j gathers),
-            // then the CSR tail of high-degree vertices
-            const int cnt = c.A.ell_cnt[i];
-            const size_t LN = (size_t)LC_ELL * c.N;
+        for (int i = lo + (int)threadIdx.x; i < hi; i += NT) {
+            const V3 zi = ld3(zs + 3 * (size_t)(i - zoff));
+            V3 y = sym3_mul(diag + 6 * (size_t)i, zi);
+            const int cnt = ell_cnt[i];
 #pragma unroll
             for (int k = 0; k < LC_ELL; ++k) {
                 if (k >= cnt) continue;
-                const size_t pos = (size_t)k * c.N + i;
-                const V3 pj = ld3(J.p + 3 * (size_t)c.A.ell_nbr[pos]);
-                const V3 d = v3(J.ell_d[pos], J.ell_d[LN + pos], J.ell_d[2 * LN + pos]);
-                y = y - (c.ec.ell_a[pos] * pj + (c.ec.ell_b[pos] * dot3(d, pj)) * d);
+                const size_t pos = (size_t)k * N + i;
+                const V3 zj = zload(ell_nbr[pos]);
+                const V3 d = v3(ell_d[pos], ell_d[LN + pos], ell_d[2 * LN + pos]);
+                y = y - (ell_a[pos] * zj + (ell_b[pos] * dot3(d, zj)) * d);
             }
             if (cnt > LC_ELL)
                 for (int k = c.A.adj_ptr[i] + LC_ELL; k < c.A.adj_ptr[i + 1]; ++k) {
                     const int e = c.A.adj_edge[k];
-                    const V3 pj = ld3(J.p + 3 * (size_t)c.A.adj_nbr[k]);
+                    const V3 zj = zload(c.A.adj_nbr[k]);
                     const V3 d = ld3(J.edir + 3 * (size_t)e);
-                    y = y - (c.ec.alpha[e] * pj + (c.ec.beta[e] * dot3(d, pj)) * d);
+                    y = y - (c.ec.alpha[e] * zj + (c.ec.beta[e] * dot3(d, zj)) * d);
                 }
-            st3(J.ap + 3 * (size_t)i, y);
-            s1[0] += pi.x * y.x + pi.y * y.y + pi.z * y.z;
-            s1[1] += pi.x * pi.x + pi.y * pi.y + pi.z * pi.z;
+            V3 p = zi, ap = y;
+            if (it > 0) {
+                p = zi + beta * ld3(ps + 3 * (size_t)(i - poff));
+                ap = y + beta * ld3(aps + 3 * (size_t)(i - poff));
+            }
+            st3(ps + 3 * (size_t)(i - poff), p);
+            st3(aps + 3 * (size_t)(i - poff), ap);
+            s1[0] += p.x * ap.x + p.y * ap.y + p.z * ap.z;
+            s1[1] += p.x * p.x + p.y * p.y + p.z * p.z;
         }
         if (it == 0) fst(2);
         T::template sums<2>(s1, c.red);
@@ -463,14 +521,17 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, int fine = -1) {
         const double pap = s1[0];
         if (pap <= 1e-14 * fmax(s1[1], 1e-300)) { breakdown = true; break; }
         const double alpha = rz / pap;
+        // ---- B: x, r, z
         double s2[2] = {0, 0};
-        for (int i = T::tid(); i < c.N; i += T::size) {
-            const V3 x = ld3(J.x + 3 * (size_t)i) + alpha * ld3(J.p + 3 * (size_t)i);
-            const V3 r = ld3(J.r + 3 * (size_t)i) - alpha * ld3(J.ap + 3 * (size_t)i);
-            const V3 z = sym3_mul(J.minv + 6 * (size_t)i, r);
-            st3(J.x + 3 * (size_t)i, x);
-            st3(J.r + 3 * (size_t)i, r);
-            st3(J.z + 3 * (size_t)i, z);
+        for (int i = lo + (int)threadIdx.x; i < hi; i += NT) {
+            V3 x = ld3(X + 3 * (size_t)i);
+            if (pend_best) st3(BEST + 3 * (size_t)i, x);
+            x = x + alpha * ld3(ps + 3 * (size_t)(i - poff));
+            const V3 r = ld3(R + 3 * (size_t)i) - alpha * ld3(aps + 3 * (size_t)(i - poff));
+            const V3 z = sym3_mul(minv + 6 * (size_t)i, r);
+            st3(X + 3 * (size_t)i, x);
+            st3(R + 3 * (size_t)i, r);
+            st3(zs + 3 * (size_t)(i - zoff), z);
             s2[0] += r.x * z.x + r.y * z.y + r.z * z.z;
             s2[1] += r.x * r.x + r.y * r.y + r.z * r.z;
         }
@@ -478,20 +539,17 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, int fine = -1) {
         T::template sums<2>(s2, c.red);
         if (it == 0) fst(5);
         const double nrm = sqrt(s2[1]);
-        const bool better = nrm < best_norm;
-        if (better) best_norm = nrm;
+        pend_best = nrm < best_norm;
+        if (pend_best) best_norm = nrm;
         const bool stop = rz <= 0.0;
-        const double beta = stop ? 0.0 : s2[0] / rz;
-        for (int i = T::tid(); i < c.N; i += T::size) {
-            if (better) st3(J.best + 3 * (size_t)i, ld3(J.x + 3 * (size_t)i));
-            if (!stop)
-                st3(J.p + 3 * (size_t)i, ld3(J.z + 3 * (size_t)i) + beta * ld3(J.p + 3 * (size_t)i));
-        }
-        T::sync();
+        beta = stop ? 0.0 : s2[0] / rz;
         if (it == 0) fst(6);
         if (stop) { breakdown = true; break; }
         rz = s2[0];
     }
+    if (pend_best)
+        for (int i = lo + (int)threadIdx.x; i < hi; i += NT) st3(BEST + 3 * (size_t)i, ld3(X + 3 * (size_t)i));
+    T::sync();   // the best iterate of every chunk, for the line search
     return breakdown;
 }
 
@@ -656,7 +714,8 @@ __device__ __forceinline__ void stamp(const SurfJob &J, int &k) {
 template <int CS>
 __global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<SurfJob> jobs, ActorDev A, CamDev cam,
                                                            EdgeConstDev ec, SurfHyperDev hp, int H,
-                                                           int W) {
+                                                           int W, int pcg_mode) {
+    extern __shared__ __align__(16) double pcg_sm[];   // surf_pcg's own-chunk vectors (pcg_mode >= 1)
     lc_pdl_wait();
     using T = Team<CS, NT>;
     // this stream's descriptor, from the parameter bank into shared memory
@@ -704,7 +763,7 @@ __global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<Sur
             surf_assemble<T>(c, level, v, en, counts, it == 1 ? 16 : -1);
             stamp<T>(J, ph);
             for (int k = 0; k < 3; ++k) tot[k] += counts[k];
-            const bool breakdown = surf_pcg<T>(c, hp.pcg, it == 1 ? 40 : -1);
+            const bool breakdown = surf_pcg<T>(c, hp.pcg, pcg_sm, pcg_mode, it == 1 ? 40 : -1);
             stamp<T>(J, ph);
             const double e0 = total_energy(en, c.has_prev);
             // halving line search (nonrigid_stage.py:386-399): the first
@@ -778,13 +837,26 @@ __global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<Sur
     T::sync();
 }
 
-template __global__ void k_surface_solve_t<1>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
-template __global__ void k_surface_solve_t<2>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
-template __global__ void k_surface_solve_t<4>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
-template __global__ void k_surface_solve_t<8>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
-template __global__ void k_surface_solve_t<16>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int);
+template __global__ void k_surface_solve_t<1>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int, int);
+template __global__ void k_surface_solve_t<2>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int, int);
+template __global__ void k_surface_solve_t<4>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int, int);
+template __global__ void k_surface_solve_t<8>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int, int);
+template __global__ void k_surface_solve_t<16>(JobArg<SurfJob>, ActorDev, CamDev, EdgeConstDev, SurfHyperDev, int, int, int);
 
 int surface_block_threads() { return NT; }
+
+// surf_pcg's shared-memory mode for a team of `cs` CTAs over N vertices and
+// the dynamic shared memory it needs: 2 = z, p, Ap of the CTA's chunk in
+// shared memory (72 B per vertex, when two CTAs still fit an SM), 1 = z only
+// (24 B per vertex), 0 = none
+int surface_pcg_mode(int N, int cs, size_t *smem_bytes) {
+    const size_t chunk = ((size_t)N + cs - 1) / cs;
+    int mode = 0;
+    if (72 * chunk <= 100 * 1024) mode = 2;
+    else if (24 * chunk <= 190 * 1024) mode = 1;
+    *smem_bytes = mode == 2 ? 72 * chunk : mode == 1 ? 24 * chunk : 0;
+    return mode;
+}
 
 #ifdef LC_NN_STATS
 extern "C" int lc_debug_nn_stats_surface(unsigned long long *o, int reset) {

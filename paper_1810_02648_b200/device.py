@@ -201,6 +201,9 @@ class DeviceActor:
             self.handle = None
 
     def __del__(self):
+        import sys
+        if sys.is_finalizing():   # the context may already be gone at interpreter exit
+            return
         try:
             self.close()
         except Exception:
@@ -327,6 +330,18 @@ class Tracker:
               arr(state.joints_prev, (self.J, 3)), arr(state.disp_rest, (self.N, 3)),
               arr(state.v_prev, (self.N, 3)), arr(state.v_prev2, (self.N, 3))]
         L.check(self.ctx.lib.lc_tracker_set_state(self.handle, stream, *[L.ptr(a) for a in xs]))
+
+    def step_stage(self, stages: int):
+        """1 = conditioning + Stage I, 2 = Stage II + state update, 3 = both
+        (consumes the queued frame; see lc_tracker_step_stage)."""
+        L.check(self.ctx.lib.lc_tracker_step_stage(self.handle, int(stages)))
+
+    def set_pose(self, stream: int, pose):
+        """The Stage I pose a following step_stage(2) solves Stage II from."""
+        x = L.f64c(pose.to_vector() if hasattr(pose, "to_vector") else pose)
+        if x.shape != (36,):
+            raise ValueError("pose must have 36 parameters")
+        L.check(self.ctx.lib.lc_tracker_set_pose(self.handle, stream, L.ptr(x)))
 
     def get_state(self, stream: int):
         from .config import TrackState

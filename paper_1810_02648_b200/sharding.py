@@ -36,7 +36,7 @@ def gather_results(poses, vertices, n_streams: int, policy: str = "block", group
     group's device).  Returns (poses, vertices) of shape (n_streams, ...)
     ordered by global stream id on rank 0, None elsewhere.  Ranks may own
     different stream counts: shards are padded to the largest one for the
-    fixed-size all_gather.
+    fixed-size gather.
     """
     import torch
     import torch.distributed as dist
@@ -51,10 +51,11 @@ def gather_results(poses, vertices, n_streams: int, policy: str = "block", group
     pad_v = torch.zeros((smax,) + tuple(v.shape[1:]), dtype=v.dtype, device=dev)
     pad_p[:p.shape[0]] = p
     pad_v[:v.shape[0]] = v
-    out_p = [torch.empty_like(pad_p) for _ in range(world)]
-    out_v = [torch.empty_like(pad_v) for _ in range(world)]
-    dist.all_gather(out_p, pad_p, group=group)
-    dist.all_gather(out_v, pad_v, group=group)
+    # a gather to rank 0 (not an all-gather): only rank 0 consumes results
+    out_p = [torch.empty_like(pad_p) for _ in range(world)] if rank == 0 else None
+    out_v = [torch.empty_like(pad_v) for _ in range(world)] if rank == 0 else None
+    dist.gather(pad_p, out_p, dst=0, group=group)
+    dist.gather(pad_v, out_v, dst=0, group=group)
     if rank != 0:
         return None
     P = np.zeros((n_streams,) + tuple(p.shape[1:]))

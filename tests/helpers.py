@@ -46,12 +46,8 @@ def oracle_state_to_mirror(st):
     return TrackState(st.x_prev, st.x_prev2, st.joints_prev, st.disp_rest, st.v_prev, st.v_prev2)
 
 
-def check_frame_strict(rep, plogs, slogs, v, vo, diag, tag, rtol=1e-4):
-    """SURVEY §8c bar for one teacher-forced frame: identical decision traces
-    (pose halvings / rejected / damped; surface halvings / rejected / PCG
-    breakdown), per-iteration energies and surface energy terms within rtol,
-    vertices within rtol of the bbox diagonal."""
-    P = rep.pose
+def check_pose_strict(P, plogs, tag, rtol=1e-4):
+    """Stage I decision trace identical, energies within rtol."""
     assert P.n_iterations == len(plogs), (tag, P.n_iterations, len(plogs))
     for k, o in enumerate(plogs):
         assert P.halvings[k] == o["halvings"], (tag, "pose halvings", k)
@@ -59,9 +55,15 @@ def check_frame_strict(rep, plogs, slogs, v, vo, diag, tag, rtol=1e-4):
         assert bool(P.damped[k]) == bool(o["damped"]), (tag, "pose damped", k)
         for key in ("energy_before", "energy_after"):
             ref = o[key]
-            assert abs(getattr(P, key)[k] - ref) <= rtol * max(abs(ref), 1e-300), (tag, "pose", key, k)
+            got = getattr(P, key)[k]
+            assert abs(got - ref) <= rtol * max(abs(ref), 1e-300), (tag, "pose", key, k, got, ref)
+
+
+def check_surface_strict(R, slogs, v, vo, diag, tag, rtol=1e-4):
+    """Stage II decision trace identical (halvings / rejected / PCG
+    breakdown), per-iteration energies and energy terms within rtol, final
+    vertices within rtol of the bbox diagonal (SURVEY §8c)."""
     if slogs is not None:
-        R = rep.nonrigid
         assert R.n_iterations == len(slogs), (tag, R.n_iterations, len(slogs))
         names = ("photo", "silhouette", "smooth", "edge", "velocity", "acceleration")
         for k, o in enumerate(slogs):
@@ -70,7 +72,9 @@ def check_frame_strict(rep, plogs, slogs, v, vo, diag, tag, rtol=1e-4):
             assert bool(R.pcg_breakdown[k]) == bool(o["pcg_breakdown"]), (tag, "pcg breakdown", k)
             for key in ("energy_before", "energy_after"):
                 ref = o[key]
-                assert abs(getattr(R, key)[k] - ref) <= rtol * max(abs(ref), 1e-300), (tag, "surface", key, k)
+                got = getattr(R, key)[k]
+                assert abs(got - ref) <= rtol * max(abs(ref), 1e-300), \
+                    (tag, "surface", key, k, got, ref, [R.terms[k][j] for j in range(6)], o["terms"])
             for j, nm in enumerate(names):
                 ref = o["terms"].get(nm, 0.0)
                 assert abs(R.terms[k][j] - ref) <= rtol * max(abs(ref), 1e-12 * o["energy_before"]), \
@@ -78,3 +82,9 @@ def check_frame_strict(rep, plogs, slogs, v, vo, diag, tag, rtol=1e-4):
     err = float(np.abs(v - vo).max()) / diag
     assert err <= rtol, (tag, "vertices / diag", err)
     return err
+
+
+def check_frame_strict(rep, plogs, slogs, v, vo, diag, tag, rtol=1e-4):
+    """Both stages of one teacher-forced frame (see the two checks above)."""
+    check_pose_strict(rep.pose, plogs, tag, rtol)
+    return check_surface_strict(rep.nonrigid, slogs, v, vo, diag, tag, rtol)

@@ -95,3 +95,26 @@ def test_assign_streams_partition():
                 flat = sorted(i for x in ids for i in x)
                 assert flat == list(range(n))
                 assert max(map(len, ids)) - min(map(len, ids)) <= 1
+
+
+def test_bench_spawns_ranks_dry_run():
+    """`bench.py --gpus 2` outside torchrun launches 2 ranks itself (the
+    driver's torchrun command line); the dry run exercises the whole
+    multi-rank path of run_ours on CPU (gloo): sharding, barrier,
+    max-over-ranks, gather to rank 0."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BENCH_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run",
+                        "--streams", "3", "--steps", "2"], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["dry_run"]
+    assert d["shards"] == [[0, 1, 2], [3, 4, 5]]
+    assert d["gathered_streams"] == 6 and d["gather_ok"]
+    assert d["config"]["total_streams"] == 6

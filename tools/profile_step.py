@@ -33,7 +33,7 @@ def main():
     cam = suggest_camera(a.res, a.res)
     frames = [bench.make_stream_frames(actor, cam, a.frames, s, bench.device_renderer(ctx),
                                        bench.device_posing(ctx)) for s in range(a.streams)]
-    tr = Tracker(actor, cam, SequenceConfig(), a.streams, ctx=ctx)
+    tr = Tracker(actor, cam, SequenceConfig(directional=False), a.streams, ctx=ctx)   # the bench workload
     stats = hasattr(ctx.lib, "lc_debug_nn_stats_pose") if False else None
     try:
         import ctypes
