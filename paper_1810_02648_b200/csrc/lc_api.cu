@@ -600,6 +600,15 @@ extern "C" int lc_actor_upload(lc_ctx *c, const lc_actor_desc *d, lc_actor **out
                 epos[2 * (size_t)e + (edges[2 * e] == i ? 0 : 1)] = pos;
             }
         }
+        std::vector<int> heavy, heavy_id(N, -1);
+        for (int i = 0; i < N; ++i)
+            if (ell_cnt[i] > LC_ELL) {
+                heavy_id[i] = (int)heavy.size();
+                heavy.push_back(i);
+            }
+        A.n_heavy = (int)heavy.size();
+        A.heavy = heavy.empty() ? nullptr : a->mem.upload(heavy.data(), heavy.size(), st);
+        A.heavy_id = a->mem.upload(heavy_id.data(), heavy_id.size(), st);
         A.ell_nbr = a->mem.upload(ell_nbr.data(), ell_nbr.size(), st);
         A.ell_cnt = a->mem.upload(ell_cnt.data(), ell_cnt.size(), st);
         A.epos = a->mem.upload(epos.data(), epos.size(), st);

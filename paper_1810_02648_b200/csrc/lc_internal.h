@@ -55,6 +55,9 @@ struct ActorDev {
     const int *ell_nbr;        // LC_ELL*N neighbour vertex
     const int *ell_cnt;        // N incident edge count (= CSR degree)
     const int *epos;           // 2E ELL position of edge e at its src (2e) / dst (2e+1), -1 = CSR tail
+    int n_heavy;               // vertices with more than LC_ELL incident edges (poles)
+    const int *heavy;          // n_heavy ascending vertex ids
+    const int *heavy_id;       // N: index into `heavy`, -1 for ELL-only vertices
     const double *w_dir;       // 2E directed material weights
     const int *skin_idx;       // N*4 (-1 padding)
     const double *skin_w;      // N*4

@@ -483,8 +483,33 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, double *sm, int mode, int 
     double best_norm = sqrt(part[1]);
     bool breakdown = false, pend_best = false;
     double beta = 0.0;
+    // CSR tails of the few high-degree vertices (mesh poles, degree up to
+    // ~50): one warp per vertex, lanes over the tail edges, into the
+    // assembly's per-edge gradient buffer (consumed before the PCG starts)
+    double *tail_y = J.eg;
     for (int it = 0; it < iters; ++it) {
         // ---- A: Az, p, Ap
+        if (c.A.n_heavy > 0) {
+            const int w = (int)threadIdx.x >> 5, lane = (int)threadIdx.x & 31;
+            for (int h = w; h < c.A.n_heavy; h += NT / 32) {
+                const int i = c.A.heavy[h];
+                if (i < lo || i >= hi) continue;
+                V3 acc = v3(0, 0, 0);
+                for (int k = c.A.adj_ptr[i] + LC_ELL + lane; k < c.A.adj_ptr[i + 1]; k += 32) {
+                    const int e = c.A.adj_edge[k];
+                    const V3 zj = zload(c.A.adj_nbr[k]);
+                    const V3 d = ld3(J.edir + 3 * (size_t)e);
+                    acc = acc + (c.ec.alpha[e] * zj + (c.ec.beta[e] * dot3(d, zj)) * d);
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+                    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+                    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+                }
+                if (lane == 0) st3(tail_y + 3 * (size_t)h, acc);
+            }
+            __syncthreads();
+        }
         double s1[2] = {0, 0};
         for (int i = lo + (int)threadIdx.x; i < hi; i += NT) {
             const V3 zi = ld3(zs + 3 * (size_t)(i - zoff));
@@ -498,13 +523,7 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, double *sm, int mode, int 
                 const V3 d = v3(ell_d[pos], ell_d[LN + pos], ell_d[2 * LN + pos]);
                 y = y - (ell_a[pos] * zj + (ell_b[pos] * dot3(d, zj)) * d);
             }
-            if (cnt > LC_ELL)
-                for (int k = c.A.adj_ptr[i] + LC_ELL; k < c.A.adj_ptr[i + 1]; ++k) {
-                    const int e = c.A.adj_edge[k];
-                    const V3 zj = zload(c.A.adj_nbr[k]);
-                    const V3 d = ld3(J.edir + 3 * (size_t)e);
-                    y = y - (c.ec.alpha[e] * zj + (c.ec.beta[e] * dot3(d, zj)) * d);
-                }
+            if (cnt > LC_ELL) y = y - ld3(tail_y + 3 * (size_t)c.A.heavy_id[i]);
             V3 p = zi, ap = y;
             if (it > 0) {
                 p = zi + beta * ld3(ps + 3 * (size_t)(i - poff));
