@@ -741,7 +741,7 @@ void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) 
     vis = mem.alloc<int>(N);
     P = mem.alloc<int>(1);
     diag = mem.alloc<double>(6 * (size_t)N);
-    minv = mem.alloc<double>(6 * (size_t)N);
+    minv = mem.alloc<double>(9 * (size_t)N);
     rhs = mem.alloc<double>(3 * (size_t)N);
     sx = mem.alloc<double>(3 * (size_t)N);
     sr = mem.alloc<double>(3 * (size_t)N);
@@ -1864,6 +1864,14 @@ extern "C" int lc_tracker_inspect(lc_tracker *t, int32_t stream, int32_t what, v
     } else if (what == 4 || what == 5) {
         require((int64_t)(3 * N) <= cap, "capacity too small");
         CK(cudaMemcpy(out, what == 4 ? s->vinit : s->vs, sizeof(double) * 3 * N, cudaMemcpyDeviceToHost));
+        *n_out = (int64_t)N;
+    } else if (what >= 6 && what <= 9) {
+        // the last Stage II GN step's normal system: 6 diag (N*6 sym), 7 rhs,
+        // 8 the PCG's best iterate (N*3), 9 the Jacobi inverse (N*9)
+        const size_t w = what == 6 ? 6 : what == 9 ? 9 : 3;
+        require((int64_t)(w * N) <= cap, "capacity too small");
+        const double *src = what == 6 ? s->diag : what == 7 ? s->rhs : what == 8 ? s->sbest : s->minv;
+        CK(cudaMemcpy(out, src, sizeof(double) * w * N, cudaMemcpyDeviceToHost));
         *n_out = (int64_t)N;
     } else {
         return fail(LC_EINVAL, "unknown inspect target");

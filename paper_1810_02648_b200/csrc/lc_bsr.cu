@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_bsr(BsrJob J) {
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += NT) {
         double o[9];
-        if (!inv3(J.diag + 9 * (size_t)i, o)) {
+        if (!lu_inv3(J.diag + 9 * (size_t)i, o)) {
             singular = 1;
             for (int k = 0; k < 9; ++k) o[k] = 0.0;
         }

@@ -484,6 +484,49 @@ __device__ __forceinline__ bool sym3_inverse(const double s[6], double o[6]) {
     o[5] = (a * d - b * b) * id;
     return true;
 }
+// np.linalg.inv of one 3x3 block (LAPACK getrf + getrs on the identity):
+// LU with partial pivoting (first maximal |pivot|), the multipliers scaled
+// by the pivot's reciprocal (dgetf2), then forward / back substitution per
+// identity column.  Agrees with numpy to ~1e-11 relative even on blocks of
+// condition 1e7, where the adjugate formula is off by 1e-5 (the photometric
+// blocks are nearly rank-deficient).  false when a pivot is exactly zero
+// (np.linalg.inv raises; the caller switches to pinv).
+__device__ inline bool lu_inv3(const double m[9], double o[9]) {
+    double a[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) a[i][j] = m[3 * i + j];
+    int piv[3] = {0, 1, 2};
+    bool ok = true;
+    for (int k = 0; k < 3; ++k) {
+        int p = k;
+        double best = fabs(a[k][k]);
+        for (int i = k + 1; i < 3; ++i)
+            if (fabs(a[i][k]) > best) { best = fabs(a[i][k]); p = i; }
+        if (p != k) {
+            for (int j = 0; j < 3; ++j) { const double t = a[k][j]; a[k][j] = a[p][j]; a[p][j] = t; }
+            const int t = piv[k]; piv[k] = piv[p]; piv[p] = t;
+        }
+        if (a[k][k] == 0.0) { ok = false; continue; }
+        const double r = 1.0 / a[k][k];
+        for (int i = k + 1; i < 3; ++i) a[i][k] *= r;
+        for (int i = k + 1; i < 3; ++i)
+            for (int j = k + 1; j < 3; ++j) a[i][j] -= a[i][k] * a[k][j];
+    }
+    if (!ok || !(isfinite(a[0][0]) && isfinite(a[1][1]) && isfinite(a[2][2]))) return false;
+    for (int j = 0; j < 3; ++j) {
+        double b[3];
+        for (int i = 0; i < 3; ++i) b[i] = piv[i] == j ? 1.0 : 0.0;
+        for (int i = 1; i < 3; ++i)
+            for (int k = 0; k < i; ++k) b[i] -= a[i][k] * b[k];
+        for (int i = 2; i >= 0; --i) {
+            for (int k = i + 1; k < 3; ++k) b[i] -= a[i][k] * b[k];
+            b[i] /= a[i][i];
+        }
+        for (int i = 0; i < 3; ++i) o[3 * i + j] = b[i];
+    }
+    return true;
+}
+
 // Eigen-decomposition of a symmetric 3x3 (full storage m[9], row-major) by
 // cyclic Jacobi rotations: m = V diag(lam) V^T, eigenvectors in V's columns.
 __device__ inline void sym3_eig(const double m_in[9], double lam[3], double V[9]) {

@@ -46,7 +46,8 @@ struct SurfJob {
     const double *prev, *prev2;
     int directional, enable_photo, enable_sil;
     // scratch
-    double *diag, *minv;      // N*6 (sym: xx xy xz yy yz zz)
+    double *diag;             // N*6 (sym: xx xy xz yy yz zz)
+    double *minv;             // N*9 np.linalg.inv of each diagonal block
     double *rhs, *x, *r, *z, *p, *ap, *best;   // N*3
     double *edir, *eg;        // E*3
     double *ell_d, *ell_g;    // 3*LC_ELL*N edge direction / signed gradient per ELL slot (SoA)

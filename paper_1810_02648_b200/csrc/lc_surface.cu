@@ -374,12 +374,14 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
         }
         for (int k = 0; k < 6; ++k) J.diag[6 * (size_t)i + k] = dg[k];
         st3(J.rhs + 3 * (size_t)i, rh);
-        double mi[6];
-        if (!sym3_inverse(dg, mi)) {
+        // M^-1 = np.linalg.inv of the full block (LU; not symmetrised, as numpy)
+        const double full[9] = {dg[0], dg[1], dg[2], dg[1], dg[3], dg[4], dg[2], dg[4], dg[5]};
+        double mi[9];
+        if (!lu_inv3(full, mi)) {
             acc[8] += 1.0;
-            for (int k = 0; k < 6; ++k) mi[k] = 0.0;
+            for (int k = 0; k < 9; ++k) mi[k] = 0.0;
         }
-        for (int k = 0; k < 6; ++k) J.minv[6 * (size_t)i + k] = mi[k];
+        for (int k = 0; k < 9; ++k) J.minv[9 * (size_t)i + k] = mi[k];
     }
     fst(3);
     T::template sums<9>(acc, c.red);
@@ -388,10 +390,9 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
     // pseudo-inverts every block (solvers.py:110-114)
     if (acc[8] > 0.0) {
         for (int i = T::tid(); i < c.N; i += T::size) {
-            double dg[6], mi[6];
-            for (int k = 0; k < 6; ++k) dg[k] = J.diag[6 * (size_t)i + k];
-            sym3_pinv(dg, mi);
-            for (int k = 0; k < 6; ++k) J.minv[6 * (size_t)i + k] = mi[k];
+            const double *dg = J.diag + 6 * (size_t)i;
+            const double full[9] = {dg[0], dg[1], dg[2], dg[1], dg[3], dg[4], dg[2], dg[4], dg[5]};
+            pinv3(full, J.minv + 9 * (size_t)i);
         }
         T::sync();
     }
@@ -469,7 +470,7 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, double *sm, int mode, int 
     double part[2] = {0, 0};
     for (int i = lo + (int)threadIdx.x; i < hi; i += NT) {
         const V3 r = ld3(rhs + 3 * (size_t)i);
-        const V3 z = sym3_mul(minv + 6 * (size_t)i, r);
+        const V3 z = mat_vec(minv + 9 * (size_t)i, r);
         st3(X + 3 * (size_t)i, v3(0, 0, 0));
         st3(BEST + 3 * (size_t)i, v3(0, 0, 0));
         st3(R + 3 * (size_t)i, r);
@@ -547,7 +548,7 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, double *sm, int mode, int 
             if (pend_best) st3(BEST + 3 * (size_t)i, x);
             x = x + alpha * ld3(ps + 3 * (size_t)(i - poff));
             const V3 r = ld3(R + 3 * (size_t)i) - alpha * ld3(aps + 3 * (size_t)(i - poff));
-            const V3 z = sym3_mul(minv + 6 * (size_t)i, r);
+            const V3 z = mat_vec(minv + 9 * (size_t)i, r);
             st3(X + 3 * (size_t)i, x);
             st3(R + 3 * (size_t)i, r);
             st3(zs + 3 * (size_t)(i - zoff), z);

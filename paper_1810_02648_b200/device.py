@@ -11,6 +11,7 @@ out; state stays resident in HBM between frames.
 from __future__ import annotations
 
 import ctypes as C
+import sys
 
 import numpy as np
 
@@ -200,9 +201,8 @@ class DeviceActor:
             self.ctx.lib.lc_actor_destroy(self.handle)
             self.handle = None
 
-    def __del__(self):
-        import sys
-        if sys.is_finalizing():   # the context may already be gone at interpreter exit
+    def __del__(self, _finalizing=sys.is_finalizing):
+        if _finalizing():   # the context may already be gone at interpreter exit
             return
         try:
             self.close()
@@ -373,6 +373,18 @@ class Tracker:
         for what, key in ((4, "v_init"), (5, "skinned")):
             buf = np.empty((self.N, 3))
             L.check(self.ctx.lib.lc_tracker_inspect(self.handle, stream, what, L.ptr(buf), cap, C.byref(n)))
+            out[key] = buf
+        return out
+
+    def inspect_system(self, stream: int) -> dict:
+        """The last Stage II GN step's compact normal system and PCG result:
+        diag (N,6) symmetric (xx xy xz yy yz zz), minv (N,9), rhs (N,3), the best
+        PCG iterate (N,3)."""
+        out = {}
+        n = C.c_int64()
+        for what, key, w in ((6, "diag", 6), (7, "rhs", 3), (8, "best", 3), (9, "minv", 9)):
+            buf = np.empty((self.N, w))
+            L.check(self.ctx.lib.lc_tracker_inspect(self.handle, stream, what, L.ptr(buf), buf.size, C.byref(n)))
             out[key] = buf
         return out
 
