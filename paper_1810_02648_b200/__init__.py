@@ -28,7 +28,9 @@ _LAZY = {
     "DistanceField": ".imageproc", "gaussian_pyramid": ".imageproc", "render_depth": ".imageproc",
     "render_attributes": ".imageproc", "render_vertex_ids": ".imageproc",
     "forward_kinematics": ".skinning", "skin_points": ".skinning",
-    "install": ".install",
+    "install": ".dropin",
+    "mean_vertex_error": ".metrics", "aligned_joint_error": ".metrics", "umeyama_alignment": ".metrics",
+    "sequence_errors": ".metrics", "iou": ".metrics", "evaluate_tracking": ".evaluation",
 }
 
 

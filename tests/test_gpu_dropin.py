@@ -106,6 +106,7 @@ def test_tracker_cache_is_bounded(montrack, ref_run):
     from paper_1810_02648_b200 import pipeline as PL
     inputs, cfg, _ = ref_run
     from paper_1810_02648_b200.config import SequenceConfig
-    for k in range(4):
-        PL._tracker_for(inputs.actor, inputs.camera, SequenceConfig(directional=False, frame0_rounds=3 + k))
+    for rounds in (1, 2, 3):
+        for d in (False, True):
+            PL._tracker_for(inputs.actor, inputs.camera, SequenceConfig(directional=d, frame0_rounds=rounds))
     assert len(PL._trackers) <= PL.TRACKER_CACHE
