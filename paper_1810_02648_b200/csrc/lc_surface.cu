@@ -10,6 +10,7 @@
 // with a_e = cs_fwd^2 + cs_rev^2 and b_e = ce_fwd^2 + ce_rev^2 per-config
 // constants and d_e the current unit edge direction.  Every CTA-wide sum is a
 // fixed-order tree (deterministic); there are no atomics.
+#include <cstdlib>
 #include "lc_pose.cuh"
 #include "lc_team.cuh"
 
@@ -113,6 +114,18 @@ __device__ __forceinline__ void sil_row(const SurfCtx &c, int b, V3 p, bool with
     }
 }
 
+// The edge's smooth + edge energies, both directed halves together:
+// |(u c_f)|^2 + |(u c_r)|^2 = alpha |u|^2 with alpha = c_f^2 + c_r^2 (and
+// beta for the length term) -- the reference's terms up to fp64 rounding.
+// The assembly (e0) and the line-search trials (e1) use this same formula,
+// so a zero step reproduces e0 exactly and is accepted (e1 <= e0) as in the
+// reference.
+__device__ __forceinline__ void edge_energy(const SurfCtx &c, int e, V3 u, double len_err, double &es,
+                                            double &ee) {
+    es = c.ec.alpha[e] * ((u.x * u.x + u.y * u.y) + u.z * u.z);
+    ee = c.ec.beta[e] * (len_err * len_err);
+}
+
 // per-edge quantities at the (trial) positions
 struct EdgeQ { V3 u, d; double len_err; bool degenerate; double e_smooth, e_edge; };
 
@@ -130,11 +143,7 @@ __device__ __forceinline__ void edge_q(const SurfCtx &c, int e, const double *v,
         q.d = v3(ev.x / l, ev.y / l, ev.z / l);
     }
     q.len_err = len - c.A.rest_len[e];
-    const double sf = c.ec.cs_f[e], sr = c.ec.cs_r[e], ef = c.ec.ce_f[e], er = c.ec.ce_r[e];
-    const double ux = q.u.x, uy = q.u.y, uz = q.u.z;
-    q.e_smooth = (ux * sf) * (ux * sf) + (uy * sf) * (uy * sf) + (uz * sf) * (uz * sf)
-               + (ux * sr) * (ux * sr) + (uy * sr) * (uy * sr) + (uz * sr) * (uz * sr);
-    q.e_edge = (q.len_err * ef) * (q.len_err * ef) + (q.len_err * er) * (q.len_err * er);
+    edge_energy(c, e, q.u, q.len_err, q.e_smooth, q.e_edge);
 }
 
 // energies at v (+ step): photo, sil, smooth, edge, vel, acc
@@ -193,35 +202,46 @@ __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v,
     if (J.enable_photo)
         for (int k = T::tid(); k < c.P; k += T::size) {
             const int i = J.vis[k];
+            const V3 vi = ld3(v + 3 * (size_t)i), si = ld3(step + 3 * (size_t)i);
             double sc = 1.0;
 #pragma unroll
             for (int h = 0; h < kSurfTrials; ++h, sc *= 0.5) {
                 if (h >= nt) break;
                 PhotoRow o;
-                photo_row(c, img, i, trial_pos(v, step, i, sc), false, o);
+                photo_row(c, img, i, vi + sc * si, false, o);
                 acc[6 * h] += o.r[0] * o.r[0] + o.r[1] * o.r[1] + o.r[2] * o.r[2];
             }
         }
     if (c.sil_on)
         for (int b = T::tid(); b < c.B; b += T::size) {
+            const int i = J.bidx[b];
+            const V3 vi = ld3(v + 3 * (size_t)i), si = ld3(step + 3 * (size_t)i);
             double sc = 1.0;
 #pragma unroll
             for (int h = 0; h < kSurfTrials; ++h, sc *= 0.5) {
                 if (h >= nt) break;
                 SilRow o;
-                sil_row(c, b, trial_pos(v, step, J.bidx[b], sc), false, o);
+                sil_row(c, b, vi + sc * si, false, o);
                 acc[6 * h + 1] += o.r * o.r;
             }
         }
     for (int e = T::tid(); e < c.E; e += T::size) {
+        // one load of the endpoints, their steps and V^S per edge for every
+        // trial; energies only (the unit direction is not needed here)
+        const int a = c.A.edges[2 * e], b = c.A.edges[2 * e + 1];
+        const V3 va = ld3(v + 3 * (size_t)a), vb = ld3(v + 3 * (size_t)b);
+        const V3 sa = ld3(step + 3 * (size_t)a), sb = ld3(step + 3 * (size_t)b);
+        const V3 sd = ld3(J.vs + 3 * (size_t)a) - ld3(J.vs + 3 * (size_t)b);
+        const double rl = c.A.rest_len[e];
         double sc = 1.0;
 #pragma unroll
         for (int h = 0; h < kSurfTrials; ++h, sc *= 0.5) {
             if (h >= nt) break;
-            EdgeQ q;
-            edge_q(c, e, v, step, q, sc);
-            acc[6 * h + 2] += q.e_smooth;
-            acc[6 * h + 3] += q.e_edge;
+            const V3 ev = (va + sc * sa) - (vb + sc * sb);
+            double es, ee;
+            edge_energy(c, e, ev - sd, norm3(ev) - rl, es, ee);
+            acc[6 * h + 2] += es;
+            acc[6 * h + 3] += ee;
         }
     }
     if (c.has_prev) {
@@ -229,11 +249,12 @@ __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v,
         for (int i = T::tid(); i < c.N; i += T::size) {
             const V3 q1 = ld3(J.prev + 3 * (size_t)i);
             const V3 q2 = J.prev2 ? ld3(J.prev2 + 3 * (size_t)i) : q1;
+            const V3 vi = ld3(v + 3 * (size_t)i), si = ld3(step + 3 * (size_t)i);
             double sc = 1.0;
 #pragma unroll
             for (int h = 0; h < kSurfTrials; ++h, sc *= 0.5) {
                 if (h >= nt) break;
-                const V3 p = trial_pos(v, step, i, sc);
+                const V3 p = vi + sc * si;
                 const V3 vr = (p - q1) * cv;
                 const V3 ar = ((p - 2.0 * q1) + q2) * ca;
                 acc[6 * h + 4] += vr.x * vr.x + vr.y * vr.y + vr.z * vr.z;
@@ -874,6 +895,15 @@ int surface_pcg_mode(int N, int cs, size_t *smem_bytes) {
     int mode = 0;
     if (72 * chunk <= 100 * 1024) mode = 2;
     else if (24 * chunk <= 190 * 1024) mode = 1;
+    // LIVECAP_PCG_MODE caps the mode (measurement sweeps)
+    // default 0: measured fastest (frames/s 3642 vs 3547 for mode 2 at the
+    // bench configuration) -- shared memory taken by the PCG vectors is L1
+    // lost to the nearest-contour queries and gathers of the other phases
+    static const int cap = [] {
+        const char *v = getenv("LIVECAP_PCG_MODE");
+        return v ? atoi(v) : 0;
+    }();
+    if (mode > cap) mode = cap < 0 ? 0 : cap;
     *smem_bytes = mode == 2 ? 72 * chunk : mode == 1 ? 24 * chunk : 0;
     return mode;
 }
