@@ -94,6 +94,10 @@ __device__ void qr_factor_quad(S &s, int n) {
                     d += __shfl_xor_sync(0xffffffffu, d, 1);
                     d += __shfl_xor_sync(0xffffffffu, d, 2);
                 }
+                // the quad's lanes have all read their rows of column j (and
+                // a_jk) before lane 0 overwrites a_jk: the shuffles above
+                // converge the warp, __syncwarp makes that ordering explicit
+                __syncwarp();
                 if (act) {
                     const double w = tau * fma(v0, ck, d);
 #pragma unroll
