@@ -236,6 +236,12 @@ int lc_render(lc_ctx *ctx, const lc_camera *cam, int32_t n, const double *verts,
 int lc_field_create(lc_ctx *ctx, int32_t h, int32_t w, const uint8_t *mask, lc_field **out);
 int lc_field_destroy(lc_field *f);
 int lc_field_n_contour(lc_field *f, int32_t *k);
+/* imageproc.py:117-124 euclidean_dt of the field's mask (DistanceField.dt,
+ * :182): H*W doubles, bit-identical to the reference */
+int lc_field_dt(lc_field *f, double *out);
+/* imageproc.py:52-115 _edt_squared of a feature image (nonzero = feature):
+ * H*W doubles, 1e18 in rows without any feature (bit-identical) */
+int lc_edt_squared(lc_ctx *ctx, int32_t h, int32_t w, const uint8_t *feature, double *out);
 /* kind 0: value(dist, clamped) 1: interface 2: residual(res, grad2) 3: gradient(vec2)
  * 4: inside.  out layout: n * 4 doubles [a, b, c, flag]. */
 int lc_field_query(lc_field *f, int64_t n, const double *pos, int32_t kind, double *out);

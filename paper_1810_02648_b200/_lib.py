@@ -118,6 +118,8 @@ _SIGS = {
     "lc_ctx_synchronize": (C.c_int, [P]),
     "lc_ctx_set_team_sizes": (C.c_int, [P, i32, i32]),
     "lc_tracker_set_pose": (C.c_int, [P, i32, P]),
+    "lc_field_dt": (C.c_int, [P, P]),
+    "lc_edt_squared": (C.c_int, [P, i32, i32, P, P]),
     "lc_surface_sets": (C.c_int, [P, P, P, P, i32, i32, i32, P, P, P, P, P, P, P]),
     "lc_kernel_launches": (C.c_int, [P, P]),
     "lc_actor_upload": (C.c_int, [P, P, P]),

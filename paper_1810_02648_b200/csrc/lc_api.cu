@@ -2339,6 +2339,56 @@ extern "C" int lc_gaussian_pyramid(lc_ctx *c, int32_t h, int32_t w, int32_t ch, 
     API_END
 }
 
+__global__ void k_edt_cols(const uint8_t *mask, int H, int W, int contour, double *g);
+__global__ void k_edt_rows(const double *g, int H, int W, int take_sqrt, long long *vs, double *zs, double *out);
+
+static void edt_launch(lc_ctx *c, const uint8_t *dmask, int H, int W, int contour, int take_sqrt, double *dout,
+                       DevArena &m) {
+    double *g = m.alloc<double>((size_t)H * W);
+    long long *vs = m.alloc<long long>((size_t)H * W);
+    double *zs = m.alloc<double>((size_t)H * (W + 1));
+    launch(c, k_edt_cols, dim3((unsigned)((W + 127) / 128)), dim3(128), 0, dmask, (int)H, (int)W, (int)contour, g);
+    launch(c, k_edt_rows, dim3((unsigned)((H + 127) / 128)), dim3(128), 0, (const double *)g, (int)H, (int)W,
+           (int)take_sqrt, vs, zs, dout);
+}
+
+// imageproc.py:52-115 _edt_squared of a feature image (H*W bytes, nonzero =
+// feature) -> H*W doubles (1e18 where a row has no feature at all)
+extern "C" int lc_edt_squared(lc_ctx *c, int32_t h, int32_t w, const uint8_t *feature, double *out) {
+    API_BEGIN
+    require(c && feature && out, "null argument");
+    require(h >= 1 && w >= 1, "bad image shape");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DevArena m;
+    const size_t HW = (size_t)h * w;
+    const uint8_t *df = m.upload(feature, HW, st);
+    double *dout = m.alloc<double>(HW);
+    edt_launch(c, df, h, w, 0, 0, dout, m);
+    CK(cudaMemcpyAsync(out, dout, sizeof(double) * HW, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return last_launch_status();
+    API_END
+}
+
+// imageproc.py:117-124 euclidean_dt / DistanceField.dt (:182): distance of
+// every pixel centre to the nearest contour pixel centre of the field's mask
+extern "C" int lc_field_dt(lc_field *f, double *out) {
+    API_BEGIN
+    require(f && out, "null argument");
+    lc_ctx *c = f->ctx;
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DevArena m;
+    const size_t HW = (size_t)f->H * f->W;
+    double *dout = m.alloc<double>(HW);
+    edt_launch(c, f->mask, f->H, f->W, 1, 1, dout, m);
+    CK(cudaMemcpyAsync(out, dout, sizeof(double) * HW, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return last_launch_status();
+    API_END
+}
+
 extern "C" int lc_field_create(lc_ctx *c, int32_t h, int32_t w, const uint8_t *mask, lc_field **out) {
     API_BEGIN
     require(c && mask && out, "null argument");

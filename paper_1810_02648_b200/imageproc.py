@@ -45,6 +45,16 @@ class DistanceField:
         return out.reshape(lead + (4,))
 
     @property
+    def dt(self) -> np.ndarray:
+        """Distance of every pixel centre to the nearest contour pixel centre
+        (imageproc.py:182, euclidean_dt), computed on the device on first use."""
+        if getattr(self, "_dt", None) is None:
+            out = np.empty(self.shape)
+            L.check(self.ctx.lib.lc_field_dt(self.handle, L.ptr(out)))
+            self._dt = out
+        return self._dt
+
+    @property
     def n_contour(self) -> int:
         k = C.c_int32()
         L.check(self.ctx.lib.lc_field_n_contour(self.handle, C.byref(k)))
@@ -79,6 +89,22 @@ class DistanceField:
                 self.handle = None
         except Exception:
             pass
+
+
+def edt_squared(feature, ctx: L.Context | None = None) -> np.ndarray:
+    """Exact squared Euclidean distance transform (imageproc.py:52-115)."""
+    ctx = ctx or L.default_context()
+    f = L.u8c(np.asarray(feature, dtype=bool))
+    if f.ndim != 2:
+        raise ValueError("feature image must be 2-D")
+    out = np.empty(f.shape)
+    L.check(ctx.lib.lc_edt_squared(ctx.handle, f.shape[0], f.shape[1], L.ptr(f), L.ptr(out)))
+    return out
+
+
+def euclidean_dt(mask, ctx: L.Context | None = None) -> np.ndarray:
+    """Unsigned distance to the nearest contour pixel centre (imageproc.py:117-124)."""
+    return DistanceField(mask, ctx).dt
 
 
 def gaussian_pyramid(image, kernel_sizes=(15, 9, 3), ctx: L.Context | None = None):

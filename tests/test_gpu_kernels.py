@@ -199,3 +199,22 @@ def test_contour_vertices_match_oracle(small):
         idx, n2 = contour_vertices(fr.gt_vertices, actor.mesh, cam)
         assert np.array_equal(c.indices, idx)
         assert np.allclose(c.normals2d, n2, atol=1e-12)
+
+
+def test_edt_bit_exact():
+    """a9: DistanceField.dt / euclidean_dt / _edt_squared (imageproc.py:52-124,
+    182) on the device, bit-identical to the reference's golden and to the
+    oracle's C restatement (random features, rows without any feature)."""
+    from oracle import imaging as OI
+    from paper_1810_02648_b200.imageproc import DistanceField, edt_squared, euclidean_dt
+    from test_oracle_golden import check_digest, gen, load
+    g = load("ref_kernels_small128.npz")
+    _, _, frames = gen("small", 128, 2, 3)
+    check_digest(g, frames)
+    assert np.array_equal(euclidean_dt(frames[1].mask), g["edt"])
+    assert np.array_equal(DistanceField(frames[1].mask).dt, g["edt"])
+    rng = np.random.default_rng(7)
+    for shape, p in (((37, 53), 0.02), ((128, 96), 0.001), ((64, 64), 0.3), ((1, 17), 0.2)):
+        feat = rng.random(shape) < p
+        feat[shape[0] // 2] = False            # a featureless row
+        assert np.array_equal(edt_squared(feat), OI.edt_squared(feat)), shape
