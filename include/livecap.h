@@ -187,6 +187,7 @@ int lc_ctx_synchronize(lc_ctx *ctx);
  * (overrides LIVECAP_POSE_CLUSTER / LIVECAP_SURFACE_CLUSTER) */
 int lc_ctx_set_team_sizes(lc_ctx *ctx, int32_t pose_ctas, int32_t surface_ctas);
 int lc_kernel_launches(lc_ctx *ctx, int64_t *count);   /* kernels launched on ctx so far */
+int lc_process_launches(int64_t *count);               /* kernels launched by every context of the process */
 
 /* ---- actor (template.py:68-256; uploaded once, immutable) ---- */
 int lc_actor_upload(lc_ctx *ctx, const lc_actor_desc *desc, lc_actor **out);

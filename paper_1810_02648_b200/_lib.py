@@ -122,6 +122,7 @@ _SIGS = {
     "lc_edt_squared": (C.c_int, [P, i32, i32, P, P]),
     "lc_surface_sets": (C.c_int, [P, P, P, P, i32, i32, i32, P, P, P, P, P, P, P]),
     "lc_kernel_launches": (C.c_int, [P, P]),
+    "lc_process_launches": (C.c_int, [P]),
     "lc_actor_upload": (C.c_int, [P, P, P]),
     "lc_actor_destroy": (C.c_int, [P]),
     "lc_pcg_solve_bsr": (C.c_int, [P, i32, i64, P, P, P, P, P, i32, P, P]),
@@ -274,6 +275,14 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def process_launches() -> int:
+    """Kernels launched by every library context of this process (the
+    per-thread default contexts of worker threads included)."""
+    n = C.c_int64()
+    check(load_library().lc_process_launches(C.byref(n)))
+    return n.value
 
 
 _tls = threading.local()

@@ -3,6 +3,7 @@
 // of solve_frame (reference pipeline.py:156-302) batched over streams, and
 // the single-call seams used by the Python mirror of the reference API.
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -24,6 +25,9 @@ static void require(bool ok, const char *msg) {
 }
 
 static thread_local std::string g_err;
+// kernels launched by every context of the process (contexts are per host
+// thread; the reference's pipelined driver solves on worker threads)
+static std::atomic<long long> g_launches{0};
 
 static int fail(int code, const std::string &msg) {
     g_err = msg;
@@ -77,6 +81,7 @@ static void launch_named(const char *name, lc_ctx *c, K kernel, dim3 g, dim3 b, 
         c->prof_events.push_back({e0, e1});
     }
     c->launches++;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     const cudaError_t e = cudaPeekAtLastError();
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -136,6 +141,7 @@ static void launch_cluster(const char *name, lc_ctx *c, void (*kernel)(KArgs...)
         c->prof_events.push_back({e0, e1});
     }
     c->launches++;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     if (e == cudaSuccess) e = cudaPeekAtLastError();
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -412,6 +418,12 @@ extern "C" int lc_profile_read(lc_ctx *c, double *total_ms, int64_t *count) {
     }
     *total_ms = tot;
     *count = (int64_t)c->prof_events.size();
+    return LC_OK;
+}
+
+extern "C" int lc_process_launches(int64_t *count) {
+    if (!count) return fail(LC_EINVAL, "null argument");
+    *count = (int64_t)g_launches.load(std::memory_order_relaxed);
     return LC_OK;
 }
 
@@ -2498,6 +2510,7 @@ extern "C" int lc_pcg_solve_bsr(lc_ctx *c, int32_t n, int64_t m_, const double *
         while ((1 << bits) < n && bits < 31) ++bits;
         CK(bsr_sort(tmp, tb, keys, skeys, vals, order, m, bits, st));
         c->launches++;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     }
     launch(c, k_bsr_rowptr, dim3(1), dim3(1024), 0, n, (const int *)count, rowptr);
     J.rowptr = rowptr;

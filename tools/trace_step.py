@@ -41,7 +41,7 @@ def main():
             img[s, f].copy_(torch.from_numpy(frames[s][f].image))
             msk[s, f].copy_(torch.from_numpy(frames[s][f].mask.astype(np.uint8)))
     torch.cuda.synchronize()
-    tr = Tracker(actor, cam, SequenceConfig(), a.streams, ctx=ctx)
+    tr = Tracker(actor, cam, SequenceConfig(directional=False), a.streams, ctx=ctx)   # the bench workload
 
     def q(f):
         for s in range(a.streams):
