@@ -60,6 +60,9 @@ def parse():
                     help="SequenceConfig(directional=True): the reference's default, which loses the subject "
                          "on this workload (VERDICT r01); the default workload tracks (directional=False)")
     ap.add_argument("--no-quality", action="store_true", help="skip the untimed tracking-quality replay")
+    ap.add_argument("--stage-pipeline", choices=["auto", "on", "off"], default="auto",
+                    help="time the paper's pose -> non-rigid GPU-pair pipeline (StagePipeline) on cuda:0/cuda:1; "
+                         "auto: when one process sees >= 2 devices")
     ap.add_argument("--dry-run", action="store_true",
                     help="multi-rank plumbing only (process group, sharding, max-over-ranks timing, gather); "
                          "no GPU, no solve - for CPU CI of the --gpus N path")
@@ -424,6 +427,16 @@ def run_ours(args):
         if rank == 0:
             gathered = int(g[0].shape[0])
     tr2.close()
+    # ---- the paper's GPU-pair stage pipeline: Stage I on
+    # cuda:0, Stage II on cuda:1, peer copies of poses / track state between
+    # them; host frames as in e2e (mask-only upload to the pose device)
+    pipe_line = None
+    ndev = torch.cuda.device_count()
+    if args.stage_pipeline == "on" or (args.stage_pipeline == "auto" and world == 1 and ndev >= 2):
+        if ndev >= 2 and world == 1:
+            pipe_line = run_stage_pipeline(actor, cam, cfg, Sn, img_h, msk_h, dets, W, K, AHEAD)
+        else:
+            pipe_line = {"skipped": f"needs one process with two devices (devices {ndev}, ranks {world})"}
     # the same e2e loop with 8-bit frames (the reference's on-disk capture
     # format, frames/*.png read by load_color): the images are the synthetic
     # frames quantized to u8, converted on the device bit-exactly as
@@ -467,6 +480,7 @@ def run_ours(args):
             "e2e": {"value": world * Sn * K / (ms_e2e / 1e3), "unit": "frames/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "e2e_u8": e2e_u8,
+            "stage_pipeline": pipe_line,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "kernel": DOMINANT, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak if peak else None,
@@ -503,6 +517,56 @@ def run_ours(args):
         import torch.distributed as dist
         dist.destroy_process_group()
     return out
+
+
+# ---------------------------------------------------------------------------
+# GPU-pair stage pipeline leg
+
+def run_stage_pipeline(actor, cam, cfg, Sn, img_h, msk_h, dets, W, K, AHEAD):
+    """frames/s of device.StagePipeline (pose device 0, surface device 1):
+    host frames queued AHEAD frames ahead, K timed steps after W warm-up
+    steps; timed with CUDA events on both devices (the max of the two)."""
+    import numpy as np
+    import torch
+
+    from paper_1810_02648_b200.device import StagePipeline
+    groups = 2 if Sn % 2 == 0 else 1
+    pipe = StagePipeline(actor, cam, cfg, Sn, pose_device=0, surface_device=1, groups=groups)
+
+    def queue(f):
+        for s in range(Sn):
+            pipe.set_frame(s, img_h[s, f].numpy(), msk_h[s, f].numpy(), dets[s][f])
+
+    for f in range(AHEAD):
+        queue(f)
+    for f in range(W):
+        queue(f + AHEAD)
+        pipe.step()
+    pipe.synchronize()
+    evs = []
+    for d in (0, 1):
+        with torch.cuda.device(d):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            evs.append((d, e0, e1))
+    for f in range(W, W + K):
+        queue(f + AHEAD)
+        pipe.step()
+    pipe.synchronize()
+    ms = 0.0
+    for d, e0, e1 in evs:
+        with torch.cuda.device(d):
+            e1.record()
+            e1.synchronize()
+            ms = max(ms, e0.elapsed_time(e1))
+    x_last = [pipe.result(s, with_report=False)[0] for s in range(Sn)]
+    pipe.close()
+    return {"value": Sn * K / (ms / 1e3), "unit": "frames/s", "devices": [0, 1], "stream_groups": groups,
+            "ms_per_step": ms / K, "finite": bool(all(bool(np.isfinite(x).all()) for x in x_last)),
+            "how": "StagePipeline: Stage I (conditioning + pose GN) on cuda:0, Stage II (surface GN, PCG, "
+                   "snapping) on cuda:1; per frame cudaMemcpyPeerAsync of the poses (0 -> 1) and the "
+                   "Stage-I track state (1 -> 0); host frames (mask-only to cuda:0)"}
 
 
 # ---------------------------------------------------------------------------

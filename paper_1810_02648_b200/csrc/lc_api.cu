@@ -1227,8 +1227,9 @@ static void launch_preprocess(lc_ctx *c, const ConfigDev &cf, const lc_config &c
     for (FrameIn *f : fs) cudaEventRecord(f->ready_obs, c->aux);
     if (cfg.mode == 0) {
         std::vector<PyrTarget> ts;
-        for (FrameIn *f : fs) ts.push_back(PyrTarget{f->image_src, f->pyr, f->tmp});
-        pyramid(c, cf, ts, H, W, cfg.nonrigid.n_levels);
+        for (FrameIn *f : fs)
+            if (f->has_image) ts.push_back(PyrTarget{f->image_src, f->pyr, f->tmp});
+        if (!ts.empty()) pyramid(c, cf, ts, H, W, cfg.nonrigid.n_levels);
     }
     mark(c, "pre:pyramid");
     for (FrameIn *f : fs) {
@@ -1320,20 +1321,21 @@ static void pose_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, cons
 
 static void surface_launch(lc_ctx *c, const lc_actor *a, const lc_camera &cam, const ConfigDev &cf,
                            const std::vector<SurfJob> &jobs) {
-    // 4-CTA teams for both solvers: a stream's solve is latency-bound, so
-    // with many streams in flight (the throughput case, bench.py: 16 streams
-    // in 4 groups) fewer SMs per stream give more frames/s per GPU
-    // (measured: pose/surface teams 4/4 3.93k frames/s, 4/8 3.76k, 8/16
-    // 3.26k, 4/1 2.83k).  A single latency-critical stream solves fastest
-    // with LIVECAP_POSE_CLUSTER=8 LIVECAP_SURFACE_CLUSTER=16.
-    // The default surface team grows with the mesh: the smallest of 4, 8, 16
-    // CTAs that leaves at most 6 vertices per thread (x5k: 4; x20k: 16,
-    // measured at cfg4 1998 frames/s vs 1790 on 8 and 1362 on 4).
+    // A stream's solve is latency-bound; the team size trades SMs per stream
+    // against latency.  The default surface team grows with the mesh: the
+    // smallest of 4, 8, 16 CTAs that leaves at most 3 vertices per thread
+    // (x5k: 8; x20k: 16).  Measured at the bench's 16 streams in 4 groups
+    // with the owner-computes assembly: x5k 8-CTA teams 3669 frames/s and
+    // 1.34 ms per launch vs 3498 and 2.04 ms on 4 (round 1, before the
+    // preprocessing contention was visible: 4/4 3.93k, 4/8 3.76k); x20k
+    // cfg4 16: 1998 frames/s vs 1790 on 8 and 1362 on 4.  A single
+    // latency-critical stream solves fastest with LIVECAP_POSE_CLUSTER=8
+    // LIVECAP_SURFACE_CLUSTER=16.
     static const int cs_env = cluster_size_for("LIVECAP_SURFACE_CLUSTER");
     static const bool cs_global = getenv("LIVECAP_CLUSTER") != nullptr;
     int cs = c->surf_cs > 0 ? c->surf_cs : cs_env > 0 ? cs_env : cluster_size();
     if (c->surf_cs <= 0 && cs_env <= 0 && !cs_global)
-        while (cs < 16 && (long long)a->dev.N > 6LL * cs * surface_block_threads()) cs *= 2;
+        while (cs < 16 && (long long)a->dev.N > 3LL * cs * surface_block_threads()) cs *= 2;
     auto k = cs == 1 ? k_surface_solve_t<1> : cs == 2 ? k_surface_solve_t<2> : cs == 4 ? k_surface_solve_t<4>
              : cs == 8 ? k_surface_solve_t<8> : k_surface_solve_t<16>;
     size_t smem = 0;
@@ -1552,12 +1554,16 @@ extern "C" int lc_tracker_set_frame(lc_tracker *t, int32_t stream, const double 
     require(t && det, "null argument");
     require(stream >= 0 && stream < t->S, "stream index out of range");
     CK(cudaSetDevice(t->ctx->device));   // the tracker's streams belong to its device
-    require(image && mask, "null image or mask");
+    // image == NULL queues the mask and detections only: Stage I reads no
+    // image, so the Stage-I tracker of a GPU pair skips the 8-byte-per-
+    // channel upload and the blur pyramid (Stage II refuses such a frame)
+    require(mask, "null mask");
     Slot *s = t->slots[stream];
     lc_ctx *c = t->ctx;
     FrameIn &f = s->in[s->in_tail];
     require(f.state == 0, "the stream's frame queue is full: call lc_tracker_step first");
     const size_t HW = (size_t)s->H * s->W;
+    f.has_image = image != nullptr;
     if (on_device) {
         f.image_src = image;
         f.mask_src = mask;
@@ -1565,11 +1571,11 @@ extern "C" int lc_tracker_set_frame(lc_tracker *t, int32_t stream, const double 
         // the host copies go on the copy stream, after the solve that last
         // read the buffer; the buffer's preprocessing waits for them
         if (f.used) CK(cudaStreamWaitEvent(c->copy, f.freed, 0));
-        CK(cudaMemcpyAsync(f.image, image, HW * 3 * sizeof(double), cudaMemcpyHostToDevice, c->copy));
+        if (image) CK(cudaMemcpyAsync(f.image, image, HW * 3 * sizeof(double), cudaMemcpyHostToDevice, c->copy));
         CK(cudaMemcpyAsync(f.mask, mask, HW, cudaMemcpyHostToDevice, c->copy));
         CK(cudaEventRecord(f.uploaded, c->copy));
         f.pending_upload = true;
-        f.image_src = f.image;
+        f.image_src = image ? f.image : nullptr;
         f.mask_src = f.mask;
     }
     const int J = t->actor->skel.J;
@@ -1622,6 +1628,7 @@ extern "C" int lc_tracker_set_frame_u8(lc_tracker *t, int32_t stream, const uint
     CK(cudaEventRecord(f.uploaded, c->copy));
     f.pending_upload = true;
     f.image_src = f.image;
+    f.has_image = true;
     const int J = t->actor->skel.J;
     stage_to(c, f.j2d, det->joints2d, sizeof(double) * 2 * (J + 4));
     stage_to(c, f.j3d_raw, det->joints3d, sizeof(double) * 3 * J);
@@ -1650,6 +1657,7 @@ extern "C" int lc_tracker_step_stage(lc_tracker *t, int32_t stages) {
     for (Slot *s : t->slots) {
         FrameIn &f = s->in[s->in_head];
         require(f.state >= 1, "no frame queued for a stream: call lc_tracker_set_frame first");
+        require(f.has_image || !(stages & 2), "Stage II needs the frame's image (it was queued without one)");
         cur.push_back(&f);
         if (f.state == 1) todo.push_back(&f);
         FrameIn &n = s->in[(s->in_head + 1) % LC_QUEUE];

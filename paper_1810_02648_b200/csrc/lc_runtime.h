@@ -104,6 +104,7 @@ struct FrameIn {
     cudaEvent_t freed = nullptr;       // last solve that read this buffer done (main stream)
     cudaEvent_t uploaded = nullptr;    // host inputs copied (copy stream)
     bool pending_upload = false;
+    bool has_image = true;             // false: mask + detections only (a Stage-I-only tracker)
     bool used = false;                 // `freed` has been recorded at least once
     int state = 0;                     // 0 empty, 1 staged, 2 preprocessing launched
 };

@@ -36,18 +36,11 @@ struct SurfCtx {
     EdgeConstDev ec;
     SurfHyperDev hp;
     int H, W, P, B, N, E;
+    int lo, hi, p0, p1, b0, b1;   // own_ranges(): this CTA's vertices, visible rows, boundary rows
     bool has_prev;
     bool sil_on;
     double *red;
 };
-
-// v_i + sc * step_i; sc is a power of two (exact), so this has the bits of
-// the reference's in-place halvings of the step
-__device__ __forceinline__ V3 trial_pos(const double *v, const double *step, int i, double sc = 1.0) {
-    const V3 a = ld3(v + 3 * (size_t)i);
-    if (!step) return a;
-    return a + sc * ld3(step + 3 * (size_t)i);
-}
 
 // one pyramid level as bilinear3 samples it
 struct LevelSrc {
@@ -126,14 +119,16 @@ __device__ __forceinline__ void edge_energy(const SurfCtx &c, int e, V3 u, doubl
     ee = c.ec.beta[e] * (len_err * len_err);
 }
 
-// per-edge quantities at the (trial) positions
-struct EdgeQ { V3 u, d; double len_err; bool degenerate; double e_smooth, e_edge; };
+// One mesh edge seen from one of its endpoints i (slot of i's adjacency):
+// the reference's per-edge quantities (nonrigid_stage.py:235-255) with the
+// edge oriented src -> dst exactly as the reference forms them, so both
+// endpoints compute the same bits.
+struct SlotEdge { V3 u, d, g; double len_err; bool degenerate; };
 
-__device__ __forceinline__ void edge_q(const SurfCtx &c, int e, const double *v, const double *step,
-                                       EdgeQ &q, double sc = 1.0) {
-    const int a = c.A.edges[2 * e], b = c.A.edges[2 * e + 1];
-    const V3 ev = trial_pos(v, step, a, sc) - trial_pos(v, step, b, sc);
-    const V3 sd = ld3(c.J->vs + 3 * (size_t)a) - ld3(c.J->vs + 3 * (size_t)b);
+__device__ __forceinline__ void slot_edge(const SurfCtx &c, int e, bool src, V3 vi, V3 vsi, V3 vj, V3 vsj,
+                                          double al, double be, SlotEdge &q) {
+    const V3 ev = src ? vi - vj : vj - vi;
+    const V3 sd = src ? vsi - vsj : vsj - vsi;
     q.u = ev - sd;
     const double len = norm3(ev);
     q.degenerate = len < 1e-9;
@@ -143,49 +138,37 @@ __device__ __forceinline__ void edge_q(const SurfCtx &c, int e, const double *v,
         q.d = v3(ev.x / l, ev.y / l, ev.z / l);
     }
     q.len_err = len - c.A.rest_len[e];
-    edge_energy(c, e, q.u, q.len_err, q.e_smooth, q.e_edge);
+    q.g = al * q.u + be * (q.len_err * q.d);
 }
 
-// energies at v (+ step): photo, sil, smooth, edge, vel, acc
+// The team's work partition, shared by the assembly and the line-search
+// trials so that both sum every energy term in the same order (a zero step
+// reproduces e0 exactly and is accepted, as in the reference): CTA r owns
+// the vertex chunk [lo, hi) (the PCG's chunk too), the visible rows
+// [p0, p1) and boundary rows [b0, b1) of its vertices (both lists are in
+// ascending vertex order), and every edge at its src endpoint's slot.
+// Everything the assembly writes for a vertex is written by the vertex's
+// own CTA, so its phases are separated by CTA barriers only.
+__device__ __forceinline__ int lower_bound_ids(const int *ids, int n, int key) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (ids[m] < key) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
+
 template <typename T>
-__device__ void surf_energy(const SurfCtx &c, int level, const double *v, const double *step,
-                            double en[6]) {
+__device__ __forceinline__ void own_ranges(SurfCtx &c) {
+    const int chunk = (c.N + T::ctas - 1) / T::ctas;
+    c.lo = min(c.N, T::rank() * chunk);
+    c.hi = min(c.N, c.lo + chunk);
     const SurfJob &J = *c.J;
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const LevelSrc img = level_src(c, level);
-    if (J.enable_photo)
-        for (int k = T::tid(); k < c.P; k += T::size) {
-            const int i = J.vis[k];
-            PhotoRow o;
-            photo_row(c, img, i, trial_pos(v, step, i), false, o);
-            acc[0] += o.r[0] * o.r[0] + o.r[1] * o.r[1] + o.r[2] * o.r[2];
-        }
-    if (c.sil_on)
-        for (int b = T::tid(); b < c.B; b += T::size) {
-            SilRow o;
-            sil_row(c, b, trial_pos(v, step, J.bidx[b]), false, o);
-            acc[1] += o.r * o.r;
-        }
-    for (int e = T::tid(); e < c.E; e += T::size) {
-        EdgeQ q;
-        edge_q(c, e, v, step, q);
-        acc[2] += q.e_smooth;
-        acc[3] += q.e_edge;
-    }
-    if (c.has_prev) {
-        const double cv = sqrt(c.hp.w_vel), ca = sqrt(c.hp.w_acc);
-        for (int i = T::tid(); i < c.N; i += T::size) {
-            const V3 p = trial_pos(v, step, i);
-            const V3 q1 = ld3(J.prev + 3 * (size_t)i);
-            const V3 q2 = J.prev2 ? ld3(J.prev2 + 3 * (size_t)i) : q1;
-            const V3 vr = (p - q1) * cv;
-            const V3 ar = ((p - 2.0 * q1) + q2) * ca;
-            acc[4] += vr.x * vr.x + vr.y * vr.y + vr.z * vr.z;
-            acc[5] += ar.x * ar.x + ar.y * ar.y + ar.z * ar.z;
-        }
-    }
-    T::template sums<8>(acc, c.red);
-    for (int k = 0; k < 6; ++k) en[k] = acc[k];
+    c.p0 = J.vis ? lower_bound_ids(J.vis, c.P, c.lo) : 0;
+    c.p1 = J.vis ? lower_bound_ids(J.vis, c.P, c.hi) : 0;
+    c.b0 = J.bidx ? lower_bound_ids(J.bidx, c.B, c.lo) : 0;
+    c.b1 = J.bidx ? lower_bound_ids(J.bidx, c.B, c.hi) : 0;
 }
 
 // energies of nt <= 4 line-search trials v + step * 0.5^h at once (h < nt):
@@ -200,7 +183,7 @@ __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v,
     for (int k = 0; k < kSurfTrials * 6; ++k) acc[k] = 0.0;
     const LevelSrc img = level_src(c, level);
     if (J.enable_photo)
-        for (int k = T::tid(); k < c.P; k += T::size) {
+        for (int k = c.p0 + (int)threadIdx.x; k < c.p1; k += NT) {
             const int i = J.vis[k];
             const V3 vi = ld3(v + 3 * (size_t)i), si = ld3(step + 3 * (size_t)i);
             double sc = 1.0;
@@ -213,7 +196,7 @@ __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v,
             }
         }
     if (c.sil_on)
-        for (int b = T::tid(); b < c.B; b += T::size) {
+        for (int b = c.b0 + (int)threadIdx.x; b < c.b1; b += NT) {
             const int i = J.bidx[b];
             const V3 vi = ld3(v + 3 * (size_t)i), si = ld3(step + 3 * (size_t)i);
             double sc = 1.0;
@@ -244,12 +227,12 @@ __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v,
             acc[6 * h + 3] += ee;
         }
     }
-    if (c.has_prev) {
-        const double cv = sqrt(c.hp.w_vel), ca = sqrt(c.hp.w_acc);
-        for (int i = T::tid(); i < c.N; i += T::size) {
+    const double cv = sqrt(c.hp.w_vel), ca = sqrt(c.hp.w_acc);
+    if (c.has_prev)
+        for (int i = c.lo + (int)threadIdx.x; i < c.hi; i += NT) {
+            const V3 vi = ld3(v + 3 * (size_t)i), si = ld3(step + 3 * (size_t)i);
             const V3 q1 = ld3(J.prev + 3 * (size_t)i);
             const V3 q2 = J.prev2 ? ld3(J.prev2 + 3 * (size_t)i) : q1;
-            const V3 vi = ld3(v + 3 * (size_t)i), si = ld3(step + 3 * (size_t)i);
             double sc = 1.0;
 #pragma unroll
             for (int h = 0; h < kSurfTrials; ++h, sc *= 0.5) {
@@ -261,8 +244,10 @@ __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v,
                 acc[6 * h + 5] += ar.x * ar.x + ar.y * ar.y + ar.z * ar.z;
             }
         }
-    }
-    T::template sums<kSurfTrials * 6>(acc, c.red);
+    // (the trials only read: v and the step were ordered by the team barrier
+    // before this phase, and the caller's next global writes come after a
+    // full barrier)
+    T::template sums_light<kSurfTrials * 6>(acc, c.red);
     for (int h = 0; h < kSurfTrials; ++h)
         for (int k = 0; k < 6; ++k) en[h][k] = acc[6 * h + k];
 }
@@ -273,7 +258,14 @@ __device__ __forceinline__ double total_energy(const double en[6], bool has_prev
     return t;
 }
 
-// GN evaluation with the normal system (diag, minv, rhs, edir); returns energies + counters
+// GN evaluation with the normal system (diag, minv, rhs, and the edge
+// directions of every ELL slot / CSR-tail edge the matvec reads); returns
+// energies + counters.  One edge-parallel pass evaluates every edge once
+// (balanced over the team) and scatters its direction and signed gradient
+// to the ELL slots of both endpoints; after that single team barrier the
+// rest is owner-computes (see own_ranges): the CTA's photometric and
+// silhouette rows, then its vertices' full blocks, separated by CTA
+// barriers only, and one light team reduction at the end.
 template <typename T>
 __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, double en[6],
                               int counts[3], int fine = -1) {
@@ -282,42 +274,48 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
         if (fine >= 0 && J.phase && T::tid() == 0) J.phase[fine + k] = gtimer();
     };
     const double cv = sqrt(c.hp.w_vel), ca = sqrt(c.hp.w_acc);
-    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // 6 energies, pruned, behind, singular blocks
-    double degen = 0.0;
-    // P0: clear data blocks; per-edge direction + gradient contribution
-    for (int i = T::tid(); i < c.N; i += T::size) {
+    // 6 energies, pruned, behind, singular blocks, degenerate directed edges
+    double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    // E: every edge once -- energies, direction, signed gradient into its
+    // ELL slots at both endpoints (CSR tails: per edge, edir / eg)
+    const size_t LN = (size_t)LC_ELL * c.N;
+    for (int e = T::tid(); e < c.E; e += T::size) {
+        const int a = c.A.edges[2 * e], b = c.A.edges[2 * e + 1];
+        const double al = c.ec.alpha[e], be = c.ec.beta[e];
+        SlotEdge q;
+        slot_edge(c, e, true, ld3(v + 3 * (size_t)a), ld3(J.vs + 3 * (size_t)a), ld3(v + 3 * (size_t)b),
+                  ld3(J.vs + 3 * (size_t)b), al, be, q);
+        double es, ee;
+        edge_energy(c, e, q.u, q.len_err, es, ee);
+        acc[2] += es;
+        acc[3] += ee;
+        acc[9] += q.degenerate ? 2.0 : 0.0;
+        const int ps = c.A.epos[2 * e], pd = c.A.epos[2 * e + 1];
+        if (ps >= 0) {   // the src side subtracts g
+            J.ell_d[ps] = q.d.x; J.ell_d[LN + ps] = q.d.y; J.ell_d[2 * LN + ps] = q.d.z;
+            J.ell_g[ps] = -q.g.x; J.ell_g[LN + ps] = -q.g.y; J.ell_g[2 * LN + ps] = -q.g.z;
+        }
+        if (pd >= 0) {
+            J.ell_d[pd] = q.d.x; J.ell_d[LN + pd] = q.d.y; J.ell_d[2 * LN + pd] = q.d.z;
+            J.ell_g[pd] = q.g.x; J.ell_g[LN + pd] = q.g.y; J.ell_g[2 * LN + pd] = q.g.z;
+        }
+        if (ps < 0 || pd < 0) {   // in a pole vertex's CSR tail
+            st3(J.edir + 3 * (size_t)e, q.d);
+            st3(J.eg + 3 * (size_t)e, q.g);
+        }
+    }
+    // R0: clear the data blocks of the CTA's vertices
+    for (int i = c.lo + (int)threadIdx.x; i < c.hi; i += NT) {
         double *dg = J.diag + 6 * (size_t)i;
         for (int k = 0; k < 6; ++k) dg[k] = 0.0;
         st3(J.rhs + 3 * (size_t)i, v3(0, 0, 0));
     }
-    for (int e = T::tid(); e < c.E; e += T::size) {
-        EdgeQ q;
-        edge_q(c, e, v, nullptr, q);
-        acc[2] += q.e_smooth;
-        acc[3] += q.e_edge;
-        degen += q.degenerate ? 2.0 : 0.0;
-        st3(J.edir + 3 * (size_t)e, q.d);
-        const double al = c.ec.alpha[e], be = c.ec.beta[e];
-        const V3 g = al * q.u + be * (q.len_err * q.d);
-        st3(J.eg + 3 * (size_t)e, g);
-        // the edge's ELL slots at its two endpoints (the src side subtracts g)
-        const size_t LN = (size_t)LC_ELL * c.N;
-        const int ps = c.A.epos[2 * e], pd = c.A.epos[2 * e + 1];
-        if (ps >= 0) {
-            J.ell_d[ps] = q.d.x; J.ell_d[LN + ps] = q.d.y; J.ell_d[2 * LN + ps] = q.d.z;
-            J.ell_g[ps] = -g.x; J.ell_g[LN + ps] = -g.y; J.ell_g[2 * LN + ps] = -g.z;
-        }
-        if (pd >= 0) {
-            J.ell_d[pd] = q.d.x; J.ell_d[LN + pd] = q.d.y; J.ell_d[2 * LN + pd] = q.d.z;
-            J.ell_g[pd] = g.x; J.ell_g[LN + pd] = g.y; J.ell_g[2 * LN + pd] = g.z;
-        }
-    }
-    T::sync();
+    T::sync();   // the only team barrier before the reduction: slots written by any CTA
     fst(0);
-    // P1: photometric data blocks (visible ids are unique)
+    // R1: photometric data blocks (visible ids are unique)
     const LevelSrc img = level_src(c, level);
     if (J.enable_photo)
-        for (int k = T::tid(); k < c.P; k += T::size) {
+        for (int k = c.p0 + (int)threadIdx.x; k < c.p1; k += NT) {
             const int i = J.vis[k];
             PhotoRow o;
             photo_row(c, img, i, ld3(v + 3 * (size_t)i), true, o);
@@ -334,11 +332,11 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
             for (int a = 0; a < 3; ++a)
                 rh[a] = -(o.J[0][a] * o.r[0] + o.J[1][a] * o.r[1] + o.J[2][a] * o.r[2]);
         }
-    T::sync();
+    __syncthreads();
     fst(1);
-    // P2: silhouette rank-1 blocks (boundary ids are unique)
+    // R2: silhouette rank-1 blocks (boundary ids are unique)
     if (c.sil_on)
-        for (int b = T::tid(); b < c.B; b += T::size) {
+        for (int b = c.b0 + (int)threadIdx.x; b < c.b1; b += NT) {
             const int i = J.bidx[b];
             SilRow o;
             sil_row(c, b, ld3(v + 3 * (size_t)i), true, o);
@@ -350,17 +348,16 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
             double *rh = J.rhs + 3 * (size_t)i;
             rh[0] += -o.g[0] * o.r; rh[1] += -o.g[1] * o.r; rh[2] += -o.g[2] * o.r;
         }
-    T::sync();
+    __syncthreads();
     fst(2);
-    // P3: full diagonal blocks, rhs, Jacobi preconditioner, temporal energies
-    for (int i = T::tid(); i < c.N; i += T::size) {
+    // R3: full diagonal blocks, rhs, Jacobi preconditioner, temporal
+    // energies of the CTA's vertices; incident edges in the reference's
+    // order: ELL slots (coalesced, independent loads), then the CSR tail
+    for (int i = c.lo + (int)threadIdx.x; i < c.hi; i += NT) {
         double dg[6];
         for (int k = 0; k < 6; ++k) dg[k] = J.diag[6 * (size_t)i + k];
         V3 rh = ld3(J.rhs + 3 * (size_t)i);
-        // incident edges in the reference's order: ELL slots (coalesced,
-        // independent loads), then the CSR tail of high-degree vertices
         const int cnt = c.A.ell_cnt[i];
-        const size_t LN = (size_t)LC_ELL * c.N;
 #pragma unroll
         for (int k = 0; k < LC_ELL; ++k) {
             if (k >= cnt) continue;
@@ -405,24 +402,24 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
         for (int k = 0; k < 9; ++k) J.minv[9 * (size_t)i + k] = mi[k];
     }
     fst(3);
-    T::template sums<9>(acc, c.red);
+    // R1-R3 write only the CTA's own vertices, which the PCG reads from the
+    // same CTA: the energies are the only team exchange left
+    T::template sums_light<10>(acc, c.red);
     fst(4);
     // np.linalg.inv raised on an exactly singular block: the reference
     // pseudo-inverts every block (solvers.py:110-114)
     if (acc[8] > 0.0) {
-        for (int i = T::tid(); i < c.N; i += T::size) {
+        for (int i = c.lo + (int)threadIdx.x; i < c.hi; i += NT) {
             const double *dg = J.diag + 6 * (size_t)i;
             const double full[9] = {dg[0], dg[1], dg[2], dg[1], dg[3], dg[4], dg[2], dg[4], dg[5]};
             pinv3(full, J.minv + 9 * (size_t)i);
         }
-        T::sync();
+        __syncthreads();
     }
     for (int k = 0; k < 6; ++k) en[k] = acc[k];
     counts[0] = (int)acc[6];
+    counts[1] = (int)acc[9];
     counts[2] = (int)acc[7];
-    double dd[1] = {degen};
-    T::template sums<1>(dd, c.red);
-    counts[1] = (int)dd[0];
 }
 
 // Block-Jacobi PCG from zero, best-residual iterate (solvers.py:104-145).
@@ -459,9 +456,16 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, double *sm, int mode, int 
     const int lo = T::rank() * chunk, hi = min(N, lo + chunk);
     // own-vertex storage: zs / ps / aps indexed by (i - off)
     const bool z_sm = mode >= 1;
+    // mode 3: z plus the chunk's ELL neighbour ids and counts in shared
+    // memory, so the matvec's dependent chain (count -> neighbour id -> z_j)
+    // never leaves the SM; the per-slot coefficients stream from L2 as
+    // independent loads
+    const bool idx_sm = mode == 3;
     double *zs = z_sm ? sm : J.z;
     double *ps = mode == 2 ? sm + 3 * (size_t)chunk : J.p;
     double *aps = mode == 2 ? sm + 6 * (size_t)chunk : J.ap;
+    int *nbr_s = reinterpret_cast<int *>(sm + 3 * (size_t)chunk);   // [LC_ELL][chunk] (mode 3)
+    int *cnt_s = nbr_s + (size_t)LC_ELL * chunk;                      // [chunk]
     const int zoff = z_sm ? lo : 0, poff = mode == 2 ? lo : 0;
     const double *__restrict__ diag = J.diag;
     const double *__restrict__ minv = J.minv;
@@ -496,10 +500,22 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, double *sm, int mode, int 
         st3(BEST + 3 * (size_t)i, v3(0, 0, 0));
         st3(R + 3 * (size_t)i, r);
         st3(zs + 3 * (size_t)(i - zoff), z);
+        if (idx_sm) {   // (read back by this thread only: no barrier needed)
+            cnt_s[i - lo] = ell_cnt[i];
+#pragma unroll
+            for (int k = 0; k < LC_ELL; ++k) nbr_s[(size_t)k * chunk + (i - lo)] = ell_nbr[(size_t)k * N + i];
+        }
         part[0] += r.x * z.x + r.y * z.y + r.z * z.z;
         part[1] += r.x * r.x + r.y * r.y + r.z * r.z;
     }
-    T::template sums<2>(part, c.red);   // (also publishes z)
+    // with z in shared memory every exchange inside the PCG is shared-memory
+    // only (x, r, best, p, Ap are owner-only), so its reductions are the
+    // light mbarrier handshake; mode 0 publishes z through global memory
+    auto team_sums2 = [&](double (&v2)[2]) {
+        if (z_sm) T::template sums_light<2>(v2, c.red);
+        else T::template sums<2>(v2, c.red);
+    };
+    team_sums2(part);   // (also publishes z)
     fst(1);
     double rz = part[0];
     double best_norm = sqrt(part[1]);
@@ -536,12 +552,12 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, double *sm, int mode, int 
         for (int i = lo + (int)threadIdx.x; i < hi; i += NT) {
             const V3 zi = ld3(zs + 3 * (size_t)(i - zoff));
             V3 y = sym3_mul(diag + 6 * (size_t)i, zi);
-            const int cnt = ell_cnt[i];
+            const int cnt = idx_sm ? cnt_s[i - lo] : ell_cnt[i];
 #pragma unroll
             for (int k = 0; k < LC_ELL; ++k) {
                 if (k >= cnt) continue;
                 const size_t pos = (size_t)k * N + i;
-                const V3 zj = zload(ell_nbr[pos]);
+                const V3 zj = zload(idx_sm ? nbr_s[(size_t)k * chunk + (i - lo)] : ell_nbr[pos]);
                 const V3 d = v3(ell_d[pos], ell_d[LN + pos], ell_d[2 * LN + pos]);
                 y = y - (ell_a[pos] * zj + (ell_b[pos] * dot3(d, zj)) * d);
             }
@@ -557,7 +573,7 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, double *sm, int mode, int 
             s1[1] += p.x * p.x + p.y * p.y + p.z * p.z;
         }
         if (it == 0) fst(2);
-        T::template sums<2>(s1, c.red);
+        team_sums2(s1);
         if (it == 0) fst(3);
         const double pap = s1[0];
         if (pap <= 1e-14 * fmax(s1[1], 1e-300)) { breakdown = true; break; }
@@ -577,7 +593,7 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, double *sm, int mode, int 
             s2[1] += r.x * r.x + r.y * r.y + r.z * r.z;
         }
         if (it == 0) fst(4);
-        T::template sums<2>(s2, c.red);
+        team_sums2(s2);
         if (it == 0) fst(5);
         const double nrm = sqrt(s2[1]);
         pend_best = nrm < best_norm;
@@ -786,6 +802,7 @@ __global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<Sur
     c.red = red;
     const bool has_field = J.has_field && c.obs.K > 0;
     c.sil_on = J.enable_sil && has_field;
+    own_ranges<T>(c);
     double *v = J.v;
     for (int i = T::tid(); i < c.N * 3; i += T::size) v[i] = J.v0[i];
     if (J.nn_hint)
@@ -887,24 +904,25 @@ template __global__ void k_surface_solve_t<16>(JobArg<SurfJob>, ActorDev, CamDev
 int surface_block_threads() { return NT; }
 
 // surf_pcg's shared-memory mode for a team of `cs` CTAs over N vertices and
-// the dynamic shared memory it needs: 2 = z, p, Ap of the CTA's chunk in
-// shared memory (72 B per vertex, when two CTAs still fit an SM), 1 = z only
-// (24 B per vertex), 0 = none
+// the dynamic shared memory it needs (per vertex of the CTA's chunk):
+//   3 = z + the ELL neighbour ids and counts (60 B),
+//   2 = z, p, Ap (72 B), 1 = z only (24 B), 0 = none (all in global scratch).
+// The default is the highest mode whose buffer leaves two CTAs per SM
+// (<= 100 KB); LIVECAP_PCG_MODE selects one explicitly (measurement sweeps;
+// falls back to 0 when it does not fit).
 int surface_pcg_mode(int N, int cs, size_t *smem_bytes) {
     const size_t chunk = ((size_t)N + cs - 1) / cs;
-    int mode = 0;
-    if (72 * chunk <= 100 * 1024) mode = 2;
-    else if (24 * chunk <= 190 * 1024) mode = 1;
-    // LIVECAP_PCG_MODE caps the mode (measurement sweeps)
-    // default 0: measured fastest (frames/s 3642 vs 3547 for mode 2 at the
-    // bench configuration) -- shared memory taken by the PCG vectors is L1
-    // lost to the nearest-contour queries and gathers of the other phases
-    static const int cap = [] {
+    const size_t per[4] = {0, 24, 72, 24 + 4 * LC_ELL + 4};
+    const size_t budget = 100 * 1024;
+    static const int env = [] {
         const char *v = getenv("LIVECAP_PCG_MODE");
-        return v ? atoi(v) : 0;
+        return v ? atoi(v) : -1;
     }();
-    if (mode > cap) mode = cap < 0 ? 0 : cap;
-    *smem_bytes = mode == 2 ? 72 * chunk : mode == 1 ? 24 * chunk : 0;
+    int mode = 0;
+    if (env >= 0 && env <= 3) mode = per[env] * chunk <= budget ? env : 0;
+    else if (per[3] * chunk <= budget) mode = 3;
+    else if (per[1] * chunk <= budget) mode = 1;
+    *smem_bytes = per[mode] * chunk;
     return mode;
 }
 

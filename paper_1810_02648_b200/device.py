@@ -281,14 +281,17 @@ class Tracker:
         d = L.Detections(L.ptr(j2d), L.ptr(j3d), L.ptr(v2d), L.ptr(v3d))
         u8 = False
         if on_device:
-            img_p, mask_p = int(image), int(mask)
+            img_p, mask_p = (None if image is None else int(image)), int(mask)
         else:
             H, W = self.camera.height, self.camera.width
-            u8 = isinstance(image, np.ndarray) and image.dtype == np.uint8
-            image = np.ascontiguousarray(image) if u8 else L.f64c(image)
             mask = L.u8c(mask)
-            if image.shape != (H, W, 3) or mask.shape != (H, W):
-                raise ValueError("image / mask shape does not match the camera")
+            if image is not None:   # None: mask + detections only (a Stage-I-only tracker)
+                u8 = isinstance(image, np.ndarray) and image.dtype == np.uint8
+                image = np.ascontiguousarray(image) if u8 else L.f64c(image)
+                if image.shape != (H, W, 3):
+                    raise ValueError("image shape does not match the camera")
+            if mask.shape != (H, W):
+                raise ValueError("mask shape does not match the camera")
             img_p, mask_p = L.ptr(image), L.ptr(mask)
         fn = self.ctx.lib.lc_tracker_set_frame_u8 if u8 else self.ctx.lib.lc_tracker_set_frame
         L.check(fn(self.handle, stream, img_p, mask_p, C.byref(d), int(on_device)))
@@ -446,7 +449,7 @@ class StagePipeline:
         g, s = self._where(stream)
         if on_device:
             raise ValueError("device-resident inputs live on one GPU; queue host frames")
-        self.A[g].set_frame(s, image, mask, det)
+        self.A[g].set_frame(s, None, mask, det)    # Stage I reads no image: mask + detections only
         self.B[g].set_frame(s, image, mask, det)
 
     def step(self):

@@ -5,6 +5,7 @@ tracker is chaotic, so only per-call / teacher-forced parity is defined)."""
 
 import numpy as np
 import pytest
+import torch
 
 from helpers import bbox_diag, scene
 
@@ -139,6 +140,48 @@ def test_stage_pipeline_gpu_pair_matches_single_tracker():
             assert np.array_equal(x0, x1) and np.array_equal(v0, v1), (fr.index, s)
     pipe.close()
     ref.close()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_stage_pipeline_two_devices_matches_single_tracker():
+    """§8e on two real devices: Stage I on cuda:0, Stage II on cuda:1, the
+    handoffs are cudaMemcpyPeerAsync between the devices."""
+    from paper_1810_02648_b200.config import SequenceConfig
+    from paper_1810_02648_b200.device import StagePipeline, Tracker
+    actor, cam, frames = scene("small", 128, 3)
+    cfg = SequenceConfig(directional=False)
+    S = 2
+    ref = Tracker(actor, cam, cfg, S)
+    pipe = StagePipeline(actor, cam, cfg, S, pose_device=0, surface_device=1, groups=2)
+    for fr in frames:
+        for s in range(S):
+            ref.set_frame(s, fr.image, fr.mask, fr.detections)
+            pipe.set_frame(s, fr.image, fr.mask, fr.detections)
+        ref.step()
+        pipe.step()
+        pipe.synchronize()
+        for s in range(S):
+            x0, v0, _, _ = ref.result(s)
+            x1, v1, _, _ = pipe.result(s)
+            assert np.array_equal(x0, x1) and np.array_equal(v0, v1), (fr.index, s)
+    pipe.close()
+    ref.close()
+
+
+def test_stage_two_refuses_frame_without_image():
+    """A frame queued mask-only (the Stage-I tracker's ingest) solves Stage I;
+    Stage II on it fails loudly instead of reading a stale pyramid."""
+    from paper_1810_02648_b200 import _lib as L
+    from paper_1810_02648_b200.config import SequenceConfig
+    from paper_1810_02648_b200.device import Tracker
+    actor, cam, frames = scene("small", 128, 2)
+    tr = Tracker(actor, cam, SequenceConfig(directional=False), 1)
+    tr.set_frame(0, None, frames[0].mask, frames[0].detections)
+    L.check(tr.ctx.lib.lc_tracker_step_stage(tr.handle, 1))
+    tr.set_frame(0, None, frames[1].mask, frames[1].detections)
+    with pytest.raises(ValueError, match="image"):
+        L.check(tr.ctx.lib.lc_tracker_step_stage(tr.handle, 2))
+    tr.close()
 
 
 def test_batch_tracker_groups_identical():
