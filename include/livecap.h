@@ -186,6 +186,12 @@ int lc_ctx_synchronize(lc_ctx *ctx);
  * from this context: 1, 2, 4, 8 or 16 CTAs per stream, 0 = default policy
  * (overrides LIVECAP_POSE_CLUSTER / LIVECAP_SURFACE_CLUSTER) */
 int lc_ctx_set_team_sizes(lc_ctx *ctx, int32_t pose_ctas, int32_t surface_ctas);
+/* blur pyramid region of interest (gaussian_pyramid, imageproc.py:276-285):
+ * trackers blur only the tiles within margin_px of the observed silhouette's
+ * bounding box and sample the others with the same arithmetic on demand
+ * (bit-identical).  -1: every tile; -2: no tile (test hook); default 64 or
+ * LIVECAP_PYR_MARGIN */
+int lc_ctx_set_pyramid_margin(lc_ctx *ctx, int32_t margin_px);
 int lc_kernel_launches(lc_ctx *ctx, int64_t *count);   /* kernels launched on ctx so far */
 int lc_process_launches(int64_t *count);               /* kernels launched by every context of the process */
 

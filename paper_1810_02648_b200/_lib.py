@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
+import weakref
 
 import numpy as np
 
@@ -117,6 +118,7 @@ _SIGS = {
     "lc_ctx_destroy": (C.c_int, [P]),
     "lc_ctx_synchronize": (C.c_int, [P]),
     "lc_ctx_set_team_sizes": (C.c_int, [P, i32, i32]),
+    "lc_ctx_set_pyramid_margin": (C.c_int, [P, i32]),
     "lc_tracker_set_pose": (C.c_int, [P, i32, P]),
     "lc_field_dt": (C.c_int, [P, P]),
     "lc_edt_squared": (C.c_int, [P, i32, i32, P, P]),
@@ -238,6 +240,14 @@ class Context:
         check(lib.lc_ctx_create(device, stream, C.byref(h)))
         self.handle = h
         self.lib = lib
+        self._dependents = []   # weakrefs to objects holding device memory of this context
+
+    def register(self, obj):
+        """`obj.close()` frees device objects of this context: close() calls
+        it first, so nothing is freed after its context."""
+        if len(self._dependents) > 64:
+            self._dependents = [r for r in self._dependents if r() is not None]
+        self._dependents.append(weakref.ref(obj))
 
     def launches(self) -> int:
         n = C.c_int64()
@@ -265,8 +275,19 @@ class Context:
         """CTAs per stream of the pose / surface solver teams (0 = default)."""
         check(self.lib.lc_ctx_set_team_sizes(self.handle, int(pose), int(surface)))
 
+    def set_pyramid_margin(self, margin_px: int):
+        """Blur pyramid region of interest in pixels around the observed
+        silhouette (-1: every tile, -2: none -- every sample on the exact
+        on-demand path)."""
+        check(self.lib.lc_ctx_set_pyramid_margin(self.handle, int(margin_px)))
+
     def close(self):
         if self.handle:
+            for r in reversed(self._dependents):   # (trackers before the actors they use)
+                obj = r()
+                if obj is not None:
+                    obj.close()
+            self._dependents = []
             self.lib.lc_ctx_destroy(self.handle)
             self.handle = None
 

@@ -658,6 +658,15 @@ extern "C" int lc_ctx_set_team_sizes(lc_ctx *c, int32_t pose_ctas, int32_t surfa
     API_END
 }
 
+extern "C" int lc_ctx_set_pyramid_margin(lc_ctx *c, int32_t margin_px) {
+    API_BEGIN
+    require(c != nullptr, "null context");
+    require(margin_px >= -2, "margin must be >= 0, -1 (every tile) or -2 (no tile)");
+    c->pyr_margin = margin_px;
+    return LC_OK;
+    API_END
+}
+
 extern "C" int lc_actor_destroy(lc_actor *a) {
     if (!a) return LC_OK;
     cudaSetDevice(a->ctx->device);
@@ -689,6 +698,10 @@ static void alloc_grid(DevArena &m, GridBufs &g, int H, int W) {
     g.quad = m.alloc<int>(quad_off(g.qP, g.qL + 1));
 }
 
+static size_t pyr_tiles(int H, int W) {
+    return (size_t)((W + LC_PYR_TILE - 1) / LC_PYR_TILE) * ((H + LC_PYR_TILE - 1) / LC_PYR_TILE);
+}
+
 void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) {
     N = N_; T = T_; E = E_; H = H_; W = W_; levels = levels_;
     const size_t HW = (size_t)H * W;
@@ -697,6 +710,8 @@ void Slot::allocate(int N_, int T_, int E_, int H_, int W_, int levels_, int J) 
     image_src = image;
     mask_src = mask;
     pyr = mem.alloc<double>(HW * 3 * std::max(levels, 1));
+    pyr_tile = mem.alloc<uint8_t>(pyr_tiles(H, W));
+    pyr_roi = mem.alloc<int>(4);
     blur_tmp = mem.alloc<double>(HW * 3);
     alloc_grid(mem, obs, H, W);   // (the own silhouette uses cell buckets, own_cnt / own_keys)
     own_mask = mem.alloc<uint8_t>(HW);
@@ -784,6 +799,7 @@ void Slot::allocate_queue() {
     FrameIn &a = in[0];
     a.image = image; a.mask = mask; a.image_src = image; a.mask_src = mask;
     a.pyr = pyr; a.obs = obs; a.j2d = j2d; a.j3d_raw = j3d_raw; a.v2d = v2d; a.v3d = v3d;
+    a.pyr_tile = pyr_tile; a.pyr_roi = pyr_roi;
     a.tmp = blur_tmp;
     for (int q = 1; q < LC_QUEUE; ++q) {
         FrameIn &b = in[q];
@@ -791,6 +807,8 @@ void Slot::allocate_queue() {
         b.mask = mem.alloc<uint8_t>(HW);
         b.image_src = b.image; b.mask_src = b.mask;
         b.pyr = mem.alloc<double>(HW * 3 * std::max(levels, 1));
+        b.pyr_tile = mem.alloc<uint8_t>(pyr_tiles(H, W));
+        b.pyr_roi = mem.alloc<int>(4);
         alloc_grid(mem, b.obs, H, W);
         b.j2d = mem.alloc<double>(2 * (LC_MAXJ + 4));
         b.j3d_raw = mem.alloc<double>(3 * LC_MAXJ);
@@ -810,6 +828,7 @@ void Slot::allocate_queue() {
 // point the slot's per-frame input fields at queued frame `f`
 void Slot::view(const FrameIn &f) {
     image_src = f.image_src; mask_src = f.mask_src; pyr = f.pyr; obs = f.obs;
+    pyr_tile = f.pyr_tile; pyr_roi = f.pyr_roi;
     j2d = f.j2d; j3d_raw = f.j3d_raw; v2d = f.v2d; v3d = f.v3d;
 }
 
@@ -1049,6 +1068,8 @@ static void build_config(lc_ctx *c, const lc_actor *a, const lc_nonrigid_hyper *
             cf.half[l] = k / 2;
         }
         cf.taps = cf.mem.upload(taps.data(), taps.size(), st);
+        cf.shp.taps = cf.taps;
+        for (int l = 0; l < 4; ++l) cf.shp.half[l] = cf.half[l];
     }
     if (ph) fill_pose_hyper(cf.php, *ph, a->skel);
     auto pr = probe_offsets();
@@ -1056,7 +1077,10 @@ static void build_config(lc_ctx *c, const lc_actor *a, const lc_nonrigid_hyper *
 }
 
 // gaussian_pyramid (imageproc.py:276-285) of a batch of images
-struct PyrTarget { const double *src; double *dst; double *tmp; };
+struct PyrTarget {
+    const double *src; double *dst; double *tmp;
+    const int *roi = nullptr; uint8_t *tile_flag = nullptr;   // region of interest (tracker frames)
+};
 
 static void pyramid(lc_ctx *c, const ConfigDev &cf, const std::vector<PyrTarget> &ts, int H, int W, int levels) {
     if (ts.empty()) return;
@@ -1064,7 +1088,7 @@ static void pyramid(lc_ctx *c, const ConfigDev &cf, const std::vector<PyrTarget>
     for (int l = 0; l < levels; ++l) fused = fused && cf.half[l] <= LC_PYR_HALO;
     if (fused) {
         std::vector<PyrAllJob> jobs;
-        for (const PyrTarget &t : ts) jobs.push_back(PyrAllJob{t.src, t.dst});
+        for (const PyrTarget &t : ts) jobs.push_back(PyrAllJob{t.src, t.dst, t.roi, t.tile_flag});
         const int tiles = ((W + LC_PYR_TILE - 1) / LC_PYR_TILE) * ((H + LC_PYR_TILE - 1) / LC_PYR_TILE);
         launch(c, k_pyramid_fused, dim3(tiles, (unsigned)ts.size()), dim3(256), pyramid_fused_smem(),
                stage(c, jobs), H, W, levels, (const double *)cf.taps, cf.half[0], cf.half[1], cf.half[2],
@@ -1073,6 +1097,8 @@ static void pyramid(lc_ctx *c, const ConfigDev &cf, const std::vector<PyrTarget>
     }
     const long long n = (long long)H * W * 3;
     const int grid = (int)std::min<long long>((n + 255) / 256, 2368);
+    for (const PyrTarget &t : ts)   // (the two-pass path computes every tile)
+        if (t.tile_flag) cudaMemsetAsync(t.tile_flag, 1, pyr_tiles(H, W), c->stream);
     for (int l = 0; l < levels; ++l) {
         std::vector<PyrJob> jobs;
         for (const PyrTarget &t : ts) jobs.push_back(PyrJob{t.src, t.tmp, t.dst + (size_t)l * n});
@@ -1084,12 +1110,6 @@ static void pyramid(lc_ctx *c, const ConfigDev &cf, const std::vector<PyrTarget>
     }
 }
 
-static void pyramid(lc_ctx *c, const ConfigDev &cf, const std::vector<Slot *> &slots, int levels) {
-    if (slots.empty()) return;
-    std::vector<PyrTarget> ts;
-    for (Slot *s : slots) ts.push_back(PyrTarget{s->image_src, s->pyr, s->blur_tmp});
-    pyramid(c, cf, ts, slots[0]->H, slots[0]->W, levels);
-}
 
 // ---------------------------------------------------------------------------
 // small per-stream kernels of the frame schedule
@@ -1192,6 +1212,15 @@ struct FrameBatch {
     std::vector<FrameIn *> in;    // the frame each slot solves (its preprocessing is launched)
 };
 
+static int pyr_margin(const lc_ctx *c) {
+    if (c->pyr_margin != INT_MIN) return c->pyr_margin;
+    static const int env = [] {
+        const char *v = getenv("LIVECAP_PYR_MARGIN");
+        return v ? atoi(v) : 64;
+    }();
+    return env;
+}
+
 // Preprocessing of queued frames (pipeline.py:156-162) on the auxiliary
 // stream: observed-silhouette contour + NN grid, then the blur pyramid.  A
 // buffer is rebuilt only after the solve that last read it has finished.
@@ -1220,15 +1249,32 @@ static void launch_preprocess(lc_ctx *c, const ConfigDev &cf, const lc_config &c
         }
         return;
     }
+    // finer probes (performance measurement only): skip just the grid or
+    // just the pyramid rebuild
+    static const bool skip_grid = getenv("LIVECAP_PROBE_SKIP_GRID") != nullptr;
+    static const bool skip_pyr = getenv("LIVECAP_PROBE_SKIP_PYR") != nullptr;
     std::vector<std::pair<const GridBufs *, const uint8_t *>> gs;
     for (FrameIn *f : fs) gs.push_back({&f->obs, f->mask_src});
-    build_grids(c, gs, H, W, obs_list_radius());
+    if (!(skip_grid && all_used)) build_grids(c, gs, H, W, obs_list_radius());
     mark(c, "pre:grid");
     for (FrameIn *f : fs) cudaEventRecord(f->ready_obs, c->aux);
-    if (cfg.mode == 0) {
+    if (cfg.mode == 0 && !(skip_pyr && all_used)) {
         std::vector<PyrTarget> ts;
+        // region of interest: only the tiles near the observed silhouette
+        // are blurred; samples elsewhere take the exact on-demand path
+        const int margin = pyr_margin(c);
+        std::vector<PyrRoiJob> rj;
         for (FrameIn *f : fs)
-            if (f->has_image) ts.push_back(PyrTarget{f->image_src, f->pyr, f->tmp});
+            if (f->has_image) {
+                ts.push_back(PyrTarget{f->image_src, f->pyr, f->tmp, margin == -1 ? nullptr : f->pyr_roi,
+                                       f->pyr_tile});
+                rj.push_back(PyrRoiJob{f->obs.cell_count, f->pyr_roi});
+            }
+        if (!rj.empty() && margin != -1) {
+            const int ncx = (W + LC_GRID_CELL - 1) / LC_GRID_CELL, ncy = (H + LC_GRID_CELL - 1) / LC_GRID_CELL;
+            launch(c, k_pyr_roi, dim3((unsigned)rj.size()), dim3(1024), 0, stage(c, rj), ncx, ncy,
+                   (W + LC_PYR_TILE - 1) / LC_PYR_TILE, (H + LC_PYR_TILE - 1) / LC_PYR_TILE, margin);
+        }
         if (!ts.empty()) pyramid(c, cf, ts, H, W, cfg.nonrigid.n_levels);
     }
     mark(c, "pre:pyramid");
@@ -1456,6 +1502,8 @@ static void run_frame(FrameBatch &fb, int stages = 3) {
             j.do_snap = cfg.enable_snapping;
             j.v0 = s->vinit; j.v = s->v; j.vs = s->vs;
             j.pyr = s->pyr;
+            j.pyr_tile = s->pyr_tile;
+            j.image = s->image_src;
             j.obs = grid_dev(s->obs, s->mask_src, H, W);
             j.obs_K = s->obs.K;
             j.has_field = 1;

@@ -447,25 +447,66 @@ __device__ __forceinline__ double side_sign(const NnGridDev &g, const NnResult &
 // bilinear sample of an (H,W,3) image with the analytic gradient
 // (sample_bilinear, imageproc.py:127-174)
 
-__device__ __forceinline__ bool bilinear3(const double *img, int W, int H, double x, double y,
-                                          double val[3], double gx[3], double gy[3]) {
-    const bool clamped = (x < 0) || (x > W - 1) || (y < 0) || (y > H - 1);
+// the sample's cell: top-left pixel (x0, y0), fractions, flags
+struct Bilin {
+    int x0, y0;
+    double fx, fy;
+    bool clamped, inx, iny;
+};
+
+__device__ __forceinline__ Bilin bilinear_cell(int W, int H, double x, double y) {
+    Bilin b;
+    b.clamped = (x < 0) || (x > W - 1) || (y < 0) || (y > H - 1);
     const double xc = fmin(fmax(x, 0.0), (double)(W - 1));
     const double yc = fmin(fmax(y, 0.0), (double)(H - 1));
-    const int x0 = min((int)floor(xc), W - 2), y0 = min((int)floor(yc), H - 2);
-    const double fx = xc - x0, fy = yc - y0;
-    const double *p00 = img + ((size_t)y0 * W + x0) * 3;
+    b.x0 = min((int)floor(xc), W - 2);
+    b.y0 = min((int)floor(yc), H - 2);
+    b.fx = xc - b.x0;
+    b.fy = yc - b.y0;
+    b.inx = (x >= 0) && (x <= W - 1);
+    b.iny = (y >= 0) && (y <= H - 1);
+    return b;
+}
+
+// value + gradient of one channel from the cell's four corner values
+__device__ __forceinline__ void bilinear_mix(const Bilin &b, double c00, double c01, double c10, double c11,
+                                             double &val, double &gx, double &gy) {
+    const double fx = b.fx, fy = b.fy;
+    const double top = c00 * (1 - fx) + c01 * fx;
+    const double bot = c10 * (1 - fx) + c11 * fx;
+    val = top * (1 - fy) + bot * fy;
+    gx = b.inx ? (c01 - c00) * (1 - fy) + (c11 - c10) * fy : 0.0;
+    gy = b.iny ? bot - top : 0.0;
+}
+
+__device__ __forceinline__ bool bilinear3(const double *img, int W, int H, double x, double y,
+                                          double val[3], double gx[3], double gy[3]) {
+    const Bilin b = bilinear_cell(W, H, x, y);
+    const double *p00 = img + ((size_t)b.y0 * W + b.x0) * 3;
     const double *p10 = p00 + (size_t)W * 3;
-    const bool inx = (x >= 0) && (x <= W - 1), iny = (y >= 0) && (y <= H - 1);
-    for (int c = 0; c < 3; ++c) {
-        const double c00 = p00[c], c01 = p00[3 + c], c10 = p10[c], c11 = p10[3 + c];
-        const double top = c00 * (1 - fx) + c01 * fx;
-        const double bot = c10 * (1 - fx) + c11 * fx;
-        val[c] = top * (1 - fy) + bot * fy;
-        gx[c] = inx ? (c01 - c00) * (1 - fy) + (c11 - c10) * fy : 0.0;
-        gy[c] = iny ? bot - top : 0.0;
-    }
-    return clamped;
+    for (int c = 0; c < 3; ++c) bilinear_mix(b, p00[c], p00[3 + c], p10[c], p10[3 + c], val[c], gx[c], gy[c]);
+    return b.clamped;
+}
+
+// One pixel of a blur-pyramid level computed from the raw frame with the
+// fused pyramid kernel's arithmetic (pyr_level, lc_setup.cu: vertical pass
+// over clamped rows, then horizontal over clamped columns, centre tap first,
+// symmetric pairs outermost inward) -- bit-identical to the stored level.
+// tp: the level's taps, centre at tp[h].
+static __device__ __noinline__ double blur_at(const double *img, int W, int H, const double *tp, int h, int y, int x,
+                                       int ch) {
+    auto vert = [&](int xx) -> double {
+        xx = min(max(xx, 0), W - 1);
+        double acc = img[((size_t)y * W + xx) * 3 + ch] * tp[h];
+        for (int j = h; j >= 1; --j) {
+            const int ya = max(y - j, 0), yb = min(y + j, H - 1);
+            acc = acc + (img[((size_t)ya * W + xx) * 3 + ch] + img[((size_t)yb * W + xx) * 3 + ch]) * tp[h + j];
+        }
+        return acc;
+    };
+    double acc = vert(x) * tp[h];
+    for (int j = h; j >= 1; --j) acc = acc + (vert(x - j) + vert(x + j)) * tp[h + j];
+    return acc;
 }
 
 // ---------------------------------------------------------------------------

@@ -120,6 +120,8 @@ struct SurfHyperDev {
     int gn, pcg, max_halvings, n_levels, dilation;
     double snap_step, snap_band;
     int snap_max_steps;
+    const double *taps;   // levels*32 pyramid taps (for the on-demand blur outside the pyramid's region)
+    int half[4];
 };
 
 // Job descriptors of a batched launch, passed by value as a kernel parameter

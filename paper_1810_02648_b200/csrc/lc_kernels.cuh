@@ -16,7 +16,16 @@ __global__ void k_blur_axis(JobArg<PyrJob> jobs, int H, int W, int C, const doub
 struct PyrAllJob {
     const double *src;   // H*W*3
     double *dst;         // levels*H*W*3
+    const int *roi;      // [tx0, ty0, tx1, ty1] tiles to compute (inclusive), or null: every tile
+    uint8_t *tile_flag;  // per LC_PYR_TILE^2 tile: 1 = computed (null: no flags)
 };
+// the pyramid's region of interest: the LC_PYR_TILE tiles within `margin`
+// pixels of the bounding box of the observed mask's contour cells
+struct PyrRoiJob {
+    const int *cell_count;   // ncx*ncy contour pixels per grid cell
+    int *roi;                // out: [tx0, ty0, tx1, ty1] (tx0 > tx1: empty)
+};
+__global__ void k_pyr_roi(JobArg<PyrRoiJob> jobs, int ncx, int ncy, int tiles_x, int tiles_y, int margin);
 __global__ void k_pyramid_fused(JobArg<PyrAllJob> jobs, int H, int W, int levels, const double *taps,
                                 int h0, int h1, int h2, int h3);
 size_t pyramid_fused_smem();

@@ -120,6 +120,11 @@ __device__ double pose_row(const PoseCtx &c, const PoseView &pv, int r, double *
         double px, py;
         const bool cok = project(c.cam, sp, px, py);
         behind = !cok;
+        if (J.enabled && !J.enabled[b]) {   // weight 0 (rim / part gating): a zero row, no query needed
+            if (jr)
+                for (int q = 0; q < LC_NP; ++q) jr[q] = 0.0;
+            return 0.0;
+        }
         NnResult nn;
         double val = 0.0, gx = 0.0, gy = 0.0;
         nn = field_nearest(c.obs, px, py, J.nn_hint ? J.nn_hint + b : nullptr);

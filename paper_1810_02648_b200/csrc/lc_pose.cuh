@@ -34,6 +34,8 @@ struct SurfJob {
     double *v;                // N*3 result
     const double *vs;         // N*3 skinned V^S
     const double *pyr;        // levels*H*W*3
+    const uint8_t *pyr_tile;  // per pyramid tile: 1 = computed; null: every tile is
+    const double *image;      // H*W*3 raw frame (the on-demand blur of uncomputed tiles)
     NnGridDev obs;
     const int *obs_K;
     int has_field;

@@ -32,6 +32,10 @@ struct lc_ctx {
     int call_w = 0, call_h = 0;
     // team (thread-block cluster) sizes of the two solvers; 0 = default policy
     int pose_cs = 0, surf_cs = 0;
+    // blur pyramid region of interest: tiles within this many pixels of the
+    // observed silhouette's bounding box (INT_MIN: LIVECAP_PYR_MARGIN or 64;
+    // -1: every tile; -2: none, every sample on the exact on-demand path)
+    int pyr_margin = INT_MIN;
 };
 
 // device allocation list owned by an object
@@ -95,6 +99,8 @@ struct FrameIn {
     const double *image_src = nullptr;  // own copy or the caller's device pointer
     const uint8_t *mask_src = nullptr;
     double *pyr = nullptr;
+    uint8_t *pyr_tile = nullptr;       // per pyramid tile: computed (1) or left to the on-demand path (0)
+    int *pyr_roi = nullptr;            // [tx0, ty0, tx1, ty1] the pyramid's region of interest
     double *tmp = nullptr;             // blur scratch (the slot's, shared by its queue)
     GridBufs obs{};
     double *j2d = nullptr, *j3d_raw = nullptr;
@@ -119,6 +125,8 @@ struct Slot {
     uint8_t *mask = nullptr;          // H*W
     const uint8_t *mask_src = nullptr;
     double *pyr = nullptr, *blur_tmp = nullptr;
+    uint8_t *pyr_tile = nullptr;
+    int *pyr_roi = nullptr;
     GridBufs obs{}, own{};
     uint8_t *own_mask = nullptr;
     int *own_cnt = nullptr, *own_keys = nullptr;   // own-silhouette contour buckets (rim)

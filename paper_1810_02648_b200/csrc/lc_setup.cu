@@ -108,6 +108,12 @@ __global__ void __launch_bounds__(256) k_pyramid_fused(JobArg<PyrAllJob> jobs, i
     double *mid = sm + E * E * 3;    // T rows x 3E
     const int tiles_x = (W + T - 1) / T;
     const int tx0 = (blockIdx.x % tiles_x) * T, ty0 = (blockIdx.x / tiles_x) * T;
+    if (J.tile_flag) {   // region of interest: tiles outside it are left to the exact on-demand path
+        const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+        const bool want = !J.roi || (tx >= J.roi[0] && tx <= J.roi[2] && ty >= J.roi[1] && ty <= J.roi[3]);
+        if (threadIdx.x == 0) J.tile_flag[blockIdx.x] = want ? 1 : 0;
+        if (!want) return;
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     // asynchronous tile copy (LDGSTS): every thread keeps ~25 loads in flight
     for (int row = warp; row < E; row += nw) {
@@ -138,6 +144,41 @@ __global__ void __launch_bounds__(256) k_pyramid_fused(JobArg<PyrAllJob> jobs, i
             case 6: pyr_level<6>(in, mid, out, tp, tx0, ty0, H, W); break;
             default: pyr_level<7>(in, mid, out, tp, tx0, ty0, H, W); break;
         }
+    }
+}
+
+// One CTA per stream: bounding box of the grid cells holding contour pixels
+// (= the observed silhouette's), dilated by `margin` pixels, as a tile
+// range.  margin < 0: an empty region (every sample takes the exact
+// on-demand path; a test hook).
+__global__ void __launch_bounds__(1024) k_pyr_roi(JobArg<PyrRoiJob> jobs, int ncx, int ncy, int tiles_x,
+                                                  int tiles_y, int margin) {
+    lc_pdl_wait();
+    const PyrRoiJob J = jobs[blockIdx.x];
+    __shared__ int b[4];
+    if (threadIdx.x == 0) { b[0] = INT_MAX; b[1] = INT_MAX; b[2] = -1; b[3] = -1; }
+    __syncthreads();
+    int x0 = INT_MAX, y0 = INT_MAX, x1 = -1, y1 = -1;
+    for (int i = threadIdx.x; i < ncx * ncy; i += blockDim.x)
+        if (J.cell_count[i] > 0) {
+            const int cx = i % ncx, cy = i / ncx;
+            x0 = min(x0, cx); x1 = max(x1, cx); y0 = min(y0, cy); y1 = max(y1, cy);
+        }
+    if (x1 >= 0) {
+        atomicMin(&b[0], x0); atomicMin(&b[1], y0); atomicMax(&b[2], x1); atomicMax(&b[3], y1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int r[4] = {1, 1, 0, 0};   // empty
+        if (b[2] >= 0 && margin >= 0) {
+            const int px0 = b[0] * LC_GRID_CELL - margin, py0 = b[1] * LC_GRID_CELL - margin;
+            const int px1 = (b[2] + 1) * LC_GRID_CELL - 1 + margin, py1 = (b[3] + 1) * LC_GRID_CELL - 1 + margin;
+            r[0] = max(0, px0) / LC_PYR_TILE;
+            r[1] = max(0, py0) / LC_PYR_TILE;
+            r[2] = min(tiles_x - 1, px1 / LC_PYR_TILE);
+            r[3] = min(tiles_y - 1, py1 / LC_PYR_TILE);
+        }
+        for (int k = 0; k < 4; ++k) J.roi[k] = r[k];
     }
 }
 

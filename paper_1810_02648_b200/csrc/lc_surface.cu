@@ -42,27 +42,68 @@ struct SurfCtx {
     double *red;
 };
 
-// one pyramid level as bilinear3 samples it
+// one pyramid level as bilinear3 samples it: the stored level where its
+// tile was computed (the pyramid's region of interest), else the same bits
+// blurred on demand from the raw frame
 struct LevelSrc {
     const double *lvl;
+    const uint8_t *flags;   // null: every tile computed
+    const double *raw;
+    const double *taps;
+    int half, tiles_x;
 };
 
 __device__ __forceinline__ LevelSrc level_src(const SurfCtx &c, int level) {
-    return LevelSrc{c.J->pyr + (size_t)level * c.H * c.W * 3};
+    LevelSrc L;
+    L.lvl = c.J->pyr + (size_t)level * c.H * c.W * 3;
+    L.flags = c.J->pyr_tile;
+    L.raw = c.J->image;
+    L.taps = c.hp.taps + 32 * level;
+    L.half = c.hp.half[level];
+    L.tiles_x = (c.W + LC_PYR_TILE - 1) / LC_PYR_TILE;
+    return L;
+}
+
+// the sample's four pixels lie in computed tiles
+__device__ __forceinline__ bool level_stored(const LevelSrc &L, int W, int H, double x, double y) {
+    if (!L.flags) return true;
+    const Bilin b = bilinear_cell(W, H, x, y);
+    const int tx0 = b.x0 / LC_PYR_TILE, tx1 = (b.x0 + 1) / LC_PYR_TILE;
+    const int ty0 = b.y0 / LC_PYR_TILE, ty1 = (b.y0 + 1) / LC_PYR_TILE;
+    return L.flags[ty0 * L.tiles_x + tx0] && L.flags[ty0 * L.tiles_x + tx1] && L.flags[ty1 * L.tiles_x + tx0] &&
+           L.flags[ty1 * L.tiles_x + tx1];
 }
 
 __device__ __forceinline__ bool bilinear3_src(const LevelSrc &L, int W, int H, double x, double y, double val[3],
                                               double gx[3], double gy[3]) {
-    return bilinear3(L.lvl, W, H, x, y, val, gx, gy);
+    if (!L.flags) return bilinear3(L.lvl, W, H, x, y, val, gx, gy);
+    const Bilin b = bilinear_cell(W, H, x, y);
+    const int tx0 = b.x0 / LC_PYR_TILE, tx1 = (b.x0 + 1) / LC_PYR_TILE;
+    const int ty0 = b.y0 / LC_PYR_TILE, ty1 = (b.y0 + 1) / LC_PYR_TILE;
+    const bool stored = L.flags[ty0 * L.tiles_x + tx0] && L.flags[ty0 * L.tiles_x + tx1] &&
+                        L.flags[ty1 * L.tiles_x + tx0] && L.flags[ty1 * L.tiles_x + tx1];
+    if (stored) return bilinear3(L.lvl, W, H, x, y, val, gx, gy);
+    for (int ch = 0; ch < 3; ++ch) {
+        const double c00 = blur_at(L.raw, W, H, L.taps, L.half, b.y0, b.x0, ch);
+        const double c01 = blur_at(L.raw, W, H, L.taps, L.half, b.y0, b.x0 + 1, ch);
+        const double c10 = blur_at(L.raw, W, H, L.taps, L.half, b.y0 + 1, b.x0, ch);
+        const double c11 = blur_at(L.raw, W, H, L.taps, L.half, b.y0 + 1, b.x0 + 1, ch);
+        bilinear_mix(b, c00, c01, c10, c11, val[ch], gx[ch], gy[ch]);
+    }
+    return b.clamped;
 }
 
 // photometric row of visible vertex i at position p (nonrigid_stage.py:196-213)
 struct PhotoRow { double r[3], J[3][3]; bool behind, pruned; };
 
-__device__ __forceinline__ void photo_row(const SurfCtx &c, const LevelSrc &img, int i, V3 p,
-                                          bool with_jac, PhotoRow &o) {
+// Returns false (o untouched) when `lazy` and the sample falls outside the
+// pyramid's computed tiles: the row is then unknown but >= 0 (see
+// surf_energy_trials).
+__device__ __forceinline__ bool photo_row(const SurfCtx &c, const LevelSrc &img, int i, V3 p,
+                                          bool with_jac, PhotoRow &o, bool lazy = false) {
     double px, py;
     const bool ok = project(c.cam, p, px, py);
+    if (lazy && !level_stored(img, c.W, c.H, px, py)) return false;
     double val[3], gx[3], gy[3];
     const bool cl = bilinear3_src(img, c.W, c.H, px, py, val, gx, gy);
     const double *col = c.A.colors + 3 * (size_t)i;
@@ -81,6 +122,7 @@ __device__ __forceinline__ void photo_row(const SurfCtx &c, const LevelSrc &img,
             o.J[ch][2] = (gx[ch] * a2 + gy[ch] * b2) * w;
         }
     }
+    return true;
 }
 
 // silhouette row of boundary slot b (nonrigid_stage.py:215-233)
@@ -91,6 +133,11 @@ __device__ __forceinline__ void sil_row(const SurfCtx &c, int b, V3 p, bool with
     double px, py;
     const bool ok = project(c.cam, p, px, py);
     o.behind = !ok;
+    if (!J.enabled[b]) {   // weight 0 (rim / part gating): the residual row is zero, no query needed
+        o.r = 0.0;
+        o.g[0] = o.g[1] = o.g[2] = 0.0;
+        return;
+    }
     const NnResult nn = field_nearest(c.obs, px, py, J.nn_hint ? J.nn_hint + b : nullptr);
     double val, gx, gy;
     field_residual(nn, val, gx, gy);
@@ -175,12 +222,20 @@ __device__ __forceinline__ void own_ranges(SurfCtx &c) {
 // each element's trials are evaluated back to back (their gathers and
 // nearest-contour queries overlap), one team reduction for all 24 sums
 constexpr int kSurfTrials = 4;
+//
+// Unless `exact`, a photometric row whose sample falls outside the blur
+// pyramid's computed tiles (a wild trial step) is not evaluated: it adds 0
+// and is counted in unk[h].  All energy terms are >= 0 and fp addition of
+// non-negative values is monotone, so such a trial's sum is a lower bound of
+// its exact energy: if it already exceeds e0 the trial is rejected exactly
+// as the reference rejects it (rejected trials' energies are not reported);
+// otherwise the caller re-evaluates the batch with `exact`.
 template <typename T>
 __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v, const double *step, int nt,
-                                   double en[kSurfTrials][6]) {
+                                   bool exact, double en[kSurfTrials][6], double unk[kSurfTrials]) {
     const SurfJob &J = *c.J;
-    double acc[kSurfTrials * 6];
-    for (int k = 0; k < kSurfTrials * 6; ++k) acc[k] = 0.0;
+    double acc[kSurfTrials * 7];
+    for (int k = 0; k < kSurfTrials * 7; ++k) acc[k] = 0.0;
     const LevelSrc img = level_src(c, level);
     if (J.enable_photo)
         for (int k = c.p0 + (int)threadIdx.x; k < c.p1; k += NT) {
@@ -191,8 +246,10 @@ __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v,
             for (int h = 0; h < kSurfTrials; ++h, sc *= 0.5) {
                 if (h >= nt) break;
                 PhotoRow o;
-                photo_row(c, img, i, vi + sc * si, false, o);
-                acc[6 * h] += o.r[0] * o.r[0] + o.r[1] * o.r[1] + o.r[2] * o.r[2];
+                if (photo_row(c, img, i, vi + sc * si, false, o, !exact))
+                    acc[6 * h] += o.r[0] * o.r[0] + o.r[1] * o.r[1] + o.r[2] * o.r[2];
+                else
+                    acc[kSurfTrials * 6 + h] += 1.0;
             }
         }
     if (c.sil_on)
@@ -247,9 +304,11 @@ __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v,
     // (the trials only read: v and the step were ordered by the team barrier
     // before this phase, and the caller's next global writes come after a
     // full barrier)
-    T::template sums_light<kSurfTrials * 6>(acc, c.red);
-    for (int h = 0; h < kSurfTrials; ++h)
+    T::template sums_light<kSurfTrials * 7>(acc, c.red);
+    for (int h = 0; h < kSurfTrials; ++h) {
         for (int k = 0; k < 6; ++k) en[h][k] = acc[6 * h + k];
+        unk[h] = acc[kSurfTrials * 6 + h];
+    }
 }
 
 __device__ __forceinline__ double total_energy(const double en[6], bool has_prev) {
@@ -651,10 +710,12 @@ __device__ void surf_snap(const SurfCtx &c, double *v) {
                 p = ld3(v + 3 * (size_t)i);
                 const bool ok = project(c.cam, p, px, py);
                 en = J.enabled[b] && ok;
-                hint = J.nn_hint ? J.nn_hint[b] : -1;
-                g = field_nearest(c.obs, px, py, &hint);
-                sign = side_sign(c.obs, g, px, py, J.n2d[2 * b], J.n2d[2 * b + 1]);
-                val = field_interface(g);
+                if (en) {   // (a disabled row is neither walked nor counted)
+                    hint = J.nn_hint ? J.nn_hint[b] : -1;
+                    g = field_nearest(c.obs, px, py, &hint);
+                    sign = side_sign(c.obs, g, px, py, J.n2d[2 * b], J.n2d[2 * b + 1]);
+                    val = field_interface(g);
+                }
             }
             double qx = px, qy = py;
             bool active = valid && en && val > hp.snap_band;
@@ -836,8 +897,18 @@ __global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<Sur
             // tried alone first; the remaining halvings are batched)
             for (int base = 0, nt = 1;; base += nt, nt = kSurfTrials) {
                 nt = min(nt, hp.max_halvings + 1 - base);
-                double et[kSurfTrials][6];
-                surf_energy_trials<T>(c, level, v, J.best, nt, et);
+                double et[kSurfTrials][6], unk[kSurfTrials];
+                surf_energy_trials<T>(c, level, v, J.best, nt, false, et, unk);
+                {   // a trial with unevaluated rows and a lower bound <= e0 before
+                    // the first exact accept: evaluate the batch exactly
+                    bool undecided = false;
+                    for (int h = 0; h < nt; ++h) {
+                        const bool le = total_energy(et[h], c.has_prev) <= e0;
+                        if (le && unk[h] > 0.0) { undecided = true; break; }
+                        if (le) break;
+                    }
+                    if (undecided) surf_energy_trials<T>(c, level, v, J.best, nt, true, et, unk);
+                }
                 int hit = -1;
                 double sc = base_sc, hit_sc = 0.0;
                 for (int h = 0; h < nt; ++h, sc *= 0.5) {

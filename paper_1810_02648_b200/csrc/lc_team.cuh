@@ -32,7 +32,7 @@ struct Team {
     // Layout of the shared reduction buffer (the same offsets in every CTA):
     // per-warp partials [kMaxSums][32], two parity slots of per-CTA partials,
     // the totals, and the parity flag.
-    static constexpr int kMaxSums = 24;
+    static constexpr int kMaxSums = 32;
     static constexpr int kSlot = kMaxSums * 32;
     static constexpr int kRes = kSlot + 2 * kMaxSums;
     static constexpr int kPar = kRes + kMaxSums;

@@ -157,6 +157,7 @@ class DeviceActor:
         h = L.P()
         L.check(self.ctx.lib.lc_actor_upload(self.ctx.handle, C.byref(d), C.byref(h)))
         self.handle = h
+        self.ctx.register(self)
         self.n_vertices = m.n_vertices
         self.n_joints = sk.n_joints
 
@@ -165,7 +166,7 @@ class DeviceActor:
     @classmethod
     def _cached(cls, key, owner, build):
         hit = cls._cache.pop(key, None)
-        if hit is not None and hit[0] is owner:
+        if hit is not None and hit[0] is owner and hit[1].handle:   # (not freed with its context)
             cls._cache[key] = hit          # most recently used last
             return hit[1]
         dev = build()
@@ -198,7 +199,8 @@ class DeviceActor:
 
     def close(self):
         if getattr(self, "handle", None):
-            self.ctx.lib.lc_actor_destroy(self.handle)
+            if self.ctx.handle:   # (a closed context already freed it)
+                self.ctx.lib.lc_actor_destroy(self.handle)
             self.handle = None
 
     def __del__(self, _finalizing=sys.is_finalizing):
@@ -267,6 +269,7 @@ class Tracker:
         L.check(self.ctx.lib.lc_tracker_create(self.ctx.handle, self.dactor.handle, C.byref(self._cam),
                                                C.byref(self._cfg), self.S, C.byref(h)))
         self.handle = h
+        self.ctx.register(self)
         self.N = self.dactor.n_vertices
         self.J = self.dactor.n_joints
         self._keep = []
@@ -407,7 +410,8 @@ class Tracker:
 
     def close(self):
         if self.handle:
-            self.ctx.lib.lc_tracker_destroy(self.handle)
+            if self.ctx.handle:
+                self.ctx.lib.lc_tracker_destroy(self.handle)
             self.handle = None
 
     def __del__(self):

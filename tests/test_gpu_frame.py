@@ -184,6 +184,38 @@ def test_stage_two_refuses_frame_without_image():
     tr.close()
 
 
+@pytest.mark.parametrize("preset,res", [("standard", 256), ("x5k", 1024)])
+def test_pyramid_region_of_interest_bit_identical(preset, res):
+    """The blur pyramid is computed only near the observed silhouette; the
+    photometric samples outside that region are blurred on demand from the
+    raw frame with the same arithmetic.  Every margin -- every tile (-1), no
+    tile (-2: every sample on the on-demand path), 0 and the default --
+    gives bit-identical tracker results."""
+    from paper_1810_02648_b200 import _lib as L
+    from paper_1810_02648_b200.config import SequenceConfig
+    from paper_1810_02648_b200.device import Tracker
+    actor, cam, frames = scene(preset, res, 3)
+    cfg = SequenceConfig(directional=False)
+    out = {}
+    for margin in (-1, -2, 0, None):
+        ctx = L.Context(0)
+        if margin is not None:
+            ctx.set_pyramid_margin(margin)
+        tr = Tracker(actor, cam, cfg, 1, ctx=ctx)
+        res_ = []
+        for fr in frames:
+            tr.set_frame(0, fr.image, fr.mask, fr.detections)
+            tr.step()
+            x, v, _, _ = tr.result(0)
+            res_.append((x, v))
+        tr.close()
+        ctx.close()
+        out[margin] = res_
+    for margin in (-2, 0, None):
+        for (x0, v0), (x1, v1) in zip(out[-1], out[margin]):
+            assert np.array_equal(x0, x1) and np.array_equal(v0, v1), margin
+
+
 def test_batch_tracker_groups_identical():
     """Streams split over concurrently stepped groups (own contexts / CUDA
     streams) give exactly the single tracker's results."""
