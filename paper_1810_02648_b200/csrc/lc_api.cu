@@ -866,13 +866,16 @@ static NnGridDev grid_dev(const GridBufs &g, const uint8_t *mask, int H, int W) 
 }
 
 // Candidate lists are built for cells whose bound U (the farthest point of
-// the cell to a nearby site) is at most this many pixels (default: all);
-// queries in farther cells take the exact quadtree search, which on B200 is
-// slower than scanning even long lists, so every cell is listed.
+// the cell to a nearby site) is at most this many pixels; queries in farther
+// cells take the exact quadtree search (slower per query than a list).  On
+// the in-track bench workload, with rim-disabled rows skipping their
+// queries, 192 px measured best (frames/s: all cells 4036, 192: 4244, 128:
+// 4167, 64: 3876, 48: 3579): the far cells' long lists cost more to build
+// than their few queries save.  LIVECAP_LIST_RADIUS overrides.
 static double obs_list_radius() {
     static double r = [] {
         const char *v = getenv("LIVECAP_LIST_RADIUS");
-        return v ? atof(v) : 1e30;
+        return v ? atof(v) : 192.0;
     }();
     return r;
 }
