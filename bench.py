@@ -114,10 +114,10 @@ def workload(args, world):
 # ---------------------------------------------------------------------------
 # synthetic inputs
 
-def make_stream_frames(actor, cam, n_frames, seed, renderer, posing):
+def make_stream_frames(actor, cam, n_frames, seed, renderer, posing, device_rng=None):
     from paper_1810_02648_b200 import synthetic as S
     script = S.default_script(n_frames, noise=S.NoiseParams(sigma2d=1.0, sigma3d=0.008, seed=seed))
-    return S.generate_sequence(actor, cam, script, renderer, posing)
+    return S.generate_sequence(actor, cam, script, renderer, posing, device_rng=device_rng)
 
 
 def device_posing(ctx):
@@ -255,7 +255,9 @@ def run_ours(args):
     AHEAD = 2         # frames queued ahead of the one being solved (the library holds 3)
     F = W + K + AHEAD  # frames beyond the timed steps are queued, never solved
     t_gen = time.perf_counter()
-    frames = [make_stream_frames(actor, cam, F, seed, device_renderer(ctx), device_posing(ctx))
+    # inputs from the restated generator on the device: raster, skinning and
+    # the numpy random stream (image noise, detections) all run on the GPU
+    frames = [make_stream_frames(actor, cam, F, seed, device_renderer(ctx), device_posing(ctx), device_rng=ctx)
               for seed in shard_seeds(rank, Sn)]
     t_gen = time.perf_counter() - t_gen
     H, Wd = args.res, args.res

@@ -359,6 +359,26 @@ int lc_tracker_phase_times(lc_tracker *tr, int32_t stream, int64_t *pose_ns, int
 /* device pointer of a stream's resident vertices (N*3) for zero-copy readers */
 int lc_tracker_device_vertices(lc_tracker *tr, int32_t stream, uint64_t *dptr);
 
+/* ---- synthetic-generator random stream on the device (lc_rng.cu) ----------
+ * numpy Generator(PCG64) as the reference's generator draws it
+ * (synthetic.py:170-203: default_rng(seed).normal / .random).  state / inc:
+ * the PCG64 128-bit state and increment as {hi, lo} 64-bit words. */
+/* n normals loc + scale*z into device `out` (add_clip != 0: out = clip(out +
+ * noise, 0, 1), the image noise).  *consumed = draws taken (advance the
+ * stream by it).  Tail samples (layer 0, libm log1p) are left for the host:
+ * tails[2t] = element, tails[2t+1] = draws of the sample, tail_draws[31 t ..]
+ * = its first 31 draws; the host writes them with lc_rng_scatter. */
+int lc_rng_normal(lc_ctx *ctx, const uint64_t *state, const uint64_t *inc, double loc, double scale,
+                  double *out, int64_t n, int32_t add_clip, int64_t *consumed, int64_t *tails,
+                  uint64_t *tail_draws, int32_t max_tails, int32_t *n_tails);
+/* n doubles of Generator.random() into device `out` (consumes n draws) */
+int lc_rng_uniform(lc_ctx *ctx, const uint64_t *state, const uint64_t *inc, double *out, int64_t n);
+/* device out[idx[k]] = v[k] / host out[k] = device src[idx[k]] (host idx, v) */
+int lc_rng_scatter(lc_ctx *ctx, const int64_t *idx, const double *v, int32_t n, double *out);
+int lc_rng_gather(lc_ctx *ctx, const int64_t *idx, int32_t n, const double *src, double *out);
+/* the device's ziggurat tables (numpy's ki_double / wi_double / fi_double) */
+int lc_rng_tables(uint64_t *ki, double *wi, double *fi);
+
 #ifdef __cplusplus
 }
 #endif

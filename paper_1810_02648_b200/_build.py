@@ -69,5 +69,26 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return LIB
 
 
+def build_variant(out: str, defines=(), verbose: bool = False) -> str:
+    """A separately compiled library with extra -D defines (e.g. the
+    sanitizer build LC_TEAM_FULL_SYNC), objects and .so under `out`'s
+    directory; load it with LIVECAP_LIB=<path>."""
+    d = os.path.dirname(os.path.abspath(out))
+    os.makedirs(d, exist_ok=True)
+    nvcc = _nvcc()
+    objs = []
+    for src in sources():
+        obj = os.path.join(d, os.path.basename(src)[:-3] + ".o")
+        objs.append(obj)
+        cmd = [nvcc, *ARCH, *FLAGS, *[f"-D{x}" for x in defines], "-c", src, "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    r = subprocess.run([nvcc, *ARCH, "-shared", "-o", out, *objs, "-lcudart"], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr)
+    return out
+
+
 if __name__ == "__main__":
     print(build(verbose=True, force="--force" in sys.argv))

@@ -16,7 +16,9 @@ import weakref
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblivecap.so")
+# LIVECAP_LIB: an alternative build of the same sources (e.g. the sanitizer
+# variant from _build.build_variant); default the in-tree library
+LIB_PATH = os.environ.get("LIVECAP_LIB") or os.path.join(HERE, "liblivecap.so")
 
 LC_OK, LC_EINVAL, LC_ECUDA, LC_ENOMEM, LC_ECAP = 0, 1, 2, 3, 4
 LC_MAX_LOG = 64
@@ -125,6 +127,11 @@ _SIGS = {
     "lc_surface_sets": (C.c_int, [P, P, P, P, i32, i32, i32, P, P, P, P, P, P, P]),
     "lc_kernel_launches": (C.c_int, [P, P]),
     "lc_process_launches": (C.c_int, [P]),
+    "lc_rng_normal": (C.c_int, [P, P, P, f64, f64, P, i64, i32, P, P, P, i32, P]),
+    "lc_rng_uniform": (C.c_int, [P, P, P, P, i64]),
+    "lc_rng_scatter": (C.c_int, [P, P, P, i32, P]),
+    "lc_rng_gather": (C.c_int, [P, P, i32, P, P]),
+    "lc_rng_tables": (C.c_int, [P, P, P]),
     "lc_actor_upload": (C.c_int, [P, P, P]),
     "lc_actor_destroy": (C.c_int, [P]),
     "lc_pcg_solve_bsr": (C.c_int, [P, i32, i64, P, P, P, P, P, i32, P, P]),
@@ -238,6 +245,7 @@ class Context:
         lib = load_library()
         h = P()
         check(lib.lc_ctx_create(device, stream, C.byref(h)))
+        self.device = int(device)
         self.handle = h
         self.lib = lib
         self._dependents = []   # weakrefs to objects holding device memory of this context

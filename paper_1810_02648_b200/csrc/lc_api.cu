@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 #include "lc_runtime.h"
+#include "lc_rng.cuh"
 
 // ---------------------------------------------------------------------------
 // errors
@@ -2733,5 +2734,143 @@ extern "C" int lc_dense_solve(lc_ctx *c, int32_t n, const double *a, const doubl
         info->damping = hi[1];
     }
     return last_launch_status();
+    API_END
+}
+
+// ---------------------------------------------------------------------------
+// numpy Generator(PCG64).normal on the device (lc_rng.cu)
+
+// n normals loc + scale * z of the PCG64 stream (state, inc: hi, lo words)
+// into the device array `out` (add_clip: out = clip(out + noise, 0, 1), the
+// generator's image noise).  Returns the draws consumed (advance the stream
+// by it) and the tail samples the host completes: tails[2t] = element,
+// tails[2t+1] = draws, tail_draws[t*31 ..] = the sample's first 31 draws.
+extern "C" int lc_rng_normal(lc_ctx *c, const uint64_t *state, const uint64_t *inc, double loc, double scale,
+                             double *out, int64_t n, int32_t add_clip, int64_t *consumed, int64_t *tails,
+                             uint64_t *tail_draws, int32_t max_tails, int32_t *n_tails) {
+    API_BEGIN
+    require(c && state && inc && out && consumed && n_tails, "null argument");
+    require(n >= 0, "negative count");
+    CK(cudaSetDevice(c->device));
+    *consumed = 0;
+    *n_tails = 0;
+    if (n == 0) return LC_OK;
+    cudaStream_t st = c->stream;
+    for (long long M = n + n / 32 + 4096;; M *= 2) {
+        DevArena mem;
+        uint64_t *u = mem.alloc<uint64_t>(M);
+        double *val = mem.alloc<double>(M);
+        int *len = mem.alloc<int>(M);
+        unsigned char *kind = mem.alloc<unsigned char>(M), *start = mem.alloc<unsigned char>(M),
+                      *flag = mem.alloc<unsigned char>(M);
+        long long *num = mem.alloc<long long>(M), *slow = mem.alloc<long long>(M);
+        int *n_slow = mem.alloc<int>(1), *sst = mem.alloc<int>(M), *err = mem.alloc<int>(1), *nt = mem.alloc<int>(1);
+        long long *cons = mem.alloc<long long>(1);
+        const int mt = std::max(max_tails, 1);
+        long long *dtails = mem.alloc<long long>(2 * (size_t)mt);
+        uint64_t *ddraws = mem.alloc<uint64_t>((size_t)mt * LC_TAIL_DRAWS);
+        CK(cudaMemsetAsync(err, 0, sizeof(int), st));
+        CK(cudaMemsetAsync(nt, 0, sizeof(int), st));
+        CK(cudaMemsetAsync(cons, 0xff, sizeof(long long), st));
+        const int grid = 148 * 8;
+        launch(c, k_rng_draws, dim3(grid), dim3(256), 0, state[0], state[1], inc[0], inc[1], u, M);
+        launch(c, k_zig_walk, dim3(grid), dim3(256), 0, (const uint64_t *)u, M, val, len, kind,
+                     start);
+        launch(c, k_slow_flags, dim3(grid), dim3(256), 0, (const int *)len, M, flag);
+        {
+            size_t tb = 0;
+            CK(rng_select_slow(nullptr, tb, flag, slow, n_slow, M, st));
+            void *tmp = mem.alloc<char>(tb);
+            CK(rng_select_slow(tmp, tb, flag, slow, n_slow, M, st));
+        }
+        launch(c, k_zig_starts, dim3(1), dim3(1024), 0, (const long long *)slow,
+                     (const int *)n_slow, (const int *)len, start, sst, M, err);
+        {
+            size_t tb = 0;
+            CK(rng_scan_starts(nullptr, tb, start, num, M, st));
+            void *tmp = mem.alloc<char>(tb);
+            CK(rng_scan_starts(tmp, tb, start, num, M, st));
+        }
+        launch(c, k_zig_emit, dim3(grid), dim3(256), 0, (const unsigned char *)start,
+                     (const long long *)num, (const double *)val, (const int *)len, (const unsigned char *)kind,
+                     (const uint64_t *)u, M, (long long)n, loc, scale, out, (int)add_clip, cons, dtails, ddraws, nt,
+                     mt, err);
+        int h_err = 0, h_nt = 0;
+        long long h_cons = -1;
+        CK(cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&h_nt, nt, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&h_cons, cons, sizeof(long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        require(h_err != 1, "ziggurat sample spans more than 64 draws (unsupported)");
+        if (h_cons < 0 || h_err == 2) continue;   // fewer than n samples in M draws: a longer buffer
+        require(h_nt <= max_tails, "more tail samples than max_tails");
+        *consumed = h_cons;
+        *n_tails = h_nt;
+        if (h_nt > 0) {
+            if (tails) CK(cudaMemcpyAsync(tails, dtails, sizeof(long long) * 2 * h_nt, cudaMemcpyDeviceToHost, st));
+            if (tail_draws)
+                CK(cudaMemcpyAsync(tail_draws, ddraws, sizeof(uint64_t) * LC_TAIL_DRAWS * h_nt, cudaMemcpyDeviceToHost,
+                                   st));
+            CK(cudaStreamSynchronize(st));
+        }
+        return LC_OK;
+    }
+    API_END
+}
+
+// out[idx[k]] = v[k] (host-completed tail samples); idx / v host arrays
+extern "C" int lc_rng_scatter(lc_ctx *c, const int64_t *idx, const double *v, int32_t n, double *out) {
+    API_BEGIN
+    require(c && out && (n == 0 || (idx && v)), "null argument");
+    CK(cudaSetDevice(c->device));
+    if (n == 0) return LC_OK;
+    DevArena mem;
+    long long *di = mem.alloc<long long>(n);
+    double *dv = mem.alloc<double>(n);
+    CK(cudaMemcpyAsync(di, idx, sizeof(long long) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dv, v, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    launch(c, k_rng_scatter, dim3((n + 255) / 256), dim3(256), 0, (const long long *)di,
+                 (const double *)dv, (int)n, out);
+    CK(cudaStreamSynchronize(c->stream));
+    return LC_OK;
+    API_END
+}
+
+// out[k] = src[idx[k]] (device src; host idx / out)
+extern "C" int lc_rng_gather(lc_ctx *c, const int64_t *idx, int32_t n, const double *src, double *out) {
+    API_BEGIN
+    require(c && src && (n == 0 || (idx && out)), "null argument");
+    CK(cudaSetDevice(c->device));
+    if (n == 0) return LC_OK;
+    DevArena mem;
+    long long *di = mem.alloc<long long>(n);
+    double *dv = mem.alloc<double>(n);
+    CK(cudaMemcpyAsync(di, idx, sizeof(long long) * n, cudaMemcpyHostToDevice, c->stream));
+    launch(c, k_rng_gather, dim3((n + 255) / 256), dim3(256), 0, (const long long *)di, (int)n,
+                 src, dv);
+    CK(cudaMemcpyAsync(out, dv, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return LC_OK;
+    API_END
+}
+
+// n doubles of Generator.random() (draws 0..n-1 of the stream) into device `out`
+extern "C" int lc_rng_uniform(lc_ctx *c, const uint64_t *state, const uint64_t *inc, double *out, int64_t n) {
+    API_BEGIN
+    require(c && state && inc && (n == 0 || out), "null argument");
+    CK(cudaSetDevice(c->device));
+    if (n == 0) return LC_OK;
+    launch(c, k_rng_uniform, dim3((unsigned)std::min<long long>((n + 255) / 256, 148 * 8)), dim3(256), 0, state[0],
+           state[1], inc[0], inc[1], out, (long long)n);
+    return last_launch_status();
+    API_END
+}
+
+// the ziggurat tables the device draws with (256 entries each)
+extern "C" int lc_rng_tables(uint64_t *ki, double *wi, double *fi) {
+    API_BEGIN
+    require(ki && wi && fi, "null argument");
+    CK(rng_tables(ki, wi, fi));
+    return LC_OK;
     API_END
 }

@@ -518,7 +518,7 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, double *sm, int mode, int 
     // mode 3: z plus the chunk's ELL neighbour ids and counts in shared
     // memory, so the matvec's dependent chain (count -> neighbour id -> z_j)
     // never leaves the SM; the per-slot coefficients stream from L2 as
-    // independent loads
+    // independent loads (the kernel prologue fills the ids once per solve)
     const bool idx_sm = mode == 3;
     double *zs = z_sm ? sm : J.z;
     double *ps = mode == 2 ? sm + 3 * (size_t)chunk : J.p;
@@ -559,11 +559,6 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, double *sm, int mode, int 
         st3(BEST + 3 * (size_t)i, v3(0, 0, 0));
         st3(R + 3 * (size_t)i, r);
         st3(zs + 3 * (size_t)(i - zoff), z);
-        if (idx_sm) {   // (read back by this thread only: no barrier needed)
-            cnt_s[i - lo] = ell_cnt[i];
-#pragma unroll
-            for (int k = 0; k < LC_ELL; ++k) nbr_s[(size_t)k * chunk + (i - lo)] = ell_nbr[(size_t)k * N + i];
-        }
         part[0] += r.x * z.x + r.y * z.y + r.z * z.z;
         part[1] += r.x * r.x + r.y * r.y + r.z * r.z;
     }
@@ -864,6 +859,15 @@ __global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<Sur
     const bool has_field = J.has_field && c.obs.K > 0;
     c.sil_on = J.enable_sil && has_field;
     own_ranges<T>(c);
+    if (pcg_mode == 3) {   // surf_pcg's ELL ids of the CTA's chunk, once per solve (read by their owner thread)
+        const int chunk = (c.N + CS - 1) / CS;
+        int *nbr_s = reinterpret_cast<int *>(pcg_sm + 3 * (size_t)chunk);
+        int *cnt_s = nbr_s + (size_t)LC_ELL * chunk;
+        for (int i = c.lo + (int)threadIdx.x; i < c.hi; i += NT) {
+            cnt_s[i - c.lo] = A.ell_cnt[i];
+            for (int k = 0; k < LC_ELL; ++k) nbr_s[(size_t)k * chunk + (i - c.lo)] = A.ell_nbr[(size_t)k * c.N + i];
+        }
+    }
     double *v = J.v;
     for (int i = T::tid(); i < c.N * 3; i += T::size) v[i] = J.v0[i];
     if (J.nn_hint)

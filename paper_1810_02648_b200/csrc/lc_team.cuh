@@ -112,6 +112,12 @@ struct Team {
     // call: use sums() / sync() where the phase boundary needs that.
     template <int M>
     __device__ static void sums_light(double (&v)[M], double *red) {
+#ifdef LC_TEAM_FULL_SYNC
+        // sanitizer build: compute-sanitizer racecheck does not model the
+        // remote-mbarrier handshake, so this variant takes the cluster barrier
+        sums<M>(v, red);
+        return;
+#endif
         if constexpr (CS == 1) {
             sums<M>(v, red);
         } else {
