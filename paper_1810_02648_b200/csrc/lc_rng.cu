@@ -168,7 +168,11 @@ __global__ void __launch_bounds__(1024) k_zig_starts(const long long *slow, cons
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const long long s = slow[i];
         const int L = len[s];
-        if (L < 0 || L > 64) { if (sst[i] || L > 64) atomicExch(err, 1); continue; }
+        if (L > 64) { atomicExch(err, 1); continue; }   // (never observed; the look-back assumes it)
+        if (L < 0) {   // ran past the buffer: only a start among the first n samples matters (k_zig_emit)
+            if (!sst[i]) start[s] = 0;
+            continue;
+        }
         if (!sst[i]) start[s] = 0;
         else
             for (int j = 1; j < L && s + j < M; ++j) start[s + j] = 0;
