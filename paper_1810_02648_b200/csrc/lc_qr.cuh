@@ -19,7 +19,6 @@ struct QrSmemT {
     double c[MAXN + 1][MAXN + 1];   // c[j][i] = column j, row i; column n is the rhs
     double rdiag[MAXN];
     double x[MAXN];
-    double v[2][40];   // qr_factor_cols: the step's reflector (double-buffered) + v0, tau, alpha, skip
     int damped;
     double lam;
 };
@@ -118,87 +117,6 @@ __device__ void qr_factor_quad(S &s, int n) {
     __syncthreads();
 }
 
-// Householder for n <= 36 (the pose system) on two warps, one column per
-// lane held in registers for the whole factorization: per step the pivot
-// column's owner forms the norm and the reflector (4 interleaved FMA chains)
-// and publishes it to shared memory (double-buffered), one 64-thread named
-// barrier, then every later column reads the reflector as broadcasts and
-// updates itself -- 36 dependent steps of ~0.2 us instead of a block-wide
-// barrier and shared-memory column traffic per step.  Same reflector and
-// update formulas as qr_factor_quad (only the association of the two sums
-// differs).  Every thread of the block calls it.
-template <int NT, typename S>
-__device__ void qr_factor_cols(S &s, int n) {
-    constexpr int NB = 36;
-    static_assert(NT >= 64, "two warps");
-    const int j = (int)threadIdx.x;
-    if (j < 64) {
-        const bool own = j <= n;
-        double col[NB];
-#pragma unroll
-        for (int i = 0; i < NB; ++i) col[i] = (own && i < n) ? s.c[j][i] : 0.0;
-        for (int k = 0; k < n; ++k) {
-            double *vb = s.v[k & 1];
-            if (j == k) {
-                double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0, akk = 0.0;
-#pragma unroll
-                for (int i = 0; i < NB; i += 4) {
-                    if (i + 0 > k && i + 0 < n) p0 = fma(col[i + 0], col[i + 0], p0);
-                    if (i + 1 > k && i + 1 < n) p1 = fma(col[i + 1], col[i + 1], p1);
-                    if (i + 2 > k && i + 2 < n) p2 = fma(col[i + 2], col[i + 2], p2);
-                    if (i + 3 > k && i + 3 < n) p3 = fma(col[i + 3], col[i + 3], p3);
-                }
-#pragma unroll
-                for (int i = 0; i < NB; ++i)
-                    if (i == k) akk = col[i];
-                const double p = (p0 + p1) + (p2 + p3);
-                const double ss = akk * akk + p;
-                const double nrm = sqrt(ss);
-                const double alpha = akk >= 0.0 ? -nrm : nrm;
-                const double v0 = akk - alpha;
-                const double vn2 = p + v0 * v0;
-                const bool skip = !(nrm > 0.0) || !(vn2 > 0.0);
-#pragma unroll
-                for (int i = 0; i < NB; ++i) vb[i] = (i > k && i < n) ? col[i] : 0.0;
-                vb[NB] = v0;
-                vb[NB + 1] = skip ? 0.0 : 2.0 / vn2;
-                vb[NB + 2] = skip ? 1.0 : 0.0;
-                const double rkk = skip ? akk : alpha;
-                s.rdiag[k] = rkk;
-#pragma unroll
-                for (int i = 0; i < NB; ++i)
-                    if (i == k) col[i] = rkk;
-            }
-            asm volatile("bar.sync 1, 64;" ::: "memory");
-            if (own && j > k && vb[NB + 2] == 0.0) {
-                double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0, ck = 0.0;
-#pragma unroll
-                for (int i = 0; i < NB; i += 4) {
-                    d0 = fma(vb[i + 0], col[i + 0], d0);
-                    d1 = fma(vb[i + 1], col[i + 1], d1);
-                    d2 = fma(vb[i + 2], col[i + 2], d2);
-                    d3 = fma(vb[i + 3], col[i + 3], d3);
-                }
-#pragma unroll
-                for (int i = 0; i < NB; ++i)
-                    if (i == k) ck = col[i];
-                const double v0 = vb[NB], tau = vb[NB + 1];
-                const double w = tau * fma(v0, ck, (d0 + d1) + (d2 + d3));
-#pragma unroll
-                for (int i = 0; i < NB; ++i) {
-                    if (i > k) col[i] = fma(-w, vb[i], col[i]);
-                    else if (i == k) col[i] = fma(-w, v0, ck);
-                }
-            }
-        }
-        if (own)
-#pragma unroll
-            for (int i = 0; i < NB; ++i)
-                if (i < n) s.c[j][i] = col[i];
-    }
-    __syncthreads();
-}
-
 // R x = Q^T b (column n), column-oriented on warp 0: x_k = c_k / R_kk, then
 // every remaining c_i -= R_ik x_k.  The result goes to s.x.
 template <typename S>
@@ -235,7 +153,7 @@ __device__ bool dense_solve_block(S &s, const double *A, const double *b, int n,
     static_assert(NT % 32 == 0, "whole warps");
     const int t = threadIdx.x;
     qr_load_block<NT>(s, A, b, n, 0.0);
-    if (n <= 36) qr_factor_cols<NT>(s, n);
+    if (n <= 36) qr_factor_quad<36, NT>(s, n);
     else qr_factor_quad<LC_QR_MAXN, NT>(s, n);
     if (t < 32) {
         const int lane = t;
@@ -265,7 +183,7 @@ __device__ bool dense_solve_block(S &s, const double *A, const double *b, int n,
     __syncthreads();
     if (s.damped) {
         qr_load_block<NT>(s, A, b, n, s.lam);
-        if (n <= 36) qr_factor_cols<NT>(s, n);
+        if (n <= 36) qr_factor_quad<36, NT>(s, n);
         else qr_factor_quad<LC_QR_MAXN, NT>(s, n);
     }
     if (t < 32) qr_backsolve_warp(s, n);
