@@ -305,6 +305,13 @@ int lc_tracker_set_frame_u8(lc_tracker *tr, int32_t stream, const uint8_t *image
 /* condition + solve_frame for the oldest queued frame of every stream
  * (asynchronous); launches the preprocessing of the next queued frames */
 int lc_tracker_step(lc_tracker *tr);
+/* CUDA-graph mode: once every stream's track state is warm and frames are
+ * queued one ahead, each lc_tracker_step replays one captured graph per
+ * frame-queue phase (the preprocessing of the next frame, both stages, the
+ * state update) instead of enqueueing its ~60 kernels; results are
+ * bit-identical.  Off by default; not while tracing or kernel profiling. */
+int lc_tracker_set_graph(lc_tracker *tr, int32_t on);
+int lc_tracker_graph_stats(lc_tracker *tr, int64_t *graphs, int64_t *replays);
 int lc_tracker_get_result(lc_tracker *tr, int32_t stream, double *pose_out, double *verts_out,
                           double *skinned_out, lc_frame_report *report);
 /* developer timeline (LIVECAP_TRACE=1 at context creation): text lines

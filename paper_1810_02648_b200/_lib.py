@@ -127,6 +127,8 @@ _SIGS = {
     "lc_surface_sets": (C.c_int, [P, P, P, P, i32, i32, i32, P, P, P, P, P, P, P]),
     "lc_kernel_launches": (C.c_int, [P, P]),
     "lc_process_launches": (C.c_int, [P]),
+    "lc_tracker_set_graph": (C.c_int, [P, i32]),
+    "lc_tracker_graph_stats": (C.c_int, [P, P, P]),
     "lc_rng_normal": (C.c_int, [P, P, P, f64, f64, P, i64, i32, P, P, P, i32, P]),
     "lc_rng_uniform": (C.c_int, [P, P, P, P, i64]),
     "lc_rng_scatter": (C.c_int, [P, P, P, i32, P]),

@@ -1216,6 +1216,18 @@ struct FrameBatch {
     std::vector<FrameIn *> in;    // the frame each slot solves (its preprocessing is launched)
 };
 
+// Events that order work across tracker steps (frame buffers freed /
+// uploaded / preprocessed): while a step is captured into a CUDA graph they
+// become external event record / wait nodes, so the replayed graph still
+// synchronises with the previous and next steps and the copy stream.
+static void ev_record_x(lc_ctx *c, cudaEvent_t e, cudaStream_t st) {
+    if (c->capturing) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    else cudaEventRecord(e, st);
+}
+static void ev_wait_x(lc_ctx *c, cudaStream_t st, cudaEvent_t e) {
+    cudaStreamWaitEvent(st, e, c->capturing ? cudaEventWaitExternal : 0);
+}
+
 static int pyr_margin(const lc_ctx *c) {
     if (c->pyr_margin != INT_MIN) return c->pyr_margin;
     static const int env = [] {
@@ -1231,11 +1243,13 @@ static int pyr_margin(const lc_ctx *c) {
 static void launch_preprocess(lc_ctx *c, const ConfigDev &cf, const lc_config &cfg,
                               const std::vector<FrameIn *> &fs, int H, int W) {
     if (fs.empty()) return;
-    cudaEventRecord(c->ev_fork, c->stream);
-    cudaStreamWaitEvent(c->aux, c->ev_fork, 0);
+    // (while the auxiliary stream is captured on its own, the fork point is
+    // recorded on the solve stream right before the graph launch)
+    if (!c->capturing) cudaEventRecord(c->ev_fork, c->stream);
+    ev_wait_x(c, c->aux, c->ev_fork);
     for (FrameIn *f : fs) {
-        if (f->used) cudaStreamWaitEvent(c->aux, f->freed, 0);
-        if (f->pending_upload) cudaStreamWaitEvent(c->aux, f->uploaded, 0);
+        if (f->used) ev_wait_x(c, c->aux, f->freed);
+        if (f->pending_upload) ev_wait_x(c, c->aux, f->uploaded);
         f->pending_upload = false;
     }
     OnStream on(c, c->aux);
@@ -1247,8 +1261,8 @@ static void launch_preprocess(lc_ctx *c, const ConfigDev &cf, const lc_config &c
     for (FrameIn *f : fs) all_used = all_used && f->used;
     if (skip_prep && all_used) {
         for (FrameIn *f : fs) {
-            cudaEventRecord(f->ready_obs, c->aux);
-            cudaEventRecord(f->ready, c->aux);
+            ev_record_x(c, f->ready_obs, c->aux);
+            ev_record_x(c, f->ready, c->aux);
             f->state = 2;
         }
         return;
@@ -1261,7 +1275,7 @@ static void launch_preprocess(lc_ctx *c, const ConfigDev &cf, const lc_config &c
     for (FrameIn *f : fs) gs.push_back({&f->obs, f->mask_src});
     if (!(skip_grid && all_used)) build_grids(c, gs, H, W, obs_list_radius());
     mark(c, "pre:grid");
-    for (FrameIn *f : fs) cudaEventRecord(f->ready_obs, c->aux);
+    for (FrameIn *f : fs) ev_record_x(c, f->ready_obs, c->aux);
     if (cfg.mode == 0 && !(skip_pyr && all_used)) {
         std::vector<PyrTarget> ts;
         // region of interest: only the tiles near the observed silhouette
@@ -1283,7 +1297,7 @@ static void launch_preprocess(lc_ctx *c, const ConfigDev &cf, const lc_config &c
     }
     mark(c, "pre:pyramid");
     for (FrameIn *f : fs) {
-        cudaEventRecord(f->ready, c->aux);
+        ev_record_x(c, f->ready, c->aux);
         f->state = 2;
     }
 }
@@ -1480,7 +1494,7 @@ static void run_frame(FrameBatch &fb, int stages = 3) {
             ++k;
         }
         if (r == 0)
-            for (FrameIn *f : fb.in) cudaStreamWaitEvent(c->stream, f->ready_obs, 0);
+            for (FrameIn *f : fb.in) ev_wait_x(c, c->stream, f->ready_obs);
         mark(c, "s1:waited-grid");
         pose_launch(c, a, fb.cam, pj);
         mark(c, "s1:pose");
@@ -1525,12 +1539,12 @@ static void run_frame(FrameBatch &fb, int stages = 3) {
             j.phase = s->phase_surf;
             sj.push_back(j);
         }
-        for (FrameIn *f : fb.in) cudaStreamWaitEvent(c->stream, f->ready, 0);
+        for (FrameIn *f : fb.in) ev_wait_x(c, c->stream, f->ready);
         mark(c, "s2:waited-pyr");
         surface_launch(c, a, fb.cam, *fb.cf, sj);
         mark(c, "s2:surface");
     }
-    for (FrameIn *f : fb.in) cudaStreamWaitEvent(c->stream, f->ready, 0);   // join the aux stream in every mode
+    for (FrameIn *f : fb.in) ev_wait_x(c, c->stream, f->ready);   // join the aux stream in every mode
     // ---- state update (pipeline.py:281-299)
     std::vector<FinishJob> fj;
     for (Slot *s : ss) {
@@ -1591,6 +1605,10 @@ extern "C" int lc_tracker_destroy(lc_tracker *t) {
     cudaStreamSynchronize(t->ctx->stream);
     cudaStreamSynchronize(t->ctx->aux);   // queued frames may still be preprocessing
     cudaStreamSynchronize(t->ctx->copy);
+    for (auto &g : t->graphs) {
+        cudaGraphExecDestroy(g.second.exec);
+        cudaGraphExecDestroy(g.second.exec_aux);
+    }
     for (Slot *s : t->slots) delete s;
     delete t;
     return LC_OK;
@@ -1616,7 +1634,17 @@ extern "C" int lc_tracker_set_frame(lc_tracker *t, int32_t stream, const double 
     require(f.state == 0, "the stream's frame queue is full: call lc_tracker_step first");
     const size_t HW = (size_t)s->H * s->W;
     f.has_image = image != nullptr;
-    if (on_device) {
+    if (on_device && t->graph_mode) {
+        // graph mode bakes buffer addresses into the captured graphs: a
+        // device frame is copied into the queue's own buffers (copy engine)
+        if (f.used) CK(cudaStreamWaitEvent(c->copy, f.freed, 0));
+        if (image) CK(cudaMemcpyAsync(f.image, image, HW * 3 * sizeof(double), cudaMemcpyDeviceToDevice, c->copy));
+        CK(cudaMemcpyAsync(f.mask, mask, HW, cudaMemcpyDeviceToDevice, c->copy));
+        CK(cudaEventRecord(f.uploaded, c->copy));
+        f.pending_upload = true;
+        f.image_src = image ? f.image : nullptr;
+        f.mask_src = f.mask;
+    } else if (on_device) {
         f.image_src = image;
         f.mask_src = mask;
     } else {
@@ -1716,6 +1744,92 @@ extern "C" int lc_tracker_step_stage(lc_tracker *t, int32_t stages) {
         if (n.state == 1) next.push_back(&n);
         else all_next = false;
     }
+    // CUDA-graph mode: the steady state -- every stream's frame preprocessed
+    // during the previous step, its next frame queued (and uploaded by an
+    // earlier step's buffer), its track state warm -- is one captured graph
+    // per frame-queue phase; the host only does the queue bookkeeping
+    std::vector<long long> key;
+    bool steady = t->graph_mode && stages == 3 && todo.empty() && all_next && !c->tracing &&
+                  c->prof_name.empty() && t->slots.size() <= LC_JOB_INLINE;
+    for (size_t i = 0; steady && i < t->slots.size(); ++i) {
+        const Slot *s = t->slots[i];
+        const FrameIn *n = next[i];
+        steady = s->has_prev && s->has_prev2 && s->has_vprev && s->has_vprev2 && s->has_disp && n->used &&
+                 cur[i]->has_image && n->has_image;
+        key.push_back(s->in_head);
+        key.push_back(n->pending_upload ? 1 : 0);
+        key.push_back((long long)(uintptr_t)cur[i]->image_src ^ (long long)(uintptr_t)cur[i]->mask_src);
+        key.push_back((long long)(uintptr_t)n->image_src ^ (long long)(uintptr_t)n->mask_src);
+    }
+    auto bookkeeping = [&]() {
+        for (FrameIn *f : next) {
+            f->pending_upload = false;
+            f->state = 2;
+        }
+        for (size_t i = 0; i < t->slots.size(); ++i) {
+            t->slots[i]->view(*cur[i]);
+            FrameIn &f = *cur[i];
+            f.used = true;
+            f.state = 0;
+            t->slots[i]->in_head = (t->slots[i]->in_head + 1) % LC_QUEUE;
+        }
+        t->frame_counter++;
+    };
+    if (steady) {
+        auto it = t->graphs.find(key);
+        if (it == t->graphs.end()) {
+            // capture the two branches separately, so that the next frame's
+            // preprocessing (auxiliary stream) keeps overlapping this and the
+            // following solves exactly as in the eager schedule
+            lc_tracker::Graph gr;
+            const long long l0 = c->launches;
+            cudaGraph_t g = nullptr;
+            c->capturing = true;
+            try {
+                CK(cudaStreamBeginCapture(c->aux, cudaStreamCaptureModeThreadLocal));
+                launch_preprocess(c, t->conf, t->cfg, next, t->cam.height, t->cam.width);
+                CK(cudaStreamEndCapture(c->aux, &g));
+                CK(cudaGraphInstantiate(&gr.exec_aux, g, 0));
+                cudaGraphDestroy(g);
+                g = nullptr;
+                for (size_t i = 0; i < next.size(); ++i) {   // (launch_preprocess's bookkeeping, undone:
+                    next[i]->state = 1;                          //  the launch below redoes it)
+                    next[i]->pending_upload = key[4 * i + 1] != 0;
+                }
+                CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+                for (size_t i = 0; i < t->slots.size(); ++i) t->slots[i]->view(*cur[i]);
+                FrameBatch fb{c, t->actor, t->cam, &t->cfg, &t->conf, t->slots, cur};
+                run_frame(fb, stages);
+                for (size_t i = 0; i < t->slots.size(); ++i) ev_record_x(c, cur[i]->freed, c->stream);
+                CK(cudaStreamEndCapture(c->stream, &g));
+                CK(cudaGraphInstantiate(&gr.exec, g, 0));
+                cudaGraphDestroy(g);
+            } catch (...) {
+                c->capturing = false;
+                cudaGraph_t junk = nullptr;
+                cudaStreamEndCapture(c->aux, &junk);
+                if (junk) cudaGraphDestroy(junk);
+                junk = nullptr;
+                cudaStreamEndCapture(c->stream, &junk);
+                if (junk) cudaGraphDestroy(junk);
+                throw;
+            }
+            c->capturing = false;
+            gr.kernels = c->launches - l0;
+            c->launches = l0;   // counted when the graphs run
+            g_launches.fetch_sub(gr.kernels, std::memory_order_relaxed);
+            it = t->graphs.emplace(key, gr).first;
+        } else {
+            t->graph_replays++;
+        }
+        bookkeeping();
+        CK(cudaEventRecord(c->ev_fork, c->stream));
+        CK(cudaGraphLaunch(it->second.exec_aux, c->aux));
+        CK(cudaGraphLaunch(it->second.exec, c->stream));
+        c->launches += it->second.kernels;
+        g_launches.fetch_add(it->second.kernels, std::memory_order_relaxed);
+        return last_launch_status();
+    }
     const int H = t->cam.height, W = t->cam.width;
     launch_preprocess(c, t->conf, t->cfg, todo, H, W);
     // every stream already has its next frame: preprocess it during this solve
@@ -1732,6 +1846,24 @@ extern "C" int lc_tracker_step_stage(lc_tracker *t, int32_t stages) {
     }
     t->frame_counter++;
     return last_launch_status();
+    API_END
+}
+
+// CUDA-graph mode for the steady state of lc_tracker_step (see there)
+extern "C" int lc_tracker_set_graph(lc_tracker *t, int32_t on) {
+    API_BEGIN
+    require(t != nullptr, "null tracker");
+    t->graph_mode = on != 0;
+    return LC_OK;
+    API_END
+}
+
+extern "C" int lc_tracker_graph_stats(lc_tracker *t, int64_t *graphs, int64_t *replays) {
+    API_BEGIN
+    require(t && graphs && replays, "null argument");
+    *graphs = (int64_t)t->graphs.size();
+    *replays = t->graph_replays;
+    return LC_OK;
     API_END
 }
 

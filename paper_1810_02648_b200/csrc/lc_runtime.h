@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <string>
+#include <map>
 #include <vector>
 #include "livecap.h"
 #include "lc_pose.cuh"
@@ -36,6 +37,10 @@ struct lc_ctx {
     // observed silhouette's bounding box (INT_MIN: LIVECAP_PYR_MARGIN or 64;
     // -1: every tile; -2: none, every sample on the exact on-demand path)
     int pyr_margin = INT_MIN;
+    // a tracker step is being captured into a CUDA graph: events that order
+    // work across steps become external event record / wait nodes
+    bool capturing = false;
+    cudaEvent_t ev_join = nullptr;   // the auxiliary stream rejoins the captured stream
 };
 
 // device allocation list owned by an object
@@ -201,4 +206,10 @@ struct lc_tracker {
     void *jobs_dev = nullptr;
     size_t jobs_bytes = 0;
     int frame_counter = 0;
+    // CUDA-graph mode (lc_tracker_set_graph): steady-state steps replay one
+    // captured graph per frame-queue phase
+    bool graph_mode = false;
+    struct Graph { cudaGraphExec_t exec = nullptr, exec_aux = nullptr; long long kernels = 0; };
+    std::map<std::vector<long long>, Graph> graphs;
+    long long graph_replays = 0;
 };

@@ -302,6 +302,15 @@ class Tracker:
     def step(self):
         L.check(self.ctx.lib.lc_tracker_step(self.handle))
 
+    def set_graph(self, on: bool = True):
+        """Replay steady-state steps as captured CUDA graphs (lc_tracker_set_graph)."""
+        L.check(self.ctx.lib.lc_tracker_set_graph(self.handle, int(bool(on))))
+
+    def graph_stats(self):
+        g, r = C.c_int64(), C.c_int64()
+        L.check(self.ctx.lib.lc_tracker_graph_stats(self.handle, C.byref(g), C.byref(r)))
+        return g.value, r.value
+
     def result(self, stream: int, with_report: bool = True):
         x = np.empty(36)
         v = np.empty((self.N, 3))
@@ -534,6 +543,14 @@ class BatchTracker:
             return
         for f in [self._pool.submit(t.step) for t in self.trackers]:
             f.result()
+
+    def set_graph(self, on: bool = True):
+        for t in self.trackers:
+            t.set_graph(on)
+
+    def graph_stats(self):
+        st = [t.graph_stats() for t in self.trackers]
+        return sum(g for g, _ in st), sum(r for _, r in st)
 
     def result(self, stream, with_report=True):
         g, s = self._where(stream)

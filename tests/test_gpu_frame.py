@@ -238,3 +238,44 @@ def test_batch_tracker_groups_identical():
             assert np.array_equal(x0, x1) and np.array_equal(v0, v1)
     bt.close()
     ref.close()
+
+
+@pytest.mark.parametrize("on_device", [False, True])
+def test_graph_mode_bit_identical(on_device):
+    """CUDA-graph mode (lc_tracker_set_graph): steady-state steps replay a
+    captured graph per frame-queue phase; results equal the eager tracker's
+    bit for bit, and the graphs are actually replayed."""
+    from paper_1810_02648_b200.config import SequenceConfig
+    from paper_1810_02648_b200.device import Tracker
+    actor, cam, frames = scene("standard", 256, 9)
+    cfg = SequenceConfig(directional=False)
+    S = 2
+    imgs = [torch.from_numpy(fr.image).cuda() for fr in frames]
+    msks = [torch.from_numpy(fr.mask.astype(np.uint8)).cuda() for fr in frames]
+    out = []
+    for graph in (False, True):
+        tr = Tracker(actor, cam, cfg, S)
+        tr.set_graph(graph)
+
+        def q(f):
+            for s in range(S):
+                if on_device:
+                    tr.set_frame(s, imgs[f].data_ptr(), msks[f].data_ptr(), frames[f].detections, on_device=True)
+                else:
+                    tr.set_frame(s, frames[f].image, frames[f].mask, frames[f].detections)
+        res = []
+        q(0)
+        q(1)
+        for f in range(len(frames)):
+            if f + 2 < len(frames):
+                q(f + 2)
+            tr.step()
+            res.append([tr.result(s)[:2] for s in range(S)])
+        if graph:
+            n_graphs, replays = tr.graph_stats()
+            assert n_graphs >= 1 and replays >= 3, (n_graphs, replays)
+        tr.close()
+        out.append(res)
+    for a, b in zip(*out):
+        for (x0, v0), (x1, v1) in zip(a, b):
+            assert np.array_equal(x0, x1) and np.array_equal(v0, v1)
