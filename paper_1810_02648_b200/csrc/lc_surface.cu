@@ -551,6 +551,17 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, double *sm, int mode, int 
             return v3(q[0], q[1], q[2]);
         }
     };
+    // mode 3: the prologue stored each slot's neighbour as (owner CTA << 20 |
+    // index in the owner's chunk), so the gather is one branch-free load
+    // through the cluster's shared window (own CTA included): the 8 slots'
+    // loads issue back to back
+    auto zload_packed = [&](int q) -> V3 {
+        const double *base;
+        if constexpr (T::ctas == 1) base = zs;
+        else base = cg::this_cluster().map_shared_rank(zs, (unsigned)q >> 20);
+        const double *p = base + 3 * (size_t)(q & 0xFFFFF);
+        return v3(p[0], p[1], p[2]);
+    };
     double part[2] = {0, 0};
     for (int i = lo + (int)threadIdx.x; i < hi; i += NT) {
         const V3 r = ld3(rhs + 3 * (size_t)i);
@@ -611,7 +622,7 @@ __device__ bool surf_pcg(const SurfCtx &c, int iters, double *sm, int mode, int 
             for (int k = 0; k < LC_ELL; ++k) {
                 if (k >= cnt) continue;
                 const size_t pos = (size_t)k * N + i;
-                const V3 zj = zload(idx_sm ? nbr_s[(size_t)k * chunk + (i - lo)] : ell_nbr[pos]);
+                const V3 zj = idx_sm ? zload_packed(nbr_s[(size_t)k * chunk + (i - lo)]) : zload(ell_nbr[pos]);
                 const V3 d = v3(ell_d[pos], ell_d[LN + pos], ell_d[2 * LN + pos]);
                 y = y - (ell_a[pos] * zj + (ell_b[pos] * dot3(d, zj)) * d);
             }
@@ -865,7 +876,10 @@ __global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<Sur
         int *cnt_s = nbr_s + (size_t)LC_ELL * chunk;
         for (int i = c.lo + (int)threadIdx.x; i < c.hi; i += NT) {
             cnt_s[i - c.lo] = A.ell_cnt[i];
-            for (int k = 0; k < LC_ELL; ++k) nbr_s[(size_t)k * chunk + (i - c.lo)] = A.ell_nbr[(size_t)k * c.N + i];
+            for (int k = 0; k < LC_ELL; ++k) {
+                const int j = A.ell_nbr[(size_t)k * c.N + i], owner = j / chunk;
+                nbr_s[(size_t)k * chunk + (i - c.lo)] = (owner << 20) | (j - owner * chunk);
+            }
         }
     }
     double *v = J.v;
