@@ -318,7 +318,7 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
     // total energy = sum of F^2 over all rows (pose_stage.py:279-281)
     {
         double v8[8] = {acc[0], acc[1], acc[2], acc[3], acc[4], (double)behind, 0.0, 0.0};
-        T::template sums<8>(v8, s.red);
+        T::template sums_light<8>(v8, s.red);   // (the phases exchange shared memory only)
         for (int k = 0; k < 5; ++k) terms[k] = v8[k];
         behind_out = (int)v8[5];
         total = (((v8[0] + v8[1]) + v8[2]) + v8[3]) + v8[4];
@@ -345,7 +345,7 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
             cta_part[e] = sum;
         }
         __syncthreads();
-        T::sum_arrays(cta_part, team_tot, per_group);
+        T::sum_arrays_light(cta_part, team_tot, per_group, s.red);
         for (int e = threadIdx.x; e < per_group; e += NT) {
             const double sum = team_tot[e];
             if (e < 21 * 36) {
@@ -409,7 +409,7 @@ __device__ void pose_trials(PoseCtx &c, TrialSmem &ts, int nt, double e[kTrials]
             if (k == slot) acc[k] += f2;
     }
     fst(3);
-    T::template sums<kTrials * 5>(acc, s.red);
+    T::template sums_light<kTrials * 5>(acc, s.red);
     fst(4);
     for (int h = 0; h < kTrials; ++h)
         e[h] = (((acc[5 * h] + acc[5 * h + 1]) + acc[5 * h + 2]) + acc[5 * h + 3]) + acc[5 * h + 4];

@@ -171,6 +171,57 @@ struct Team {
         }
     }
 
+    // the team barrier of sums_light alone, for shared-memory-only exchanges
+    // (the same mbarrier and phase sequence; no GPU-scope fence)
+    __device__ static void sync_light(double *red) {
+#ifdef LC_TEAM_FULL_SYNC
+        sync();
+        return;
+#endif
+        if constexpr (CS == 1) {
+            __syncthreads();
+        } else {
+            int *phase = reinterpret_cast<int *>(red + kBar + 1);
+            const int ph = *phase;
+            __syncthreads();   // this CTA's shared-memory writes are done (and every thread read ph)
+            const unsigned bar = (unsigned)__cvta_generic_to_shared(red + kBar);
+            if (threadIdx.x < CS) {
+                unsigned remote;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"((int)threadIdx.x));
+                asm volatile("fence.release.sync_restrict::shared::cta.cluster;" ::: "memory");
+                asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+            }
+            unsigned done = 0;
+            while (!done)
+                asm volatile(
+                    "{ .reg .pred p; mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%1], %2; "
+                    "selp.u32 %0, 1, 0, p; }"
+                    : "=r"(done) : "r"(bar), "r"(ph & 1) : "memory");
+            asm volatile("fence.acquire.sync_restrict::shared::cluster.cluster;" ::: "memory");
+            __syncthreads();
+            if (threadIdx.x == 0) *phase = ph + 1;
+            __syncthreads();
+        }
+    }
+
+    // sum_arrays over the light barrier: the per-CTA arrays and the totals
+    // are shared memory only
+    __device__ static void sum_arrays_light(const double *part, double *out, int n, double *red) {
+        if constexpr (CS == 1) {
+            for (int e = threadIdx.x; e < n; e += NT) out[e] = part[e];
+            __syncthreads();
+        } else {
+            sync_light(red);
+            auto cl = cg::this_cluster();
+            for (int e = threadIdx.x; e < n; e += NT) {
+                double s = 0.0;
+                for (int r = 0; r < CS; ++r) s += cl.map_shared_rank(part, r)[e];
+                out[e] = s;
+            }
+            sync_light(red);   // every peer has read this CTA's partials
+        }
+    }
+
     // element-wise sum of a per-CTA shared array `part[n]` over the team, in
     // rank order, into `out[n]` (shared, every CTA).  Caller syncs after.
     __device__ static void sum_arrays(const double *part, double *out, int n) {
