@@ -338,6 +338,8 @@ extern "C" int lc_ctx_destroy(lc_ctx *c) {
     }
     cudaEventDestroy(c->ev_obs);
     cudaEventDestroy(c->ev_pyr);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    delete c->rng;
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
     return LC_OK;
@@ -2889,18 +2891,41 @@ extern "C" int lc_rng_normal(lc_ctx *c, const uint64_t *state, const uint64_t *i
     if (n == 0) return LC_OK;
     cudaStream_t st = c->stream;
     for (long long M = n + n / 32 + 4096;; M *= 2) {
-        DevArena mem;
-        uint64_t *u = mem.alloc<uint64_t>(M);
-        double *val = mem.alloc<double>(M);
-        int *len = mem.alloc<int>(M);
-        unsigned char *kind = mem.alloc<unsigned char>(M), *start = mem.alloc<unsigned char>(M),
-                      *flag = mem.alloc<unsigned char>(M);
-        long long *num = mem.alloc<long long>(M), *slow = mem.alloc<long long>(M);
-        int *n_slow = mem.alloc<int>(1), *sst = mem.alloc<int>(M), *err = mem.alloc<int>(1), *nt = mem.alloc<int>(1);
-        long long *cons = mem.alloc<long long>(1);
+        if (!c->rng) c->rng = new lc_ctx::RngScratch();
+        lc_ctx::RngScratch &R = *c->rng;
         const int mt = std::max(max_tails, 1);
-        long long *dtails = mem.alloc<long long>(2 * (size_t)mt);
-        uint64_t *ddraws = mem.alloc<uint64_t>((size_t)mt * LC_TAIL_DRAWS);
+        if (M > R.M || mt > R.mt) {   // (grow-only: the generator calls this once per frame)
+            cudaStreamSynchronize(st);
+            R.mem.release();
+            R.M = std::max(M, R.M);
+            R.mt = std::max(mt, R.mt);
+            const long long m = R.M;
+            R.u = R.mem.alloc<uint64_t>(m);
+            R.val = R.mem.alloc<double>(m);
+            R.len = R.mem.alloc<int>(m);
+            R.kind = R.mem.alloc<unsigned char>(m);
+            R.start = R.mem.alloc<unsigned char>(m);
+            R.flag = R.mem.alloc<unsigned char>(m);
+            R.num = R.mem.alloc<long long>(m);
+            R.slow = R.mem.alloc<long long>(m);
+            R.n_slow = R.mem.alloc<int>(1);
+            R.sst = R.mem.alloc<int>(m);
+            R.err = R.mem.alloc<int>(1);
+            R.nt = R.mem.alloc<int>(1);
+            R.cons = R.mem.alloc<long long>(1);
+            R.dtails = R.mem.alloc<long long>(2 * (size_t)R.mt);
+            R.ddraws = R.mem.alloc<uint64_t>((size_t)R.mt * LC_TAIL_DRAWS);
+            R.tb1 = R.tb2 = 0;
+            CK(rng_select_slow(nullptr, R.tb1, R.flag, R.slow, R.n_slow, m, st));
+            CK(rng_scan_starts(nullptr, R.tb2, R.start, R.num, m, st));
+            R.tmp1 = R.mem.alloc<char>(R.tb1);
+            R.tmp2 = R.mem.alloc<char>(R.tb2);
+        }
+        uint64_t *u = R.u, *ddraws = R.ddraws;
+        double *val = R.val;
+        int *len = R.len, *n_slow = R.n_slow, *sst = R.sst, *err = R.err, *nt = R.nt;
+        unsigned char *kind = R.kind, *start = R.start, *flag = R.flag;
+        long long *num = R.num, *slow = R.slow, *cons = R.cons, *dtails = R.dtails;
         CK(cudaMemsetAsync(err, 0, sizeof(int), st));
         CK(cudaMemsetAsync(nt, 0, sizeof(int), st));
         CK(cudaMemsetAsync(cons, 0xff, sizeof(long long), st));
@@ -2912,16 +2937,16 @@ extern "C" int lc_rng_normal(lc_ctx *c, const uint64_t *state, const uint64_t *i
         {
             size_t tb = 0;
             CK(rng_select_slow(nullptr, tb, flag, slow, n_slow, M, st));
-            void *tmp = mem.alloc<char>(tb);
-            CK(rng_select_slow(tmp, tb, flag, slow, n_slow, M, st));
+            require(tb <= R.tb1, "rng scratch too small");
+            CK(rng_select_slow(R.tmp1, tb, flag, slow, n_slow, M, st));
         }
         launch(c, k_zig_starts, dim3(1), dim3(1024), 0, (const long long *)slow,
                      (const int *)n_slow, (const int *)len, start, sst, M, err);
         {
             size_t tb = 0;
             CK(rng_scan_starts(nullptr, tb, start, num, M, st));
-            void *tmp = mem.alloc<char>(tb);
-            CK(rng_scan_starts(tmp, tb, start, num, M, st));
+            require(tb <= R.tb2, "rng scratch too small");
+            CK(rng_scan_starts(R.tmp2, tb, start, num, M, st));
         }
         launch(c, k_zig_emit, dim3(grid), dim3(256), 0, (const unsigned char *)start,
                      (const long long *)num, (const double *)val, (const int *)len, (const unsigned char *)kind,

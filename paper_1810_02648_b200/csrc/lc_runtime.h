@@ -8,6 +8,29 @@
 #include "lc_pose.cuh"
 #include "lc_bsr.cuh"
 
+struct DevArena {
+    std::vector<void *> ptrs;
+    template <typename T>
+    T *alloc(size_t count) {
+        void *p = nullptr;
+        if (count == 0) count = 1;
+        if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) throw std::bad_alloc();
+        ptrs.push_back(p);
+        return static_cast<T *>(p);
+    }
+    template <typename T>
+    T *upload(const T *host, size_t count, cudaStream_t st) {
+        T *d = alloc<T>(count);
+        if (count) cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, st);
+        return d;
+    }
+    void release() {
+        for (void *p : ptrs) cudaFree(p);
+        ptrs.clear();
+    }
+    ~DevArena() { release(); }
+};
+
 struct lc_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -41,31 +64,22 @@ struct lc_ctx {
     // work across steps become external event record / wait nodes
     bool capturing = false;
     cudaEvent_t ev_join = nullptr;   // the auxiliary stream rejoins the captured stream
+    // lc_rng_normal's scratch, kept across calls (grow-only)
+    struct RngScratch {
+        DevArena mem;
+        long long M = 0;
+        int mt = 0;
+        size_t tb1 = 0, tb2 = 0;
+        uint64_t *u = nullptr, *ddraws = nullptr;
+        double *val = nullptr;
+        int *len = nullptr, *n_slow = nullptr, *sst = nullptr, *err = nullptr, *nt = nullptr;
+        unsigned char *kind = nullptr, *start = nullptr, *flag = nullptr;
+        long long *num = nullptr, *slow = nullptr, *cons = nullptr, *dtails = nullptr;
+        void *tmp1 = nullptr, *tmp2 = nullptr;
+    } *rng = nullptr;
 };
 
 // device allocation list owned by an object
-struct DevArena {
-    std::vector<void *> ptrs;
-    template <typename T>
-    T *alloc(size_t count) {
-        void *p = nullptr;
-        if (count == 0) count = 1;
-        if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) throw std::bad_alloc();
-        ptrs.push_back(p);
-        return static_cast<T *>(p);
-    }
-    template <typename T>
-    T *upload(const T *host, size_t count, cudaStream_t st) {
-        T *d = alloc<T>(count);
-        if (count) cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, st);
-        return d;
-    }
-    void release() {
-        for (void *p : ptrs) cudaFree(p);
-        ptrs.clear();
-    }
-    ~DevArena() { release(); }
-};
 
 struct lc_actor {
     lc_ctx *ctx = nullptr;

@@ -45,9 +45,12 @@ __global__ void k_blur_axis(JobArg<PyrJob> jobs, int H, int W, int C, const doub
 // vertical pass fills a shared intermediate over the tile columns +- halo and
 // the horizontal pass writes the level.  Each output is the same expression
 // in the same order as the two-pass version, so results are bit-identical.
+// shared memory: the haloed input tile (rows of 3E doubles, shifted by one
+// double so interior rows load as 16-byte cp.async), the vertical pass's
+// intermediate, and the output tile staged for coalesced 16-byte stores
 size_t pyramid_fused_smem() {
     const int T = LC_PYR_TILE, E = LC_PYR_TILE + 2 * LC_PYR_HALO;
-    return sizeof(double) * 3 * ((size_t)E * E + (size_t)T * E);
+    return sizeof(double) * ((size_t)E * (3 * E + 2) + 3 * ((size_t)T * E + (size_t)T * T));
 }
 
 // Register-blocked passes: a thread owns RB consecutive outputs along the
@@ -55,19 +58,20 @@ size_t pyramid_fused_smem() {
 // still  w[c]*x[0] + (x[-h]+x[h])*w[h] + ... + (x[-1]+x[1])*w[1]  in that order.
 template <int HH>
 __device__ __forceinline__ void pyr_level(const double *__restrict__ in, double *__restrict__ mid,
-                                          double *__restrict__ out, const double *__restrict__ tp,
-                                          int tx0, int ty0, int H, int W) {
+                                          double *__restrict__ ot, double *__restrict__ out,
+                                          const double *__restrict__ tp, int tx0, int ty0, int H, int W) {
     constexpr int T = LC_PYR_TILE, R = LC_PYR_HALO, E = T + 2 * R, RB = 8, NWIN = RB + 2 * HH;
+    constexpr int SI = 3 * E + 2;   // input row stride (a padding double on either side)
     double t[HH + 1];
 #pragma unroll
     for (int j = 0; j <= HH; ++j) t[j] = tp[HH + j];
     // vertical: unit = (tile column col in [0,3E), row block rb in [0,T/RB))
     for (int u = threadIdx.x; u < 3 * E * (T / RB); u += blockDim.x) {
         const int col = u % (3 * E), rb = u / (3 * E);
-        const double *p = in + (rb * RB + R - HH) * 3 * E + col;
+        const double *p = in + (rb * RB + R - HH) * SI + col;
         double win[NWIN];
 #pragma unroll
-        for (int k = 0; k < NWIN; ++k) win[k] = p[k * 3 * E];
+        for (int k = 0; k < NWIN; ++k) win[k] = p[k * SI];
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
             double acc = win[r + HH] * t[0];
@@ -86,13 +90,28 @@ __device__ __forceinline__ void pyr_level(const double *__restrict__ in, double 
         double win[NWIN];
 #pragma unroll
         for (int k = 0; k < NWIN; ++k) win[k] = p[3 * k];
-        double *o = out + ((size_t)gy * W + tx0 + cb * RB) * 3 + c;
+        double *o = ot + (size_t)row * 3 * T + (cb * RB) * 3 + c;   // the staged output tile
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
             double acc = win[r + HH] * t[0];
 #pragma unroll
             for (int j = HH; j >= 1; --j) acc = acc + (win[r + HH - j] + win[r + HH + j]) * t[j];
-            if (tx0 + cb * RB + r < W) o[3 * r] = acc;
+            o[3 * r] = acc;
+        }
+    }
+    __syncthreads();
+    // the tile's rows are 3T contiguous doubles in the level: 16-byte stores
+    // when the row segment is whole and aligned, else element by element
+    const int wx = min(T, W - tx0);
+    const bool vec = wx == T && ((((size_t)tx0 * 3) & 1) == 0) && ((((size_t)W * 3) & 1) == 0);
+    for (int row = 0; row < T && ty0 + row < H; ++row) {
+        double *dst = out + ((size_t)(ty0 + row) * W + tx0) * 3;
+        const double *src = ot + (size_t)row * 3 * T;
+        if (vec) {
+            for (int k = threadIdx.x; k < 3 * T / 2; k += blockDim.x)
+                reinterpret_cast<double2 *>(dst)[k] = reinterpret_cast<const double2 *>(src)[k];
+        } else {
+            for (int k = threadIdx.x; k < 3 * wx; k += blockDim.x) dst[k] = src[k];
         }
     }
     __syncthreads();
@@ -104,8 +123,10 @@ __global__ void __launch_bounds__(256) k_pyramid_fused(JobArg<PyrAllJob> jobs, i
     const PyrAllJob J = jobs[blockIdx.y];
     constexpr int T = LC_PYR_TILE, R = LC_PYR_HALO, E = T + 2 * R;
     extern __shared__ double sm[];
-    double *in = sm;                 // E rows x 3E
-    double *mid = sm + E * E * 3;    // T rows x 3E
+    constexpr int SI = 3 * E + 2;        // input row stride: element -1 of every row is 16-byte aligned
+    double *in = sm + 1;                 // E rows x SI
+    double *mid = sm + E * SI;           // T rows x 3E
+    double *ot = mid + T * E * 3;        // T rows x 3T (staged output)
     const int tiles_x = (W + T - 1) / T;
     const int tx0 = (blockIdx.x % tiles_x) * T, ty0 = (blockIdx.x / tiles_x) * T;
     if (J.tile_flag) {   // region of interest: tiles outside it are left to the exact on-demand path
@@ -115,16 +136,31 @@ __global__ void __launch_bounds__(256) k_pyramid_fused(JobArg<PyrAllJob> jobs, i
         if (!want) return;
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    // asynchronous tile copy (LDGSTS): every thread keeps ~25 loads in flight
+    // asynchronous tile copy (LDGSTS).  Interior tiles (no clamped column):
+    // each row's 3E doubles start one double after a 16-byte boundary in both
+    // the frame and shared memory, so the row moves as 16-byte copies of
+    // elements [-1, 3E) (the extra leading double is harmless); tiles at the
+    // left / right border clamp per element with 8-byte copies
+    const bool interior = tx0 - R - 1 >= 0 && tx0 + T + R < W && (((size_t)W * 3) & 1) == 0 &&
+                          ((((size_t)(tx0 - R) * 3) & 1) == 1) && ((reinterpret_cast<uintptr_t>(J.src) & 15) == 0);
     for (int row = warp; row < E; row += nw) {
         const int gy = min(max(ty0 + row - R, 0), H - 1);
         const double *src = J.src + (size_t)gy * W * 3;
-        for (int col = lane; col < 3 * E; col += 32) {
-            const int x = col / 3;
-            const int gx = min(max(tx0 + x - R, 0), W - 1);
-            const unsigned dst = (unsigned)__cvta_generic_to_shared(in + row * 3 * E + col);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
-                         "l"(src + gx * 3 + (col - 3 * x)));
+        if (interior) {
+            const double *s0 = src + (size_t)(tx0 - R) * 3 - 1;
+            double *d0 = in + row * SI - 1;
+            for (int k = lane; k < SI / 2; k += 32) {   // elements [-1, 3E + 1): the row's padding included
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(d0 + 2 * k);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(s0 + 2 * k));
+            }
+        } else {
+            for (int col = lane; col < 3 * E; col += 32) {
+                const int x = col / 3;
+                const int gx = min(max(tx0 + x - R, 0), W - 1);
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(in + row * SI + col);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                             "l"(src + gx * 3 + (col - 3 * x)));
+            }
         }
     }
     asm volatile("cp.async.commit_group;\n" ::);
@@ -135,14 +171,14 @@ __global__ void __launch_bounds__(256) k_pyramid_fused(JobArg<PyrAllJob> jobs, i
         double *out = J.dst + (size_t)l * H * W * 3;
         const double *tp = taps + 32 * l;
         switch (hs[l]) {
-            case 0: pyr_level<0>(in, mid, out, tp, tx0, ty0, H, W); break;
-            case 1: pyr_level<1>(in, mid, out, tp, tx0, ty0, H, W); break;
-            case 2: pyr_level<2>(in, mid, out, tp, tx0, ty0, H, W); break;
-            case 3: pyr_level<3>(in, mid, out, tp, tx0, ty0, H, W); break;
-            case 4: pyr_level<4>(in, mid, out, tp, tx0, ty0, H, W); break;
-            case 5: pyr_level<5>(in, mid, out, tp, tx0, ty0, H, W); break;
-            case 6: pyr_level<6>(in, mid, out, tp, tx0, ty0, H, W); break;
-            default: pyr_level<7>(in, mid, out, tp, tx0, ty0, H, W); break;
+            case 0: pyr_level<0>(in, mid, ot, out, tp, tx0, ty0, H, W); break;
+            case 1: pyr_level<1>(in, mid, ot, out, tp, tx0, ty0, H, W); break;
+            case 2: pyr_level<2>(in, mid, ot, out, tp, tx0, ty0, H, W); break;
+            case 3: pyr_level<3>(in, mid, ot, out, tp, tx0, ty0, H, W); break;
+            case 4: pyr_level<4>(in, mid, ot, out, tp, tx0, ty0, H, W); break;
+            case 5: pyr_level<5>(in, mid, ot, out, tp, tx0, ty0, H, W); break;
+            case 6: pyr_level<6>(in, mid, ot, out, tp, tx0, ty0, H, W); break;
+            default: pyr_level<7>(in, mid, ot, out, tp, tx0, ty0, H, W); break;
         }
     }
 }
