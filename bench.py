@@ -60,7 +60,8 @@ def parse():
                     help="SequenceConfig(directional=True): the reference's default, which loses the subject "
                          "on this workload (VERDICT r01); the default workload tracks (directional=False)")
     ap.add_argument("--no-quality", action="store_true", help="skip the untimed tracking-quality replay")
-    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay leg")
+    ap.add_argument("--graph", action="store_true",
+                    help="also time the CUDA-graph replay leg (opt-in: ncu's injection crashes on it)")
     ap.add_argument("--stage-pipeline", choices=["auto", "on", "off"], default="auto",
                     help="time the paper's pose -> non-rigid GPU-pair pipeline (StagePipeline) on cuda:0/cuda:1; "
                          "auto: when one process sees >= 2 devices")
@@ -372,7 +373,7 @@ def run_ours(args):
     # steady-state steps (lc_tracker_set_graph; no per-launch profiling, so it
     # is reported beside `value`, whose roofline needs the kernel events)
     graph_leg = None
-    if not args.no_graph:
+    if args.graph:
         trg = BatchTracker(actor, cam, cfg, Sn, groups=args.groups, device=local,
                            host_threads=bool(args.host_threads))
         trg.set_graph(True)

@@ -102,16 +102,20 @@ __device__ __forceinline__ void pyr_level(const double *__restrict__ in, double 
     __syncthreads();
     // the tile's rows are 3T contiguous doubles in the level: 16-byte stores
     // when the row segment is whole and aligned, else element by element
-    const int wx = min(T, W - tx0);
-    const bool vec = wx == T && ((((size_t)tx0 * 3) & 1) == 0) && ((((size_t)W * 3) & 1) == 0);
-    for (int row = 0; row < T && ty0 + row < H; ++row) {
-        double *dst = out + ((size_t)(ty0 + row) * W + tx0) * 3;
-        const double *src = ot + (size_t)row * 3 * T;
-        if (vec) {
-            for (int k = threadIdx.x; k < 3 * T / 2; k += blockDim.x)
-                reinterpret_cast<double2 *>(dst)[k] = reinterpret_cast<const double2 *>(src)[k];
-        } else {
-            for (int k = threadIdx.x; k < 3 * wx; k += blockDim.x) dst[k] = src[k];
+    const int wx = min(T, W - tx0), hy = min(T, H - ty0);
+    const bool vec = wx == T && ((((size_t)tx0 * 3) & 1) == 0) && ((((size_t)W * 3) & 1) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    if (vec) {
+        constexpr int PR = 3 * T / 2;   // 16-byte pairs per row
+        for (int q = threadIdx.x; q < hy * PR; q += blockDim.x) {
+            const int row = q / PR, k = q - row * PR;
+            double2 *dst = reinterpret_cast<double2 *>(out + ((size_t)(ty0 + row) * W + tx0) * 3);
+            dst[k] = reinterpret_cast<const double2 *>(ot + (size_t)row * 3 * T)[k];
+        }
+    } else {
+        for (int q = threadIdx.x; q < hy * 3 * wx; q += blockDim.x) {
+            const int row = q / (3 * wx), k = q - row * 3 * wx;
+            out[((size_t)(ty0 + row) * W + tx0) * 3 + k] = ot[(size_t)row * 3 * T + k];
         }
     }
     __syncthreads();
