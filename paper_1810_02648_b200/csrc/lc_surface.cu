@@ -265,10 +265,15 @@ __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v,
                 acc[6 * h + 1] += o.r * o.r;
             }
         }
+    // (the next edge's endpoint ids are loaded one iteration ahead, so each
+    // edge costs one dependent round trip: its vertex gathers)
+    const int2 *edges2 = reinterpret_cast<const int2 *>(c.A.edges);
+    int2 ab_next = T::tid() < c.E ? edges2[T::tid()] : make_int2(0, 0);
     for (int e = T::tid(); e < c.E; e += T::size) {
         // one load of the endpoints, their steps and V^S per edge for every
         // trial; energies only (the unit direction is not needed here)
-        const int a = c.A.edges[2 * e], b = c.A.edges[2 * e + 1];
+        const int a = ab_next.x, b = ab_next.y;
+        if (e + T::size < c.E) ab_next = edges2[e + T::size];
         const V3 va = ld3(v + 3 * (size_t)a), vb = ld3(v + 3 * (size_t)b);
         const V3 sa = ld3(step + 3 * (size_t)a), sb = ld3(step + 3 * (size_t)b);
         const V3 sd = ld3(J.vs + 3 * (size_t)a) - ld3(J.vs + 3 * (size_t)b);
@@ -338,8 +343,11 @@ __device__ void surf_assemble(const SurfCtx &c, int level, const double *v, doub
     // E: every edge once -- energies, direction, signed gradient into its
     // ELL slots at both endpoints (CSR tails: per edge, edir / eg)
     const size_t LN = (size_t)LC_ELL * c.N;
+    const int2 *edges2 = reinterpret_cast<const int2 *>(c.A.edges);
+    int2 ab_next = T::tid() < c.E ? edges2[T::tid()] : make_int2(0, 0);   // (one edge ahead)
     for (int e = T::tid(); e < c.E; e += T::size) {
-        const int a = c.A.edges[2 * e], b = c.A.edges[2 * e + 1];
+        const int a = ab_next.x, b = ab_next.y;
+        if (e + T::size < c.E) ab_next = edges2[e + T::size];
         const double al = c.ec.alpha[e], be = c.ec.beta[e];
         SlotEdge q;
         slot_edge(c, e, true, ld3(v + 3 * (size_t)a), ld3(J.vs + 3 * (size_t)a), ld3(v + 3 * (size_t)b),

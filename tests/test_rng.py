@@ -37,3 +37,20 @@ def test_standard_normal_bit_exact(seed):
     assert np.array_equal(want, got)
     # the stream position after the draws is numpy's too
     assert n.g.s == g.bit_generator.state["state"]["state"]
+
+
+def test_committed_device_tables_match_numpy():
+    """csrc/lc_ziggurat_tables.h (the device's tables) is what
+    tools/extract_ziggurat.py reads from the installed numpy."""
+    import os
+    import re
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(root, "tools"))
+    import extract_ziggurat
+    t = extract_ziggurat.tables()
+    src = open(os.path.join(root, "paper_1810_02648_b200", "csrc", "lc_ziggurat_tables.h")).read()
+    ki = [int(x, 16) for x in re.findall(r"0x([0-9a-f]{16})ULL", src)]
+    assert ki == list(t["ki_double"])
+    fl = [float.fromhex(x) for x in re.findall(r"(-?0x[0-9a-f.]+p[-+]?\d+|0x0\.0p\+0)", src)]
+    assert fl == list(t["wi_double"]) + list(t["fi_double"])
