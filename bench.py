@@ -682,9 +682,27 @@ def cpu_baseline(actor, cam, frames, n_timed, cfg):
             _, _, _, st, _, _ = OF.solve_frame(prep, actor, cam, cfg, st)
             n += 1
         dt = time.perf_counter() - t0
+        # the PCG alone: the next frame's first Stage II system
+        # in the reference's explicit block layout, pcg_solve best of 5
+        from oracle import linsolve as OL, surface as OSF
+        fr = frames[min(1 + n_timed, len(frames) - 1)]
+        prep = OF.prepare(fr.image, fr.mask, fr.detections, actor, cfg)
+        drest = actor.mesh.rest_vertices + st.disp_rest
+        x, _ = OF.stage1(prep, actor, cam, cfg, st, drest)
+        pb, v_init, _, _ = OF.stage2_problem(prep, actor, cam, cfg, st, x, drest)
+        system = OSF.normal_system(pb, OSF.surface_evaluate(pb, v_init, 0))
+        iters = cfg.nonrigid.pcg_iterations
+        best = float("inf")
+        for _ in range(5):
+            p0 = time.perf_counter()
+            OL.pcg(*system, iterations=iters)
+            best = min(best, time.perf_counter() - p0)
     return {"value": n / dt, "unit": "frames/s", "cores": 1, "kind": "port",
             "sample": f"1 stream, {n} steady frames (after an untimed frame 0), preprocess + solve_frame, "
-                      f"1 thread, oracle port of the reference (bit-identical outputs)"}
+                      f"1 thread, oracle port of the reference (bit-identical outputs)",
+            "pcg_iter_us": 1e6 * best / iters,
+            "pcg_note": f"pcg_solve on one Stage II system (N={actor.mesh.n_vertices}, explicit block layout), "
+                        f"{iters} iterations, best of 5, 1 thread"}
 
 
 # ---------------------------------------------------------------------------
