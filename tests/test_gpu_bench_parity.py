@@ -115,6 +115,17 @@ def test_bench_workload_teacher_forced_25_frames():
     print(f"x5k@1024 frames 0-24: worst vertex err / diag {worst:.2e}")
 
 
+def test_reference_default_directional_teacher_forced():
+    """The reference's default SequenceConfig() (directional silhouette rows,
+    the configuration round 1 benchmarked) on the bench's seed-1 stream,
+    frames 0-7, teacher-forced per stage: the directional side-sign path of
+    both solvers and the snapping walk at x5k@1024^2."""
+    from paper_1810_02648_b200.config import SequenceConfig
+    actor, cam, frames = scene_bench("x5k", 1024, 8, seed=1)
+    worst = _teacher_forced(actor, cam, frames, SequenceConfig(), streams=2, screen=True)
+    print(f"x5k@1024 directional frames 0-7: worst vertex err / diag {worst:.2e}")
+
+
 def test_cfg4_x20k_teacher_forced():
     from paper_1810_02648_b200.config import SequenceConfig
     actor, cam, frames = scene_bench("x20k", 1024, 3, seed=0)
