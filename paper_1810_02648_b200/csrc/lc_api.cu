@@ -1760,8 +1760,10 @@ extern "C" int lc_tracker_step_stage(lc_tracker *t, int32_t stages) {
                  cur[i]->has_image && n->has_image;
         key.push_back(s->in_head);
         key.push_back(n->pending_upload ? 1 : 0);
-        key.push_back((long long)(uintptr_t)cur[i]->image_src ^ (long long)(uintptr_t)cur[i]->mask_src);
-        key.push_back((long long)(uintptr_t)n->image_src ^ (long long)(uintptr_t)n->mask_src);
+        key.push_back((long long)(uintptr_t)cur[i]->image_src);
+        key.push_back((long long)(uintptr_t)cur[i]->mask_src);
+        key.push_back((long long)(uintptr_t)n->image_src);
+        key.push_back((long long)(uintptr_t)n->mask_src);
     }
     auto bookkeeping = [&]() {
         for (FrameIn *f : next) {
@@ -1796,7 +1798,7 @@ extern "C" int lc_tracker_step_stage(lc_tracker *t, int32_t stages) {
                 g = nullptr;
                 for (size_t i = 0; i < next.size(); ++i) {   // (launch_preprocess's bookkeeping, undone:
                     next[i]->state = 1;                          //  the launch below redoes it)
-                    next[i]->pending_upload = key[4 * i + 1] != 0;
+                    next[i]->pending_upload = key[6 * i + 1] != 0;
                 }
                 CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
                 for (size_t i = 0; i < t->slots.size(); ++i) t->slots[i]->view(*cur[i]);

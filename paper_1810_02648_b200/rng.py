@@ -112,6 +112,8 @@ class DeviceStream:
             idx = np.ascontiguousarray(tails[0:2 * k:2])
             want = tails[1:2 * k:2]
             vals = np.empty(k)
+            if int(want.max()) > TAIL_DRAWS:   # (a tail sample of > 15 rejection rounds: never observed)
+                raise RuntimeError("a ziggurat tail sample took more draws than the device records")
             for t in range(k):
                 z, used = _walk(draws[t * TAIL_DRAWS:(t + 1) * TAIL_DRAWS])
                 if used != int(want[t]):
