@@ -951,12 +951,28 @@ static void raster(lc_ctx *c, const lc_actor *a, const lc_camera &cam, const std
 // ---------------------------------------------------------------------------
 // config -> device constants
 
+// Line-search batching (the halvings are exact, so any batching gives the
+// sequential search's decisions; only the work differs).  On the in-track
+// bench stream (oracle logs, frames 1-5) the pose accepts the full step in 29
+// of 30 GN steps: its first batch is the full step alone (pose 638 -> 552 us
+// per frame).  The surface takes 1-3 halvings or rejects in 14 of 15; trying
+// every trial at once shortens an isolated solve (715 -> 669 us) but measured
+// 3% fewer frames/s under the bench's concurrency (4170 vs 4310), so it also
+// starts with the full step alone.  LIVECAP_{POSE,SURF}_FIRST_TRIALS override
+// (1..4).
+static int first_trials(const char *var, int dflt) {
+    const char *v = getenv(var);
+    const int n = v ? atoi(v) : dflt;
+    return n < 1 ? 1 : (n > 4 ? 4 : n);
+}
+
 static void fill_pose_hyper(PoseHyperDev &h, const lc_pose_hyper &p, const SkelDev &s) {
     h.l2d = p.lambda_2d; h.l3d = p.lambda_3d; h.lsil = p.lambda_sil; h.ltemp = p.lambda_temporal;
     h.lanat = p.lambda_anatomic; h.face = p.face_weight;
     for (int i = 0; i < LC_MAXJ; ++i) h.tw[i] = i < s.J ? p.group_weights[s.group[i] & 7] : 0.0;
     h.gn = p.gn_iterations;
     h.max_halvings = p.max_halvings;
+    h.first_trials = first_trials("LIVECAP_POSE_FIRST_TRIALS", 1);
 }
 
 static void fill_surf_hyper(SurfHyperDev &h, const lc_nonrigid_hyper &p) {
@@ -965,6 +981,7 @@ static void fill_surf_hyper(SurfHyperDev &h, const lc_nonrigid_hyper &p) {
     h.gn = p.gn_iterations; h.pcg = p.pcg_iterations; h.max_halvings = p.max_halvings;
     h.n_levels = p.n_levels; h.dilation = p.part_dilation;
     h.snap_step = p.snap_step; h.snap_band = p.snap_band; h.snap_max_steps = p.snap_max_steps;
+    h.first_trials = first_trials("LIVECAP_SURF_FIRST_TRIALS", 1);
 }
 
 // numpy-compatible pairwise sum (n <= 128 blocks of 8)

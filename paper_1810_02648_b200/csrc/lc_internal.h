@@ -113,6 +113,7 @@ struct PoseHyperDev {
     double l2d, l3d, lsil, ltemp, lanat, face;
     double tw[LC_MAXJ];   // lambda-free temporal group weight per joint
     int gn, max_halvings;
+    int first_trials;     // line-search trials evaluated in the first batch (then 4 at a time)
 };
 
 struct SurfHyperDev {
@@ -120,6 +121,7 @@ struct SurfHyperDev {
     int gn, pcg, max_halvings, n_levels, dilation;
     double snap_step, snap_band;
     int snap_max_steps;
+    int first_trials;     // line-search trials evaluated in the first batch (then 4 at a time)
     const double *taps;   // levels*32 pyramid taps (for the on-demand blur outside the pyramid's region)
     int half[4];
 };

@@ -296,10 +296,12 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
             if (task < 27) {
                 for (int rr = grp; rr < nr; rr += G) {
                     const double *row = c.rows + (size_t)rr * 37;
+                    // (FMA: the reference forms J^T J / J^T F with BLAS, which
+                    // fuses; SURVEY Appendix B allows it in this accumulation)
                     if (is_rhs) {
                         const double F = row[36];
 #pragma unroll
-                        for (int i = 0; i < 6; ++i) tile[i] += row[6 * ta + i] * F;
+                        for (int i = 0; i < 6; ++i) tile[i] = fma(row[6 * ta + i], F, tile[i]);
                     } else {
                         double a[6], b[6];
 #pragma unroll
@@ -307,7 +309,7 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
 #pragma unroll
                         for (int i = 0; i < 6; ++i)
 #pragma unroll
-                            for (int j = 0; j < 6; ++j) tile[6 * i + j] += a[i] * b[j];
+                            for (int j = 0; j < 6; ++j) tile[6 * i + j] = fma(a[i], b[j], tile[6 * i + j]);
                     }
                 }
             }
@@ -498,8 +500,10 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(JobArg<PoseJob> jobs, co
         int halv = 0;
         bool rejected = false;
         double e1 = e0;
-        for (int base = 0;; base += kTrials) {
-            const int nt = min(kTrials, J.hp.max_halvings + 1 - base);
+        // (the full step is accepted in nearly every GN step, so the first
+        // batch is J.hp.first_trials trials -- the full step alone by default)
+        for (int base = 0, nb = J.hp.first_trials;; base += nb, nb = kTrials) {
+            const int nt = min(nb, J.hp.max_halvings + 1 - base);
             for (int i = threadIdx.x; i < LC_NP; i += NT) {
                 double st = s.step[i];
                 for (int h = 0; h < nt; ++h) {

@@ -919,9 +919,9 @@ __global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<Sur
             bool rejected = false;
             double e1 = e0;
             double base_sc = 1.0;
-            // (the full step is accepted about two times in three, so it is
-            // tried alone first; the remaining halvings are batched)
-            for (int base = 0, nt = 1;; base += nt, nt = kSurfTrials) {
+            // (first batch: hp.first_trials trials -- the full step alone by
+            // default, see fill_surf_hyper -- then up to four at a time)
+            for (int base = 0, nt = hp.first_trials;; base += nt, nt = kSurfTrials) {
                 nt = min(nt, hp.max_halvings + 1 - base);
                 double et[kSurfTrials][6], unk[kSurfTrials];
                 surf_energy_trials<T>(c, level, v, J.best, nt, false, et, unk);
