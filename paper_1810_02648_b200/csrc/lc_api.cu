@@ -958,8 +958,10 @@ static void raster(lc_ctx *c, const lc_actor *a, const lc_camera &cam, const std
 // per frame).  The surface takes 1-3 halvings or rejects in 14 of 15; trying
 // every trial at once shortens an isolated solve (715 -> 669 us) but measured
 // 3% fewer frames/s under the bench's concurrency (4170 vs 4310), so it also
-// starts with the full step alone.  LIVECAP_{POSE,SURF}_FIRST_TRIALS override
-// (1..4).
+// starts with the full step alone; later batches take the remaining halvings
+// together (batches of 1 / 2 / 4 after the full step: 4317 / 4394 / 4368
+// frames/s, within noise).  LIVECAP_{POSE,SURF}_FIRST_TRIALS and
+// LIVECAP_SURF_NEXT_TRIALS override (1..4).
 static int first_trials(const char *var, int dflt) {
     const char *v = getenv(var);
     const int n = v ? atoi(v) : dflt;
@@ -982,6 +984,7 @@ static void fill_surf_hyper(SurfHyperDev &h, const lc_nonrigid_hyper &p) {
     h.n_levels = p.n_levels; h.dilation = p.part_dilation;
     h.snap_step = p.snap_step; h.snap_band = p.snap_band; h.snap_max_steps = p.snap_max_steps;
     h.first_trials = first_trials("LIVECAP_SURF_FIRST_TRIALS", 1);
+    h.next_trials = first_trials("LIVECAP_SURF_NEXT_TRIALS", 4);
 }
 
 // numpy-compatible pairwise sum (n <= 128 blocks of 8)

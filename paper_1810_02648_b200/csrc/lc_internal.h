@@ -121,7 +121,8 @@ struct SurfHyperDev {
     int gn, pcg, max_halvings, n_levels, dilation;
     double snap_step, snap_band;
     int snap_max_steps;
-    int first_trials;     // line-search trials evaluated in the first batch (then 4 at a time)
+    int first_trials;     // line-search trials evaluated in the first batch
+    int next_trials;      // ... and in each later batch
     const double *taps;   // levels*32 pyramid taps (for the on-demand blur outside the pyramid's region)
     int half[4];
 };

@@ -920,8 +920,8 @@ __global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<Sur
             double e1 = e0;
             double base_sc = 1.0;
             // (first batch: hp.first_trials trials -- the full step alone by
-            // default, see fill_surf_hyper -- then up to four at a time)
-            for (int base = 0, nt = hp.first_trials;; base += nt, nt = kSurfTrials) {
+            // default -- then hp.next_trials at a time; see fill_surf_hyper)
+            for (int base = 0, nt = hp.first_trials;; base += nt, nt = hp.next_trials) {
                 nt = min(nt, hp.max_halvings + 1 - base);
                 double et[kSurfTrials][6], unk[kSurfTrials];
                 surf_energy_trials<T>(c, level, v, J.best, nt, false, et, unk);
