@@ -1375,6 +1375,7 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
     const unsigned S = (unsigned)ss.size();
     launch(c, k_tri_front, dim3(64, S), dim3(256), 0, dcj, a->dev);
     launch(c, k_sil_edges, dim3(64, S), dim3(256), 0, dcj, a->dev);
+    launch(c, k_vis_flags, dim3((a->dev.N + 255) / 256, S), dim3(256), 0, dcj, a->dev, cam_dev(fb.cam));
     launch(c, k_contour_compact, dim3(S), dim3(1024), 0, dcj, a->dev, cam_dev(fb.cam));
     std::vector<RimJob> rjs;
     for (Slot *s : ss) {
@@ -1391,7 +1392,7 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
         r.dilation = fb.cfg->nonrigid.part_dilation;
         rjs.push_back(r);
     }
-    launch(c, k_rim, dim3(32, S), dim3(256), 0, stage(c, rjs), a->dev, cam_dev(fb.cam),
+    launch(c, k_rim, dim3(128, S), dim3(256), 0, stage(c, rjs), a->dev, cam_dev(fb.cam),
            (const double *)fb.cf->probe);
 }
 
@@ -2375,6 +2376,7 @@ extern "C" int lc_contour_vertices(lc_ctx *c, const lc_actor *a, const lc_camera
     const auto dj = stage(c, std::vector<ContourJob>{j});
     launch(c, k_tri_front, dim3(64), dim3(256), 0, dj, a->dev);
     launch(c, k_sil_edges, dim3(64), dim3(256), 0, dj, a->dev);
+    launch(c, k_vis_flags, dim3((a->dev.N + 255) / 256), dim3(256), 0, dj, a->dev, cam_dev(*cam));
     launch(c, k_contour_compact, dim3(1), dim3(1024), 0, dj, a->dev, cam_dev(*cam));
     int B = 0;
     CK(cudaMemcpyAsync(&B, s->B, sizeof(int), cudaMemcpyDeviceToHost, st));

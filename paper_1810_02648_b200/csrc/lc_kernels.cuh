@@ -133,6 +133,7 @@ struct ContourJob {
 };
 __global__ void k_tri_front(JobArg<ContourJob> jobs, ActorDev A);
 __global__ void k_sil_edges(JobArg<ContourJob> jobs, ActorDev A);
+__global__ void k_vis_flags(JobArg<ContourJob> jobs, ActorDev A, CamDev cam);
 __global__ void k_contour_compact(JobArg<ContourJob> jobs, ActorDev A, CamDev cam);
 
 // own-silhouette contour pixels bucketed by 16x16 cell (fixed 256 slots per

@@ -1069,6 +1069,19 @@ __device__ __forceinline__ bool depth_visible(CamDev cam, const unsigned long lo
 // one CTA per stream: ordered compaction of contour candidates (np.unique
 // order = ascending vertex id) and, optionally, of visible vertices; then the
 // image-plane normals of the contour vertices.
+// the depth-visibility test of every vertex, grid-wide (the compaction below
+// is one CTA per stream and only scans these flags): vflag[v] becomes
+// bit 0 = visible, bit 1 = visible and on a silhouette edge
+__global__ void k_vis_flags(JobArg<ContourJob> jobs, ActorDev A, CamDev cam) {
+    lc_pdl_wait();
+    const ContourJob J = jobs[blockIdx.y];
+    if (!J.active) return;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < A.N; v += gridDim.x * blockDim.x) {
+        const bool vis = depth_visible(cam, J.zbuf, ld3(J.verts + 3 * (size_t)v));
+        J.vflag[v] = (uint8_t)((vis ? 1 : 0) | ((vis && J.vflag[v]) ? 2 : 0));
+    }
+}
+
 __global__ void __launch_bounds__(1024) k_contour_compact(JobArg<ContourJob> jobs, ActorDev A,
                                                           CamDev cam) {
     lc_pdl_wait();
@@ -1081,11 +1094,10 @@ __global__ void __launch_bounds__(1024) k_contour_compact(JobArg<ContourJob> job
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int base = 0; base < A.N; base += blockDim.x) {
         const int v = base + threadIdx.x;
-        bool vis = false;
-        if (v < A.N) vis = depth_visible(cam, J.zbuf, ld3(J.verts + 3 * (size_t)v));
+        const int fl = v < A.N ? J.vflag[v] : 0;   // (k_vis_flags)
         for (int list = 0; list < 2; ++list) {
             if (list == 1 && !J.vis) break;
-            const bool f = v < A.N && vis && (list == 1 || J.vflag[v]);
+            const bool f = (fl & (list == 0 ? 2 : 1)) != 0;
             const unsigned bal = __ballot_sync(0xffffffffu, f);
             if (lane == 0) wsum[w] = __popc(bal);
             __syncthreads();
