@@ -1150,6 +1150,8 @@ struct PrepJob {
     int *fallbacks;
     const double *x_prev, *x_prev2;  // null when absent
     double *x;                       // out: initial pose
+    lc_pose_report *pose_rep;        // zeroed here (or null)
+    lc_nonrigid_report *nr_rep;      // zeroed here (or null)
     int N;
 };
 
@@ -1159,33 +1161,51 @@ __global__ void k_prep(JobArg<PrepJob> jobs, const SkelDev *skg) {
     const SkelDev &sk = *skg;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 3 * J.N; i += gridDim.x * blockDim.x)
         J.drest[i] = J.disp ? J.rest[i] + J.disp[i] : J.rest[i];
-    if (blockIdx.x != 0 || threadIdx.x != 0) return;
-    // rescale_detections: root outward, bone lengths from local offsets
-    int fb = 0;
-    for (int k = 0; k < 3; ++k) J.j3d[k] = J.j3d_raw[k];
-    for (int i = 1; i < sk.J; ++i) {
-        const int p = sk.parents[i];
-        double d[3] = {J.j3d_raw[3 * i] - J.j3d_raw[3 * p], J.j3d_raw[3 * i + 1] - J.j3d_raw[3 * p + 1],
-                       J.j3d_raw[3 * i + 2] - J.j3d_raw[3 * p + 2]};
-        double n = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-        const bool usable = n > 1e-9 && J.v3d[i] && J.v3d[p];
-        if (!usable) {
-            for (int k = 0; k < 3; ++k) d[k] = sk.rest[i][k] - sk.rest[p][k];
-            n = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-            ++fb;
-        }
-        const double bl = sqrt(sk.off[i][0] * sk.off[i][0] + sk.off[i][1] * sk.off[i][1] + sk.off[i][2] * sk.off[i][2]);
-        for (int k = 0; k < 3; ++k) J.j3d[3 * i + k] = J.j3d[3 * p + k] + bl * d[k] / n;
+    if (blockIdx.x == 1) {   // the frame's reports start from zero
+        for (int i = threadIdx.x; J.pose_rep && i < (int)(sizeof(lc_pose_report) / 4); i += blockDim.x)
+            reinterpret_cast<int *>(J.pose_rep)[i] = 0;
+        for (int i = threadIdx.x; J.nr_rep && i < (int)(sizeof(lc_nonrigid_report) / 4); i += blockDim.x)
+            reinterpret_cast<int *>(J.nr_rep)[i] = 0;
+        return;
     }
-    *J.fallbacks = fb;
+    if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+    // rescale_detections: root outward, bone lengths from local offsets.  One
+    // warp, lane = joint; the tree levels in order (FK schedule), so every
+    // joint reads its parent's final value: the sequential loop's arithmetic
+    const int lane = threadIdx.x;
+    int fb = 0;
+    if (lane == 0)
+        for (int k = 0; k < 3; ++k) J.j3d[k] = J.j3d_raw[k];
+    __syncwarp();
+    for (int L = 1; L < sk.n_tree_levels; ++L) {
+        const int q = sk.level_start[L] + lane;
+        if (q < sk.level_start[L + 1]) {
+            const int i = sk.level_joint[q];
+            const int p = sk.parents[i];
+            double d[3] = {J.j3d_raw[3 * i] - J.j3d_raw[3 * p], J.j3d_raw[3 * i + 1] - J.j3d_raw[3 * p + 1],
+                           J.j3d_raw[3 * i + 2] - J.j3d_raw[3 * p + 2]};
+            double n = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+            const bool usable = n > 1e-9 && J.v3d[i] && J.v3d[p];
+            if (!usable) {
+                for (int k = 0; k < 3; ++k) d[k] = sk.rest[i][k] - sk.rest[p][k];
+                n = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+                ++fb;
+            }
+            const double bl =
+                sqrt(sk.off[i][0] * sk.off[i][0] + sk.off[i][1] * sk.off[i][1] + sk.off[i][2] * sk.off[i][2]);
+            for (int k = 0; k < 3; ++k) J.j3d[3 * i + k] = J.j3d[3 * p + k] + bl * d[k] / n;
+        }
+        __syncwarp();
+    }
+    for (int o = 16; o > 0; o >>= 1) fb += __shfl_xor_sync(0xffffffffu, fb, o);
+    if (lane == 0) *J.fallbacks = fb;
     if (J.x) {
-        for (int k = 0; k < LC_NP; ++k) {
+        for (int k = lane; k < LC_NP; k += 32) {
             double v = 0.0;
             if (J.x_prev) v = J.x_prev2 ? 2.0 * J.x_prev[k] - J.x_prev2[k] : J.x_prev[k];
+            if (J.x_prev && k >= 6 && k < 6 + LC_NDOF) v = fmin(fmax(v, sk.tmin[k - 6]), sk.tmax[k - 6]);
             J.x[k] = v;
         }
-        if (J.x_prev)
-            for (int k = 0; k < LC_NDOF; ++k) J.x[6 + k] = fmin(fmax(J.x[6 + k], sk.tmin[k]), sk.tmax[k]);
     }
 }
 
@@ -1455,15 +1475,13 @@ static void run_frame(FrameBatch &fb, int stages = 3) {
             p.x_prev = s->has_prev ? s->x_prev : nullptr;
             p.x_prev2 = s->has_prev2 ? s->x_prev2 : nullptr;
             p.x = (stages & 1) ? s->x : nullptr;
+            p.pose_rep = (stages & 1) ? s->pose_rep : nullptr;
+            p.nr_rep = (stages & 2) ? s->nr_rep : nullptr;
             p.N = a->dev.N;
             pj.push_back(p);
         }
         mark(c, "frame:start");
         launch(c, k_prep, dim3(16, S), dim3(256), 0, stage(c, pj), (const SkelDev *)a->skel_dev);
-        for (Slot *s : ss) {
-            if (stages & 1) cudaMemsetAsync(s->pose_rep, 0, sizeof(lc_pose_report), c->stream);
-            if (stages & 2) cudaMemsetAsync(s->nr_rep, 0, sizeof(lc_nonrigid_report), c->stream);
-        }
     }
     if (stages & 1) {
     // ---- Stage I (pipeline.py:173-224)
