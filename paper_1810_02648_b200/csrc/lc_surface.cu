@@ -218,7 +218,8 @@ __device__ __forceinline__ void own_ranges(SurfCtx &c) {
     c.b1 = J.bidx ? lower_bound_ids(J.bidx, c.B, c.hi) : 0;
 }
 
-// energies of nt <= 4 line-search trials v + step * 0.5^h at once (h < nt):
+// energies of nt <= 4 line-search trials v + step * sc0 * 0.5^h at once (h < nt;
+// sc0 a power of two, so every product is exact):
 // each element's trials are evaluated back to back (their gathers and
 // nearest-contour queries overlap), one team reduction for all 24 sums
 constexpr int kSurfTrials = 4;
@@ -232,7 +233,7 @@ constexpr int kSurfTrials = 4;
 // otherwise the caller re-evaluates the batch with `exact`.
 template <typename T>
 __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v, const double *step, int nt,
-                                   bool exact, double en[kSurfTrials][6], double unk[kSurfTrials]) {
+                                   double sc0, bool exact, double en[kSurfTrials][6], double unk[kSurfTrials]) {
     const SurfJob &J = *c.J;
     double acc[kSurfTrials * 7];
     for (int k = 0; k < kSurfTrials * 7; ++k) acc[k] = 0.0;
@@ -241,7 +242,7 @@ __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v,
         for (int k = c.p0 + (int)threadIdx.x; k < c.p1; k += NT) {
             const int i = J.vis[k];
             const V3 vi = ld3(v + 3 * (size_t)i), si = ld3(step + 3 * (size_t)i);
-            double sc = 1.0;
+            double sc = sc0;
 #pragma unroll
             for (int h = 0; h < kSurfTrials; ++h, sc *= 0.5) {
                 if (h >= nt) break;
@@ -256,7 +257,7 @@ __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v,
         for (int b = c.b0 + (int)threadIdx.x; b < c.b1; b += NT) {
             const int i = J.bidx[b];
             const V3 vi = ld3(v + 3 * (size_t)i), si = ld3(step + 3 * (size_t)i);
-            double sc = 1.0;
+            double sc = sc0;
 #pragma unroll
             for (int h = 0; h < kSurfTrials; ++h, sc *= 0.5) {
                 if (h >= nt) break;
@@ -278,7 +279,7 @@ __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v,
         const V3 sa = ld3(step + 3 * (size_t)a), sb = ld3(step + 3 * (size_t)b);
         const V3 sd = ld3(J.vs + 3 * (size_t)a) - ld3(J.vs + 3 * (size_t)b);
         const double rl = c.A.rest_len[e];
-        double sc = 1.0;
+        double sc = sc0;
 #pragma unroll
         for (int h = 0; h < kSurfTrials; ++h, sc *= 0.5) {
             if (h >= nt) break;
@@ -295,7 +296,7 @@ __device__ void surf_energy_trials(const SurfCtx &c, int level, const double *v,
             const V3 vi = ld3(v + 3 * (size_t)i), si = ld3(step + 3 * (size_t)i);
             const V3 q1 = ld3(J.prev + 3 * (size_t)i);
             const V3 q2 = J.prev2 ? ld3(J.prev2 + 3 * (size_t)i) : q1;
-            double sc = 1.0;
+            double sc = sc0;
 #pragma unroll
             for (int h = 0; h < kSurfTrials; ++h, sc *= 0.5) {
                 if (h >= nt) break;
@@ -924,7 +925,7 @@ __global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<Sur
             for (int base = 0, nt = hp.first_trials;; base += nt, nt = hp.next_trials) {
                 nt = min(nt, hp.max_halvings + 1 - base);
                 double et[kSurfTrials][6], unk[kSurfTrials];
-                surf_energy_trials<T>(c, level, v, J.best, nt, false, et, unk);
+                surf_energy_trials<T>(c, level, v, J.best, nt, base_sc, false, et, unk);
                 {   // a trial with unevaluated rows and a lower bound <= e0 before
                     // the first exact accept: evaluate the batch exactly
                     bool undecided = false;
@@ -933,7 +934,7 @@ __global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<Sur
                         if (le && unk[h] > 0.0) { undecided = true; break; }
                         if (le) break;
                     }
-                    if (undecided) surf_energy_trials<T>(c, level, v, J.best, nt, true, et, unk);
+                    if (undecided) surf_energy_trials<T>(c, level, v, J.best, nt, base_sc, true, et, unk);
                 }
                 int hit = -1;
                 double sc = base_sc, hit_sc = 0.0;
@@ -948,11 +949,10 @@ __global__ void __launch_bounds__(NT, LC_SURF_MINB) k_surface_solve_t(JobArg<Sur
                     break;
                 }
                 if (base + nt > hp.max_halvings) { halv = hp.max_halvings; rejected = true; e1 = e0; break; }
+                // later batches start at step * 0.5^base: a power of two,
+                // so sc * step has the bits of the reference's repeated
+                // in-place halvings (no rescaling pass, no team barrier)
                 for (int h = 0; h < nt; ++h) base_sc *= 0.5;
-                // later batches scale the step in place (keeps trial_pos's sc <= 1 exact)
-                for (int i = T::tid(); i < c.N * 3; i += T::size) J.best[i] = base_sc * J.best[i];
-                T::sync();
-                base_sc = 1.0;
             }
             stamp<T>(J, ph);
             if (T::tid() == 0 && J.counters) {
