@@ -913,7 +913,15 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
     launch(c, k_contour_fill, dim3(64, S), dim3(256), 0, dj, ncx);
     if (!lists) return;
     launch(c, k_cell_jfa, dim3(S), dim3(1024), sizeof(int) * 2 * ncx * ncy, dj, ncx, ncy);
-    launch(c, k_cand_build, dim3((ncx * ncy + 3) / 4, S), dim3(128), 0, dj, H, W);
+    // (measurement knob: LIVECAP_CAND_GRID caps the CTAs per stream of this
+    // grid-stride kernel, bounding the SMs the auxiliary stream can hold)
+    static const int cand_cap = [] {
+        const char *v = getenv("LIVECAP_CAND_GRID");
+        return v ? atoi(v) : 0;
+    }();
+    int cand_grid = (ncx * ncy + 3) / 4;
+    if (cand_cap > 0) cand_grid = std::min(cand_grid, cand_cap);
+    launch(c, k_cand_build, dim3(cand_grid, S), dim3(128), 0, dj, H, W);
 }
 
 // depth buffer + winning triangle ids (+ mask) of a batch of meshes with
@@ -1115,7 +1123,16 @@ static void pyramid(lc_ctx *c, const ConfigDev &cf, const std::vector<PyrTarget>
     if (fused) {
         std::vector<PyrAllJob> jobs;
         for (const PyrTarget &t : ts) jobs.push_back(PyrAllJob{t.src, t.dst, t.roi, t.tile_flag});
-        const int tiles = ((W + LC_PYR_TILE - 1) / LC_PYR_TILE) * ((H + LC_PYR_TILE - 1) / LC_PYR_TILE);
+        int tiles = ((W + LC_PYR_TILE - 1) / LC_PYR_TILE) * ((H + LC_PYR_TILE - 1) / LC_PYR_TILE);
+        // at most 296 CTAs per frame (two per SM), each striding over tiles:
+        // the low-priority preprocessing holds fewer SM slots at a time
+        // (frames/s 4528-4545 with one CTA per tile, 4564-4574 capped at
+        // 148-592; LIVECAP_PYR_GRID overrides, 0 = one CTA per tile)
+        static const int pyr_cap = [] {
+            const char *v = getenv("LIVECAP_PYR_GRID");
+            return v ? atoi(v) : 296;
+        }();
+        if (pyr_cap > 0) tiles = std::min(tiles, pyr_cap);
         launch(c, k_pyramid_fused, dim3(tiles, (unsigned)ts.size()), dim3(256), pyramid_fused_smem(),
                stage(c, jobs), H, W, levels, (const double *)cf.taps, cf.half[0], cf.half[1], cf.half[2],
                cf.half[3]);

@@ -131,13 +131,15 @@ __global__ void __launch_bounds__(256) k_pyramid_fused(JobArg<PyrAllJob> jobs, i
     double *in = sm + 1;                 // E rows x SI
     double *mid = sm + E * SI;           // T rows x 3E
     double *ot = mid + T * E * 3;        // T rows x 3T (staged output)
-    const int tiles_x = (W + T - 1) / T;
-    const int tx0 = (blockIdx.x % tiles_x) * T, ty0 = (blockIdx.x / tiles_x) * T;
+    const int tiles_x = (W + T - 1) / T, ntiles = tiles_x * ((H + T - 1) / T);
+    // grid-stride over the tiles (one tile per CTA at the default grid)
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int tx0 = (tile % tiles_x) * T, ty0 = (tile / tiles_x) * T;
     if (J.tile_flag) {   // region of interest: tiles outside it are left to the exact on-demand path
-        const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+        const int tx = tile % tiles_x, ty = tile / tiles_x;
         const bool want = !J.roi || (tx >= J.roi[0] && tx <= J.roi[2] && ty >= J.roi[1] && ty <= J.roi[3]);
-        if (threadIdx.x == 0) J.tile_flag[blockIdx.x] = want ? 1 : 0;
-        if (!want) return;
+        if (threadIdx.x == 0) J.tile_flag[tile] = want ? 1 : 0;
+        if (!want) continue;
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     // asynchronous tile copy (LDGSTS).  Interior tiles (no clamped column):
@@ -185,6 +187,7 @@ __global__ void __launch_bounds__(256) k_pyramid_fused(JobArg<PyrAllJob> jobs, i
             default: pyr_level<7>(in, mid, ot, out, tp, tx0, ty0, H, W); break;
         }
     }
+    }   // tiles (pyr_level ends with a block barrier: `in` is free for the next tile)
 }
 
 // One CTA per stream: bounding box of the grid cells holding contour pixels
