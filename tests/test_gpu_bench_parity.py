@@ -126,6 +126,30 @@ def test_reference_default_directional_teacher_forced():
     print(f"x5k@1024 directional frames 0-7: worst vertex err / diag {worst:.2e}")
 
 
+LONG = pytest.mark.skipif(not __import__("os").environ.get("LIVECAP_LONG_TESTS"),
+                          reason="long sequence (minutes of CPU oracle); LIVECAP_LONG_TESTS=1")
+
+
+@LONG
+def test_cfg3_300_frames_teacher_forced():
+    """full two-stage tracking over a 300-frame synthetic
+    x5k@1024^2 sequence (the reference's default config), teacher-forced per
+    stage at every frame (log: profiles/r02/long_sequences.txt)."""
+    from paper_1810_02648_b200.config import SequenceConfig
+    actor, cam, frames = scene_bench("x5k", 1024, 300, seed=0)
+    worst = _teacher_forced(actor, cam, frames, SequenceConfig(), streams=1, screen=True)
+    print(f"cfg3 x5k@1024 300 frames: worst vertex err / diag {worst:.2e}")
+
+
+@LONG
+def test_cfg2_pose_only_100_frames_teacher_forced():
+    """the pose stage alone over a 100-frame sequence."""
+    from paper_1810_02648_b200.config import SequenceConfig
+    actor, cam, frames = scene_bench("x5k", 1024, 100, seed=0)
+    _teacher_forced(actor, cam, frames, SequenceConfig(mode="pose_only"), streams=1)
+    print("cfg2 x5k@1024 100 frames pose-only: decisions identical, energies within 1e-4")
+
+
 def test_cfg4_x20k_teacher_forced():
     from paper_1810_02648_b200.config import SequenceConfig
     actor, cam, frames = scene_bench("x20k", 1024, 3, seed=0)
