@@ -17,6 +17,11 @@ namespace {
 
 constexpr int NT = 256;
 constexpr int G = NT / 32;  // row groups for the J^T J accumulation
+#ifdef LC_POSE_JTJ_NOFMA    // (comparison build: unfused products and sums)
+#define LC_JTJ_MAD(a, b, c) ((c) + (a) * (b))
+#else
+#define LC_JTJ_MAD(a, b, c) fma((a), (b), (c))
+#endif
 
 struct PoseSmem {
     SkelDev sk;
@@ -301,7 +306,7 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
                     if (is_rhs) {
                         const double F = row[36];
 #pragma unroll
-                        for (int i = 0; i < 6; ++i) tile[i] = fma(row[6 * ta + i], F, tile[i]);
+                        for (int i = 0; i < 6; ++i) tile[i] = LC_JTJ_MAD(row[6 * ta + i], F, tile[i]);
                     } else {
                         double a[6], b[6];
 #pragma unroll
@@ -309,7 +314,7 @@ __device__ double pose_eval(PoseCtx &c, bool with_jac, double terms[5], int &beh
 #pragma unroll
                         for (int i = 0; i < 6; ++i)
 #pragma unroll
-                            for (int j = 0; j < 6; ++j) tile[6 * i + j] = fma(a[i], b[j], tile[6 * i + j]);
+                            for (int j = 0; j < 6; ++j) tile[6 * i + j] = LC_JTJ_MAD(a[i], b[j], tile[6 * i + j]);
                     }
                 }
             }
