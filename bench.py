@@ -462,6 +462,7 @@ def run_ours(args):
         return tr2, max_over_ranks(e0.elapsed_time(e1)), x_h, v_h
 
     tr2, ms_e2e, x_h, v_h = run_e2e(img_h)
+    torch.cuda.set_device(local)
     # results of every stream to rank 0 (the tracking job's only collective,
     # NCCL; outside the timed regions): the last solved frame of each stream
     gathered = None
@@ -480,7 +481,10 @@ def run_ours(args):
     ndev = torch.cuda.device_count()
     if args.stage_pipeline == "on" or (args.stage_pipeline == "auto" and world == 1 and ndev >= 2):
         if ndev >= 2 and world == 1:
-            pipe_line = run_stage_pipeline(actor, cam, cfg, Sn, img_h, msk_h, dets, W, K, AHEAD)
+            try:   # (an informational leg: a failure here must not cost the bench line)
+                pipe_line = run_stage_pipeline(actor, cam, cfg, Sn, img_h, msk_h, dets, W, K, AHEAD)
+            except Exception as exc:  # noqa: BLE001
+                pipe_line = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         else:
             pipe_line = {"skipped": f"needs one process with two devices (devices {ndev}, ranks {world})"}
     # the same e2e loop with 8-bit frames (the reference's on-disk capture
