@@ -970,7 +970,7 @@ static void raster(lc_ctx *c, const lc_actor *a, const lc_camera &cam, const std
 // together (batches of 1 / 2 / 4 after the full step: 4317 / 4394 / 4368
 // frames/s, within noise).  LIVECAP_{POSE,SURF}_FIRST_TRIALS and
 // LIVECAP_SURF_NEXT_TRIALS override (1..4).
-static int first_trials(const char *var, int dflt) {
+static int trials_env(const char *var, int dflt) {
     const char *v = getenv(var);
     const int n = v ? atoi(v) : dflt;
     return n < 1 ? 1 : (n > 4 ? 4 : n);
@@ -982,7 +982,7 @@ static void fill_pose_hyper(PoseHyperDev &h, const lc_pose_hyper &p, const SkelD
     for (int i = 0; i < LC_MAXJ; ++i) h.tw[i] = i < s.J ? p.group_weights[s.group[i] & 7] : 0.0;
     h.gn = p.gn_iterations;
     h.max_halvings = p.max_halvings;
-    h.first_trials = first_trials("LIVECAP_POSE_FIRST_TRIALS", 1);
+    h.first_trials = trials_env("LIVECAP_POSE_FIRST_TRIALS", 1);
 }
 
 static void fill_surf_hyper(SurfHyperDev &h, const lc_nonrigid_hyper &p) {
@@ -991,8 +991,8 @@ static void fill_surf_hyper(SurfHyperDev &h, const lc_nonrigid_hyper &p) {
     h.gn = p.gn_iterations; h.pcg = p.pcg_iterations; h.max_halvings = p.max_halvings;
     h.n_levels = p.n_levels; h.dilation = p.part_dilation;
     h.snap_step = p.snap_step; h.snap_band = p.snap_band; h.snap_max_steps = p.snap_max_steps;
-    h.first_trials = first_trials("LIVECAP_SURF_FIRST_TRIALS", 1);
-    h.next_trials = first_trials("LIVECAP_SURF_NEXT_TRIALS", 4);
+    h.first_trials = trials_env("LIVECAP_SURF_FIRST_TRIALS", 1);
+    h.next_trials = trials_env("LIVECAP_SURF_NEXT_TRIALS", 4);
 }
 
 // numpy-compatible pairwise sum (n <= 128 blocks of 8)
