@@ -85,6 +85,7 @@ __device__ double pose_row(const PoseCtx &c, const PoseView &pv, int r, double *
         const double lam = n < nj ? hp.l2d : hp.l2d * hp.face;
         const double w2 = (sqrt(lam) * (J.v2d[n] ? 1.0 : 0.0)) * (pv.okz[n] ? 1.0 : 0.0);
         const double F = (pv.pix[n][comp] - J.j2d[2 * n + comp]) * w2;
+        behind = comp == 0 && !pv.okz[n];   // each joint / marker once (pose_stage.py:334)
         if (jr) {
             const V3 p = n < nj ? ld3(f.pos[n]) : ld3(f.markers[n - nj]);
             double a0, a2, b1, b2;
