@@ -521,12 +521,20 @@ __global__ void k_cell_jfa(JobArg<GridJob> jobs, int ncx, int ncy) {
 #ifndef LC_SEED_PRUNE
 #define LC_SEED_PRUNE 1
 #endif
+// breadth-first candidate collection (0: the depth-first walk only);
+// frontiers / leaf lists beyond LC_BFS_CAP nodes fall back to the walk
+#ifndef LC_CAND_BFS
+#define LC_CAND_BFS 1
+#endif
+#define LC_BFS_CAP 256
 __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H, int W) {
     lc_pdl_wait();
     const GridJob J = jobs[blockIdx.y];
     const NnGridDev g = grid_of(J, H, W);
     const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     __shared__ unsigned long long keys_all[4][LC_CAND_MAX];
+    __shared__ int bfs_all[4][2][LC_BFS_CAP];
+    __shared__ int leaf_all[4][LC_BFS_CAP];
     unsigned long long *key = keys_all[threadIdx.x >> 5];
     for (int c = blockIdx.x * wpb + (threadIdx.x >> 5); c < g.ncx * g.ncy; c += gridDim.x * wpb) {
         const int cx = c % g.ncx, cy = c / g.ncx;
@@ -560,29 +568,122 @@ __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H,
             return a * X0 + b * Y0 + c0 >= 1 && a * X1 + b * Y0 + c0 >= 1 && a * X0 + b * Y1 + c0 >= 1 &&
                    a * X1 + b * Y1 + c0 >= 1;
         };
-        if (ok) {
+        // collect the candidates: the sites within u2 of the cell that the
+        // seed does not dominate (appended in any order: the list is sorted
+        // by (distance, key) below, so the visit order does not matter)
+        auto consider = [&](int kk, bool valid) {
+            bool take = false;
+            int pid = 0;
+            int2 p = make_int2(0, 0);
+            if (valid) {
+                pid = g.cell_pts[kk];
+                p = g.pts[pid];
+                take = cell_near2(cx, cy, p) <= u2 && !seed_dominates(p);
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, take);
+            const int at = n + __popc(bal & ((1u << lane) - 1u));
+            if (take && at < LC_CAND_MAX)
+                key[at] = ((unsigned long long)cell_near2_int(cx, cy, p) << 32) | (unsigned)pid;
+            n += __popc(bal);
+        };
+        bool walked = false;
+        if (ok && LC_CAND_BFS) {
+            // breadth-first over the site quadtree, the lanes testing one
+            // frontier node each (the same node set as the depth-first walk:
+            // every non-empty node with near2 <= u2), then the sites of all
+            // reached leaf cells flattened over the lanes, so the dependent
+            // loads (node count; leaf range -> site id -> site) issue a warp
+            // at a time instead of one node / one leaf at a time
+            int *fr0 = bfs_all[threadIdx.x >> 5][0], *fr1 = bfs_all[threadIdx.x >> 5][1];
+            int *leaf = leaf_all[threadIdx.x >> 5];
+            const CellBox cb = cell_box(cx, cy);
+            if (lane == 0) fr0[0] = g.qL << 24;
+            __syncwarp();
+            int nf = 1, nleaf = 0;
+            bool over = false;
+            while (nf > 0) {
+                int nn = 0;
+                for (int b = 0; b < nf; b += 32) {
+                    const int i = b + lane;
+                    bool inner = false, isleaf = false;
+                    int l = 0, ny = 0, nx = 0;
+                    if (i < nf) {
+                        const int e = fr0[i];
+                        l = e >> 24; ny = (e >> 12) & 0xfff; nx = e & 0xfff;
+                        const int side = g.qP >> l;
+                        if (g.quad[quad_off(g.qP, l) + ny * side + nx] != 0) {
+                            const double sz = (double)(LC_GRID_CELL << l);
+                            if (near2_box(cb, nx * sz, ny * sz, nx * sz + sz - 1.0, ny * sz + sz - 1.0) <= u2) {
+                                if (l > 0) inner = true;
+                                else isleaf = nx < g.ncx && ny < g.ncy;
+                            }
+                        }
+                    }
+                    const unsigned lt = (1u << lane) - 1u;
+                    const unsigned bi = __ballot_sync(0xffffffffu, inner);
+                    const int at = nn + 4 * __popc(bi & lt);
+                    if (inner && at + 4 <= LC_BFS_CAP)
+                        for (int k = 0; k < 4; ++k)
+                            fr1[at + k] = ((l - 1) << 24) | ((2 * ny + (k >> 1)) << 12) | (2 * nx + (k & 1));
+                    nn += 4 * __popc(bi);
+                    const unsigned bl = __ballot_sync(0xffffffffu, isleaf);
+                    const int al = nleaf + __popc(bl & lt);
+                    if (isleaf && al < LC_BFS_CAP) leaf[al] = ny * g.ncx + nx;
+                    nleaf += __popc(bl);
+                }
+                __syncwarp();
+                if (nn > LC_BFS_CAP || nleaf > LC_BFS_CAP) { over = true; break; }
+                int *t = fr0; fr0 = fr1; fr1 = t;
+                nf = nn;
+            }
+            if (!over) {
+                walked = true;
+                // sites of the reached leaves, 32 leaves' ranges at a time
+                for (int lb = 0; lb < nleaf; lb += 32) {
+                    const int li = lb + lane;
+                    int s0 = 0, cntl = 0;
+                    if (li < nleaf) {
+                        const int cc = leaf[li];
+                        s0 = g.cell_start[cc];
+                        cntl = g.cell_start[cc + 1] - s0;
+                    }
+                    int incl = cntl;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    const int total = __shfl_sync(0xffffffffu, incl, 31);
+                    int *excl = fr1;   // the frontier buffers are free now
+                    int *sbase = fr0;
+                    excl[lane] = incl - cntl;
+                    sbase[lane] = s0;
+                    __syncwarp();
+                    const int nl = min(32, nleaf - lb);
+                    for (int t0 = 0; t0 < total; t0 += 32) {
+                        const int t = t0 + lane;
+                        int kk = 0;
+                        if (t < total) {
+                            int lo = 0, hi = nl - 1;   // the last leaf whose start <= t
+                            while (lo < hi) {
+                                const int m = (lo + hi + 1) >> 1;
+                                if (excl[m] <= t) lo = m; else hi = m - 1;
+                            }
+                            kk = sbase[lo] + (t - excl[lo]);
+                        }
+                        consider(kk, t < total);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        if (ok && !walked)
             quad_walk_warp(g, cell_box(cx, cy), [&](double n2) { return n2 <= u2; },
                            [&](int k0, int k1) {
-                               for (int k = k0; k < k1; k += 32) {
-                                   const int kk = k + lane;
-                                   bool take = false;
-                                   int pid = 0;
-                                   int2 p = make_int2(0, 0);
-                                   if (kk < k1) {
-                                       pid = g.cell_pts[kk];
-                                       p = g.pts[pid];
-                                       take = cell_near2(cx, cy, p) <= u2 && !seed_dominates(p);
-                                   }
-                                   const unsigned bal = __ballot_sync(0xffffffffu, take);
-                                   const int at = n + __popc(bal & ((1u << lane) - 1u));
-                                   if (take && at < LC_CAND_MAX)
-                                       key[at] = ((unsigned long long)cell_near2_int(cx, cy, p) << 32) | (unsigned)pid;
-                                   n += __popc(bal);
-                               }
+                               for (int k = k0; k < k1; k += 32) consider(k + lane, k + lane < k1);
                            },
                            [&]() {});
-            ok = n <= LC_CAND_MAX;
-        }
+        if (ok) ok = n <= LC_CAND_MAX;
         if (ok) {
             int P = 1;
             while (P < n) P <<= 1;
