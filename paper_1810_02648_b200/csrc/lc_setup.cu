@@ -527,6 +527,18 @@ __global__ void k_cell_jfa(JobArg<GridJob> jobs, int ncx, int ncy) {
 #define LC_CAND_BFS 1
 #endif
 #define LC_BFS_CAP 256
+// Site s = (px, py) is dominated over the closed 16-px cell at (X0, Y0) by
+// site t when |q-s|^2 - |q-t|^2 >= 1 at every point q of the cell: the
+// difference is affine in q, so its minimum over the cell is at a corner,
+// f(X0, Y0) + min(0, 16 a) + min(0, 16 b).  Exact integer arithmetic (I =
+// int while every coordinate is below 8192, else long long); t == s gives 0.
+template <typename I>
+__device__ __forceinline__ bool cell_dominated(int tx, int ty, I t2, int px, int py, I s2, int X0, int Y0) {
+    const I a = (I)(2 * (tx - px)), b = (I)(2 * (ty - py));
+    const I f = a * X0 + b * Y0 + (s2 - t2) + min((I)0, a * LC_GRID_CELL) + min((I)0, b * LC_GRID_CELL);
+    return f >= 1;
+}
+
 __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H, int W) {
     lc_pdl_wait();
     const GridJob J = jobs[blockIdx.y];
@@ -553,20 +565,20 @@ __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H,
         // argument as the dominance pruning: |q-s|^2 - |q-t|^2 >= 1 over the
         // whole cell means s is never the nearest, nor tied with it)
         const int X0 = cx * LC_GRID_CELL, Y0 = cy * LC_GRID_CELL;
-        const int X1 = X0 + LC_GRID_CELL, Y1 = Y0 + LC_GRID_CELL;
         int2 sd = make_int2(0, 0);
         bool has_sd = false;
         if (ok && LC_SEED_PRUNE) {
             const int seed = J.cell_seed[c];
             if (seed >= 0) { sd = g.pts[seed]; has_sd = true; }
         }
+        const bool small = W <= 8192 && H <= 8192;   // int32 dominance tests cannot overflow
         auto seed_dominates = [&](int2 p) {
-            if (!has_sd || (sd.x == p.x && sd.y == p.y)) return false;
-            const long long s2 = (long long)p.x * p.x + (long long)p.y * p.y;
-            const long long a = 2LL * (sd.x - p.x), b = 2LL * (sd.y - p.y);
-            const long long c0 = s2 - ((long long)sd.x * sd.x + (long long)sd.y * sd.y);
-            return a * X0 + b * Y0 + c0 >= 1 && a * X1 + b * Y0 + c0 >= 1 && a * X0 + b * Y1 + c0 >= 1 &&
-                   a * X1 + b * Y1 + c0 >= 1;
+            if (!has_sd) return false;
+            if (small)
+                return cell_dominated<int>(sd.x, sd.y, sd.x * sd.x + sd.y * sd.y, p.x, p.y, p.x * p.x + p.y * p.y,
+                                           X0, Y0);
+            return cell_dominated<long long>(sd.x, sd.y, (long long)sd.x * sd.x + (long long)sd.y * sd.y, p.x, p.y,
+                                             (long long)p.x * p.x + (long long)p.y * p.y, X0, Y0);
         };
         // collect the candidates: the sites within u2 of the cell that the
         // seed does not dominate (appended in any order: the list is sorted
@@ -687,27 +699,42 @@ __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H,
         if (ok) {
             int P = 1;
             while (P < n) P <<= 1;
-            for (int i = n + lane; i < P; i += 32) key[i] = ~0ull;
-            __syncwarp();
-            for (int k = 2; k <= P; k <<= 1)
-                for (int j = k >> 1; j > 0; j >>= 1) {
-                    for (int i = lane; i < P; i += 32) {
-                        const int ixj = i ^ j;
-                        if (ixj > i) {
-                            const unsigned long long a = key[i], b = key[ixj];
-                            if ((a > b) == ((i & k) == 0)) { key[i] = b; key[ixj] = a; }
-                        }
+            if (P <= 32) {
+                // one key per lane: the bitonic network over shuffles
+                unsigned long long v = lane < n ? key[lane] : ~0ull;
+#pragma unroll
+                for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+                    for (int j = k >> 1; j > 0; j >>= 1) {
+                        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, j);
+                        v = (((lane & j) == 0) == ((lane & k) == 0)) ? (v < o ? v : o) : (v < o ? o : v);
                     }
-                    __syncwarp();
-                }
+                __syncwarp();
+                if (lane < n) key[lane] = v;
+                __syncwarp();
+            } else {
+                for (int i = n + lane; i < P; i += 32) key[i] = ~0ull;
+                __syncwarp();
+                for (int k = 2; k <= P; k <<= 1)
+                    for (int j = k >> 1; j > 0; j >>= 1) {
+                        for (int i = lane; i < P; i += 32) {
+                            const int ixj = i ^ j;
+                            if (ixj > i) {
+                                const unsigned long long a = key[i], b = key[ixj];
+                                if ((a > b) == ((i & k) == 0)) { key[i] = b; key[ixj] = a; }
+                            }
+                        }
+                        __syncwarp();
+                    }
+            }
             // Dominance pruning.  A candidate s is dropped when one of the
-            // cell's LC_DOMINATORS closest candidates t satisfies |q-s|^2 - |q-t|^2 >= 1
-            // at the 4 corners of the (closed) cell: that difference is affine
-            // in q, so it is >= 1 on the whole cell, far beyond the rounding of
-            // the fp64 squared distances (< 1e-7 px^2 here), so s is never the
-            // nearest site -- nor tied with it -- for any query in the cell.
-            // Exact; it removes most of a far cell's list (the contour sites
-            // far along the contour from the cell's nearest ones).
+            // cell's LC_DOMINATORS closest candidates t dominates it over the
+            // cell (cell_dominated: |q-s|^2 - |q-t|^2 >= 1 on the whole cell,
+            // far beyond the rounding of the fp64 squared distances, < 1e-7
+            // px^2 here), so s is never the nearest site -- nor tied with it
+            // -- for any query in the cell.  Exact; it removes most of a far
+            // cell's list (the contour sites far along the contour from the
+            // cell's nearest ones).
             const int nd = min(n, LC_DOMINATORS);
             int tx[LC_DOMINATORS], ty[LC_DOMINATORS];
 #pragma unroll
@@ -725,15 +752,27 @@ __global__ void __launch_bounds__(128) k_cand_build(JobArg<GridJob> jobs, int H,
                     const int2 p = g.pts[(int)(unsigned)(key[i] & 0xffffffffu)];
                     k = site_key(p);
                     keep = true;
-                    const long long s2 = (long long)p.x * p.x + (long long)p.y * p.y;
+                    if (small) {
+                        const int s2 = p.x * p.x + p.y * p.y;
 #pragma unroll
-                    for (int d = 0; d < LC_DOMINATORS; ++d) {
-                        if (d >= nd || (tx[d] == p.x && ty[d] == p.y)) continue;
-                        const long long a = 2LL * (tx[d] - p.x), b = 2LL * (ty[d] - p.y);
-                        const long long c0 = s2 - ((long long)tx[d] * tx[d] + (long long)ty[d] * ty[d]);
-                        const long long f00 = a * X0 + b * Y0 + c0, f10 = a * X1 + b * Y0 + c0;
-                        const long long f01 = a * X0 + b * Y1 + c0, f11 = a * X1 + b * Y1 + c0;
-                        if (f00 >= 1 && f10 >= 1 && f01 >= 1 && f11 >= 1) { keep = false; break; }
+                        for (int d = 0; d < LC_DOMINATORS; ++d) {
+                            if (d >= nd) break;
+                            if (cell_dominated<int>(tx[d], ty[d], tx[d] * tx[d] + ty[d] * ty[d], p.x, p.y, s2, X0, Y0)) {
+                                keep = false;
+                                break;
+                            }
+                        }
+                    } else {
+                        const long long s2 = (long long)p.x * p.x + (long long)p.y * p.y;
+#pragma unroll
+                        for (int d = 0; d < LC_DOMINATORS; ++d) {
+                            if (d >= nd) break;
+                            if (cell_dominated<long long>(tx[d], ty[d], (long long)tx[d] * tx[d] + (long long)ty[d] * ty[d],
+                                                          p.x, p.y, s2, X0, Y0)) {
+                                keep = false;
+                                break;
+                            }
+                        }
                     }
                 }
                 const unsigned bal = __ballot_sync(0xffffffffu, keep);
