@@ -1022,9 +1022,12 @@ __global__ void __launch_bounds__(256) k_rt_tiles(JobArg<RasterJob> jobs, CamDev
     __shared__ TriRec sr[CH];
     __shared__ int sid[CH];
     const int total = J.ioff[nt];
+    const int extra = total - nt;   // items beyond one per tile (multi-chunk tiles)
     for (int item = blockIdx.x; item < total; item += gridDim.x) {
-        // the tile owning this item: last tile with ioff[tile] <= item
-        int lo = 0, hi = nt - 1;
+        // the tile owning this item: last tile with ioff[tile] <= item.  Every
+        // tile has at least one item, so tile <= ioff[tile] <= tile + extra:
+        // the owner lies in [item - extra, item] (one probe when no tile is split)
+        int lo = max(0, item - extra), hi = min(nt - 1, item);
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (J.ioff[mid] <= item) lo = mid;
