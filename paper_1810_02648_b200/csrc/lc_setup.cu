@@ -48,9 +48,14 @@ __global__ void k_blur_axis(JobArg<PyrJob> jobs, int H, int W, int C, const doub
 // shared memory: the haloed input tile (rows of 3E doubles, shifted by one
 // double so interior rows load as 16-byte cp.async), the vertical pass's
 // intermediate, and the output tile staged for coalesced 16-byte stores
+// (the intermediate and the staged output have odd row strides, 3E + 1 and
+// 3T + 1 doubles, so the horizontal pass -- one row per lane -- is free of
+// bank conflicts)
+#define LC_PYR_MS (3 * (LC_PYR_TILE + 2 * LC_PYR_HALO) + 1)
+#define LC_PYR_OS (3 * LC_PYR_TILE + 1)
 size_t pyramid_fused_smem() {
     const int T = LC_PYR_TILE, E = LC_PYR_TILE + 2 * LC_PYR_HALO;
-    return sizeof(double) * ((size_t)E * (3 * E + 2) + 3 * ((size_t)T * E + (size_t)T * T));
+    return sizeof(double) * ((size_t)E * (3 * E + 2) + (size_t)T * LC_PYR_MS + (size_t)T * LC_PYR_OS);
 }
 
 // Register-blocked passes: a thread owns RB consecutive outputs along the
@@ -77,20 +82,21 @@ __device__ __forceinline__ void pyr_level(const double *__restrict__ in, double 
             double acc = win[r + HH] * t[0];
 #pragma unroll
             for (int j = HH; j >= 1; --j) acc = acc + (win[r + HH - j] + win[r + HH + j]) * t[j];
-            mid[(rb * RB + r) * 3 * E + col] = acc;
+            mid[(rb * RB + r) * LC_PYR_MS + col] = acc;
         }
     }
     __syncthreads();
-    // horizontal: unit = (row, channel, column block); mid holds clamped columns
+    // horizontal: unit = (row, channel, column block), the row fastest (a
+    // warp's lanes read / write 32 rows at odd strides); mid holds clamped columns
     for (int u = threadIdx.x; u < T * 3 * (T / RB); u += blockDim.x) {
-        const int cb = u % (T / RB), rc = u / (T / RB), c = rc % 3, row = rc / 3;
+        const int row = u % T, cc = u / T, c = cc % 3, cb = cc / 3;
         const int gy = ty0 + row;
         if (gy >= H) continue;
-        const double *p = mid + row * 3 * E + (cb * RB + R - HH) * 3 + c;
+        const double *p = mid + row * LC_PYR_MS + (cb * RB + R - HH) * 3 + c;
         double win[NWIN];
 #pragma unroll
         for (int k = 0; k < NWIN; ++k) win[k] = p[3 * k];
-        double *o = ot + (size_t)row * 3 * T + (cb * RB) * 3 + c;   // the staged output tile
+        double *o = ot + (size_t)row * LC_PYR_OS + (cb * RB) * 3 + c;   // the staged output tile
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
             double acc = win[r + HH] * t[0];
@@ -110,12 +116,13 @@ __device__ __forceinline__ void pyr_level(const double *__restrict__ in, double 
         for (int q = threadIdx.x; q < hy * PR; q += blockDim.x) {
             const int row = q / PR, k = q - row * PR;
             double2 *dst = reinterpret_cast<double2 *>(out + ((size_t)(ty0 + row) * W + tx0) * 3);
-            dst[k] = reinterpret_cast<const double2 *>(ot + (size_t)row * 3 * T)[k];
+            const double *src = ot + (size_t)row * LC_PYR_OS + 2 * k;
+            dst[k] = make_double2(src[0], src[1]);
         }
     } else {
         for (int q = threadIdx.x; q < hy * 3 * wx; q += blockDim.x) {
             const int row = q / (3 * wx), k = q - row * 3 * wx;
-            out[((size_t)(ty0 + row) * W + tx0) * 3 + k] = ot[(size_t)row * 3 * T + k];
+            out[((size_t)(ty0 + row) * W + tx0) * 3 + k] = ot[(size_t)row * LC_PYR_OS + k];
         }
     }
     __syncthreads();
@@ -129,8 +136,8 @@ __global__ void __launch_bounds__(256) k_pyramid_fused(JobArg<PyrAllJob> jobs, i
     extern __shared__ double sm[];
     constexpr int SI = 3 * E + 2;        // input row stride: element -1 of every row is 16-byte aligned
     double *in = sm + 1;                 // E rows x SI
-    double *mid = sm + E * SI;           // T rows x 3E
-    double *ot = mid + T * E * 3;        // T rows x 3T (staged output)
+    double *mid = sm + E * SI;           // T rows x 3E (stride LC_PYR_MS)
+    double *ot = mid + T * LC_PYR_MS;    // T rows x 3T (staged output, stride LC_PYR_OS)
     const int tiles_x = (W + T - 1) / T, ntiles = tiles_x * ((H + T - 1) / T);
     // grid-stride over the tiles (one tile per CTA at the default grid)
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -1337,11 +1344,14 @@ __global__ void __launch_bounds__(256) k_own_cells(JobArg<OwnCellsJob> jobs, int
     if (threadIdx.x == 0) J.cnt[c] = total;
 }
 
-// nn_within2 over the own-silhouette cell buckets
-__device__ inline double own_within2(const NnGridDev &g, const int *cnt, const int *keys, double qx, double qy,
-                                     double R) {
-    double best = LC_INF;
-    if (!(isfinite(qx) && isfinite(qy))) return best;
+// Is some own-contour pixel at squared distance < lim2 (<= lim2 when
+// `inclusive`) from (qx, qy)?  The cells within R >= sqrt(lim2) are scanned
+// and the scan stops at the first such pixel.  The squared distance is the
+// same expression as the nearest-distance search, so every threshold decision
+// on the minimum is reproduced exactly.
+__device__ inline bool own_any_within(const NnGridDev &g, const int *cnt, const int *keys, double qx, double qy,
+                                      double R, double lim2, bool inclusive) {
+    if (!(isfinite(qx) && isfinite(qy))) return false;
     const int cx0 = max(0, (int)floor((qx - R) / LC_GRID_CELL));
     const int cx1 = min(g.ncx - 1, (int)floor((qx + R) / LC_GRID_CELL));
     const int cy0 = max(0, (int)floor((qy - R) / LC_GRID_CELL));
@@ -1354,10 +1364,11 @@ __device__ inline double own_within2(const NnGridDev &g, const int *cnt, const i
             for (int k = 0; k < n; ++k) {
                 const int key = kk[k];
                 const double dx = qx - (double)(key & 0xffff), dy = qy - (double)(key >> 16);
-                best = fmin(best, dx * dx + dy * dy);
+                const double d2 = dx * dx + dy * dy;
+                if (inclusive ? d2 <= lim2 : d2 < lim2) return true;
             }
         }
-    return best <= R * R ? best : LC_INF;
+    return false;
 }
 
 __global__ void k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double *probe_offs) {
@@ -1377,26 +1388,28 @@ __global__ void k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double 
         // contour is within 1.5 px, and in Stage I some interior probe is at
         // least 6 px (2 * depth >= 12) from it.  Both are threshold tests, so
         // bounded exact searches decide them (nn_within2).
+        // sqrt is correctly rounded and monotone with sqrt(2.25) = 1.5 and
+        // sqrt(36) = 6 exact, so sqrt(d2) <= 1.5 <=> d2 <= 2.25 and
+        // sqrt(d2) >= 6 <=> d2 >= 36: the threshold tests on the nearest
+        // distance become "is any contour pixel that close" (early exit)
         bool keep = false;
-        if (ok) {
-            const double d2 = own_within2(own, J.own_cnt, J.own_keys, px, py, 2.0);
-            keep = d2 != LC_INF && sqrt(d2) <= 1.5;
-        }
+        if (ok) keep = own_any_within(own, J.own_cnt, J.own_keys, px, py, 2.0, 2.25, true);
         if (J.stage1) {
             if (keep) {
-                // 16 directions x radii 1..8: depth = max over interior probes;
-                // lane = (direction, half of the radii)
-                double deep = 0.0;
+                // 16 directions x radii 1..8: depth = max over interior probes
+                // of the nearest contour distance, keep iff 2 * depth >= 12,
+                // i.e. iff some interior probe has no contour pixel closer
+                // than 6 px; lane = (direction, half of the radii)
+                bool deep = false;
                 const int dir = lane >> 1, r0 = (lane & 1) * 4;
                 for (int r = r0; r < r0 + 4; ++r) {
                     const int k = dir * 8 + r;
                     const double qx = px + probe_offs[2 * k], qy = py + probe_offs[2 * k + 1];
-                    if (!field_inside(own, qx, qy)) continue;
-                    const double d2 = own_within2(own, J.own_cnt, J.own_keys, qx, qy, 7.0);
-                    deep = fmax(deep, d2 == LC_INF ? 7.0 : sqrt(d2));   // > 7 px: any value >= 6 decides
+                    if (field_inside(own, qx, qy) && !own_any_within(own, J.own_cnt, J.own_keys, qx, qy, 6.0, 36.0, false))
+                        deep = true;
+                    if (__any_sync(0xffffffffu, deep)) break;   // warp-uniform
                 }
-                for (int o = 16; o > 0; o >>= 1) deep = fmax(deep, __shfl_xor_sync(0xffffffffu, deep, o));
-                keep = 2.0 * deep >= 12.0;
+                keep = __any_sync(0xffffffffu, deep);
             }
             keep = keep && A.rigidity[v] >= 2.0;
         } else if (J.part_gate) {
