@@ -695,6 +695,7 @@ static void alloc_grid(DevArena &m, GridBufs &g, int H, int W) {
     g.cand_pts = m.alloc<int>((size_t)ncx * ncy * LC_CAND_MAX);   // fixed-capacity per-cell lists
     g.cand_blk = m.alloc<int>((size_t)ncx * ncy * 32);
     g.cell_seed = m.alloc<int>(ncx * ncy);
+    g.fg_rows = m.alloc<uint8_t>((size_t)H * ((W + LC_PYR_TILE - 1) / LC_PYR_TILE));
     g.qP = 1;
     g.qL = 0;
     while (g.qP < std::max(ncx, ncy)) { g.qP *= 2; g.qL++; }
@@ -898,6 +899,7 @@ static void build_grids(lc_ctx *c, const std::vector<std::pair<const GridBufs *,
         j.cand_blk = p.first->cand_blk;
         j.max_u2 = max_u * max_u;
         j.quad = p.first->quad; j.qP = p.first->qP; j.qL = p.first->qL;
+        j.fg_rows = p.first->fg_rows;
         j.cell_seed = p.first->cell_seed;
         jobs.push_back(j);
     }
@@ -1345,12 +1347,12 @@ static void launch_preprocess(lc_ctx *c, const ConfigDev &cf, const lc_config &c
             if (f->has_image) {
                 ts.push_back(PyrTarget{f->image_src, f->pyr, f->tmp, margin == -1 ? nullptr : f->pyr_roi,
                                        f->pyr_tile});
-                rj.push_back(PyrRoiJob{f->obs.cell_count, f->pyr_roi});
+                rj.push_back(PyrRoiJob{f->obs.cell_count, f->pyr_roi, f->obs.fg_rows, f->pyr_tile});
             }
         if (!rj.empty() && margin != -1) {
             const int ncx = (W + LC_GRID_CELL - 1) / LC_GRID_CELL, ncy = (H + LC_GRID_CELL - 1) / LC_GRID_CELL;
             launch(c, k_pyr_roi, dim3((unsigned)rj.size()), dim3(1024), 0, stage(c, rj), ncx, ncy,
-                   (W + LC_PYR_TILE - 1) / LC_PYR_TILE, (H + LC_PYR_TILE - 1) / LC_PYR_TILE, margin);
+                   (W + LC_PYR_TILE - 1) / LC_PYR_TILE, (H + LC_PYR_TILE - 1) / LC_PYR_TILE, margin, H);
         }
         if (!ts.empty()) pyramid(c, cf, ts, H, W, cfg.nonrigid.n_levels);
     }

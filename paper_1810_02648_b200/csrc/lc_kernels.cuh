@@ -16,16 +16,19 @@ __global__ void k_blur_axis(JobArg<PyrJob> jobs, int H, int W, int C, const doub
 struct PyrAllJob {
     const double *src;   // H*W*3
     double *dst;         // levels*H*W*3
-    const int *roi;      // [tx0, ty0, tx1, ty1] tiles to compute (inclusive), or null: every tile
+    const int *roi;      // non-null: tile_flag was decided by k_pyr_roi; null: every tile
     uint8_t *tile_flag;  // per LC_PYR_TILE^2 tile: 1 = computed (null: no flags)
 };
 // the pyramid's region of interest: the LC_PYR_TILE tiles within `margin`
-// pixels of the bounding box of the observed mask's contour cells
+// pixels (rounded up to whole tiles) of a foreground tile of the observed
+// mask, inside the margin-dilated bounding box of its contour cells
 struct PyrRoiJob {
     const int *cell_count;   // ncx*ncy contour pixels per grid cell
     int *roi;                // out: [tx0, ty0, tx1, ty1] (tx0 > tx1: empty)
+    const uint8_t *fg_rows;  // H x tiles_x foreground flags (GridJob::fg_rows)
+    uint8_t *tile_flag;      // out: 1 = the pyramid computes the tile
 };
-__global__ void k_pyr_roi(JobArg<PyrRoiJob> jobs, int ncx, int ncy, int tiles_x, int tiles_y, int margin);
+__global__ void k_pyr_roi(JobArg<PyrRoiJob> jobs, int ncx, int ncy, int tiles_x, int tiles_y, int margin, int H);
 __global__ void k_pyramid_fused(JobArg<PyrAllJob> jobs, int H, int W, int levels, const double *taps,
                                 int h0, int h1, int h2, int h3);
 size_t pyramid_fused_smem();
@@ -47,6 +50,7 @@ struct GridJob {
     int qP, qL;
     double max_u2;         // cells whose bound U^2 exceeds this keep the quadtree search
     int *cell_seed;        // ncells: a nearby site per cell (jump flooding), -1 = none
+    uint8_t *fg_rows;      // H x ceil(W / LC_PYR_TILE): foreground in the row's tile segment (or null)
 };
 __global__ void k_contour_rows(JobArg<GridJob> jobs, int H, int W);
 __global__ void k_contour_scan_rows(JobArg<GridJob> jobs, int H, int ncells);

@@ -102,6 +102,7 @@ struct GridBufs {
     int *cell_seed;
     int *quad;
     int qP, qL;
+    uint8_t *fg_rows;   // H x ceil(W / LC_PYR_TILE): any foreground in the row's 32-px segment
 };
 
 #define LC_QUEUE 3   // queued frames per tracker stream (solve, preprocess, upload)

@@ -142,11 +142,12 @@ __global__ void __launch_bounds__(256) k_pyramid_fused(JobArg<PyrAllJob> jobs, i
     // grid-stride over the tiles (one tile per CTA at the default grid)
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int tx0 = (tile % tiles_x) * T, ty0 = (tile / tiles_x) * T;
-    if (J.tile_flag) {   // region of interest: tiles outside it are left to the exact on-demand path
-        const int tx = tile % tiles_x, ty = tile / tiles_x;
-        const bool want = !J.roi || (tx >= J.roi[0] && tx <= J.roi[2] && ty >= J.roi[1] && ty <= J.roi[3]);
-        if (threadIdx.x == 0) J.tile_flag[tile] = want ? 1 : 0;
-        if (!want) continue;
+    if (J.tile_flag) {   // region of interest (k_pyr_roi's flags): other tiles take the exact on-demand path
+        if (J.roi) {
+            if (!J.tile_flag[tile]) continue;
+        } else if (threadIdx.x == 0) {
+            J.tile_flag[tile] = 1;
+        }
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     // asynchronous tile copy (LDGSTS).  Interior tiles (no clamped column):
@@ -197,15 +198,20 @@ __global__ void __launch_bounds__(256) k_pyramid_fused(JobArg<PyrAllJob> jobs, i
     }   // tiles (pyr_level ends with a block barrier: `in` is free for the next tile)
 }
 
-// One CTA per stream: bounding box of the grid cells holding contour pixels
-// (= the observed silhouette's), dilated by `margin` pixels, as a tile
-// range.  margin < 0: an empty region (every sample takes the exact
-// on-demand path; a test hook).
+// One CTA per stream: the pyramid's region of interest.  The bounding box
+// of the grid cells holding contour pixels (= the observed silhouette's),
+// dilated by `margin` pixels, as a tile range; inside it, the tiles within
+// ceil(margin / LC_PYR_TILE) tiles of a tile holding foreground (the
+// per-row flags k_contour_rows leaves) get tile_flag = 1.  margin < 0: an
+// empty region (every sample takes the exact on-demand path; a test hook).
+#define LC_ROI_MAX_TILES 16384
 __global__ void __launch_bounds__(1024) k_pyr_roi(JobArg<PyrRoiJob> jobs, int ncx, int ncy, int tiles_x,
-                                                  int tiles_y, int margin) {
+                                                  int tiles_y, int margin, int H) {
     lc_pdl_wait();
     const PyrRoiJob J = jobs[blockIdx.x];
     __shared__ int b[4];
+    __shared__ int r[4];
+    __shared__ uint8_t fg[LC_ROI_MAX_TILES];
     if (threadIdx.x == 0) { b[0] = INT_MAX; b[1] = INT_MAX; b[2] = -1; b[3] = -1; }
     __syncthreads();
     int x0 = INT_MAX, y0 = INT_MAX, x1 = -1, y1 = -1;
@@ -219,16 +225,41 @@ __global__ void __launch_bounds__(1024) k_pyr_roi(JobArg<PyrRoiJob> jobs, int nc
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        int r[4] = {1, 1, 0, 0};   // empty
+        int q[4] = {1, 1, 0, 0};   // empty
         if (b[2] >= 0 && margin >= 0) {
             const int px0 = b[0] * LC_GRID_CELL - margin, py0 = b[1] * LC_GRID_CELL - margin;
             const int px1 = (b[2] + 1) * LC_GRID_CELL - 1 + margin, py1 = (b[3] + 1) * LC_GRID_CELL - 1 + margin;
-            r[0] = max(0, px0) / LC_PYR_TILE;
-            r[1] = max(0, py0) / LC_PYR_TILE;
-            r[2] = min(tiles_x - 1, px1 / LC_PYR_TILE);
-            r[3] = min(tiles_y - 1, py1 / LC_PYR_TILE);
+            q[0] = max(0, px0) / LC_PYR_TILE;
+            q[1] = max(0, py0) / LC_PYR_TILE;
+            q[2] = min(tiles_x - 1, px1 / LC_PYR_TILE);
+            q[3] = min(tiles_y - 1, py1 / LC_PYR_TILE);
         }
-        for (int k = 0; k < 4; ++k) J.roi[k] = r[k];
+        for (int k = 0; k < 4; ++k) { J.roi[k] = q[k]; r[k] = q[k]; }
+    }
+    __syncthreads();
+    if (!J.tile_flag) return;
+    const int nt = tiles_x * tiles_y;
+    const bool fine = J.fg_rows && nt <= LC_ROI_MAX_TILES;   // else the whole box
+    if (fine)
+        for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+            const int tx = t % tiles_x, ty = t / tiles_x;
+            uint8_t any = 0;
+            for (int y = ty * LC_PYR_TILE; y < min(H, (ty + 1) * LC_PYR_TILE); ++y) any |= J.fg_rows[(size_t)y * tiles_x + tx];
+            fg[t] = any;
+        }
+    __syncthreads();
+    const int d = margin >= 0 ? (margin + LC_PYR_TILE - 1) / LC_PYR_TILE : 0;
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+        const int tx = t % tiles_x, ty = t / tiles_x;
+        bool want = tx >= r[0] && tx <= r[2] && ty >= r[1] && ty <= r[3];
+        if (want && fine) {
+            bool near = false;
+            for (int yy = max(0, ty - d); yy <= min(tiles_y - 1, ty + d) && !near; ++yy)
+                for (int xx = max(0, tx - d); xx <= min(tiles_x - 1, tx + d); ++xx)
+                    if (fg[yy * tiles_x + xx]) { near = true; break; }
+            want = near;
+        }
+        J.tile_flag[t] = want ? 1 : 0;
     }
 }
 
@@ -255,6 +286,12 @@ __global__ void k_contour_rows(JobArg<GridJob> jobs, int H, int W) {
         __syncthreads();
         int local = 0;
         for (int x = threadIdx.x; x < W; x += blockDim.x) local += is_contour(J.mask, H, W, x, y);
+        if (J.fg_rows)   // foreground per LC_PYR_TILE-px segment of the row (for the pyramid's region of interest)
+            for (int x0 = (threadIdx.x >> 5) * 32; x0 < W; x0 += blockDim.x) {
+                const int x = x0 + (threadIdx.x & 31);
+                const bool f = __any_sync(0xffffffffu, x < W && J.mask[(size_t)y * W + x] != 0);
+                if ((threadIdx.x & 31) == 0) J.fg_rows[(size_t)y * ((W + LC_PYR_TILE - 1) / LC_PYR_TILE) + x0 / LC_PYR_TILE] = f;
+            }
         for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
         if ((threadIdx.x & 31) == 0 && local) atomicAdd(&cnt, local);
         __syncthreads();
