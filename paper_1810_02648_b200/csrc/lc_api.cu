@@ -1398,7 +1398,7 @@ static void contour_and_rim(FrameBatch &fb, const std::vector<Slot *> &ss, doubl
         std::vector<OwnCellsJob> oj;
         for (Slot *s : ss) oj.push_back(OwnCellsJob{s->own_mask, s->own_cnt, s->own_keys});
         const int ncx = (W + LC_GRID_CELL - 1) / LC_GRID_CELL, ncy = (H + LC_GRID_CELL - 1) / LC_GRID_CELL;
-        launch(c, k_own_cells, dim3(ncx * ncy, (unsigned)ss.size()), dim3(256), 0, stage(c, oj), H, W, ncx);
+        launch(c, k_own_cells, dim3((ncx * ncy + 7) / 8, (unsigned)ss.size()), dim3(256), 0, stage(c, oj), H, W, ncx);
     }
     std::vector<ContourJob> cj;
     for (Slot *s : ss) {

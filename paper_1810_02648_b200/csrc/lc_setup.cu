@@ -1277,39 +1277,48 @@ __global__ void __launch_bounds__(1024) k_contour_compact(JobArg<ContourJob> job
     lc_pdl_wait();
     const ContourJob J = jobs[blockIdx.x];
     if (!J.active) return;
-    __shared__ int wsum[32];
-    __shared__ int carry[2];
-    if (threadIdx.x == 0) carry[0] = carry[1] = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int base = 0; base < A.N; base += blockDim.x) {
-        const int v = base + threadIdx.x;
-        const int fl = v < A.N ? J.vflag[v] : 0;   // (k_vis_flags)
-        for (int list = 0; list < 2; ++list) {
-            if (list == 1 && !J.vis) break;
-            const bool f = (fl & (list == 0 ? 2 : 1)) != 0;
-            const unsigned bal = __ballot_sync(0xffffffffu, f);
-            if (lane == 0) wsum[w] = __popc(bal);
-            __syncthreads();
-            int before = carry[list];
-            for (int k = 0; k < w; ++k) before += wsum[k];
-            if (f) {
-                const int slot = before + __popc(bal & ((1u << lane) - 1u));
-                (list == 0 ? J.idx : J.vis)[slot] = v;
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                int t = 0;
-                for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += wsum[k];
-                carry[list] += t;
-            }
-            __syncthreads();
-        }
+    // each thread owns a run of consecutive vertices: count both lists' flags,
+    // one block scan of the (contour, visible) count pairs, then every
+    // thread writes its run in ascending order (two block barriers in all)
+    __shared__ unsigned long long wsum[32];
+    __shared__ int tot[2];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int per = (A.N + blockDim.x - 1) / blockDim.x;
+    const int v0 = min(A.N, (int)threadIdx.x * per), v1 = min(A.N, v0 + per);
+    unsigned long long cnt = 0;   // contour count | visible count << 32
+    for (int v = v0; v < v1; ++v) {
+        const int fl = J.vflag[v];   // (k_vis_flags)
+        cnt += ((fl & 2) ? 1ull : 0ull) + ((fl & 1) ? (1ull << 32) : 0ull);
     }
-    const int B = carry[0];
+    unsigned long long inc = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long u = lane < nw ? wsum[lane] : 0ull;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, u, o);
+            if (lane >= o) u += t;
+        }
+        if (lane < nw) wsum[lane] = u;   // inclusive warp totals
+        if (lane == nw - 1) { tot[0] = (int)(u & 0xffffffffu); tot[1] = (int)(u >> 32); }
+    }
+    __syncthreads();
+    const unsigned long long before = (w > 0 ? wsum[w - 1] : 0ull) + inc - cnt;
+    int p0 = (int)(before & 0xffffffffu), p1 = (int)(before >> 32);
+    for (int v = v0; v < v1; ++v) {
+        const int fl = J.vflag[v];
+        if (fl & 2) J.idx[p0++] = v;
+        if ((fl & 1) && J.vis) J.vis[p1++] = v;
+    }
+    __syncthreads();   // the contour ids, for the normals below
+    const int B = tot[0];
     if (threadIdx.x == 0) {
         *J.B = B;
-        if (J.P) *J.P = carry[1];
+        if (J.P) *J.P = J.vis ? tot[1] : 0;
     }
     // vertex normals: area-weighted, accumulated in np.add.at slot order
     // (pose_stage.py:139-148), projected with d(pix)/d(p), normalized
@@ -1352,33 +1361,33 @@ __device__ __forceinline__ int part_at(const ActorDev &A, CamDev cam, const doub
     return A.vpart[A.tris[3 * t + w]];
 }
 
-// One CTA per 16x16 cell: the cell's contour pixels of the own mask
-// (foreground with a background 4-neighbour, the image border counting as
-// background; imageproc.py:34-49), compacted in row-major order.
+// One warp per 16x16 cell (8 cells per CTA): the cell's contour pixels of
+// the own mask (foreground with a background 4-neighbour, the image border
+// counting as background; imageproc.py:34-49), compacted in row-major order
+// two cell rows per ballot (lanes 0-15 the upper row, 16-31 the lower).
 __global__ void __launch_bounds__(256) k_own_cells(JobArg<OwnCellsJob> jobs, int H, int W, int ncx) {
     lc_pdl_wait();
     const OwnCellsJob J = jobs[blockIdx.y];
-    const int c = blockIdx.x;
-    const int x = (c % ncx) * LC_GRID_CELL + (threadIdx.x & (LC_GRID_CELL - 1));
-    const int y = (c / ncx) * LC_GRID_CELL + (threadIdx.x >> LC_GRID_SHIFT);
-    bool on = false;
-    if (x < W && y < H && J.mask[(size_t)y * W + x]) {
-        const bool l = x > 0 && J.mask[(size_t)y * W + x - 1], r = x + 1 < W && J.mask[(size_t)y * W + x + 1];
-        const bool u = y > 0 && J.mask[(size_t)(y - 1) * W + x], d = y + 1 < H && J.mask[(size_t)(y + 1) * W + x];
-        on = !(l && r && u && d);
+    const int lane = threadIdx.x & 31;
+    const int ncells = ncx * ((H + LC_GRID_CELL - 1) / LC_GRID_CELL);
+    static_assert(LC_GRID_CELL == 16, "two cell rows per warp ballot");
+    for (int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < ncells; c += gridDim.x * (blockDim.x >> 5)) {
+        const int x = (c % ncx) * LC_GRID_CELL + (lane & 15);
+        int n = 0;
+        for (int r = 0; r < LC_GRID_CELL; r += 2) {
+            const int y = (c / ncx) * LC_GRID_CELL + r + (lane >> 4);
+            bool on = false;
+            if (x < W && y < H && J.mask[(size_t)y * W + x]) {
+                const bool l = x > 0 && J.mask[(size_t)y * W + x - 1], rr = x + 1 < W && J.mask[(size_t)y * W + x + 1];
+                const bool u = y > 0 && J.mask[(size_t)(y - 1) * W + x], d = y + 1 < H && J.mask[(size_t)(y + 1) * W + x];
+                on = !(l && rr && u && d);
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, on);
+            if (on) J.keys[(size_t)c * 256 + n + __popc(bal & ((1u << lane) - 1u))] = (y << 16) | x;
+            n += __popc(bal);
+        }
+        if (lane == 0) J.cnt[c] = n;
     }
-    __shared__ int wcount[8];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const unsigned bal = __ballot_sync(0xffffffffu, on);
-    if (lane == 0) wcount[w] = __popc(bal);
-    __syncthreads();
-    int before = 0, total = 0;
-    for (int k = 0; k < 8; ++k) {
-        before += k < w ? wcount[k] : 0;
-        total += wcount[k];
-    }
-    if (on) J.keys[(size_t)c * 256 + before + __popc(bal & ((1u << lane) - 1u))] = (y << 16) | x;
-    if (threadIdx.x == 0) J.cnt[c] = total;
 }
 
 // Is some own-contour pixel at squared distance < lim2 (<= lim2 when
