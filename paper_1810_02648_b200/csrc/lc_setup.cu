@@ -1417,6 +1417,37 @@ __device__ inline bool own_any_within(const NnGridDev &g, const int *cnt, const 
     return false;
 }
 
+// own_any_within by a whole warp for one query point (warp-uniform
+// arguments): the lanes split each cell's pixels, one vote per cell.
+__device__ inline bool own_any_within_warp(const NnGridDev &g, const int *cnt, const int *keys, double qx, double qy,
+                                           double R, double lim2, bool inclusive) {
+    if (!(isfinite(qx) && isfinite(qy))) return false;
+    const int lane = threadIdx.x & 31;
+    const int cx0 = max(0, (int)floor((qx - R) / LC_GRID_CELL));
+    const int cx1 = min(g.ncx - 1, (int)floor((qx + R) / LC_GRID_CELL));
+    const int cy0 = max(0, (int)floor((qy - R) / LC_GRID_CELL));
+    const int cy1 = min(g.ncy - 1, (int)floor((qy + R) / LC_GRID_CELL));
+    for (int cy = cy0; cy <= cy1; ++cy)
+        for (int cx = cx0; cx <= cx1; ++cx) {
+            const int c = cy * g.ncx + cx;
+            const int n = cnt[c];
+            const int *kk = keys + (size_t)c * 256;
+            bool hit = false;
+            for (int k0 = 0; k0 < n; k0 += 32) {
+                const int k = k0 + lane;
+                if (k < n) {
+                    const int key = kk[k];
+                    const double dx = qx - (double)(key & 0xffff), dy = qy - (double)(key >> 16);
+                    const double d2 = dx * dx + dy * dy;
+                    hit = hit || (inclusive ? d2 <= lim2 : d2 < lim2);
+                }
+            }
+            if (__any_sync(0xffffffffu, hit)) return true;
+        }
+    return false;
+}
+
+#define LC_RIM_LIST 128   // own-contour pixels near one rim vertex, per warp
 __global__ void k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double *probe_offs) {
     lc_pdl_wait();
     const RimJob J = jobs[blockIdx.y];
@@ -1425,6 +1456,8 @@ __global__ void k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double 
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     const NnGridDev own = J.own;
+    __shared__ int near_all[8][LC_RIM_LIST];
+    int *near = near_all[(threadIdx.x >> 5) & 7];
     for (int b = blockIdx.x * wpb + (threadIdx.x >> 5); b < B; b += gridDim.x * wpb) {
         const int v = J.idx[b];
         const V3 p = ld3(J.verts + 3 * (size_t)v);
@@ -1439,23 +1472,70 @@ __global__ void k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double 
         // sqrt(d2) >= 6 <=> d2 >= 36: the threshold tests on the nearest
         // distance become "is any contour pixel that close" (early exit)
         bool keep = false;
-        if (ok) keep = own_any_within(own, J.own_cnt, J.own_keys, px, py, 2.0, 2.25, true);
+        if (ok) keep = own_any_within_warp(own, J.own_cnt, J.own_keys, px, py, 2.0, 2.25, true);
         if (J.stage1) {
             if (keep) {
                 // 16 directions x radii 1..8: depth = max over interior probes
                 // of the nearest contour distance, keep iff 2 * depth >= 12,
                 // i.e. iff some interior probe has no contour pixel closer
-                // than 6 px; lane = (direction, half of the radii)
+                // than 6 px; lane = (direction, half of the radii).  A pixel
+                // within 6 px of a probe (at most 8 px out) is within 14 px of
+                // the vertex: the warp first gathers the pixels within 15 px
+                // (d2 <= 226, a superset through any rounding) into shared
+                // memory, and every probe scans that short list (broadcast
+                // reads); a list over LC_RIM_LIST falls back to the cell scans
+                int nl = 0;
+                {
+                    const double R = 15.0;
+                    const int cx0 = max(0, (int)floor((px - R) / LC_GRID_CELL));
+                    const int cx1 = min(own.ncx - 1, (int)floor((px + R) / LC_GRID_CELL));
+                    const int cy0 = max(0, (int)floor((py - R) / LC_GRID_CELL));
+                    const int cy1 = min(own.ncy - 1, (int)floor((py + R) / LC_GRID_CELL));
+                    for (int cy = cy0; cy <= cy1; ++cy)
+                        for (int cx = cx0; cx <= cx1; ++cx) {
+                            const int c = cy * own.ncx + cx;
+                            const int n = J.own_cnt[c];
+                            const int *kk = J.own_keys + (size_t)c * 256;
+                            for (int k0 = 0; k0 < n; k0 += 32) {
+                                const int k = k0 + lane;
+                                bool take = false;
+                                int key = 0;
+                                if (k < n) {
+                                    key = kk[k];
+                                    const double dx = px - (double)(key & 0xffff), dy = py - (double)(key >> 16);
+                                    take = dx * dx + dy * dy <= 226.0;
+                                }
+                                const unsigned bal = __ballot_sync(0xffffffffu, take);
+                                const int at = nl + __popc(bal & ((1u << lane) - 1u));
+                                if (take && at < LC_RIM_LIST) near[at] = key;
+                                nl += __popc(bal);
+                            }
+                        }
+                    __syncwarp();
+                }
+                const bool listed = nl <= LC_RIM_LIST;
                 bool deep = false;
                 const int dir = lane >> 1, r0 = (lane & 1) * 4;
                 for (int r = r0; r < r0 + 4; ++r) {
                     const int k = dir * 8 + r;
                     const double qx = px + probe_offs[2 * k], qy = py + probe_offs[2 * k + 1];
-                    if (field_inside(own, qx, qy) && !own_any_within(own, J.own_cnt, J.own_keys, qx, qy, 6.0, 36.0, false))
-                        deep = true;
+                    if (field_inside(own, qx, qy)) {
+                        bool shallow = false;
+                        if (listed) {
+                            for (int j = 0; j < nl && !shallow; ++j) {
+                                const int key = near[j];
+                                const double dx = qx - (double)(key & 0xffff), dy = qy - (double)(key >> 16);
+                                shallow = dx * dx + dy * dy < 36.0;
+                            }
+                        } else {
+                            shallow = own_any_within(own, J.own_cnt, J.own_keys, qx, qy, 6.0, 36.0, false);
+                        }
+                        if (!shallow) deep = true;
+                    }
                     if (__any_sync(0xffffffffu, deep)) break;   // warp-uniform
                 }
                 keep = __any_sync(0xffffffffu, deep);
+                __syncwarp();   // the list is rewritten for the warp's next vertex
             }
             keep = keep && A.rigidity[v] >= 2.0;
         } else if (J.part_gate) {
