@@ -1549,6 +1549,7 @@ static void run_frame(FrameBatch &fb, int stages = 3) {
             p.log_offset = log_off[i];
             p.phase = s->phase_pose;
             p.nn_hint = s->nn_hint;
+            p.fk_out = s->fk;
             log_off[i] += h.gn_iterations;
             pj.push_back(p);
             ++k;
@@ -1562,11 +1563,13 @@ static void run_frame(FrameBatch &fb, int stages = 3) {
     }
     if (!(stages & 2)) return;
     // ---- Stage II (pipeline.py:227-260) or the pose-only surface
+    // the pose kernel leaves FK(x) in s->fk when Stage I ran in this step
+    const bool fk_from_x = !(stages & 1) || cfg.pose.gn_iterations <= 0;
     if (cfg.mode == 0) {
-        fk_skin(fb, ss, true, true, &Slot::vinit, nullptr);
+        fk_skin(fb, ss, fk_from_x, true, &Slot::vinit, nullptr);
         fk_skin(fb, ss, false, false, &Slot::vs, &Slot::rot);
     } else {
-        fk_skin(fb, ss, true, false, &Slot::vs, &Slot::rot);
+        fk_skin(fb, ss, fk_from_x, false, &Slot::vs, &Slot::rot);
     }
     if (cfg.mode == 0) {
         mark(c, "s2:skin");

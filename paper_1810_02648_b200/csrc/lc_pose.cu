@@ -558,8 +558,16 @@ __global__ void __launch_bounds__(NT, 1) k_pose_solve_t(JobArg<PoseJob> jobs, co
         }
         __syncthreads();
     }
-    if (T::rank() == 0)
+    if (T::rank() == 0) {
         for (int i = threadIdx.x; i < LC_NP; i += NT) J.x_out[i] = s.x[i];
+        // s.f = FK(s.x) after every GN step (the accepted trial's FK, or the
+        // unchanged point's): Stage II skins from it instead of a k_fk launch
+        if (J.fk_out && J.hp.gn > 0) {
+            const unsigned long long *src = reinterpret_cast<const unsigned long long *>(&s.f);
+            unsigned long long *dst = reinterpret_cast<unsigned long long *>(J.fk_out);
+            for (int i = threadIdx.x; i < (int)(sizeof(FkState) / 8); i += NT) dst[i] = src[i];
+        }
+    }
     if (T::tid() == 0 && rep) {
         rep->n_iterations = log0 + J.hp.gn;
         rep->behind_camera += behind_total;

@@ -25,6 +25,7 @@ struct PoseJob {
     int log_offset;
     long long *phase;         // LC_NPHASE timestamps (or null)
     int *nn_hint;             // B: last nearest contour pixel per silhouette row (or null)
+    FkState *fk_out;          // FK of x_out at exit (rank 0; null: not written)
 };
 
 struct SurfJob {

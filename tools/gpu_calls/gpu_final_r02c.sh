@@ -1,0 +1,18 @@
+# final build: full gpu suite, smoke, bench lines (ours + reference arm), A/B of the pose-kernel FK handoff
+# against build_var/prev, launch list
+O=gpurun_out/r02fc; mkdir -p $O
+timeout 1500 python -m pytest tests -m gpu -q -rs --durations=10 > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -6 $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 $O/smoke.log
+timeout 900 python bench.py > $O/bench_n1.json 2> $O/bench.err; echo "bench rc=$?"; head -c 300 $O/bench_n1.json; echo
+B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e-u8 --no-quality"
+P='import json,sys; d=json.load(sys.stdin); print(round(d["value"]), round(d["ms_per_step"],3), d["pcg_iter_us"], round(d["roofline"]["kernel_ms_per_launch"],3), round(d["roofline"]["frac"],4), round(d["roofline"]["frac_concurrent"],4))'
+{
+for v in default prev default prev; do
+  if [ $v = default ]; then L=""; else L="LIVECAP_LIB=build_var/$v/liblivecap.so"; fi
+  echo "== $v"; env $L timeout 300 $B 2>/dev/null | python -c "$P"
+done
+} > $O/sweep.txt 2>&1; cat $O/sweep.txt
+timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > $O/bench_reference.json 2> $O/bench_ref.err; echo "ref rc=$?"; head -c 200 $O/bench_reference.json; echo
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
+    python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-e2e-u8 --no-quality > /dev/null 2>&1; echo "ncu list rc=$?"
+ls -la $O
