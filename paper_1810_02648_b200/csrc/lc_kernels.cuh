@@ -164,7 +164,7 @@ struct RimJob {
     int part_gate;
     int dilation;
 };
-__global__ void k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double *probe_offs);
+__global__ void __launch_bounds__(256) k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double *probe_offs);
 __global__ void k_part_labels(ActorDev A, CamDev cam, const double *verts, const int *tri_id, int dilation,
                               int *labels);
 

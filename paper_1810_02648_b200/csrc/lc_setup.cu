@@ -1448,7 +1448,7 @@ __device__ inline bool own_any_within_warp(const NnGridDev &g, const int *cnt, c
 }
 
 #define LC_RIM_LIST 128   // own-contour pixels near one rim vertex, per warp
-__global__ void k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double *probe_offs) {
+__global__ void __launch_bounds__(256) k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double *probe_offs) {
     lc_pdl_wait();
     const RimJob J = jobs[blockIdx.y];
     if (!J.active) return;
@@ -1456,8 +1456,8 @@ __global__ void k_rim(JobArg<RimJob> jobs, ActorDev A, CamDev cam, const double 
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     const NnGridDev own = J.own;
-    __shared__ int near_all[8][LC_RIM_LIST];
-    int *near = near_all[(threadIdx.x >> 5) & 7];
+    __shared__ int near_all[8][LC_RIM_LIST];   // one list per warp: launched with 256 threads
+    int *near = near_all[threadIdx.x >> 5];
     for (int b = blockIdx.x * wpb + (threadIdx.x >> 5); b < B; b += gridDim.x * wpb) {
         const int v = J.idx[b];
         const V3 p = ld3(J.verts + 3 * (size_t)v);
