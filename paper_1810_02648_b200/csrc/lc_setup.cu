@@ -1109,6 +1109,7 @@ __global__ void __launch_bounds__(256) k_rt_tiles(JobArg<RasterJob> jobs, CamDev
 __global__ void __launch_bounds__(256) k_rt_merge(JobArg<RasterJob> jobs, CamDev cam, int ntx, int nt) {
     lc_pdl_wait();
     const RasterJob J = jobs[blockIdx.y];
+    if (J.ioff[nt] == nt) return;   // one item per tile: no tile was split, nothing to merge
     for (int tile = blockIdx.x; tile < nt; tile += gridDim.x) {
         const int i0 = J.ioff[tile], i1 = J.ioff[tile + 1];
         if (i1 - i0 <= 1) continue;
